@@ -1,0 +1,99 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, sequential CPU oracle for the mixed-precision one-sided Jacobi
+ * SVD of arXiv 2209.04626 ("Mixed precision Jacobi SVD algorithm").  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference legs may load this library.  It shares no code, header, table or
+ * constant generator with the CUDA path (paper_2209_04626_b200/csrc).
+ *
+ * Two oracles:
+ *   O-MIX  om_*  : Algorithm 3 step by step, with the
+ *                  block round-robin ordering and every reading fixed in
+ *                  DESIGN.md sec. "Readings".
+ *   O-CYC  oc_*  : textbook Algorithm 1 in fp64 with the
+ *                  row-cyclic order of eq. (2.1).
+ *
+ * All matrices are column-major.  Return codes: 0 ok, 1 not converged
+ * (outputs filled), -1 invalid argument, -2 non-finite input, -3 rank
+ * deficient.
+ *
+ * Parity pins: see tests/test_oracle_pins.py.  Every function below is
+ * pinned by at least one test that does not re-type its formula.
+ */
+#ifndef MPJSVD_ORACLE_H
+#define MPJSVD_ORACLE_H
+#include <stdint.h>
+
+#define OM_PATH_FORCE_MIXED 0
+#define OM_PATH_FORCE_FP64 2
+
+typedef struct {
+    int32_t b;              /* block width (columns per block) */
+    double tol_mult32;      /* eps_tol = tol_mult * sqrt(n) * u  (reading c-1) */
+    double tol_mult64;
+    int32_t inner_tol_div;  /* inner solve threshold = eps_tol / inner_tol_div (c-5) */
+    int32_t max_sweeps32;
+    int32_t max_sweeps64;
+    int32_t max_inner;      /* inner sweeps cap (c-5) */
+    int32_t path;           /* OM_PATH_* */
+    int32_t x_from_lq;      /* 1: X = L (default, F1); 0: X = R */
+    int32_t nthreads;       /* OpenMP threads over disjoint pairs (0 = default) */
+} om_opts;
+
+typedef struct {
+    int32_t sweeps32, sweeps64, converged, path_taken;
+    double orth_measure, tail_fraction, cond_estimate;
+    double final_off32, final_off64;
+    double off_trace32[64], off_trace64[64];
+    int32_t upd_trace32[64], upd_trace64[64];
+    int32_t perm[1];        /* unused placeholder (keeps layout simple) */
+} om_stats;
+
+void om_default_opts(om_opts* o);
+
+/* --- building blocks (exported for step-level parity tests) ------------- */
+/* Householder reflector of x[0..len-1] with beta = +||x|| >= 0 (c-13):
+   on exit x[0] = beta, x[1..] = v[1..] (v[0] = 1 implicit), returns tau. */
+double om_house(double* x, int64_t len);
+/* Unpivoted Householder QR in place, diag(R) >= 0.  PAPER.md:416-420. */
+int om_qr(double* A, int64_t m, int64_t n, int64_t lda, double* tau);
+/* Businger-Golub column-pivoted QR (LAPACK xGEQP3 semantics, diag(R) >= 0,
+   pivot = largest partial norm, ties -> lowest index).  PAPER.md:332-335. */
+int om_qrp(double* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, double* tau);
+/* C <- Q*C with Q = H_0 H_1 ... H_{k-1} stored as in om_qr (rows m). */
+void om_apply_q(const double* Vr, int64_t m, int64_t k, int64_t ldv, const double* tau,
+                double* C, int64_t ldc, int64_t ncols);
+/* 2b x 2b inner solve (c-5): two-sided round-robin Jacobi on symmetric G
+   (w x w, full storage, ld = w), E = V_blk - I on exit (ld = w).
+   Returns the number of rotations; *inner_sweeps receives the sweeps used. */
+int64_t om_inner_solve_f64(double* G, int32_t w, double tol_in, int32_t max_inner,
+                           double* E, int32_t* inner_sweeps);
+int64_t om_inner_solve_f32(float* G, int32_t w, float tol_in, int32_t max_inner,
+                           float* E, int32_t* inner_sweeps);
+/* Block round-robin one-sided Jacobi (Alg. 1 in block form, c-4..c-6, c-10).
+   X is m x n (ldx), V is nv x n (ldv) or NULL.  Returns sweeps (negative if
+   not converged within max_sweeps).  off_trace/upd_trace may be NULL. */
+int32_t om_block_jacobi_f64(double* X, int64_t m, int64_t n, int64_t ldx,
+                            double* V, int64_t nv, int64_t ldv, int32_t b,
+                            double tol, double tol_in, int32_t max_sweeps, int32_t max_inner,
+                            double* off_trace, int32_t* upd_trace, int32_t nthreads);
+int32_t om_block_jacobi_f32(float* X, int64_t m, int64_t n, int64_t ldx,
+                            float* V, int64_t nv, int64_t ldv, int32_t b,
+                            float tol, float tol_in, int32_t max_sweeps, int32_t max_inner,
+                            int32_t stagnation,
+                            double* off_trace, int32_t* upd_trace, int32_t nthreads);
+/* Precision lift (c-11): Q = V * Rv^-1 with Rv = chol(V^T V), V = fl64(V32). */
+int om_lift(const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq);
+
+/* --- the whole method ------------------------------------------------- */
+int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_opts* opts,
+                 double* U, int64_t ldu, double* S, double* V, int64_t ldv, om_stats* st);
+
+/* --- O-CYC: textbook Algorithm 1, fp64, row-cyclic order eq. (2.1) ---- */
+/* On exit X holds X*V_X (unnormalised), V (n x n, ldv) the accumulated
+   rotations (V seeded by the caller).  Returns sweeps (<0: not converged). */
+int32_t oc_cyclic_jacobi(double* X, int64_t m, int64_t n, int64_t ldx, double* V, int64_t ldv,
+                         double tol, int32_t max_sweeps, int64_t* rotations);
+
+#endif

@@ -1,0 +1,383 @@
+"""Pins for the CPU oracle (oracle/), run without a GPU.
+
+Each test checks the oracle against something other than itself: a closed
+form, an exact construction, brute force in high precision, a LAPACK routine
+standing in for a textbook special case, or a mathematical invariant.  A
+plausible slip in the oracle (a dropped term, wrong sign, transposed operand,
+wrong index) fails at least one of them; DESIGN.md lists which pin covers
+which step.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import testmat
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "closed_forms.json")))
+U = 2.0 ** -53
+
+
+def orth(q):
+    return np.abs(q.T @ q - np.eye(q.shape[1])).max()
+
+
+def tiered_tol(sigma_ref, kappa):
+    """max(1e-12, 1e3 u min(kappa, sigma_1/sigma_i))."""
+    return np.maximum(1e-12, 1e3 * U * np.minimum(kappa, sigma_ref[0] / sigma_ref))
+
+
+# ---------------------------------------------------------------- P1 closed forms
+def test_golden_ratio_2x2():
+    g = GOLD["golden_ratio_2x2"]
+    a = np.array(g["A_rowmajor"], order="F")
+    u, s, v, st, rc = oracle.mixed_svd(a)
+    assert rc == 0
+    np.testing.assert_allclose(s, g["sigma"], rtol=2e-16 * 4, atol=0)
+    assert np.linalg.norm(a - (u * s) @ v.T) < 4e-16 * 4
+
+
+def test_rotation_closed_form():
+    """G = [[a, c], [c, b]] with a=1, b=2, c=0.5: one rotation, t = tan(pi/8)."""
+    g = GOLD["rotation_a1_b2_c05"]
+    G = np.array([[g["a"], g["c"]], [g["c"], g["b"]]])
+    gout, e, nrot, isw = oracle.inner_solve(G, 1e-15)
+    assert nrot == 1
+    J = np.eye(2) + e
+    np.testing.assert_allclose(J, [[g["cs"], g["sn"]], [-g["sn"], g["cs"]]], rtol=0, atol=2e-16)
+    # diagonal = eigenvalues (3 -+ sqrt 2)/2 of G, off-diagonal exactly 0
+    np.testing.assert_allclose(np.diag(gout), [(3 - np.sqrt(2)) / 2, (3 + np.sqrt(2)) / 2], rtol=4e-16)
+    assert gout[0, 1] == 0.0 and gout[1, 0] == 0.0
+
+
+def test_rotation_closed_form_fp32():
+    g = GOLD["rotation_a1_b2_c05"]
+    G = np.array([[g["a"], g["c"]], [g["c"], g["b"]]], dtype=np.float32)
+    gout, e, nrot, isw = oracle.inner_solve(G, 1e-6, dtype=np.float32)
+    J = np.eye(2) + e.astype(np.float64)
+    np.testing.assert_allclose(J, [[g["cs"], g["sn"]], [-g["sn"], g["cs"]]], rtol=0, atol=2e-7)
+
+
+def test_symmetric_case_45_degrees():
+    """a = b, c > 0: zeta = 0, t = 1, cs = sn = 1/sqrt2 (SPEC.md jacobi example)."""
+    G = np.array([[2.0, 0.5], [0.5, 2.0]])
+    gout, e, nrot, _ = oracle.inner_solve(G, 1e-15)
+    np.testing.assert_allclose(np.eye(2) + e, np.array([[1, 1], [-1, 1]]) / np.sqrt(2), atol=2e-16)
+    np.testing.assert_allclose(np.diag(gout), [1.5, 2.5], rtol=2e-16)
+
+
+@pytest.mark.parametrize("b", [1, 4, 32])
+def test_identity_one_sweep(b):
+    g = GOLD["identity_one_sweep"]
+    x = np.eye(40)
+    xo, vo, sw, offs, upds = oracle.block_jacobi(x, np.eye(40), b, oracle.tol(40), oracle.tol(40) / 8)
+    assert sw == g["sweeps"] and upds.sum() == g["rotations"]
+    assert np.array_equal(xo, np.eye(40))
+
+
+def test_householder_maps_to_positive_multiple_of_e1():
+    rng = np.random.default_rng(1)
+    for x0 in ([3.0, 4.0], [-3.0, 4.0], [5.0, 0.0], [-5.0, 0.0], rng.standard_normal(17), -np.abs(rng.standard_normal(9))):
+        x0 = np.asarray(x0, dtype=float)
+        out, tau = oracle.house(x0)
+        v = np.concatenate([[1.0], out[1:]])
+        H = np.eye(x0.size) - tau * np.outer(v, v)
+        assert orth(H) < 8 * U
+        hx = H @ x0
+        assert out[0] >= 0
+        np.testing.assert_allclose(hx[0], np.linalg.norm(x0), rtol=4 * U)
+        np.testing.assert_allclose(out[0], np.linalg.norm(x0), rtol=4 * U)
+        assert np.abs(hx[1:]).max() <= 8 * U * np.linalg.norm(x0)
+    out, tau = oracle.house(np.array([3.0, 4.0]))
+    assert out[0] == 5.0
+
+
+# ---------------------------------------------------------------- QR building blocks
+def test_qr_against_lapack_and_invariants():
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((50, 20))
+    packed, tau, rc = oracle.qr(a)
+    assert rc == 0
+    r = np.triu(packed[:20, :])
+    q = oracle.form_q(packed, tau, 20)
+    assert orth(q) < 1e-14
+    assert np.abs(q @ r - a).max() < 1e-14
+    assert np.all(np.diag(r) >= 0)
+    r_lapack = np.linalg.qr(a, mode="r")
+    np.testing.assert_allclose(np.abs(r), np.abs(r_lapack), atol=1e-13)
+
+
+def test_qrp_against_lapack_dgeqp3():
+    import scipy.linalg as sl
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((60, 60)) * 10.0 ** rng.uniform(-3, 3, 60)
+    packed, perm, tau, rc = oracle.qrp(a)
+    _, r_l, piv = sl.qr(a, pivoting=True)
+    assert np.array_equal(perm, piv)       # same Businger-Golub pivot sequence
+    r = np.triu(packed)
+    np.testing.assert_allclose(np.abs(r), np.abs(r_l), rtol=1e-12, atol=1e-12 * np.abs(r_l).max())
+    q = oracle.form_q(packed, tau)
+    assert np.abs(q @ r - a[:, perm]).max() < 1e-13 * np.abs(a).max()
+    d = np.diag(r)
+    assert np.all(d >= 0) and np.all(d[:-1] >= d[1:] * (1 - 1e-12))
+    # RRQR property: R_kk >= ||R(k:j, j)|| for j > k
+    for k in range(59):
+        assert d[k] >= np.linalg.norm(r[k:, k + 1:], axis=0).max() * (1 - 1e-12)
+
+
+def test_qrp_ties_lowest_index():
+    a = np.asfortranarray(np.eye(6) * 2.0)
+    packed, perm, tau, rc = oracle.qrp(a)
+    assert list(perm) == list(range(6))
+
+
+def test_rank_deficient_and_invalid():
+    a = testmat.config_matrix("C1", 16)
+    a[:, 5] = 0.0
+    assert oracle.mixed_svd(a)[4] == -3
+    b = testmat.config_matrix("C1", 16)
+    b[3, 3] = np.nan
+    assert oracle.mixed_svd(b)[4] == -2
+    assert oracle.mixed_svd(np.ones((4, 6)))[4] == -1
+
+
+# ---------------------------------------------------------------- inner solve
+@pytest.mark.parametrize("w", [2, 7, 64])
+def test_inner_solve_diagonalises(w):
+    rng = np.random.default_rng(w)
+    b = rng.standard_normal((3 * w, w)) * 10.0 ** rng.uniform(-2, 2, w)
+    G0 = b.T @ b
+    tol_in = oracle.tol(3 * w) / 8
+    g, e, nrot, isw = oracle.inner_solve(G0, tol_in)
+    J = np.eye(w) + e
+    assert orth(J) < 50 * U * w ** 0.5
+    D = J.T @ G0 @ J
+    dd = np.sqrt(np.diag(D))
+    off = np.abs(D - np.diag(np.diag(D))) / np.outer(dd, dd)
+    assert off.max() < 20 * tol_in
+    # LAPACK dsyevd is absolutely (not relatively) accurate: Weyl-type bound
+    lam = np.linalg.eigvalsh(G0)
+    assert np.abs(np.sort(np.diag(g)) - lam).max() <= 64 * w * U * lam[-1]
+
+
+# ---------------------------------------------------------------- block Jacobi
+@pytest.mark.parametrize("n,b", [(96, 16), (100, 16), (7, 4), (50, 64), (33, 1)])
+def test_block_jacobi_orthogonalises(n, b):
+    rng = np.random.default_rng(n + b)
+    x0 = rng.standard_normal((n, n))
+    tol_ = oracle.tol(n)
+    x, v, sw, offs, upds = oracle.block_jacobi(x0, np.eye(n), b, tol_, tol_ / 8, max_sweeps=40)
+    assert sw > 0
+    nrm = np.linalg.norm(x, axis=0)
+    c = np.abs(x.T @ x) / np.outer(nrm, nrm)
+    np.fill_diagonal(c, 0)
+    assert c.max() <= 4 * tol_
+    assert orth(v) < 16 * n * U
+    assert np.abs(x0 @ v - x).max() < 1e-13 * np.abs(x0).max() * n ** 0.5
+    np.testing.assert_allclose(np.sort(nrm)[::-1], np.linalg.svd(x0, compute_uv=False), rtol=1e-12)
+    assert upds[-1] == 0
+
+
+def test_block_jacobi_f32_stage():
+    rng = np.random.default_rng(5)
+    n = 64
+    x0 = rng.standard_normal((n, n)).astype(np.float32)
+    tol_ = np.float32(4 * np.sqrt(n) * 2.0 ** -24)
+    x, v, sw, offs, upds = oracle.block_jacobi(x0, np.eye(n, dtype=np.float32), 8, tol_, tol_ / 8,
+                                               stagnation=True, dtype=np.float32)
+    assert sw > 0
+    assert orth(v.astype(np.float64)) < 1e-5
+    s = np.sort(np.linalg.norm(x.astype(np.float64), axis=0))[::-1]
+    np.testing.assert_allclose(s, np.linalg.svd(x0.astype(np.float64), compute_uv=False), rtol=1e-5)
+
+
+# ---------------------------------------------------------------- lift (switch repair)
+def test_lift_repairs_orthogonality():
+    """orth(fl64(V32)) ~ u_low while orth(Q) <= 1e-14; Q^T V is
+    upper triangular with positive diagonal (V = Q R_v)."""
+    import scipy.linalg as sl
+    a = testmat.config_matrix("C1", 128)
+    _, r, _ = sl.qr(a, pivoting=True)
+    x = np.linalg.qr(r.T)[1].T
+    e = np.frexp(np.abs(x).max())[1]
+    x32 = np.ldexp(x, -e).astype(np.float32)
+    t32 = np.float32(4 * np.sqrt(128) * 2.0 ** -24)
+    _, v32, sw, _, _ = oracle.block_jacobi(x32, np.eye(128, dtype=np.float32), 32, t32, t32 / 8,
+                                           stagnation=True, dtype=np.float32)
+    o32 = orth(v32.astype(np.float64))
+    assert 1e-8 <= o32 <= 1e-4
+    q, rc = oracle.lift(v32)
+    assert rc == 0 and orth(q) < 1e-14
+    rv = q.T @ v32.astype(np.float64)
+    assert np.abs(np.tril(rv, -1)).max() < 1e-14
+    assert np.all(np.diag(rv) > 0)
+    assert np.abs(q - v32).max() < 1e-4
+
+
+# ---------------------------------------------------------------- P2 exact sigma
+@pytest.mark.parametrize("n", [16, 64, 256])
+def test_exact_sigma(n):
+    a, sigma = testmat.exact_sigma_matrix(n)
+    u, s, v, st, rc = oracle.mixed_svd(a)
+    assert rc == 0
+    rel = np.abs(s - sigma) / sigma
+    assert np.all(rel <= tiered_tol(sigma, sigma[0] / sigma[-1]))
+    assert rel.max() < 1e-12
+    assert orth(u) < 1e-13 and orth(v) < 1e-13
+
+
+# ---------------------------------------------------------------- P3 brute force n <= 8
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_brute_force_small(n):
+    import mpmath
+    mpmath.mp.dps = 50
+    rng = np.random.default_rng(100 + n)
+    a = rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-1, 1, n)
+    fa = [[Fraction(float(a[i, j])) for j in range(n)] for i in range(n)]
+    ata = [[sum(fa[k][i] * fa[k][j] for k in range(n)) for j in range(n)] for i in range(n)]
+    M = mpmath.matrix([[mpmath.mpf(ata[i][j].numerator) / ata[i][j].denominator for j in range(n)]
+                       for i in range(n)])
+    ev = mpmath.eigsy(M, eigvals_only=True)
+    ref = np.array(sorted([float(mpmath.sqrt(x)) for x in ev], reverse=True))
+    u, s, v, st, rc = oracle.mixed_svd(np.asfortranarray(a))
+    assert rc == 0
+    kappa = ref[0] / ref[-1]
+    assert np.all(np.abs(s - ref) / ref <= np.maximum(64 * n * U, 64 * U * kappa))
+
+
+# ---------------------------------------------------------------- P4 high relative accuracy
+@pytest.mark.parametrize("n,span", [(16, 20), (32, 20), (32, 40)])
+def test_high_relative_accuracy_graded(n, span):
+    import mpmath
+    mpmath.mp.dps = 80
+    a, d = testmat.graded_matrix(n, span)
+    M = mpmath.matrix(a.tolist())
+    ref = np.array(sorted([float(x) for x in mpmath.svd_r(M, compute_uv=False)], reverse=True))
+    u, s, v, st, rc = oracle.mixed_svd(a)
+    assert rc == 0
+    assert ref[0] / ref[-1] > 1e10
+    assert np.max(np.abs(s - ref) / ref) < 1e-13
+
+
+# ---------------------------------------------------------------- P5 invariances
+def test_power_of_two_scaling_bitwise():
+    a = testmat.config_matrix("C2", 64)
+    u1, s1, v1, _, _ = oracle.mixed_svd(a)
+    u2, s2, v2, _, _ = oracle.mixed_svd(np.asfortranarray(a * 2.0 ** 37))
+    assert np.array_equal(s2, s1 * 2.0 ** 37)
+    assert np.array_equal(u1, u2) and np.array_equal(v1, v2)
+
+
+def test_column_permutation_invariance():
+    a = testmat.config_matrix("C1", 64)
+    pi = np.random.default_rng(9).permutation(64)
+    u1, s1, v1, _, _ = oracle.mixed_svd(a)
+    u2, s2, v2, _, _ = oracle.mixed_svd(np.asfortranarray(a[:, pi]))
+    assert np.array_equal(s1, s2)
+    assert np.array_equal(u1, u2)
+    assert np.array_equal(v1[pi, :], v2)
+
+
+def test_thread_count_independence():
+    a = testmat.config_matrix("C1", 128)
+    r1 = oracle.mixed_svd(a, nthreads=1)
+    r4 = oracle.mixed_svd(a, nthreads=4)
+    for x, y in zip(r1[:3], r4[:3]):
+        assert np.array_equal(x, y)
+
+
+# ---------------------------------------------------------------- P6/P7 structure, sweeps
+@pytest.mark.parametrize("name,n", [("C1", 256), ("C2", 256), ("C3", 256), ("C4", 128), ("C5", 256)])
+def test_structural_bounds_and_sweeps(name, n):
+    a = testmat.config_matrix(name, n)
+    m = a.shape[0]
+    u, s, v, st, rc = oracle.mixed_svd(a)
+    assert rc == 0
+    assert orth(u) <= 1e-13 and orth(v) <= 1e-13
+    res = np.linalg.norm(a - (u * s) @ v.T) / np.linalg.norm(a)
+    assert res <= 1e-13
+    # columnwise backward error (preconditioned Jacobi, sec. 4)
+    colres = np.linalg.norm(a - (u * s) @ v.T, axis=0) / np.linalg.norm(a, axis=0)
+    assert colres.max() <= 200 * n * U
+    assert np.all(s[:-1] >= s[1:]) and np.all(s > 0)
+    # "typically three sweeps"; +1 slack
+    assert st["sweeps64"] <= GOLD["refinement_sweeps"]["max_with_slack"]
+    assert st["upd_trace64"][-1] == 0
+    assert st["sweeps32"] >= 2
+
+
+def test_force_fp64_path_agrees():
+    a = testmat.config_matrix("C1", 128)
+    u1, s1, v1, st1, _ = oracle.mixed_svd(a)
+    u2, s2, v2, st2, _ = oracle.mixed_svd(a, path=2)
+    assert st2["sweeps32"] == 0 and st2["sweeps64"] > st1["sweeps64"]
+    assert np.max(np.abs(s1 - s2) / s2) < 1e-12
+
+
+def test_x_from_r_ablation_agrees():
+    a = testmat.config_matrix("C1", 96)
+    s1 = oracle.mixed_svd(a)[1]
+    s2 = oracle.mixed_svd(a, x_from_lq=0)[1]
+    assert np.max(np.abs(s1 - s2) / s2) < 1e-12
+
+
+# ---------------------------------------------------------------- P8 / P9 cross-checks
+def _dgejsv_sigma(a):
+    from scipy.linalg import lapack
+    sva, _, _, wo, _, info = lapack.dgejsv(a, joba=0, jobu=3, jobv=3)
+    assert info == 0
+    return np.sort(sva * wo[0] / wo[1])[::-1]
+
+
+@pytest.mark.parametrize("name,n,kappa_s", [("C1", 256, 1e4), ("C2", 512, 1e3), ("C5", 256, 1e8)])
+def test_against_dgejsv(name, n, kappa_s):
+    a = testmat.config_matrix(name, n)
+    s = oracle.mixed_svd(a)[1]
+    sj = _dgejsv_sigma(a)
+    assert np.all(np.abs(s - sj) / sj <= tiered_tol(sj, kappa_s))
+
+
+def test_graded_vs_dgejsv_paper_scale():
+    """max relative difference vs DGEJSV 4.7879e-14 on
+    1024^2 graded test matrices; C2 (kappa_s ~ 1e3, columns graded 1e12) at
+    n = 512 must land on the same scale."""
+    a = testmat.config_matrix("C2", 512)
+    s = oracle.mixed_svd(a)[1]
+    sj = _dgejsv_sigma(a)
+    assert np.max(np.abs(s - sj) / sj) < 10 * GOLD["mixed_vs_dgejsv_max_rel"]["value"]
+
+
+@pytest.mark.parametrize("name,n", [("C1", 128), ("C2", 128), ("C4", 64)])
+def test_omix_vs_ocyc(name, n):
+    a = testmat.config_matrix(name, n)
+    u1, s1, v1, st, _ = oracle.mixed_svd(a)
+    u2, s2, v2, sw = oracle.cyclic_svd(a)
+    assert sw > 0
+    assert np.all(np.abs(s1 - s2) / s2 <= tiered_tol(s2, 1e4))
+    # singular vectors agree up to sign where sigma is well separated
+    gap = np.minimum(np.abs(np.diff(s2, prepend=np.inf)), np.abs(np.diff(s2, append=-np.inf))) / s2
+    ok = gap > 1e-3
+    dots = np.abs(np.sum(v1 * v2, axis=0))
+    assert np.all(np.abs(dots[ok] - 1) < 1e-9)
+
+
+def test_ocyc_unpreconditioned_textbook():
+    """O-CYC directly on A (no preconditioning) against the exact sigma."""
+    a, sigma = testmat.exact_sigma_matrix(32)
+    u, s, v, sw = oracle.cyclic_svd(a, precondition=False)
+    assert sw > 0
+    assert np.max(np.abs(s - sigma) / sigma) < 1e-12
+    assert orth(v) < 1e-14
+
+
+# ---------------------------------------------------------------- P2b planted sigma
+@pytest.mark.parametrize("name", ["C1", "C5"])
+def test_planted_sigma_construction_bound(name):
+    n = 256
+    a = testmat.config_matrix(name, n)
+    s = oracle.mixed_svd(a)[1]
+    planted = testmat.planted_sigma(name, n)
+    assert np.abs(s - planted).max() <= 8 * np.sqrt(n) * U * planted[0]
