@@ -1,0 +1,176 @@
+/*
+ * mpjsvd.h -- C-ABI of the B200-native mixed-precision one-sided Jacobi SVD.
+ *
+ * Computes the full SVD A = U * diag(S) * V^T of a dense real m x n fp64
+ * matrix with m >= n (Alg. 3 "Require A ... with m >= n,
+ * Ensure the full singular value decomposition A = U Sigma V^*"), by the
+ * paper's four stages:
+ *   (1) preconditioning: [m > n] Householder QR A = Q_tall R1,
+ *       column-pivoted QR A1 P = Q_p R, LQ R = L Q_2 and
+ *       X = L (reading R1);
+ *   (2) fp32 one-sided block Jacobi on fl32(X 2^-e) accumulating V32
+ *       (Alg. 1);
+ *   (3) precision switch: Q = qr(fl64(V32)) by CholeskyQR, Y = X Q
+ *       (PAPER.md:553-561, 450);
+ *   (4) fp64 one-sided block Jacobi on (Y, V := Q) to eps_tol, then
+ *       sigma_j = ||y_j||, U_X = Y diag(1/sigma), descending sort
+ *       (PAPER.md:452-455, 575-597, 305-310);
+ * and assembles U = Q_tall Q_p U_X, V = P Q_t V_X.
+ *
+ * Conventions (all entry points):
+ *   - Matrices are column-major fp64.  A is m x n with leading dimension lda,
+ *     U is m x n (ldu), S has n entries (descending, > 0), V is n x n (ldv).
+ *   - Pointers may be DEVICE pointers on the handle's device (the fast path;
+ *     nothing crosses PCIe) or HOST pointers (pageable or pinned): the library
+ *     detects host memory with cudaPointerGetAttributes and stages it through
+ *     device buffers inside the call (that is the end-to-end path bench.py
+ *     times).  A may not alias U, S or V.
+ *   - Ownership: the caller owns A (never modified), U, S and V.  The handle
+ *     owns every device workspace, stream event and NCCL object; they are
+ *     freed by mpjsvd_destroy.  Workspaces are (re)allocated on the first call
+ *     for a given (m, n) and reused after that.
+ *   - Threading: one mpjsvd_factor at a time per handle; distinct handles may
+ *     be used concurrently from different host threads.
+ *   - The call is stream-ordered on options.stream (NULL: a stream owned by
+ *     the handle) and synchronises the host once per Jacobi sweep (16-byte
+ *     convergence read-back) and once at exit.
+ *   - No C++ exception, abort or exit crosses this boundary.  Errors are
+ *     negative return codes; mpjsvd_strerror() maps any code to a static
+ *     string.
+ */
+#ifndef MPJSVD_H
+#define MPJSVD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPJSVD_VERSION 100
+
+/* return codes */
+#define MPJSVD_OK 0
+#define MPJSVD_WARN_NOT_CONVERGED 1   /* outputs filled; fp64 stage hit max_sweeps64 */
+#define MPJSVD_ERR_INVALID_ARG (-1)   /* null pointer, m < n, n < 2, lda < m, ldu < m, ldv < n, bad option */
+#define MPJSVD_ERR_NONFINITE (-2)     /* A contains NaN or Inf */
+#define MPJSVD_ERR_RANK_DEFICIENT (-3)/* zero R diagonal / zero column / singular V^T V */
+#define MPJSVD_ERR_CUDA (-4)          /* CUDA runtime error (see mpjsvd_last_cuda_error) */
+#define MPJSVD_ERR_NCCL (-5)
+#define MPJSVD_ERR_OUT_OF_MEMORY (-6)
+#define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1 in this build, block_cols unsupported */
+
+/* path (Alg. 3 gates; reading c-15) */
+#define MPJSVD_PATH_FORCE_MIXED 0     /* always run the fp32 Jacobi stage (default) */
+#define MPJSVD_PATH_AUTO 1            /* reserved: gate-driven choice (next) */
+#define MPJSVD_PATH_FORCE_FP64 2      /* skip the fp32 stage: Q = I, Y = X */
+
+typedef struct mpjsvd_handle_s* mpjsvd_handle;
+
+typedef struct {
+    int32_t num_gpus;          /* 1 in this build */
+    int32_t device_id;         /* CUDA device ordinal (default: current device) */
+    int32_t block_cols;        /* b, columns per Jacobi block: 8, 16 or 32 (default 32) */
+    double tol_mult32;         /* eps_tol32 = tol_mult32 * sqrt(n) * 2^-24 (default 4) */
+    double tol_mult64;         /* eps_tol64 = tol_mult64 * sqrt(n) * 2^-53 (default 4) */
+    int32_t inner_tol_div;     /* 2b x 2b inner solve runs to eps_tol / inner_tol_div (default 8) */
+    int32_t max_sweeps32;      /* default 20 (+ stagnation exit, reading c-10) */
+    int32_t max_sweeps64;      /* default 30 */
+    int32_t max_inner;         /* inner sweeps cap (default 30) */
+    int32_t path;              /* MPJSVD_PATH_* (default FORCE_MIXED) */
+    int32_t x_from_lq;         /* 1 (default): X = L; 0: X = R (ablation) */
+    int32_t compute_gates;     /* 1 (default): report orth / tail / cond measures */
+    void* stream;              /* cudaStream_t on device_id, or NULL */
+} mpjsvd_options;
+
+typedef struct {
+    int32_t path_taken;        /* MPJSVD_PATH_FORCE_MIXED or _FORCE_FP64 */
+    int32_t sweeps32, sweeps64, converged;
+    double stage_ms[8];        /* qr_tall, qrp, lq, gates, fp32, lift, fp64, assemble (CUDA events) */
+    double total_ms;           /* device time from entry to outputs written */
+    double orth_measure;       /* ||X_t^T X_t - I||_max, X_t = fl32(X) D^-1 */
+    double tail_fraction;      /* fraction of columns of X with norm < 2^-60 max */
+    double cond_estimate;      /* max_k R_kk / min_k R_kk */
+    double final_off32, final_off64;
+    double off_trace32[32], off_trace64[32];   /* per-sweep max normalised off-diagonal */
+    int32_t upd_trace32[32], upd_trace64[32];  /* per-sweep number of updated block pairs */
+    int64_t kernel_launches;   /* kernels launched by this call */
+} mpjsvd_stats;
+
+/* Fill *opts with the defaults above. */
+void mpjsvd_default_options(mpjsvd_options* opts);
+
+/* Create a handle bound to opts->device_id (opts may be NULL: defaults).
+   Returns 0 or a negative error code; *h is NULL on error. */
+int mpjsvd_create(mpjsvd_handle* h, const mpjsvd_options* opts);
+
+/* The SVD.  See the conventions above.  stats may be NULL. */
+int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
+                  double* U, int64_t ldu, double* S, double* V, int64_t ldv,
+                  mpjsvd_stats* stats);
+
+/* Free every resource of the handle.  Safe on NULL. */
+int mpjsvd_destroy(mpjsvd_handle h);
+
+/* Static description of a return code. */
+const char* mpjsvd_strerror(int code);
+
+/* Last CUDA error string recorded by the library (static storage). */
+const char* mpjsvd_last_cuda_error(void);
+
+int mpjsvd_version(void);
+
+/* ------------------------------------------------------------------------
+ * Step-level entry points (used by the parity tests to compare one step of
+ * the path with the oracle's same step).  Same conventions: column-major,
+ * device or host pointers, stream-ordered on the handle's stream.
+ * ------------------------------------------------------------------------ */
+
+/* One-sided block round-robin Jacobi in fp64 on X (m x n, ldx), accumulating
+   into V (nv x n, ldv; may be NULL) -- the refinement stage (PAPER.md:452-454,
+   575-597) run on an injected X.  tol / tol_in as in the options.  Returns
+   sweeps (> 0 converged, < 0 not converged) through *sweeps and the traces
+   through stats (sweeps64, off_trace64, upd_trace64). */
+int mpjsvd_block_jacobi_f64(mpjsvd_handle h, double* X, int64_t m, int64_t n, int64_t ldx,
+                            double* V, int64_t nv, int64_t ldv, double tol, double tol_in,
+                            int32_t max_sweeps, int32_t* sweeps, mpjsvd_stats* stats);
+
+/* Same in fp32 (the low-precision stage), with the
+   stagnation exit of reading c-10 when `stagnation` != 0. */
+int mpjsvd_block_jacobi_f32(mpjsvd_handle h, float* X, int64_t m, int64_t n, int64_t ldx,
+                            float* V, int64_t nv, int64_t ldv, float tol, float tol_in,
+                            int32_t max_sweeps, int32_t stagnation, int32_t* sweeps,
+                            mpjsvd_stats* stats);
+
+/* Inner 2b x 2b solve on `count` independent symmetric matrices G (w x w
+   each, packed back to back, ld = w): two-sided round-robin Jacobi to
+   tol_in (reading c-5); on exit G holds the rotated matrix and E = V_blk - I.
+   fp64 when is_f64 != 0 (double*), else fp32 (float*).  w <= 64. */
+int mpjsvd_inner_solve(mpjsvd_handle h, int32_t is_f64, void* G, void* E, int32_t w, int32_t count,
+                       double tol_in, int32_t max_inner, int32_t* rotations);
+
+/* Column-pivoted Householder QR A P = Q R in place (n x n or m x n, lda):
+   on exit R in the upper triangle (diag >= 0), reflectors below, tau[n],
+   perm[n] (0-based original column at position k).  pivot = 0: plain QR
+   (perm = identity).  PAPER.md:332-335 / 416-420. */
+int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, double* tau,
+              int32_t* perm, int32_t pivot);
+
+/* Precision lift: Q = V * Rv^-1, Rv = chol(V^T V),
+   V = fl64(V32) (n x n, ldv32 / ldq). */
+int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq);
+
+/* C <- Q C with Q = H_0 ... H_{k-1} packed as returned by mpjsvd_qr (rows m). */
+int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv,
+                   const double* tau, double* C, int64_t ldc, int64_t ncols);
+
+/* C = alpha op(A) op(B) + beta C, fp64, column-major (the library GEMM used by
+   the lift, R*V product and assembly).  transa/transb: 0 = N, 1 = T. */
+int mpjsvd_gemm_f64(mpjsvd_handle h, int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t K,
+                    double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                    double beta, double* C, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

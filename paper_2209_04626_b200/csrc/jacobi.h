@@ -1,0 +1,101 @@
+// jacobi.h -- internal interfaces between the engine (mpjsvd.cu) and the
+// kernels of the mpjsvd CUDA path.  Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpj {
+
+// Arguments of one block round-robin Jacobi round (k_jacobi.cu).
+template <typename T>
+struct JacobiRound {
+    T* X;               // m_pad x n, column-major, rows >= m zero
+    long long ldx;
+    long long m_pad;    // multiple of 32
+    int n;
+    T* V;               // nv_pad x n or nullptr
+    long long ldv;
+    long long nv_pad;   // multiple of 32
+    int b, nblk, M, round, npairs;
+    int nsplit;
+    long long rows_per_split;   // multiple of 32
+    T* partial;         // npairs * nsplit * W * W
+    T* E;               // npairs * W * W
+    int* flag;          // npairs
+    T tol, tol_in;
+    int max_inner;
+    double* sweep_off;  // device scalar, atomic max (this sweep)
+    int* sweep_upd;     // device scalar, atomic add (this sweep)
+};
+
+template <typename T>
+int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st);
+template <typename T>
+int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
+
+// ---- QR (k_qr.cu) --------------------------------------------------------
+struct QrWork {
+    int* phys_all;      // grid * n
+    int* pos_all;       // grid * n
+    double* vn1;        // n
+    double* vn2;        // n
+    double* cand_val;   // 2 * grid
+    int* cand_pos;      // 2 * grid
+    int* cand_col;      // 2 * grid
+    int grid;           // cooperative grid size used
+};
+// In-place Householder QR (pivot = 1: Businger-Golub column pivoting) of the
+// m x n matrix A (lda).  Columns stay at their physical place; phys[k] (copy
+// of CTA 0) gives the column at logical position k.  tau[k] per logical k.
+int qr_coop(double* A, long long lda, int m, int n, double* tau, int pivot, QrWork& w,
+            int* phys_out, cudaStream_t st);
+int qr_coop_grid(int m, int* grid);  // cooperative grid size for this m
+// out[:, k] = A[:, perm[k]] for k < n (rows m_pad)
+int gather_cols(const double* A, long long lda, const int* perm, double* out, long long ldo,
+                long long rows, int n, cudaStream_t st);
+
+// ---- dense linear algebra (k_linalg.cu) ---------------------------------
+int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A,
+             long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
+             cudaStream_t st);
+// Cholesky of the n x n SPD matrix G (upper, in place): G = R^T R.  *bad set
+// (device int) if a pivot is not positive.
+int potrf_upper(double* G, long long ldg, int n, int* bad, cudaStream_t st);
+// Q = V R^-1 (R upper n x n), in place on Q (initialised with V), rows nrows.
+int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, long long nrows, int n,
+                     cudaStream_t st);
+// C <- Q C, Q = H_0 ... H_{k-1} packed in Vr (rows m, ld ldv), blocked WY.
+int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C,
+               long long ldc, long long ncols, double* work, cudaStream_t st);
+size_t apply_q_work_elems(long long m, long long ncols);
+
+// ---- misc (k_misc.cu) ----------------------------------------------------
+int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st);
+int copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows, long long cols,
+                cudaStream_t st);
+template <typename T>
+int set_identity(T* A, long long lda, long long rows_pad, long long n, cudaStream_t st);
+int transpose_upper(const double* R, long long ldr, double* Rt, long long ldt, int n, long long rows_pad,
+                    cudaStream_t st);
+int lower_from_rt(const double* Rt, long long ldt, double* X, long long ldx, int n, long long rows_pad,
+                  cudaStream_t st);
+int upper_of(const double* A, long long lda, double* R, long long ldr, int n, long long rows_pad,
+             cudaStream_t st);
+int maxabs(const double* A, long long lda, long long rows, long long cols, double* out, cudaStream_t st);
+int downcast_scaled(const double* X, long long ldx, float* X32, long long ld32, long long rows_pad, int n,
+                    const double* maxabs_dev, cudaStream_t st);
+template <typename T>
+int col_norms(const T* X, long long ldx, long long rows, int n, double* out, int safe, cudaStream_t st);
+int rank_desc(const double* key, int n, int* rank, cudaStream_t st);
+int sort_upcast_v(const float* V32, long long ld32, const int* rank, double* V, long long ldv,
+                  long long rows_pad, int n, cudaStream_t st);
+int finalize(const double* Y, long long ldy, const double* Q, long long ldq, const double* sig,
+             const int* rank, double* UX, long long ldu, double* VX, long long ldvx, double* S,
+             long long rows_pad, int n, cudaStream_t st);
+int scatter_rows_perm(const double* M, long long ldm, const int* perm, double* V, long long ldv, int n,
+                      cudaStream_t st);
+int diag_stats(const double* R, long long ldr, int n, double* out2, int* bad, cudaStream_t st);
+int gates_orth(const double* X, long long ldx, long long rows_pad, int n, float* Xt, long long ldt,
+               double* out, cudaStream_t st);
+
+}  // namespace mpj

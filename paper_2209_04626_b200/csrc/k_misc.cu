@@ -1,0 +1,365 @@
+// k_misc.cu -- bandwidth-bound kernels of the path: input validation, layout
+// moves between the factorisation stages, the fp32 downcast (reading c-9),
+// column norms / descending sort (Alg. 1),
+// finalisation and the permutation of V, gate measures
+// (PAPER.md:429-431).
+#include <cuda_runtime.h>
+#include <float.h>
+#include "common.cuh"
+#include "jacobi.h"
+
+namespace mpj {
+
+static inline dim3 grid2d(long long rows, long long cols, int bx = 256) {
+    long long gx = ceil_div(rows, bx);
+    if (gx > 64) gx = 64;
+    long long gy = cols > 65535 ? 65535 : cols;
+    return dim3((unsigned)gx, (unsigned)gy);
+}
+
+__global__ void k_check_finite(const double* A, long long lda, long long m, long long n, int* bad) {
+    int found = 0;
+    for (long long j = blockIdx.y; j < n; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+            if (!isfinite(A[i + j * lda])) found = 1;
+    if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st) {
+    k_check_finite<<<grid2d(m, n), 256, 0, st>>>(A, lda, m, n, bad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+__global__ void k_copy(const double* src, long long lds, double* dst, long long ldd, long long rows, long long cols) {
+    for (long long j = blockIdx.y; j < cols; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows; i += (long long)gridDim.x * blockDim.x)
+            dst[i + j * ldd] = src[i + j * lds];
+}
+int copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows, long long cols,
+                cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return 0;
+    k_copy<<<grid2d(rows, cols), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+template <typename T>
+__global__ void k_set_identity(T* A, long long lda, long long rows_pad, long long n) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            A[i + j * lda] = i == j ? T(1) : T(0);
+}
+template <typename T>
+int set_identity(T* A, long long lda, long long rows_pad, long long n, cudaStream_t st) {
+    k_set_identity<T><<<grid2d(rows_pad, n), 256, 0, st>>>(A, lda, rows_pad, n);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+template int set_identity<float>(float*, long long, long long, long long, cudaStream_t);
+template int set_identity<double>(double*, long long, long long, long long, cudaStream_t);
+
+// Rt = R^T for the upper triangle of R (zeros elsewhere, padding rows zero)
+__global__ void k_transpose_upper(const double* R, long long ldr, double* Rt, long long ldt, int n, long long rows_pad) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;   // tile of Rt: rows bx.., cols by..
+    const int tx = threadIdx.x, ty = threadIdx.y;           // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        int rr = by + tx, cc = bx + k;                      // coalesced read of R[rr][cc] (-> Rt[cc][rr])
+        double v = 0.0;
+        if (rr < n && cc < n && rr <= cc) v = R[rr + (long long)cc * ldr];
+        tile[k][tx] = v;                                    // tile[k][t] = R[by+t][bx+k]
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        long long row = bx + tx, col = by + k;              // Rt[row][col] = R[col][row]
+        if (row < rows_pad && col < n) Rt[row + col * ldt] = (row < n) ? tile[tx][k] : 0.0;
+    }
+}
+int transpose_upper(const double* R, long long ldr, double* Rt, long long ldt, int n, long long rows_pad,
+                    cudaStream_t st) {
+    dim3 g((unsigned)ceil_div(rows_pad, 32), (unsigned)ceil_div(n, 32));
+    k_transpose_upper<<<g, dim3(32, 8), 0, st>>>(R, ldr, Rt, ldt, n, rows_pad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// X = L = (upper(Rt))^T : X[i][j] = Rt[j][i] for i >= j, else 0
+__global__ void k_lower_from_rt(const double* Rt, long long ldt, double* X, long long ldx, int n, long long rows_pad) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;   // tile of X: rows bx.., cols by..
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int k = ty; k < 32; k += 8) {
+        int rr = by + tx, cc = bx + k;                      // coalesced read of Rt[rr][cc] (-> X[cc][rr])
+        double v = 0.0;
+        if (rr < n && cc < n && rr <= cc) v = Rt[rr + (long long)cc * ldt];
+        tile[k][tx] = v;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        long long row = bx + tx, col = by + k;
+        if (row < rows_pad && col < n) X[row + col * ldx] = (row < n) ? tile[tx][k] : 0.0;
+    }
+}
+int lower_from_rt(const double* Rt, long long ldt, double* X, long long ldx, int n, long long rows_pad,
+                  cudaStream_t st) {
+    dim3 g((unsigned)ceil_div(rows_pad, 32), (unsigned)ceil_div(n, 32));
+    k_lower_from_rt<<<g, dim3(32, 8), 0, st>>>(Rt, ldt, X, ldx, n, rows_pad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+__global__ void k_upper_of(const double* A, long long lda, double* R, long long ldr, int n, long long rows_pad) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            R[i + j * ldr] = (i <= j && i < n) ? A[i + j * lda] : 0.0;
+}
+int upper_of(const double* A, long long lda, double* R, long long ldr, int n, long long rows_pad, cudaStream_t st) {
+    k_upper_of<<<grid2d(rows_pad, n), 256, 0, st>>>(A, lda, R, ldr, n, rows_pad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+__global__ void k_maxabs(const double* A, long long lda, long long rows, long long cols, double* out) {
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (long long j = blockIdx.y; j < cols; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows; i += (long long)gridDim.x * blockDim.x)
+            mx = fmax(mx, fabs(A[i + j * lda]));
+    mx = block_max(mx, red);
+    if (threadIdx.x == 0) atomic_max_nonneg(out, mx);
+}
+int maxabs(const double* A, long long lda, long long rows, long long cols, double* out, cudaStream_t st) {
+    MPJ_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+    dim3 g = grid2d(rows, cols);
+    if (g.y > 2048) g.y = 2048;
+    k_maxabs<<<g, 256, 0, st>>>(A, lda, rows, cols, out);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// X32 = fl32(X 2^-e), e = exponent of max|X| (max 2^-e in [0.5, 1)), reading c-9
+__global__ void k_downcast(const double* X, long long ldx, float* X32, long long ld32, long long rows_pad, int n,
+                           const double* mx) {
+    int e = 0;
+    frexp(*mx, &e);
+    for (long long j = blockIdx.y; j < n; j += gridDim.y)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            X32[i + j * ld32] = (float)ldexp(X[i + j * ldx], -e);
+}
+int downcast_scaled(const double* X, long long ldx, float* X32, long long ld32, long long rows_pad, int n,
+                    const double* maxabs_dev, cudaStream_t st) {
+    k_downcast<<<grid2d(rows_pad, n), 256, 0, st>>>(X, ldx, X32, ld32, rows_pad, n, maxabs_dev);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// column norms in fp64: safe = two-pass scaled (overflow-free), else plain
+template <typename T>
+__global__ void k_col_norms(const T* X, long long ldx, long long rows, double* out, int safe) {
+    __shared__ double red[32];
+    const T* col = X + (long long)blockIdx.x * ldx;
+    double scale = 1.0;
+    if (safe) {
+        double mx = 0.0;
+        for (long long i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs((double)col[i]));
+        mx = block_max(mx, red);
+        if (mx == 0.0) { if (threadIdx.x == 0) out[blockIdx.x] = 0.0; return; }
+        scale = mx;
+    }
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < rows; i += blockDim.x) {
+        double y = safe ? (double)col[i] / scale : (double)col[i];
+        s += y * y;
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[blockIdx.x] = safe ? scale * sqrt(s) : sqrt(s);
+}
+template <typename T>
+int col_norms(const T* X, long long ldx, long long rows, int n, double* out, int safe, cudaStream_t st) {
+    k_col_norms<T><<<n, 256, 0, st>>>(X, ldx, rows, out, safe);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+template int col_norms<float>(const float*, long long, long long, int, double*, int, cudaStream_t);
+template int col_norms<double>(const double*, long long, long long, int, double*, int, cudaStream_t);
+
+// stable descending rank: rank_j = #{k : key_k > key_j or (key_k == key_j and k < j)}
+__global__ void k_rank_desc(const double* key, int n, int* rank) {
+    __shared__ double tile[1024];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const double kj = j < n ? key[j] : 0.0;
+    int r = 0;
+    for (int base = 0; base < n; base += 1024) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < 1024; t += blockDim.x) tile[t] = base + t < n ? key[base + t] : -1.0;
+        __syncthreads();
+        const int lim = min(1024, n - base);
+        for (int t = 0; t < lim; ++t) {
+            const double kk = tile[t];
+            const int k = base + t;
+            r += (kk > kj || (kk == kj && k < j)) ? 1 : 0;
+        }
+    }
+    if (j < n) rank[j] = r;
+}
+int rank_desc(const double* key, int n, int* rank, cudaStream_t st) {
+    k_rank_desc<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(key, n, rank);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// V[:, rank_j] = fl64(V32[:, j])
+__global__ void k_sort_upcast(const float* V32, long long ld32, const int* rank, double* V, long long ldv,
+                              long long rows_pad, int n) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y) {
+        const long long dj = rank[j];
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            V[i + dj * ldv] = (double)V32[i + j * ld32];
+    }
+}
+int sort_upcast_v(const float* V32, long long ld32, const int* rank, double* V, long long ldv, long long rows_pad,
+                  int n, cudaStream_t st) {
+    k_sort_upcast<<<grid2d(rows_pad, n), 256, 0, st>>>(V32, ld32, rank, V, ldv, rows_pad, n);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// U_X[:, rank_j] = Y[:, j] / sigma_j ; V_X[:, rank_j] = Q[:, j] ; S[rank_j] = sigma_j
+__global__ void k_finalize(const double* Y, long long ldy, const double* Q, long long ldq, const double* sig,
+                           const int* rank, double* UX, long long ldu, double* VX, long long ldvx, double* S,
+                           long long rows_pad, int n) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y) {
+        const long long dj = rank[j];
+        const double s = sig[j];
+        if (blockIdx.x == 0 && threadIdx.x == 0) S[dj] = s;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x) {
+            UX[i + dj * ldu] = Y[i + j * ldy] / s;
+            VX[i + dj * ldvx] = Q[i + j * ldq];
+        }
+    }
+}
+int finalize(const double* Y, long long ldy, const double* Q, long long ldq, const double* sig, const int* rank,
+             double* UX, long long ldu, double* VX, long long ldvx, double* S, long long rows_pad, int n,
+             cudaStream_t st) {
+    k_finalize<<<grid2d(rows_pad, n), 256, 0, st>>>(Y, ldy, Q, ldq, sig, rank, UX, ldu, VX, ldvx, S, rows_pad, n);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// V[perm[k]][:] = M[k][:]
+__global__ void k_scatter_rows(const double* M, long long ldm, const int* perm, double* V, long long ldv, int n) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y)
+        for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+            V[perm[k] + j * ldv] = M[k + j * ldm];
+}
+int scatter_rows_perm(const double* M, long long ldm, const int* perm, double* V, long long ldv, int n,
+                      cudaStream_t st) {
+    k_scatter_rows<<<grid2d(n, n), 256, 0, st>>>(M, ldm, perm, V, ldv, n);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// out2[0] = max_k R_kk, out2[1] = min_k R_kk ; bad if some R_kk <= 0
+__global__ void k_diag_stats(const double* R, long long ldr, int n, double* out2, int* bad) {
+    __shared__ double red[32];
+    double mx = 0.0, mn = DBL_MAX;
+    int z = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        double d = R[k + (long long)k * ldr];
+        mx = fmax(mx, d);
+        mn = fmin(mn, d);
+        if (!(d > 0.0)) z = 1;
+    }
+    mx = block_max(mx, red);
+    mn = -block_max(-mn, red);
+    if (__syncthreads_or(z) && threadIdx.x == 0) atomicOr(bad, 1);
+    if (threadIdx.x == 0) { out2[0] = mx; out2[1] = mn; }
+}
+int diag_stats(const double* R, long long ldr, int n, double* out2, int* bad, cudaStream_t st) {
+    k_diag_stats<<<1, 1024, 0, st>>>(R, ldr, n, out2, bad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// ---- gate measure orth = || X_t^T X_t - I ||_max (fp32), PAPER.md:429-431 --
+__global__ void k_gate_scale(const double* X, long long ldx, long long rows_pad, int n, float* Xt, long long ldt) {
+    __shared__ double red[32];
+    const long long j = blockIdx.x;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < rows_pad; i += blockDim.x) {
+        float f = (float)X[i + j * ldx];
+        s += (double)f * (double)f;
+    }
+    s = block_sum(s, red);
+    const float d = (float)sqrt(s);
+    for (long long i = threadIdx.x; i < rows_pad; i += blockDim.x)
+        Xt[i + j * ldt] = d > 0.0f ? (float)X[i + j * ldx] / d : 0.0f;
+}
+
+// 64 x 64 tiles of X_t^T X_t (lower tiles only), max |g - delta| -> out
+__global__ void __launch_bounds__(256) k_gate_orth(const float* Xt, long long ldt, long long rows_pad, int n, double* out) {
+    const int bi = blockIdx.x, bj = blockIdx.y;
+    if (bj > bi) return;
+    __shared__ float As[32][65], Bs[32][65];
+    __shared__ double red[32];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    float acc[4][4] = {};
+    for (long long k0 = 0; k0 < rows_pad; k0 += 32) {
+        for (int e = tid; e < 32 * 64; e += 256) {
+            int kk = e & 31, c = e >> 5;
+            long long ci = (long long)bi * 64 + c, cj = (long long)bj * 64 + c;
+            As[kk][c] = ci < n ? Xt[k0 + kk + ci * ldt] : 0.f;
+            Bs[kk][c] = cj < n ? Xt[k0 + kk + cj * ldt] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty + 16 * i]; b[i] = Bs[kk][tx + 16 * i]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            long long gi = (long long)bi * 64 + ty + 16 * i, gj = (long long)bj * 64 + tx + 16 * j;
+            if (gi < n && gj < n) mx = fmax(mx, fabs((double)acc[i][j] - (gi == gj ? 1.0 : 0.0)));
+        }
+    mx = block_max(mx, red);
+    if (tid == 0) atomic_max_nonneg(out, mx);
+}
+
+int gates_orth(const double* X, long long ldx, long long rows_pad, int n, float* Xt, long long ldt, double* out,
+               cudaStream_t st) {
+    k_gate_scale<<<n, 256, 0, st>>>(X, ldx, rows_pad, n, Xt, ldt);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+    dim3 g((unsigned)ceil_div(n, 64), (unsigned)ceil_div(n, 64));
+    k_gate_orth<<<g, 256, 0, st>>>(Xt, ldt, rows_pad, n, out);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace mpj

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Run on a B200 via gpurun:  pytest -m gpu tests/
+
+Tolerances:
+  sigma: rel <= 1e-12 when kappa_s <= 1e4, else the tiered
+         max(1e-12, 1e3 u min(kappa_s, sigma_1/sigma_i));
+  ||U^T U - I||_max, ||V^T V - I||_max <= 1e-13;  ||A - U S V^T||_F/||A||_F <= 1e-13;
+  sweeps32 / sweeps64 within +-1 of the oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import testmat
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+U64 = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def mp():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2209_04626_b200 as m
+    m.lib()
+    return m
+
+
+def dev(a, dtype=torch.float64):
+    return torch.from_numpy(np.asfortranarray(a)).to(dtype).cuda().t().contiguous().t()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def orth(q):
+    return np.abs(q.T @ q - np.eye(q.shape[1])).max()
+
+
+def tiered(sref, kappa):
+    return np.maximum(1e-12, 1e3 * U64 * np.minimum(kappa, sref[0] / sref))
+
+
+def kappa_s(a):
+    d = np.linalg.norm(a, axis=0)
+    s = np.linalg.svd(a / d, compute_uv=False)
+    return s[0] / s[-1]
+
+
+# ------------------------------------------------------------------- kernels
+def test_gemm_matches_plain_reference(mp):
+    rng = np.random.default_rng(0)
+    for (M, N, K, ta, tb) in [(130, 70, 33, 0, 0), (64, 64, 64, 1, 0), (100, 37, 211, 0, 1), (5, 200, 129, 1, 1)]:
+        A = rng.standard_normal((K, M) if ta else (M, K))
+        B = rng.standard_normal((N, K) if tb else (K, N))
+        C = host(mp.gemm(bool(ta), bool(tb), dev(A), dev(B)))
+        ref = (A.T if ta else A) @ (B.T if tb else B)
+        assert np.abs(C - ref).max() <= 4 * K * U64 * (np.abs(A).max() * np.abs(B).max() * K)
+
+
+@pytest.mark.parametrize("w,dtype", [(64, np.float64), (37, np.float64), (64, np.float32), (16, np.float32)])
+def test_inner_solve_vs_oracle(mp, w, dtype):
+    rng = np.random.default_rng(w)
+    count = 5
+    Gs, tol_in = [], (oracle.tol(4096) if dtype == np.float64 else 4 * 64 * 2.0 ** -24) / 8
+    for c in range(count):
+        b = rng.standard_normal((2 * w, w)) * 10.0 ** rng.uniform(-1, 1, w)
+        Gs.append((b.T @ b).astype(dtype))
+    Gd = torch.from_numpy(np.stack(Gs)).cuda()
+    Go, Eo, rot = mp.inner_solve(Gd, tol_in)
+    Go, Eo = host(Go), host(Eo)
+    for c in range(count):
+        g_ref, e_ref, nrot, isw = oracle.inner_solve(Gs[c], tol_in, dtype=dtype)
+        J = np.eye(w) + Eo[c].astype(np.float64)
+        eps = 2.0 ** -53 if dtype == np.float64 else 2.0 ** -24
+        assert orth(J) < 100 * eps * w
+        # diagonalised: off-diagonal of J^T G J below the inner threshold scale
+        D = J.T @ Gs[c].astype(np.float64) @ J
+        dd = np.sqrt(np.diag(D))
+        off = np.abs(D - np.diag(np.diag(D))) / np.outer(dd, dd)
+        assert off.max() < 50 * tol_in + 100 * eps
+        # same eigenvalues as the oracle's solve (relative, SDD matrices)
+        np.testing.assert_allclose(np.sort(np.diag(Go[c])), np.sort(np.diag(g_ref)),
+                                   rtol=1e3 * eps, atol=1e3 * eps * np.abs(np.diag(g_ref)).max())
+        assert abs(rot[c] - nrot) <= max(3, 0.02 * nrot)
+
+
+@pytest.mark.parametrize("n,b,m", [(256, 32, 256), (100, 16, 100), (96, 8, 130), (33, 32, 40), (512, 32, 512)])
+def test_block_jacobi_f64_vs_oracle(mp, n, b, m):
+    rng = np.random.default_rng(n * 7 + b)
+    a = testmat.config_matrix("C1", max(n, m))[:m, :n].copy()
+    # start from a nearly orthogonal Y like the refinement stage sees it
+    q, _ = np.linalg.qr(a)
+    x0 = np.asfortranarray(q[:, :n] * np.geomspace(1, 1e-6, n) + 1e-7 * rng.standard_normal((m, n)))
+    t = oracle.tol(m)
+    xo, vo, sw_o, offs_o, upd_o = oracle.block_jacobi(x0, np.eye(n), b, t, t / 8)
+    X, V = dev(x0), dev(np.eye(n))
+    sw, st = mp.block_jacobi(X, V, t, t / 8, 30, block_cols=b)
+    X, V = host(X), host(V)
+    assert sw > 0 and sw_o > 0 and abs(sw - sw_o) <= 1
+    s_gpu = np.sort(np.linalg.norm(X, axis=0))[::-1]
+    s_or = np.sort(np.linalg.norm(xo, axis=0))[::-1]
+    assert np.max(np.abs(s_gpu - s_or) / s_or) < 1e-12
+    assert orth(V) < 1e-13
+    assert np.abs(x0 @ V - X).max() < 1e-13 * np.abs(x0).max()
+
+
+@pytest.mark.parametrize("n,b", [(256, 32), (130, 16)])
+def test_block_jacobi_f32_vs_oracle(mp, n, b):
+    a = testmat.config_matrix("C1", n)
+    x0 = np.asfortranarray(np.linalg.qr(a.T)[1].T).astype(np.float32)
+    t = np.float32(4 * np.sqrt(n) * 2.0 ** -24)
+    xo, vo, sw_o, _, _ = oracle.block_jacobi(x0, np.eye(n, dtype=np.float32), b, t, t / 8,
+                                             stagnation=True, dtype=np.float32)
+    X, V = dev(x0, torch.float32), dev(np.eye(n), torch.float32)
+    sw, st = mp.block_jacobi(X, V, float(t), float(t / 8), 20, stagnation=True, block_cols=b)
+    X, V = host(X).astype(np.float64), host(V).astype(np.float64)
+    assert abs(abs(sw) - abs(sw_o)) <= 1
+    s_gpu = np.sort(np.linalg.norm(X, axis=0))[::-1]
+    s_or = np.sort(np.linalg.norm(xo.astype(np.float64), axis=0))[::-1]
+    assert np.max(np.abs(s_gpu - s_or) / s_or) < 1e-4
+    assert orth(V) < 1e-4
+
+
+@pytest.mark.parametrize("m,n,pivot", [(300, 300, True), (257, 100, True), (1000, 77, False), (64, 64, False)])
+def test_qr_vs_oracle(mp, m, n, pivot):
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
+    packed, tau, perm = mp.qr(dev(a), pivot=pivot)
+    packed, tau, perm = host(packed), host(tau), host(perm)
+    if pivot:
+        p_o, perm_o, tau_o, _ = oracle.qrp(a)
+    else:
+        p_o, tau_o, _ = oracle.qr(a)
+        perm_o = np.arange(n)
+    assert np.array_equal(perm, perm_o)
+    r, r_o = np.triu(packed[:n]), np.triu(p_o[:n])
+    assert np.abs(r - r_o).max() <= 1e-12 * np.abs(r_o).max()
+    assert np.abs(tau - tau_o).max() <= 1e-12
+    q = oracle.form_q(packed, tau, n)
+    assert orth(q) < 1e-13
+    assert np.abs(q @ r - a[:, perm]).max() <= 1e-13 * np.abs(a).max()
+
+
+def test_apply_q_vs_oracle(mp):
+    rng = np.random.default_rng(4)
+    m, n = 500, 140
+    a = rng.standard_normal((m, n))
+    p_o, tau_o, _ = oracle.qr(a)
+    c = rng.standard_normal((m, 90))
+    ref = oracle.apply_q(p_o, tau_o, c)
+    out = host(mp.apply_q(dev(p_o), torch.from_numpy(tau_o).cuda(), dev(c)))
+    assert np.abs(out - ref).max() < 1e-13 * np.abs(c).max() * 10
+
+
+def test_lift_vs_oracle(mp):
+    n = 200
+    a = testmat.config_matrix("C1", n)
+    x = np.linalg.qr(a.T)[1].T
+    x32 = x.astype(np.float32)
+    t = np.float32(4 * np.sqrt(n) * 2.0 ** -24)
+    _, v32, _, _, _ = oracle.block_jacobi(x32, np.eye(n, dtype=np.float32), 32, t, t / 8, stagnation=True,
+                                          dtype=np.float32)
+    q_ref, rc = oracle.lift(v32)
+    q = host(mp.lift(torch.from_numpy(v32).cuda()))
+    assert orth(q) < 1e-14
+    assert np.abs(q - q_ref).max() < 1e-13
+
+
+# ------------------------------------------------------------------- end to end
+def check_svd(a, U, S, V, tol_orth=1e-13, tol_res=1e-13):
+    assert np.all(S[:-1] >= S[1:]) and np.all(S > 0)
+    assert orth(U) <= tol_orth, orth(U)
+    assert orth(V) <= tol_orth, orth(V)
+    res = np.linalg.norm(a - (U * S) @ V.T) / np.linalg.norm(a)
+    assert res <= tol_res, res
+
+
+@pytest.mark.parametrize("name,n,kappa", [("C1", 256, 1e4), ("C2", 1024, 1e3), ("C3", 512, None),
+                                          ("C4", 256, None), ("C5", 512, None)])
+def test_factor_vs_oracle(mp, name, n, kappa):
+    a = testmat.config_matrix(name, n)
+    U, S, V, st = mp.factor(dev(a))
+    U, S, V = host(U), host(S), host(V)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a)
+    assert rc == 0 and st["rc"] == 0
+    check_svd(a, U, S, V)
+    k = kappa if kappa is not None else kappa_s(a)
+    rel = np.abs(S - so) / so
+    if k <= 1e4:
+        assert rel.max() <= 1e-12, rel.max()
+    assert np.all(rel <= tiered(so, k))
+    assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1, (st["sweeps32"], sto["sweeps32"])
+    assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1, (st["sweeps64"], sto["sweeps64"])
+    # singular vectors agree with the oracle up to sign where sigma is well separated
+    gap = np.minimum(np.abs(np.diff(so, prepend=np.inf)), np.abs(np.diff(so, append=-np.inf))) / so
+    ok = gap > 1e-6
+    assert np.all(np.abs(np.abs(np.sum(V * vo, axis=0))[ok] - 1) < 1e-8)
+
+
+@pytest.mark.parametrize("m,n", [(100, 100), (257, 257), (77, 33), (1000, 77), (2, 2), (40, 3)])
+def test_factor_ragged_shapes(mp, m, n):
+    rng = np.random.default_rng(m * n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
+    U, S, V, st = mp.factor(dev(a))
+    U, S, V = host(U), host(S), host(V)
+    check_svd(a, U, S, V)
+    so = oracle.mixed_svd(a)[1]
+    assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+
+
+def test_exact_sigma(mp):
+    for n in (256, 1024):
+        a, sigma = testmat.exact_sigma_matrix(n)
+        U, S, V, st = mp.factor(dev(a))
+        rel = np.abs(host(S) - sigma) / sigma
+        assert np.all(rel <= tiered(sigma, sigma[0] / sigma[-1]))
+        check_svd(a, host(U), host(S), host(V))
+
+
+def test_graded_high_relative_accuracy(mp):
+    import mpmath
+    mpmath.mp.dps = 80
+    a, _ = testmat.graded_matrix(32, 40)
+    ref = np.array(sorted([float(x) for x in mpmath.svd_r(mpmath.matrix(a.tolist()), compute_uv=False)],
+                          reverse=True))
+    U, S, V, st = mp.factor(dev(a))
+    assert np.max(np.abs(host(S) - ref) / ref) < 1e-13
+
+
+def test_host_pointers_e2e_equal_device_path(mp):
+    a = testmat.config_matrix("C1", 128)
+    U1, S1, V1, _ = mp.factor(dev(a))
+    At = torch.from_numpy(a.T.copy()).t()          # host, column-major
+    U2, S2, V2, st = mp.factor(At)
+    assert not U2.is_cuda
+    assert np.array_equal(host(S1), S2.numpy())
+    assert np.array_equal(host(U1), U2.numpy()) and np.array_equal(host(V1), V2.numpy())
+
+
+def test_deterministic(mp):
+    a = testmat.config_matrix("C2", 256)
+    r1 = mp.factor(dev(a))
+    r2 = mp.factor(dev(a))
+    for x, y in zip(r1[:3], r2[:3]):
+        assert torch.equal(x, y)
+
+
+def test_power_of_two_scaling_bitwise(mp):
+    a = testmat.config_matrix("C2", 128)
+    S1 = host(mp.factor(dev(a))[1])
+    S2 = host(mp.factor(dev(a * 2.0 ** -40))[1])
+    assert np.array_equal(S2, S1 * 2.0 ** -40)
+
+
+def test_force_fp64_path(mp):
+    a = testmat.config_matrix("C1", 256)
+    U, S, V, st = mp.factor(dev(a), path=2)
+    so = oracle.mixed_svd(a, path=2)
+    assert st["sweeps32"] == 0 and abs(st["sweeps64"] - so[3]["sweeps64"]) <= 1
+    check_svd(a, host(U), host(S), host(V))
+
+
+def test_errors(mp):
+    a = testmat.config_matrix("C1", 64)
+    bad = a.copy()
+    bad[5, 7] = np.nan
+    with pytest.raises(mp.MpjsvdError) as e:
+        mp.factor(dev(bad))
+    assert e.value.code == -2
+    z = a.copy()
+    z[:, 3] = 0.0
+    with pytest.raises(mp.MpjsvdError) as e:
+        mp.factor(dev(z))
+    assert e.value.code == -3
+    with pytest.raises(mp.MpjsvdError) as e:
+        mp.factor(dev(np.ones((4, 8))))
+    assert e.value.code == -1
+    # not converged: soft warning, outputs filled
+    U, S, V, st = mp.factor(dev(a), max_sweeps64=1)
+    assert st["rc"] == 1 and not st["converged"]
