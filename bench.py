@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- time-to-SVD of the B200 mixed-precision Jacobi SVD (C-ABI path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl mpjsvd|reference]
+
+A step is one full fp64 SVD A = U S V^T (mpjsvd_factor: QRP + LQ
+preconditioning, fp32 block Jacobi, CholeskyQR lift, fp64 block Jacobi
+refinement, assembly) of BASELINE.json's config on inputs resident in HBM.
+Metric (BASELINE.json): "fp64 SVD time at n=4096 and 8192 (1/2/4/8 B200);
+sweep HBM GB/s vs peak" -> value = seconds per SVD (lower is better).
+
+Rank 0 prints ONE JSON line.  Multi-GPU (torchrun, N > 1): every rank runs
+its own replica SVD of the config on its GPU (the column-block sharded
+solver is not in this build), the timed region is
+bracketed by barrier + synchronize and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 SVD time at n=4096 and 8192 (1/2/4/8 B200); sweep HBM GB/s vs peak"
+SAMPLE_N = 1024          # oracle sample size for the CPU baseline
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("MPJSVD_BENCH_CONFIG", "C5"))
+    ap.add_argument("--impl", default="mpjsvd", choices=["mpjsvd", "reference"])
+    ap.add_argument("--block-cols", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------- CPU oracle
+def oracle_sample(config: str, n_full: int, m_full: int):
+    """Time O-MIX (oracle/, as it stands, all host threads) on the config's
+    recipe at n = SAMPLE_N and scale by the flop ratio to the full size."""
+    import oracle
+    import testmat
+    import numpy as np
+    n_s = min(SAMPLE_N, n_full)
+    a = testmat.config_matrix(config, n_s)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    _, s, _, st, rc = oracle.mixed_svd(a, nthreads=cores)
+    dt = time.perf_counter() - t0
+    m_s = a.shape[0]
+    # O-MIX cost ~ (2 m n^2 [tall QR] + c n^3): scale both terms by the size ratio
+    scale = (n_full / n_s) ** 3 if m_full == n_full else (m_full * n_full ** 2) / (m_s * n_s ** 2)
+    return {
+        "value": dt * scale, "unit": "s", "cores": cores, "kind": "oracle",
+        "sample": (f"O-MIX mixed_svd on the {config} recipe at {m_s}x{n_s} (same seeds), {dt:.2f} s "
+                   f"measured, scaled x{scale:.0f} by the n^3 flop ratio to {m_full}x{n_full}; "
+                   f"sweeps32={st['sweeps32']} sweeps64={st['sweeps64']}"),
+        "sample_seconds": dt,
+    }
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the only reference in this tier) timed on
+    the host cores; each step a bounded sample (see oracle_sample)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import testmat
+    m_full, n_full, _ = testmat.CONFIGS[args.config]
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        cb = oracle_sample(args.config, n_full, m_full)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            last = cb
+    v = statistics.median(vals)
+    cb = dict(last)
+    cb["value"] = v
+    cb.pop("sample_seconds", None)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "config": {"workload": args.config, "m": m_full, "n": n_full},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        rows = [[c.strip() for c in l.split(",")] for l in out.strip().splitlines() if l.strip()]
+        rows = [r for r in rows if len(r) == len(self.FIELDS)]
+        if not rows:
+            return None
+        sm = []
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+            except ValueError:
+                pass
+        load = [x for x in sm if x > 500] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        try:
+            mx = float(rows[0][1])
+        except ValueError:
+            mx = None
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- peaks
+def load_peaks():
+    peaks = {}
+    try:
+        peaks["measured"] = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        peaks["measured"] = None
+    try:
+        peaks["micro"] = json.load(open(os.path.join(ROOT, "profiles", "peaks.json")))
+    except Exception:
+        peaks["micro"] = None
+    return peaks
+
+
+def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks: dict, n: int, b: int):
+    """Roofline entry for the dominant kernel from algorithmic work (DESIGN.md
+    "Algorithmic work per unit")."""
+    hbm = (peaks["measured"] or {}).get("hbm_gbs", 6650.0)
+    micro = peaks["micro"] or {}
+    sec = ms_total / 1e3
+    if kernel.startswith("pair_") and ("gram" in kernel or "update" in kernel):
+        is64 = kernel.endswith("f64")
+        flops = work["flops"].get(kernel, 0.0)
+        byts = work["bytes"].get(kernel, 0.0)
+        ach_f = flops / sec / 1e12
+        if is64:
+            peak = micro.get("dfma_tflops") or (148 * 64 * 2 * 1.965e9 / 1e12)
+            src = "measured DFMA microbenchmark (profiles/peaks.json)" if micro.get("dfma_tflops") else \
+                "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+        else:
+            peak = micro.get("ffma_tflops") or (148 * 128 * 2 * 1.965e9 / 1e12)
+            src = "measured FFMA microbenchmark (profiles/peaks.json)" if micro.get("ffma_tflops") else \
+                "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz"
+        return {"kernel": kernel, "bound": "alu", "achieved": ach_f, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach_f / peak, "traffic": work.get("traffic", {}).get(kernel),
+                "algorithmic_bytes_per_launch": byts / max(launches, 1),
+                "algorithmic_flops_per_launch": flops / max(launches, 1),
+                "hbm_gbs_achieved": byts / sec / 1e9, "hbm_frac": byts / sec / 1e9 / hbm,
+                "peak_source": src, "launches": launches, "avg_launch_us": ms_total * 1e3 / max(launches, 1)}
+    return {"kernel": kernel, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+            "traffic": None, "launches": launches}
+
+
+def algorithmic_work(stats_list, n: int, b: int):
+    """Algorithmic flops/bytes of the Jacobi kernels summed over the timed steps.
+    Per sweep: Gram 4n^3 flops over all pairs (reads X once
+    per round: n^2 s bytes); update 16 n b^2 flops per updated pair for X and
+    V, bytes 2 x (read + write of n x 2b) x s for X and V."""
+    flops, byts = {}, {}
+    nblk = -(-n // b)
+    M = nblk + (nblk & 1)
+    npairs = M // 2
+    rounds = M - 1
+    for st in stats_list:
+        for tag, s, key in (("f32", 4, "32"), ("f64", 8, "64")):
+            sweeps = st["sweeps" + key]
+            upd = sum(st["upd_trace" + key])
+            g = f"pair_gram_{tag}"
+            u = f"pair_update_{tag}"
+            flops[g] = flops.get(g, 0.0) + sweeps * rounds * npairs * 8.0 * n * b * b
+            byts[g] = byts.get(g, 0.0) + sweeps * rounds * float(n) * n * s
+            flops[u] = flops.get(u, 0.0) + upd * 16.0 * n * b * b
+            byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * 2.0 * n * 2 * b * s
+    return {"flops": flops, "bytes": byts}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_04626_b200 as mp
+    import testmat
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    m, n, _ = testmat.CONFIGS[args.config]
+    a = testmat.cached_config(args.config)
+    A = torch.from_numpy(np.ascontiguousarray(a.T)).t().cuda()     # column-major, resident in HBM
+    stream = torch.cuda.current_stream()
+    h = mp.Handle(stream=stream.cuda_stream, block_cols=args.block_cols)
+    U = mp.empty_col_major(m, n, torch.float64, A.device)
+    V = mp.empty_col_major(n, n, torch.float64, A.device)
+    S = torch.empty(n, dtype=torch.float64, device=A.device)
+    l2_flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=A.device)
+
+    def step():
+        rc, st = mp.mpjsvd_factor(h, A, U, S, V, m, n, m, m, n)
+        if rc < 0:
+            raise mp.MpjsvdError(rc, "mpjsvd_factor")
+        return st.as_dict()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, L2 flushed between steps
+    h.set_profiling(True)
+    stats = []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        l2_flush.zero_()
+        evs[i][0].record(stream)
+        stats.append(step())
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    prof = h.profile()
+    h.set_profiling(False)
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    ms = max_over_ranks(ms)
+    launches = int(sum(s["kernel_launches"] for s in stats))
+
+    # ---------------- result check (plumbing: torch on the device)
+    Ud, Sd, Vd = U, S, V
+    eye = torch.eye(n, dtype=torch.float64, device=A.device)
+    orth_u = float((Ud.T @ Ud - eye).abs().max())
+    orth_v = float((Vd.T @ Vd - eye).abs().max())
+    res = float(torch.linalg.norm(A - (Ud * Sd) @ Vd.T) / torch.linalg.norm(A))
+
+    # ---------------- e2e: host buffers through the same C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.from_numpy(np.ascontiguousarray(a.T)).t().pin_memory()
+        Uh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+        Vh = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
+        Sh = torch.empty(n, dtype=torch.float64).pin_memory()
+        e2e_ms = []
+        for i in range(max(1, args.steps)):
+            l2_flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rc, _ = mp.mpjsvd_factor(h, Ah, Uh, Sh, Vh, m, n, m, m, n)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rc < 0:
+                raise mp.MpjsvdError(rc, "mpjsvd_factor (host buffers)")
+            e2e_ms.append(e0.elapsed_time(e1))
+        e2e_v = max_over_ranks(statistics.mean(e2e_ms)) / 1e3
+        e2e = {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": int(m * n * 8),
+               "d2h_bytes_per_step": int((m * n + n + n * n) * 8)}
+
+    # ---------------- roofline of the dominant kernel
+    peaks = load_peaks()
+    work = algorithmic_work(stats, n, args.block_cols)
+    try:
+        work["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        work["traffic"] = {}
+    dominant = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
+    roof = roofline_for(dominant[0], dominant[1][0], dominant[1][1], work, peaks, n, args.block_cols) \
+        if dominant else None
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                   "share": v[0] / max(1e-9, sum(x[0] for x in prof.values()))} for k, v in prof.items()}
+    jacobi = {}
+    for k in ("pair_gram_f64", "pair_update_f64", "pair_gram_f32", "pair_update_f32"):
+        if k in prof:
+            r = roofline_for(k, prof[k][0], prof[k][1], work, peaks, n, args.block_cols)
+            jacobi[k] = {kk: r[kk] for kk in ("achieved", "peak", "frac", "hbm_gbs_achieved", "hbm_frac")}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = oracle_sample(args.config, n, m)
+        cpu.pop("sample_seconds", None)
+    st0 = stats[-1]
+    out = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic",
+        "config": {"workload": args.config, "m": m, "n": n, "block_cols": args.block_cols,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "inputs (A 8n^2 B) and working set > L2; 512 MiB L2 flush between timed steps",
+                   "recipe": testmat.CONFIGS[args.config][2]},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "sweeps32": st0["sweeps32"], "sweeps64": st0["sweeps64"],
+        "upd_trace32": st0["upd_trace32"], "upd_trace64": st0["upd_trace64"],
+        "stage_ms": st0["stage_ms"],
+        "check": {"orth_u": orth_u, "orth_v": orth_v, "residual": res},
+        "kernels": kernels, "jacobi_roofline": jacobi,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,10 +120,23 @@ const char* mpjsvd_last_cuda_error(void);
 
 int mpjsvd_version(void);
 
+/* Per-kernel timing for benchmarking.  mpjsvd_set_profiling(h, 1) clears the
+   accumulators and brackets every subsequent kernel launch of the Jacobi
+   rounds (pair_gram / pair_solve / pair_update, fp32 and fp64) and each
+   stage-level launch group (qrp_coop, lq_coop, qr_coop_tall, gates_orth,
+   lift_cholqr, rv_gemm, assemble_wy) with CUDA events on the handle's
+   stream; mpjsvd_get_profile(h, idx, ...) returns the number of entries and
+   fills entry idx (name, summed device ms, launch count).  idx < 0: count
+   only.  Profiling adds two event records per launch and no synchronisation. */
+int mpjsvd_set_profiling(mpjsvd_handle h, int32_t on);
+int mpjsvd_get_profile(mpjsvd_handle h, int32_t idx, char* name, int32_t name_len, double* total_ms,
+                       int64_t* launches);
+
 /* ------------------------------------------------------------------------
  * Step-level entry points (used by the parity tests to compare one step of
  * the path with the oracle's same step).  Same conventions: column-major,
  * device or host pointers, stream-ordered on the handle's stream.
+ * Unlike mpjsvd_factor, these take DEVICE pointers only.
  * ------------------------------------------------------------------------ */
 
 /* One-sided block round-robin Jacobi in fp64 on X (m x n, ldx), accumulating

@@ -73,6 +73,7 @@ EXPORTS = [
     "mpjsvd_default_options", "mpjsvd_create", "mpjsvd_factor", "mpjsvd_destroy", "mpjsvd_strerror",
     "mpjsvd_last_cuda_error", "mpjsvd_version", "mpjsvd_block_jacobi_f64", "mpjsvd_block_jacobi_f32",
     "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
+    "mpjsvd_set_profiling", "mpjsvd_get_profile",
 ]
 
 
@@ -103,6 +104,8 @@ def lib():
         L.mpjsvd_lift.argtypes = [vp, vp, i64, i64, vp, i64]
         L.mpjsvd_apply_q.argtypes = [vp, vp, i64, i64, i64, vp, vp, i64, i64]
         L.mpjsvd_gemm_f64.argtypes = [vp, i32, i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]
+        L.mpjsvd_set_profiling.argtypes = [vp, i32]
+        L.mpjsvd_get_profile.argtypes = [vp, i32, C.c_char_p, i32, C.POINTER(dbl), C.POINTER(i64)]
         _lib = L
         return L
 
@@ -154,6 +157,22 @@ class Handle:
     @property
     def ptr(self):
         return self._h
+
+    def set_profiling(self, on: bool = True):
+        _check(lib().mpjsvd_set_profiling(self._h, int(on)), "mpjsvd_set_profiling")
+
+    def profile(self) -> dict:
+        """{kernel name: (summed device ms, launches)} since set_profiling(True)."""
+        L = lib()
+        n = L.mpjsvd_get_profile(self._h, -1, None, 0, None, None)
+        out = {}
+        for i in range(max(n, 0)):
+            buf = C.create_string_buffer(64)
+            ms = C.c_double()
+            cnt = C.c_int64()
+            L.mpjsvd_get_profile(self._h, i, buf, 64, C.byref(ms), C.byref(cnt))
+            out[buf.value.decode()] = (ms.value, cnt.value)
+        return out
 
 
 def _col_major(t):

@@ -28,8 +28,15 @@ struct JacobiRound {
     int* sweep_upd;     // device scalar, atomic add (this sweep)
 };
 
+// Optional per-launch timing hook (bench profiling): begin/end bracket one launch.
+struct ProfHook {
+    void* ctx;
+    void (*begin)(void* ctx, const char* name);
+    void (*end)(void* ctx, const char* name);
+};
+
 template <typename T>
-int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st);
+int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook = nullptr);
 template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
 

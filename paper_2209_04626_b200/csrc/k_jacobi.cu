@@ -421,18 +421,34 @@ __global__ void __launch_bounds__(256) k_inner_solve_batch(T* G, T* E, int w, T 
 // ------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------
+template <typename T> struct KName;
+template <> struct KName<float> {
+    static constexpr const char* gram = "pair_gram_f32";
+    static constexpr const char* solve = "pair_solve_f32";
+    static constexpr const char* update = "pair_update_f32";
+};
+template <> struct KName<double> {
+    static constexpr const char* gram = "pair_gram_f64";
+    static constexpr const char* solve = "pair_solve_f64";
+    static constexpr const char* update = "pair_update_f64";
+};
+
 template <typename T, int W>
-static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st) {
+static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHook* hook) {
+    if (hook) hook->begin(hook->ctx, KName<T>::gram);
     k_pair_gram<T, W><<<dim3(a.nsplit, a.npairs), 64, 0, st>>>(a);
     MPJ_LAUNCHED();
+    if (hook) hook->end(hook->ctx, KName<T>::gram);
     const size_t sms = sizeof(InnerSmem<T, W>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_pair_solve<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
         attr_set = true;
     }
+    if (hook) hook->begin(hook->ctx, KName<T>::solve);
     k_pair_solve<T, W><<<a.npairs, 256, sms, st>>>(a);
     MPJ_LAUNCHED();
+    if (hook) hook->end(hook->ctx, KName<T>::solve);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
     constexpr int VEC = 16 / sizeof(T);
     const size_t usm = sizeof(T) * (size_t)W * ((64 + VEC) + (W + VEC)) + sizeof(long long) * W;
@@ -441,8 +457,10 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st) {
         cudaFuncSetAttribute(k_pair_update<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
         attr_u = true;
     }
+    if (hook) hook->begin(hook->ctx, KName<T>::update);
     k_pair_update<T, W><<<dim3((unsigned)ceil_div(rows_pad, 64), a.npairs, a.V ? 2 : 1), 64, usm, st>>>(a);
     MPJ_LAUNCHED();
+    if (hook) hook->end(hook->ctx, KName<T>::update);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         mpj_record_cuda_error(e, "jacobi round launch", __FILE__, __LINE__);
@@ -452,16 +470,16 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st) {
 }
 
 template <typename T>
-int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st) {
+int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook) {
     switch (W) {
-        case 16: return launch_round_w<T, 16>(a, st);
-        case 32: return launch_round_w<T, 32>(a, st);
-        case 64: return launch_round_w<T, 64>(a, st);
+        case 16: return launch_round_w<T, 16>(a, st, hook);
+        case 32: return launch_round_w<T, 32>(a, st, hook);
+        case 64: return launch_round_w<T, 64>(a, st, hook);
         default: return -7;
     }
 }
-template int launch_jacobi_round<float>(const JacobiRound<float>&, int, cudaStream_t);
-template int launch_jacobi_round<double>(const JacobiRound<double>&, int, cudaStream_t);
+template int launch_jacobi_round<float>(const JacobiRound<float>&, int, cudaStream_t, const ProfHook*);
+template int launch_jacobi_round<double>(const JacobiRound<double>&, int, cudaStream_t, const ProfHook*);
 
 template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {

@@ -7,7 +7,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "../../include/mpjsvd.h"
@@ -44,7 +46,54 @@ constexpr double U32 = 5.9604644775390625e-08;
 
 }  // namespace
 
+// Per-kernel CUDA-event timing (bench profiling, mpjsvd_set_profiling).
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Pending { const char* name; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> open;     // begin event of the launch in flight
+    std::map<std::string, std::pair<double, long long>> acc;
+    cudaStream_t st = nullptr;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void begin(const char* name) {
+        (void)name;
+        cudaEvent_t e = get();
+        cudaEventRecord(e, st);
+        open.push_back(e);
+    }
+    void end(const char* name) {
+        cudaEvent_t e = get();
+        cudaEventRecord(e, st);
+        pending.push_back({name, open.back(), e});
+        open.pop_back();
+    }
+    void resolve() {   // after a stream synchronisation
+        for (auto& p : pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.a, p.b);
+            auto& x = acc[p.name];
+            x.first += ms;
+            x.second += 1;
+        }
+        pending.clear();
+        open.clear();
+        used = 0;
+    }
+    static void hb(void* c, const char* n) { static_cast<Profiler*>(c)->begin(n); }
+    static void he(void* c, const char* n) { static_cast<Profiler*>(c)->end(n); }
+};
+
 struct mpjsvd_handle_s {
+    Profiler prof;
     mpjsvd_options opts;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -131,13 +180,15 @@ int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int 
     for (int sw = 1; sw <= max_sweeps && sw <= 64; ++sw) {
         a.sweep_off = d_off + (sw - 1);
         a.sweep_upd = d_upd + (sw - 1);
+        ProfHook hook{&h->prof, &Profiler::hb, &Profiler::he};
         for (int r = 0; r < M - 1; ++r) {
             a.round = r;
-            MPJ_TRY(launch_jacobi_round<T>(a, W, st));
+            MPJ_TRY(launch_jacobi_round<T>(a, W, st, h->prof.on ? &hook : nullptr));
         }
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h->prof.on) h->prof.resolve();
         const double off = hp[0];
         int upd = 0;
         memcpy(&upd, hp + 1, sizeof(int));
@@ -192,9 +243,13 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
+#define PROF_B(name) do { if (h->prof.on) h->prof.begin(name); } while (0)
+#define PROF_E(name) do { if (h->prof.on) h->prof.end(name); } while (0)
+
 int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, double* U, int64_t ldu,
                 double* S, double* V, int64_t ldv, mpjsvd_stats* stats) {
     const mpjsvd_options& o = h->opts;
+    h->prof.st = h->stream;
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32), n_pad = round_up(n, 32);
     const bool a_dev = is_device_ptr(A), u_dev = is_device_ptr(U), s_dev = is_device_ptr(S),
@@ -257,7 +312,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     QrWork qw;
     if (m > n) {
         MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
+        PROF_B("qr_coop_tall");
         MPJ_TRY(qr_coop(dA, m_pad, (int)m, (int)n, P<double>(h, S_TAU_T0), 0, qw, nullptr, st));
+        PROF_E("qr_coop_tall");
         MPJ_TRY(upper_of(dA, m_pad, dA1, n_pad, (int)n, n_pad, st));
     } else {
         MPJ_TRY(copy_matrix(dA, m_pad, dA1, n_pad, n_pad, n, st));
@@ -265,14 +322,18 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_CUDA_TRY(cudaEventRecord(ev[1], st));
     // ---- stage 1: column-pivoted QR  A1 P = Q_p R
     MPJ_TRY(ensure_qr_work(h, (int)n, (int)n, qw));
+    PROF_B("qrp_coop");
     MPJ_TRY(qr_coop(dA1, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), 1, qw, P<int>(h, S_PERM), st));
+    PROF_E("qrp_coop");
     MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
     MPJ_TRY(diag_stats(dA1L, n_pad, (int)n, scal + 1, flags + 1, st));
     MPJ_CUDA_TRY(cudaEventRecord(ev[2], st));
     // ---- stage 2: R = L Q_2 via QR of R^T; X = L
     if (o.x_from_lq) {
         MPJ_TRY(transpose_upper(dA1L, n_pad, dRt, n_pad, (int)n, n_pad, st));
+        PROF_B("lq_coop");
         MPJ_TRY(qr_coop(dRt, n_pad, (int)n, (int)n, P<double>(h, S_TAU_T), 0, qw, nullptr, st));
+        PROF_E("lq_coop");
         MPJ_TRY(lower_from_rt(dRt, n_pad, dX, n_pad, (int)n, n_pad, st));
     } else {
         MPJ_TRY(upper_of(dA1L, n_pad, dX, n_pad, (int)n, n_pad, st));
@@ -281,7 +342,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- stage 3: gate measures, report only
     std::vector<double> xnorms;
     if (o.compute_gates) {
+        PROF_B("gates_orth");
         MPJ_TRY(gates_orth(dX, n_pad, n_pad, (int)n, dX32, n_pad, scal + 3, st));
+        PROF_E("gates_orth");
         MPJ_TRY(col_norms<double>(dX, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 1, st));
         xnorms.resize(n);
         MPJ_CUDA_TRY(cudaMemcpyAsync(xnorms.data(), P<double>(h, S_KEYS), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -303,8 +366,12 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(sort_upcast_v(dV32, n_pad, P<int>(h, S_RANK), dQ, n_pad, n_pad, (int)n, st));
         MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
         // ---- stage 5: lift Q = qr(fl64(V32)), Y = X Q
+        PROF_B("lift_cholqr");
         MPJ_TRY(lift_inplace(h, dQ, n_pad, (int)n, flags + 2));
+        PROF_E("lift_cholqr");
+        PROF_B("rv_gemm");
         MPJ_TRY(gemm_f64(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, st));
+        PROF_E("rv_gemm");
         s.path_taken = MPJSVD_PATH_FORCE_MIXED;
     } else {
         MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
@@ -325,6 +392,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_TRY(rank_desc(P<double>(h, S_SOUT), (int)n, P<int>(h, S_RANK), st));
     MPJ_TRY(finalize(dY, n_pad, dQ, n_pad, P<double>(h, S_SOUT), P<int>(h, S_RANK), dUX, n_pad, dVX, n_pad,
                      P<double>(h, S_KEYS) /* sorted sigma */, n_pad, (int)n, st));
+    PROF_B("assemble_wy");
     MPJ_TRY(apply_q_wy(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), dUX, n_pad, n, P<double>(h, S_WY), st));
     double* Ufin = dUX;
     long long ldUf = n_pad;
@@ -339,6 +407,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (o.x_from_lq)
         MPJ_TRY(apply_q_wy(dRt, n, (int)n, n_pad, P<double>(h, S_TAU_T), dVX, n_pad, n, P<double>(h, S_WY), st));
     MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, st));
+    PROF_E("assemble_wy");
     MPJ_CUDA_TRY(cudaEventRecord(ev[8], st));
     // ---- outputs (device -> device, or device -> host on the e2e path)
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(U, sizeof(double) * ldu, Ufin, sizeof(double) * ldUf, sizeof(double) * m, n,
@@ -354,6 +423,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h->prof.on) h->prof.resolve();
     if (hflags[0]) return MPJSVD_ERR_NONFINITE;
     if (hflags[1] || hflags[2]) return MPJSVD_ERR_RANK_DEFICIENT;
 
@@ -513,6 +583,7 @@ int mpjsvd_destroy(mpjsvd_handle h) {
         if (h->buf[i]) cudaFree(h->buf[i]);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : h->prof.pool) cudaEventDestroy(e);
     if (h->host_pinned) cudaFreeHost(h->host_pinned);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -538,6 +609,33 @@ const char* mpjsvd_strerror(int code) {
 const char* mpjsvd_last_cuda_error(void) { return g_last_cuda_err; }
 
 int mpjsvd_version(void) { return MPJSVD_VERSION; }
+
+int mpjsvd_set_profiling(mpjsvd_handle h, int32_t on) {
+    if (!h) return MPJSVD_ERR_INVALID_ARG;
+    h->prof.on = on != 0;
+    h->prof.acc.clear();
+    h->prof.pending.clear();
+    h->prof.open.clear();
+    h->prof.used = 0;
+    return 0;
+}
+
+int mpjsvd_get_profile(mpjsvd_handle h, int32_t idx, char* name, int32_t name_len, double* total_ms,
+                       int64_t* launches) {
+    if (!h) return MPJSVD_ERR_INVALID_ARG;
+    const int count = (int)h->prof.acc.size();
+    if (idx < 0) return count;
+    if (idx >= count) return MPJSVD_ERR_INVALID_ARG;
+    auto it = h->prof.acc.begin();
+    std::advance(it, idx);
+    if (name && name_len > 0) {
+        strncpy(name, it->first.c_str(), (size_t)name_len - 1);
+        name[name_len - 1] = 0;
+    }
+    if (total_ms) *total_ms = it->second.first;
+    if (launches) *launches = it->second.second;
+    return count;
+}
 
 int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, double* U, int64_t ldu,
                   double* S, double* V, int64_t ldv, mpjsvd_stats* stats) {
