@@ -202,10 +202,11 @@ def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks:
 
 
 def algorithmic_work(stats_list, n: int, b: int):
-    """Algorithmic flops/bytes of the Jacobi kernels summed over the timed steps.
-    Per sweep: Gram 4n^3 flops over all pairs (reads X once
-    per round: n^2 s bytes); update 16 n b^2 flops per updated pair for X and
-    V, bytes 2 x (read + write of n x 2b) x s for X and V."""
+    """Algorithmic flops/bytes of the Jacobi kernels summed over the timed steps
+    (DESIGN.md sec. 8).  Gram of a pair (w = 2b columns, n rows): the
+    symmetric half incl. the diagonal, n w (w+1) flops, reading W once
+    (n w s bytes; per round the whole X: n^2 s); update: 2 n w^2 flops for X
+    and again for V per updated pair, bytes 2 x (read + write of n x w) x s."""
     flops, byts = {}, {}
     nblk = -(-n // b)
     M = nblk + (nblk & 1)
@@ -217,7 +218,8 @@ def algorithmic_work(stats_list, n: int, b: int):
             upd = sum(st["upd_trace" + key])
             g = f"pair_gram_{tag}"
             u = f"pair_update_{tag}"
-            flops[g] = flops.get(g, 0.0) + sweeps * rounds * npairs * 8.0 * n * b * b
+            w = 2 * b
+            flops[g] = flops.get(g, 0.0) + sweeps * rounds * npairs * float(n) * w * (w + 1)
             byts[g] = byts.get(g, 0.0) + sweeps * rounds * float(n) * n * s
             flops[u] = flops.get(u, 0.0) + upd * 16.0 * n * b * b
             byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * 2.0 * n * 2 * b * s

@@ -62,6 +62,8 @@ int gather_cols(const double* A, long long lda, const int* perm, double* out, lo
                 long long rows, int n, cudaStream_t st);
 
 // ---- dense linear algebra (k_linalg.cu) ---------------------------------
+// Workspace the GEMM may use for split-K partials (thread-local, set by the engine).
+void gemm_set_workspace(double* ws, size_t elems);
 int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A,
              long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
              cudaStream_t st);
@@ -75,6 +77,8 @@ int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, l
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C,
                long long ldc, long long ncols, double* work, cudaStream_t st);
 size_t apply_q_work_elems(long long m, long long ncols);
+// Blocked Householder QR (no pivoting) in place; work >= apply_q_work_elems(m, n).
+int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st);
 
 // ---- misc (k_misc.cu) ----------------------------------------------------
 int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st);

@@ -137,134 +137,212 @@ __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
 }
 
 // ------------------------------------------------------------------------
-// Inner 2b x 2b solve (reading c-5), one CTA.  G (w x w, stride GS) and
-// E in shared memory.  Each inner round: phase A computes the P = w2/2
-// rotations of the circle-method round (disjoint pairs, so their parameters
-// do not depend on each other); phase B applies J^T G J blockwise on the
-// 2 x 2 blocks (writing each block and its mirror from the same numbers, so
-// G stays exactly symmetric) and E <- (I + E) J - I in delta form.
-// Returns the number of rotations; *sweeps_used receives inner sweeps.
+// Inner 2b x 2b solve (reading c-5), one CTA per pair, G and E in shared
+// memory.  The circle-method schedule of the 2b indices is tabulated once per
+// CTA (pairs of a round, pair and partner of an index).  The rotation
+// parameters are the oracle's (c-3) formulas with IEEE div/sqrt; inactive
+// pairs carry the identity (c, s) = (1, 0).  See inner_solve_dev for the
+// thread organisation.
 // ------------------------------------------------------------------------
+constexpr int INNER_NT = 256;
+
 template <typename T, int W>
 struct InnerSmem {
     static constexpr int GS = W + 1;
+    static constexpr int R = W - 1;                    // max rounds per inner sweep
     T G[W * (W + 1)];
     T E[W * (W + 1)];
-    T rc[W / 2], rs[W / 2], rt[W / 2], rm[W / 2], rg[W / 2], rpp[W / 2], rqq[W / 2];
-    int pp[W / 2], qq[W / 2], act[W / 2];
-    int nrot;
+    T rc[2][W / 2], rs[2][W / 2], rt[2][W / 2], rm[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];
+    int act[2][W / 2];
+    unsigned char sp[R][W / 2], sq[R][W / 2];          // pair k of round r (p < q; q may be the bye)
+    unsigned char spk[R][W], spart[R][W];              // pair index / partner of index x in round r
+    int nrot[2];
     T red[32];
 };
 
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// (x, y) <- (c x - s y, s x + c y); identity exactly when (c, s) = (1, 0)
+template <typename T>
+__device__ __forceinline__ void rot2(T c, T s, T& x, T& y) {
+    const T nx = fma_rn(c, x, -mul_rn(s, y));
+    const T ny = fma_rn(s, x, mul_rn(c, y));
+    x = nx;
+    y = ny;
+}
+
+// rotation parameters of pair k (indices p < q) into buffer `buf`; returns active
+template <typename T, int W>
+__device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k, int q, int w, T gpp, T gqq, T gpq,
+                                            T tol_in) {
+    int active = 0;
+    T c = T(1), sn = T(0), t = T(0), cm1 = T(0);
+    // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||
+    if (q < w && gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq)) {
+        // closest-to-identity rotation (reading c-3)
+        T zeta = (gqq - gpp) / (T(2) * gpq);
+        if (fabs(zeta) > RealTraits<T>::rsqrt_u) {
+            t = T(1) / (T(2) * zeta);
+        } else {
+            T sg = zeta >= T(0) ? T(1) : T(-1);
+            t = sg / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
+        }
+        T rt = sqrt(T(1) + t * t);
+        c = T(1) / rt;
+        sn = t * c;
+        cm1 = -(t * t * c) / (T(1) + rt);
+        active = 1;
+    }
+    sm.rc[buf][k] = c;
+    sm.rs[buf][k] = sn;
+    sm.rt[buf][k] = t;
+    sm.rm[buf][k] = cm1;
+    sm.rg[buf][k] = gpq;
+    sm.rpp[buf][k] = gpp;
+    sm.rqq[buf][k] = gqq;
+    sm.act[buf][k] = active;
+    return active;
+}
+
+// G'[x][x] after the current round (pair kx of index x, parameter buffer buf)
+template <typename T, int W>
+__device__ __forceinline__ T diag_after(const InnerSmem<T, W>& sm, int buf, int kx, int x, int px) {
+    constexpr int GS = InnerSmem<T, W>::GS;
+    if (!sm.act[buf][kx]) return sm.G[x * GS + x];
+    const T t = sm.rt[buf][kx], g = sm.rg[buf][kx];
+    return x == px ? fma_rn(-t, g, sm.rpp[buf][kx]) : fma_rn(t, g, sm.rqq[buf][kx]);
+}
+
+constexpr int INNER_TPP = 8;   // threads owning one rotation pair (INNER_NT / (W/2) at W = 64)
+
+// Row-owner inner solve: INNER_TPP threads own pair A = (p_A, q_A) of the
+// current round and rewrite rows p_A, q_A of G (blocks G[{p_A,q_A}][{p_B,q_B}]
+// <- R_A^T X R_B for every pair B, higher pair index rotated first so that
+// the two owners of a block and its mirror perform identical operations and
+// G stays exactly symmetric) and columns p_A, q_A of E.  The owner of row x
+// then computes the rotation of x's next-round pair (x, y), x < y, from its
+// fresh row and pair(y)'s published parameters; one barrier per inner round.
 template <typename T, int W>
 __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used) {
     constexpr int GS = InnerSmem<T, W>::GS;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int w2 = w + (w & 1);
-    const int P = w2 / 2;
-    int total = 0, used = 0;
+    const int P = w2 / 2, NR = w2 - 1;
+    const int tpp = nt / (W / 2);                      // threads per pair (8 at W = 64, 256 threads)
+    const int grp = tid / tpp, gl = tid - (tid / tpp) * tpp;
+    for (int e = tid; e < NR * P; e += nt) {
+        const int r = e / P, k = e - (e / P) * P;
+        const int x = rr_slot(r, k, w2), y = rr_slot(r, w2 - 1 - k, w2);
+        const int p = min(x, y), q = max(x, y);
+        sm.sp[r][k] = (unsigned char)p;
+        sm.sq[r][k] = (unsigned char)q;
+        sm.spk[r][p] = (unsigned char)k;
+        sm.spk[r][q] = (unsigned char)k;
+        sm.spart[r][p] = (unsigned char)q;
+        sm.spart[r][q] = (unsigned char)p;
+    }
     for (int i = tid; i < W * GS; i += nt) sm.E[i] = T(0);
-    for (int isw = 0; isw < max_inner; ++isw) {
-        if (tid == 0) sm.nrot = 0;
-        __syncthreads();
-        used = isw + 1;
-        for (int ir = 0; ir < w2 - 1; ++ir) {
-            // ---- phase A: rotation parameters
-            if (tid < P) {
-                int x = rr_slot(ir, tid, w2), y = rr_slot(ir, w2 - 1 - tid, w2);
-                int p = min(x, y), q = max(x, y);
-                sm.pp[tid] = p;
-                sm.qq[tid] = q;
-                int active = 0;
-                if (q < w) {
-                    T gpp = sm.G[p * GS + p], gqq = sm.G[q * GS + q], gpq = sm.G[p * GS + q];
-                    // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||
-                    if (gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq)) {
-                        // closest-to-identity rotation (reading c-3)
-                        T zeta = (gqq - gpp) / (T(2) * gpq);
-                        T t;
-                        if (fabs(zeta) > RealTraits<T>::rsqrt_u) {
-                            t = T(1) / (T(2) * zeta);
-                        } else {
-                            T sg = zeta >= T(0) ? T(1) : T(-1);
-                            t = sg / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
-                        }
-                        T rt = sqrt(T(1) + t * t);
-                        T c = T(1) / rt;
-                        sm.rc[tid] = c;
-                        sm.rs[tid] = t * c;
-                        sm.rt[tid] = t;
-                        sm.rm[tid] = -(t * t * c) / (T(1) + rt);
-                        sm.rg[tid] = gpq;
-                        sm.rpp[tid] = gpp;
-                        sm.rqq[tid] = gqq;
-                        active = 1;
-                        atomicAdd(&sm.nrot, 1);
-                    }
-                }
-                sm.act[tid] = active;
-            }
-            __syncthreads();
-            // ---- phase B1: G <- J^T G J on 2x2 blocks (A <= B)
-            for (int idx = tid; idx < P * P; idx += nt) {
-                const int A = idx / P, B = idx - (idx / P) * P;
-                if (A > B) continue;
-                const int aA = sm.act[A], aB = sm.act[B];
-                const int pa = sm.pp[A], qa = sm.qq[A], pb = sm.pp[B], qb = sm.qq[B];
-                if (A == B) {
+    if (tid < 2) sm.nrot[tid] = 0;
+    __syncthreads();
+    if (max_inner < 1) { if (sweeps_used) *sweeps_used = 0; return 0; }
+    if (tid < P) {
+        const int p = sm.sp[0][tid], q = sm.sq[0][tid];
+        const T gpp = sm.G[p * GS + p];
+        const T gqq = q < w ? sm.G[q * GS + q] : T(0);
+        const T gpq = q < w ? sm.G[p * GS + q] : T(0);
+        if (set_rotation<T, W>(sm, 0, tid, q, w, gpp, gqq, gpq, tol_in)) atomicAdd(&sm.nrot[0], 1);
+    }
+    __syncthreads();
+    int total = 0, sweep = 0, r = 0, buf = 0;
+    while (true) {
+        const bool last = (r == NR - 1);
+        const int rn = last ? 0 : r + 1;
+        const int sn = last ? sweep + 1 : sweep;
+        if (grp < P) {
+            const int k = grp;
+            const int pa = sm.sp[r][k], qa = sm.sq[r][k], aA = sm.act[buf][k];
+            const bool qav = qa < w;
+            const T cA = sm.rc[buf][k], sA = sm.rs[buf][k];
+            for (int B = gl; B < P; B += tpp) {
+                if (B == k) {
                     if (aA) {
-                        const T t = sm.rt[A], g = sm.rg[A];
-                        sm.G[pa * GS + pa] = sm.rpp[A] - t * g;
-                        sm.G[qa * GS + qa] = sm.rqq[A] + t * g;
+                        const T t = sm.rt[buf][k], g = sm.rg[buf][k];
+                        sm.G[pa * GS + pa] = fma_rn(-t, g, sm.rpp[buf][k]);
+                        sm.G[qa * GS + qa] = fma_rn(t, g, sm.rqq[buf][k]);
                         sm.G[pa * GS + qa] = T(0);
                         sm.G[qa * GS + pa] = T(0);
                     }
                     continue;
                 }
+                const int aB = sm.act[buf][B];
                 if (!aA && !aB) continue;
-                const bool qav = qa < w, qbv = qb < w;
+                const int pb = sm.sp[r][B], qb = sm.sq[r][B];
+                const bool qbv = qb < w;
                 T x00 = sm.G[pa * GS + pb];
                 T x01 = qbv ? sm.G[pa * GS + qb] : T(0);
                 T x10 = qav ? sm.G[qa * GS + pb] : T(0);
                 T x11 = (qav && qbv) ? sm.G[qa * GS + qb] : T(0);
-                if (aB) {   // columns (pb, qb) <- (c x_p - s x_q, s x_p + c x_q)
-                    const T c = sm.rc[B], s = sm.rs[B];
-                    T y00 = c * x00 - s * x01, y01 = s * x00 + c * x01;
-                    T y10 = c * x10 - s * x11, y11 = s * x10 + c * x11;
-                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                const T cB = sm.rc[buf][B], sB = sm.rs[buf][B];
+                if (B > k) {        // higher pair B first (column op), then own rows
+                    rot2(cB, sB, x00, x01); rot2(cB, sB, x10, x11);
+                    rot2(cA, sA, x00, x10); rot2(cA, sA, x01, x11);
+                } else {            // own pair is the higher one: own rows first, then B's columns
+                    rot2(cA, sA, x00, x10); rot2(cA, sA, x01, x11);
+                    rot2(cB, sB, x00, x01); rot2(cB, sB, x10, x11);
                 }
-                if (aA) {   // rows (pa, qa)
-                    const T c = sm.rc[A], s = sm.rs[A];
-                    T z00 = c * x00 - s * x10, z10 = s * x00 + c * x10;
-                    T z01 = c * x01 - s * x11, z11 = s * x01 + c * x11;
-                    x00 = z00; x01 = z01; x10 = z10; x11 = z11;
+                sm.G[pa * GS + pb] = x00;
+                if (qbv) sm.G[pa * GS + qb] = x01;
+                if (qav) sm.G[qa * GS + pb] = x10;
+                if (qav && qbv) sm.G[qa * GS + qb] = x11;
+            }
+            if (aA) {
+                const T cm1 = sm.rm[buf][k];
+                for (int rho = gl; rho < w; rho += tpp) {
+                    T ep = sm.E[rho * GS + pa], eq = sm.E[rho * GS + qa];
+                    rot2(cA, sA, ep, eq);
+                    if (rho == pa) { ep += cm1; eq += sA; }
+                    if (rho == qa) { ep -= sA; eq += cm1; }
+                    sm.E[rho * GS + pa] = ep;
+                    sm.E[rho * GS + qa] = eq;
                 }
-                sm.G[pa * GS + pb] = x00; sm.G[pb * GS + pa] = x00;
-                if (qbv) { sm.G[pa * GS + qb] = x01; sm.G[qb * GS + pa] = x01; }
-                if (qav) { sm.G[qa * GS + pb] = x10; sm.G[pb * GS + qa] = x10; }
-                if (qav && qbv) { sm.G[qa * GS + qb] = x11; sm.G[qb * GS + qa] = x11; }
             }
-            // ---- phase B2: E <- (I + E) J - I (delta form)
-            for (int idx = tid; idx < P * w; idx += nt) {
-                const int k = idx / w, rho = idx - (idx / w) * w;
-                if (!sm.act[k]) continue;
-                const int p = sm.pp[k], q = sm.qq[k];
-                const T c = sm.rc[k], s = sm.rs[k], cm1 = sm.rm[k];
-                const T ep = sm.E[rho * GS + p], eq = sm.E[rho * GS + q];
-                T np = c * ep - s * eq, nq = s * ep + c * eq;
-                if (rho == p) { np += cm1; nq += s; }
-                if (rho == q) { np -= s; nq += cm1; }
-                sm.E[rho * GS + p] = np;
-                sm.E[rho * GS + q] = nq;
-            }
-            __syncthreads();
         }
-        const int nr = sm.nrot;
-        total += nr;
+        __syncwarp();
+        // parameters of the next round: the owner of the lower index x of each next pair (x, y)
+        if (grp < P && gl < 2) {
+            const int x = gl == 0 ? sm.sp[r][grp] : sm.sq[r][grp];
+            if (x < w) {
+                const int y = sm.spart[rn][x];
+                if (x < y) {
+                    const int kn = sm.spk[rn][x];
+                    T gxx = sm.G[x * GS + x];
+                    T gxy = y < w ? sm.G[x * GS + y] : T(0);
+                    T gyy = T(0);
+                    if (y < w) {
+                        const int B = sm.spk[r][y];
+                        gyy = B == grp ? sm.G[y * GS + y] : diag_after<T, W>(sm, buf, B, y, sm.sp[r][B]);
+                    }
+                    if (set_rotation<T, W>(sm, buf ^ 1, kn, y, w, gxx, gyy, gxy, tol_in))
+                        atomicAdd(&sm.nrot[sn & 1], 1);
+                }
+            }
+        }
         __syncthreads();
-        if (nr == 0) break;
+        if (last) {
+            const int nr = sm.nrot[sweep & 1];
+            total += nr;
+            __syncthreads();
+            if (tid == 0) sm.nrot[sweep & 1] = 0;
+            if (nr == 0 || sweep + 1 >= max_inner) break;
+        }
+        r = rn;
+        sweep = sn;
+        buf ^= 1;
     }
-    if (sweeps_used) *sweeps_used = used;
+    if (sweeps_used) *sweeps_used = sweep + 1;
     return total;
 }
 
@@ -272,7 +350,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
 // k_pair_solve: one CTA per pair.
 // ------------------------------------------------------------------------
 template <typename T, int W>
-__global__ void __launch_bounds__(256) k_pair_solve(JacobiRound<T> a) {
+__global__ void __launch_bounds__(INNER_NT) k_pair_solve(JacobiRound<T> a) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -283,7 +361,7 @@ __global__ void __launch_bounds__(256) k_pair_solve(JacobiRound<T> a) {
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
     for (int e = tid; e < W * W; e += nt) {
         const int p = e / W, q = e - (e / W) * W;
-        if (p < w && q < w && p <= q) {
+        if (p < w && q < w && p >= q) {      // partials hold (at least) the lower triangle
             T s = T(0);
             for (int sp = 0; sp < a.nsplit; ++sp) s += part[(long long)sp * (W * W) + p * W + q];
             sm.G[p * GS + q] = s;
@@ -292,13 +370,16 @@ __global__ void __launch_bounds__(256) k_pair_solve(JacobiRound<T> a) {
     }
     __syncthreads();
     // pair metric: max_{p<q} |g_pq| / (sqrt(g_pp) sqrt(g_qq))
+    T* dsq = sm.E;   // scratch (E is initialised inside the inner solve)
+    for (int p = tid; p < w; p += nt) dsq[p] = sqrt(sm.G[p * GS + p]);
+    __syncthreads();
     T off = T(0);
     for (int e = tid; e < w * w; e += nt) {
         const int p = e / w, q = e - (e / w) * w;
         if (p < q) {
             T gpp = sm.G[p * GS + p], gqq = sm.G[q * GS + q];
             if (gpp > T(0) && gqq > T(0)) {
-                T v = fabs(sm.G[p * GS + q]) / (sqrt(gpp) * sqrt(gqq));
+                T v = fabs(sm.G[p * GS + q]) / (dsq[p] * dsq[q]);
                 off = v > off ? v : off;
             }
         }
@@ -398,11 +479,297 @@ __global__ void __launch_bounds__(64) k_pair_update(JacobiRound<T> a) {
     }
 }
 
+
+// ========================================================================
+// FP64 tensor-pipe (DMMA) versions: mma.sync.aligned.m8n8k4.row.col.f64.
+// B200 has no tcgen05 kind::f64; DMMA runs on the FP64 pipe (measured 36.9
+// TFLOP/s, profiles/peaks.json).  Fragment layout (PTX ISA, m8n8k4 f64):
+//   A (8x4, row): lane l holds A[l>>2][l&3];  B (4x8, col): B[l&3][l>>2];
+//   C/D (8x8): lane l holds D[l>>2][2(l&3)], D[l>>2][2(l&3)+1].
+// ========================================================================
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// lower-triangle tile t -> (i, j), i >= j, row-major over the lower triangle
+__host__ __device__ constexpr int tri_i(int t) {
+    int ii = 0;
+    while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+    return ii;
+}
+__host__ __device__ constexpr int tri_j(int t) { return t - tri_i(t) * (tri_i(t) + 1) / 2; }
+
+constexpr int GRAM_KT = 32, GRAM_S = GRAM_KT + 4, GRAM_STAGES = 3, GRAM_NWARP = 4;
+
+// The k-loop of one warp with a compile-time tile list (tiles WARP, WARP+4, ...)
+template <int W, int WARP>
+__device__ __forceinline__ void gram_warp(const double* __restrict__ X, const long long* colofs, double* Wsm,
+                                          long long rbeg, int ntile, double* out) {
+    constexpr int KT = GRAM_KT, S = GRAM_S, STAGES = GRAM_STAGES, NTI = W / 8;
+    constexpr int NTILE = NTI * (NTI + 1) / 2;
+    constexpr int TPW = (NTILE - WARP + GRAM_NWARP - 1) / GRAM_NWARP;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double acc[TPW > 0 ? TPW : 1][2];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
+    constexpr int CH = KT / 2;
+    auto load_tile = [&](int t, int stage) {
+        const long long r0 = rbeg + (long long)t * KT;
+        double* ws = Wsm + stage * (W * S);
+        for (int v = tid; v < W * CH; v += 128) {
+            const int c = v / CH, ch = v % CH;
+            double* dst = &ws[c * S + ch * 2];
+            const long long off = colofs[c];
+            if (off >= 0) cp_async16(dst, X + off + r0 + ch * 2);
+            else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        }
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+        if (s0 < ntile) load_tile(s0, s0);
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (t + STAGES - 1 < ntile) load_tile(t + STAGES - 1, (t + STAGES - 1) % STAGES);
+        cp_async_commit();
+        const double* ws = Wsm + (t % STAGES) * (W * S);
+#pragma unroll
+        for (int k0 = 0; k0 < KT; k0 += 4) {
+            double f[NTI];
+#pragma unroll
+            for (int i = 0; i < NTI; ++i) f[i] = ws[(8 * i + (lane >> 2)) * S + k0 + (lane & 3)];
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int tt = WARP + GRAM_NWARP * u;
+                dmma884(acc[u][0], acc[u][1], f[tri_i(tt)], f[tri_j(tt)]);
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+        const int tt = WARP + GRAM_NWARP * u;
+        const int row = 8 * tri_i(tt) + (lane >> 2), col = 8 * tri_j(tt) + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(&out[row * W + col]) = make_double2(acc[u][0], acc[u][1]);
+    }
+}
+
+// ------------------------------------------------------------------------
+// k_pair_gram_dmma: grid (nsplit, npairs), 128 threads (4 warps).  The CTA
+// streams its row slab of W = [X_I X_J] through a 3-stage cp.async pipeline
+// (k-tile 32 rows, column-major staging, column stride 36 doubles: the
+// 16-lane phases of an m8n8k4 fragment load hit 16 distinct 8-byte banks).
+// Per 4-row k-step every warp loads the W/8 fragments (they serve as both A
+// and B: G = W^T W) and issues one DMMA per lower-triangle tile it owns
+// (tiles warp, warp+4, ...: 9 of the 36 at W = 64).  Writes the lower
+// triangle of the partial Gram.
+// ------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
+    extern __shared__ __align__(16) unsigned char gram_smem[];
+    double* Wsm = reinterpret_cast<double*>(gram_smem);
+    long long* colofs = reinterpret_cast<long long*>(Wsm + GRAM_STAGES * W * GRAM_S);
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
+    const int w = pc.wI + pc.wJ;
+    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * a.ldx : -1;
+    __syncthreads();
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg) / GRAM_KT);
+    double* out = a.partial + ((long long)pair * a.nsplit + split) * (W * W);
+    switch (warp) {
+        case 0: gram_warp<W, 0>(a.X, colofs, Wsm, rbeg, ntile, out); break;
+        case 1: gram_warp<W, 1>(a.X, colofs, Wsm, rbeg, ntile, out); break;
+        case 2: gram_warp<W, 2>(a.X, colofs, Wsm, rbeg, ntile, out); break;
+        default: gram_warp<W, 3>(a.X, colofs, Wsm, rbeg, ntile, out); break;
+    }
+}
+static size_t gram_dmma_smem(int W) { return sizeof(double) * (size_t)GRAM_STAGES * W * GRAM_S + sizeof(long long) * W; }
+
+// ------------------------------------------------------------------------
+// k_pair_update_dmma: grid (row chunks of 128, npairs, 2 [X, V]), 256
+// threads (8 warps).  out = W + W E on a 128-row slab: the slab and E are
+// staged in shared memory (W column stride 132, E^T stride W+4: conflict-free
+// fragment loads), each warp owns (128/WR) x (W/WC) of the output and runs
+// K = w/4 DMMA k-steps; the result is added in place into the staged slab
+// and stored back with coalesced 16-byte stores.
+// ------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) k_pair_update_dmma(JacobiRound<double> a) {
+    constexpr int RC = 128, SW = RC + 4, SE = W + 4;
+    constexpr int WC = W >= 64 ? 2 : 1, WR = 8 / WC;
+    constexpr int TM = RC / WR / 8, TN = W / WC / 8;
+    extern __shared__ __align__(16) unsigned char upd_smem[];
+    double* Ws = reinterpret_cast<double*>(upd_smem);      // [W][SW]  (column k, row rho)
+    double* Et = Ws + W * SW;                                // [W][SE]  (Et[j][k] = E[k][j])
+    long long* colofs = reinterpret_cast<long long*>(Et + W * SE);
+    const int pair = blockIdx.y, which = blockIdx.z;
+    if (!a.flag[pair]) return;
+    double* Mx = which ? a.V : a.X;
+    if (Mx == nullptr) return;
+    const long long ld = which ? a.ldv : a.ldx;
+    const long long rows_pad = which ? a.nv_pad : a.m_pad;
+    const long long row0 = (long long)blockIdx.x * RC;
+    if (row0 >= rows_pad) return;
+    const int nrow = (int)min((long long)RC, rows_pad - row0);    // multiple of 32
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
+    const int w = pc.wI + pc.wJ;
+    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * ld : -1;
+    __syncthreads();
+    // stage the slab (cp.async) and E^T
+    for (int v = tid; v < W * (RC / 2); v += 256) {
+        const int c = v / (RC / 2), ch = v % (RC / 2);
+        double* dst = &Ws[c * SW + ch * 2];
+        if (colofs[c] >= 0 && ch * 2 < nrow) cp_async16(dst, Mx + colofs[c] + row0 + ch * 2);
+        else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+    const double* Eg = a.E + (long long)pair * (W * W);
+    for (int e = tid; e < W * W; e += 256) {
+        const int k = e / W, j = e - (e / W) * W;
+        Et[j * SE + k] = Eg[e];
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    const int wr = warp / WC, wc = warp % WC;
+    const int rb = wr * (RC / WR), cb = wc * (W / WC);
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int kend = (w + 3) & ~3;
+    for (int k0 = 0; k0 < kend; k0 += 4) {
+        double fa[TM], fb[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) fa[i] = Ws[(k0 + (lane & 3)) * SW + rb + 8 * i + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) fb[j] = Et[(cb + 8 * j + (lane >> 2)) * SE + k0 + (lane & 3)];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    __syncthreads();   // all fragment reads done before the in-place add
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int rho = rb + 8 * i + (lane >> 2);
+            const int col = cb + 8 * j + 2 * (lane & 3);
+            Ws[col * SW + rho] += acc[i][j][0];
+            Ws[(col + 1) * SW + rho] += acc[i][j][1];
+        }
+    __syncthreads();
+    for (int v = tid; v < W * (RC / 2); v += 256) {
+        const int c = v / (RC / 2), ch = v % (RC / 2);
+        if (c < w && ch * 2 < nrow)
+            *reinterpret_cast<double2*>(Mx + colofs[c] + row0 + ch * 2) =
+                *reinterpret_cast<const double2*>(&Ws[c * SW + ch * 2]);
+    }
+}
+
+
+// ------------------------------------------------------------------------
+// k_pair_update_f32: fp32 SIMT version of the update (FFMA pipe).  Grid
+// (row chunks of 128, npairs, 2), 256 threads; thread tile 8 rows x (W/16)
+// columns of out = W + W E; slab and E staged in shared memory (16-byte
+// vector reads: 3 LDS.128 per 32 FFMA at W = 64), result added in place in
+// the staged slab and stored with coalesced 16-byte stores.
+// ------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
+    constexpr int RC = 128, SW = RC + 4, SE = W + 4, TN = W / 16;
+    extern __shared__ __align__(16) unsigned char upd_smem[];
+    float* Ws = reinterpret_cast<float*>(upd_smem);     // [W][SW]  (column k, row rho)
+    float* Es = Ws + W * SW;                            // [W][SE]  (Es[k][j] = E[k][j])
+    long long* colofs = reinterpret_cast<long long*>(Es + W * SE);
+    const int pair = blockIdx.y, which = blockIdx.z;
+    if (!a.flag[pair]) return;
+    float* Mx = which ? a.V : a.X;
+    if (Mx == nullptr) return;
+    const long long ld = which ? a.ldv : a.ldx;
+    const long long rows_pad = which ? a.nv_pad : a.m_pad;
+    const long long row0 = (long long)blockIdx.x * RC;
+    if (row0 >= rows_pad) return;
+    const int nrow = (int)min((long long)RC, rows_pad - row0);
+    const int tid = threadIdx.x;
+    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
+    const int w = pc.wI + pc.wJ;
+    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * ld : -1;
+    __syncthreads();
+    for (int v = tid; v < W * (RC / 4); v += 256) {
+        const int c = v / (RC / 4), ch = v % (RC / 4);
+        float* dst = &Ws[c * SW + ch * 4];
+        if (colofs[c] >= 0 && ch * 4 < nrow) cp_async16(dst, Mx + colofs[c] + row0 + ch * 4);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    cp_async_commit();
+    const float* Eg = a.E + (long long)pair * (W * W);
+    for (int e = tid * 4; e < W * W; e += 256 * 4) {
+        const int k = e / W, j = e - (e / W) * W;
+        *reinterpret_cast<float4*>(&Es[k * SE + j]) = *reinterpret_cast<const float4*>(&Eg[e]);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    const int cg = tid & 15, rg = tid >> 4;          // 16 column groups x 16 row groups
+    const int rb = rg * 8, cb = cg * TN;
+    float acc[8][TN];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int k = 0; k < w; ++k) {
+        float av[8], bv[TN];
+        *reinterpret_cast<float4*>(&av[0]) = *reinterpret_cast<const float4*>(&Ws[k * SW + rb]);
+        *reinterpret_cast<float4*>(&av[4]) = *reinterpret_cast<const float4*>(&Ws[k * SW + rb + 4]);
+        if constexpr (TN == 4) {
+            *reinterpret_cast<float4*>(&bv[0]) = *reinterpret_cast<const float4*>(&Es[k * SE + cb]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bv[j] = Es[k * SE + cb + j];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Ws[(cb + j) * SW + rb + i] += acc[i][j];
+    __syncthreads();
+    for (int v = tid; v < W * (RC / 4); v += 256) {
+        const int c = v / (RC / 4), ch = v % (RC / 4);
+        if (c < w && ch * 4 < nrow)
+            *reinterpret_cast<float4*>(Mx + colofs[c] + row0 + ch * 4) =
+                *reinterpret_cast<const float4*>(&Ws[c * SW + ch * 4]);
+    }
+}
+
 // ------------------------------------------------------------------------
 // k_inner_solve_batch: test entry (mpjsvd_inner_solve): count matrices.
 // ------------------------------------------------------------------------
 template <typename T, int W>
-__global__ void __launch_bounds__(256) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
+__global__ void __launch_bounds__(INNER_NT) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -436,7 +803,17 @@ template <> struct KName<double> {
 template <typename T, int W>
 static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHook* hook) {
     if (hook) hook->begin(hook->ctx, KName<T>::gram);
-    k_pair_gram<T, W><<<dim3(a.nsplit, a.npairs), 64, 0, st>>>(a);
+    if constexpr (sizeof(T) == 8) {
+        static bool attr_g = false;
+        if (!attr_g) {
+            cudaFuncSetAttribute(k_pair_gram_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gram_dmma_smem(W));
+            attr_g = true;
+        }
+        k_pair_gram_dmma<W><<<dim3(a.nsplit, a.npairs), 128, gram_dmma_smem(W), st>>>(a);
+    } else {
+        k_pair_gram<T, W><<<dim3(a.nsplit, a.npairs), 64, 0, st>>>(a);
+    }
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::gram);
     const size_t sms = sizeof(InnerSmem<T, W>);
@@ -446,7 +823,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
         attr_set = true;
     }
     if (hook) hook->begin(hook->ctx, KName<T>::solve);
-    k_pair_solve<T, W><<<a.npairs, 256, sms, st>>>(a);
+    k_pair_solve<T, W><<<a.npairs, INNER_NT, sms, st>>>(a);
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::solve);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
@@ -458,7 +835,24 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
         attr_u = true;
     }
     if (hook) hook->begin(hook->ctx, KName<T>::update);
-    k_pair_update<T, W><<<dim3((unsigned)ceil_div(rows_pad, 64), a.npairs, a.V ? 2 : 1), 64, usm, st>>>(a);
+    if constexpr (sizeof(T) == 8) {
+        const size_t dsm = sizeof(double) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
+        static bool attr_d = false;
+        if (!attr_d) {
+            cudaFuncSetAttribute(k_pair_update_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+            attr_d = true;
+        }
+        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.V ? 2 : 1), 256, dsm, st>>>(a);
+    } else {
+        const size_t fsm = sizeof(float) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
+        static bool attr_f = false;
+        if (!attr_f) {
+            cudaFuncSetAttribute(k_pair_update_f32<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+            attr_f = true;
+        }
+        (void)usm;
+        k_pair_update_f32<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.V ? 2 : 1), 256, fsm, st>>>(a);
+    }
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::update);
     cudaError_t e = cudaGetLastError();
@@ -485,7 +879,7 @@ template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     const size_t sms = sizeof(InnerSmem<T, W>);
     cudaFuncSetAttribute(k_inner_solve_batch<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-    k_inner_solve_batch<T, W><<<count, 256, sms, st>>>(G, E, w, tol_in, max_inner, rot);
+    k_inner_solve_batch<T, W><<<count, INNER_NT, sms, st>>>(G, E, w, tol_in, max_inner, rot);
     MPJ_LAUNCHED();
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }

@@ -9,98 +9,203 @@
 namespace mpj {
 
 // ------------------------------------------------------------------------
-// fp64 GEMM: C = alpha op(A) op(B) + beta C (column-major).  64 x 64 tile,
-// BK = 16, 256 threads, 4 x 4 register tile per thread, FP64 FMA pipe.
+// fp64 GEMM on the FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64):
+// C = alpha op(A) op(B) + beta C, column-major, any M, N, K, lda, ldb.
+// CTA tile 128 x 64, k-tile 16, 8 warps (4 x 2) with 32 x 32 warp tiles
+// (4 x 4 DMMA tiles, 32 fp64 accumulators per thread), 3-stage cp.async
+// pipeline.  Both operands are staged k-major (As[k][m], Bs[k][n]) with row
+// strides 132 / 68 doubles (= 4 mod 16): the 16-lane phases of every
+// fragment load hit 16 distinct 8-byte banks.  Contiguous, aligned runs are
+// copied with 16-byte cp.async, everything else (transposed operands,
+// ragged edges) with 8-byte cp.async; out-of-range elements are zero-filled.
 // ------------------------------------------------------------------------
-constexpr int GB_M = 64, GB_N = 64, GB_K = 16;
+constexpr int GM_BM = 128, GM_BN = 64, GM_BK = 16, GM_ST = 3;
+constexpr int GM_SA = GM_BM + 4, GM_SB = GM_BN + 4;
+
+__device__ __forceinline__ void dmma884_l(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
+    unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+    int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cpa16(double* dst, const double* src, int valid_elems) {
+    unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+    int sz = valid_elems * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src), "r"(sz));
+}
+
+// Stage a (rows x 16) k-slab of op(A) (rows = M direction) into S[k][r].
+// contiguous: op(A) element (r, k) at P[r + k*ld] (r fast); else at P[k + r*ld].
+template <int ROWS, int SROW>
+__device__ __forceinline__ void gm_stage(double* S, const double* __restrict__ P, long long ld, bool r_fast,
+                                         bool vec_ok, long long r0, long long k0, long long R, long long K) {
+    const int tid = threadIdx.x;
+    if (r_fast && vec_ok) {
+        // 16-byte chunks along r: ROWS/2 chunks per k
+        for (int v = tid; v < GM_BK * (ROWS / 2); v += 256) {
+            const int kk = v / (ROWS / 2), rr = (v % (ROWS / 2)) * 2;
+            const long long gr = r0 + rr, gk = k0 + kk;
+            int valid = (gk < K) ? (int)max(0LL, min(2LL, R - gr)) : 0;
+            const double* src = valid ? P + gr + gk * ld : P;
+            cpa16(&S[kk * SROW + rr], src, valid);
+        }
+    } else if (r_fast) {
+        for (int v = tid; v < GM_BK * ROWS; v += 256) {
+            const int kk = v / ROWS, rr = v % ROWS;
+            const long long gr = r0 + rr, gk = k0 + kk;
+            const bool valid = gr < R && gk < K;
+            cpa8(&S[kk * SROW + rr], valid ? P + gr + gk * ld : P, valid);
+        }
+    } else {
+        // k fast in memory: consecutive threads walk k (coalesced), scatter into S[k][r]
+        for (int v = tid; v < GM_BK * ROWS; v += 256) {
+            const int kk = v % GM_BK, rr = v / GM_BK;
+            const long long gr = r0 + rr, gk = k0 + kk;
+            const bool valid = gr < R && gk < K;
+            cpa8(&S[kk * SROW + rr], valid ? P + gk + gr * ld : P, valid);
+        }
+    }
+}
 
 __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, long long N, long long K,
                                                   double alpha, const double* __restrict__ A, long long lda,
                                                   const double* __restrict__ B, long long ldb, double beta,
-                                                  double* __restrict__ C, long long ldc) {
-    __shared__ __align__(16) double As[2][GB_K][GB_M + 2];
-    __shared__ __align__(16) double Bs[2][GB_K][GB_N + 2];
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const long long i0 = (long long)blockIdx.x * GB_M, j0 = (long long)blockIdx.y * GB_N;
-    double acc[4][4];
+                                                  double* __restrict__ C, long long ldc, int vec_a, int vec_b,
+                                                  long long kchunk, double* __restrict__ part) {
+    extern __shared__ __align__(16) unsigned char gm_smem[];
+    double* As = reinterpret_cast<double*>(gm_smem);                  // [ST][BK][SA]
+    double* Bs = As + GM_ST * GM_BK * GM_SA;                          // [ST][BK][SB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;                          // 4 x 2 warps
+    const long long i0 = (long long)blockIdx.x * GM_BM, j0 = (long long)blockIdx.y * GM_BN;
+    // split-K: this CTA covers k in [kb, kb + kchunk) of op(A)/op(B); partial results go to part
+    const long long kb = (long long)blockIdx.z * kchunk;
+    if (kchunk > 0) {
+        const long long ke = min(K, kb + kchunk);
+        if (ta == 0) A += kb * lda; else A += kb;
+        if (tb == 0) B += kb; else B += kb * ldb;
+        K = ke - kb;
+    }
+    double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-
-    double ra[4], rb[4];
-    auto fetch = [&](long long k0) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            int e = tid + 256 * t;
-            int ii, kk;
-            if (!ta) { ii = e & 63; kk = e >> 6; } else { kk = e & 15; ii = e >> 4; }
-            long long gi = i0 + ii, gk = k0 + kk;
-            double v = 0.0;
-            if (gi < M && gk < K) v = ta ? A[gk + gi * lda] : A[gi + gk * lda];
-            ra[t] = v;
-            int jj, kb;
-            if (!tb) { kb = e & 15; jj = e >> 4; } else { jj = e & 63; kb = e >> 6; }
-            long long gj = j0 + jj, gkb = k0 + kb;
-            double w = 0.0;
-            if (gj < N && gkb < K) w = tb ? B[gj + gkb * ldb] : B[gkb + gj * ldb];
-            rb[t] = w;
-        }
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const long long nk = (K + GM_BK - 1) / GM_BK;
+    // op(A) (i,k): ta == 0 -> A[i + k lda] (i fast); ta == 1 -> A[k + i lda]
+    // op(B) (k,j): tb == 0 -> B[k + j ldb] (k fast); tb == 1 -> B[j + k ldb] (j fast)
+    auto stage = [&](long long kt, int st) {
+        gm_stage<GM_BM, GM_SA>(As + st * GM_BK * GM_SA, A, lda, ta == 0, vec_a, i0, kt * GM_BK, M, K);
+        gm_stage<GM_BN, GM_SB>(Bs + st * GM_BK * GM_SB, B, ldb, tb == 1, vec_b, j0, kt * GM_BK, N, K);
     };
-    auto store = [&](int st) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            int e = tid + 256 * t;
-            int ii, kk;
-            if (!ta) { ii = e & 63; kk = e >> 6; } else { kk = e & 15; ii = e >> 4; }
-            As[st][kk][ii] = ra[t];
-            int jj, kb;
-            if (!tb) { kb = e & 15; jj = e >> 4; } else { jj = e & 63; kb = e >> 6; }
-            Bs[st][kb][jj] = rb[t];
-        }
-    };
-    const long long nk = (K + GB_K - 1) / GB_K;
-    if (nk > 0) { fetch(0); store(0); }
-    __syncthreads();
+    for (int s0 = 0; s0 < GM_ST - 1; ++s0) {
+        if (s0 < nk) stage(s0, s0);
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
     for (long long kt = 0; kt < nk; ++kt) {
-        const int st = kt & 1;
-        if (kt + 1 < nk) fetch((kt + 1) * GB_K);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(GM_ST - 2));
+        __syncthreads();
+        if (kt + GM_ST - 1 < nk) stage(kt + GM_ST - 1, (int)((kt + GM_ST - 1) % GM_ST));
+        asm volatile("cp.async.commit_group;\n" ::);
+        const double* as = As + (kt % GM_ST) * GM_BK * GM_SA;
+        const double* bs = Bs + (kt % GM_ST) * GM_BK * GM_SB;
 #pragma unroll
-        for (int kk = 0; kk < GB_K; ++kk) {
-            const double2 a01 = *reinterpret_cast<const double2*>(&As[st][kk][ty * 4]);
-            const double2 a23 = *reinterpret_cast<const double2*>(&As[st][kk][ty * 4 + 2]);
-            const double2 b01 = *reinterpret_cast<const double2*>(&Bs[st][kk][tx * 4]);
-            const double2 b23 = *reinterpret_cast<const double2*>(&Bs[st][kk][tx * 4 + 2]);
-            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+        for (int k0 = 0; k0 < GM_BK; k0 += 4) {
+            double fa[4], fb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fa[i] = as[(k0 + (lane & 3)) * GM_SA + wm * 32 + 8 * i + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fb[j] = bs[(k0 + (lane & 3)) * GM_SB + wn * 32 + 8 * j + (lane >> 2)];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-        }
-        if (kt + 1 < nk) store(st ^ 1);
-        __syncthreads();
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        long long gj = j0 + tx * 4 + j;
-        if (gj >= N) continue;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            long long gi = i0 + ty * 4 + i;
-            if (gi >= M) continue;
-            double* c = C + gi + gj * ldc;
-            *c = beta == 0.0 ? alpha * acc[i][j] : alpha * acc[i][j] + beta * *c;
+                for (int j = 0; j < 4; ++j) dmma884_l(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const long long gi = i0 + wm * 32 + 8 * i + (lane >> 2);
+        if (gi >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long gj = j0 + wn * 32 + 8 * j + 2 * (lane & 3) + h;
+                if (gj >= N) continue;
+                if (part) {
+                    part[((long long)blockIdx.z * N + gj) * M + gi] = acc[i][j][h];
+                } else {
+                    double* c = C + gi + gj * ldc;
+                    *c = beta == 0.0 ? alpha * acc[i][j][h] : alpha * acc[i][j][h] + beta * *c;
+                }
+            }
+        }
+    }
+}
+
+// deterministic split-K reduction: C = alpha sum_s part_s + beta C (fixed order)
+__global__ void k_splitk_reduce(const double* __restrict__ part, int nsplit, long long M, long long N, double alpha,
+                                double beta, double* __restrict__ C, long long ldc) {
+    const long long total = M * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e % M, j = e / M;
+        double s = 0.0;
+        for (int z = 0; z < nsplit; ++z) s += part[(long long)z * total + e];
+        double* c = C + i + j * ldc;
+        *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
+    }
+}
+
+static thread_local double* g_gemm_ws = nullptr;
+static thread_local size_t g_gemm_ws_elems = 0;
+void gemm_set_workspace(double* ws, size_t elems) {
+    g_gemm_ws = ws;
+    g_gemm_ws_elems = elems;
 }
 
 int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
              const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t st) {
     if (M <= 0 || N <= 0) return 0;
-    dim3 grid((unsigned)ceil_div(M, GB_M), (unsigned)ceil_div(N, GB_N));
-    k_gemm_f64<<<grid, 256, 0, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    MPJ_LAUNCHED();
+    static bool attr = false;
+    const size_t smem = sizeof(double) * (size_t)GM_ST * GM_BK * (GM_SA + GM_SB);
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int vec_a = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
+    const int vec_b = (ldb % 2 == 0) && (((uintptr_t)B & 15) == 0);
+    dim3 grid((unsigned)ceil_div(M, GM_BM), (unsigned)ceil_div(N, GM_BN));
+    // split K when the output tiles cannot fill the GPU (skinny WY / Gram products)
+    const long long tiles = (long long)grid.x * grid.y;
+    long long nsplit = 1;
+    if (tiles < 148 && K >= 1024 && g_gemm_ws) {
+        nsplit = ceil_div(2 * 148, tiles);
+        nsplit = min(nsplit, K / 256);
+        nsplit = min(nsplit, (long long)(g_gemm_ws_elems / (size_t)(M * N)));
+        nsplit = min(nsplit, 64LL);
+    }
+    if (nsplit > 1) {
+        const long long kchunk = round_up(ceil_div(K, nsplit), GM_BK);
+        nsplit = ceil_div(K, kchunk);
+        grid.z = (unsigned)nsplit;
+        k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
+                                            kchunk, g_gemm_ws);
+        MPJ_LAUNCHED();
+        long long gr = ceil_div(M * N, 256);
+        if (gr > 4096) gr = 4096;
+        k_splitk_reduce<<<(unsigned)gr, 256, 0, st>>>(g_gemm_ws, (int)nsplit, M, N, alpha, beta, C, ldc);
+        MPJ_LAUNCHED();
+    } else {
+        k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
+                                            0, nullptr);
+        MPJ_LAUNCHED();
+    }
     MPJ_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -249,9 +354,9 @@ __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j
                              long long ldp) {
     const int c = blockIdx.y;
     const long long rows = m - j0;
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < ldp; r += (long long)gridDim.x * blockDim.x) {
         double v;
-        if (c >= kb) v = 0.0;
+        if (c >= kb || r >= rows) v = 0.0;
         else if (r == c) v = 1.0;
         else if (r < c) v = 0.0;
         else v = Vr[(j0 + r) + (long long)(j0 + c) * ldv];
@@ -262,15 +367,18 @@ __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j
 __global__ void k_larft(const double* S, int kb, const double* tau, int j0, double* T) {
     // S, T: WY_NB x WY_NB column-major (ld WY_NB); T upper triangular
     __shared__ double t[WY_NB][WY_NB + 1];
+    __shared__ double zs[WY_NB];
     const int r = threadIdx.x;
     for (int e = r; e < WY_NB * WY_NB; e += blockDim.x) t[e % WY_NB][e / WY_NB] = 0.0;
     __syncthreads();
     for (int i = 0; i < kb; ++i) {
         const double ti = tau[j0 + i];
+        if (r < i) zs[r] = S[r + i * WY_NB];
+        __syncthreads();
         double val = 0.0;
         if (r < i) {
             double s = 0.0;
-            for (int c = r; c < i; ++c) s += t[r][c] * S[c + i * WY_NB];
+            for (int c = r; c < i; ++c) s += t[r][c] * zs[c];
             val = -ti * s;
         }
         __syncthreads();
@@ -282,36 +390,70 @@ __global__ void k_larft(const double* S, int kb, const double* tau, int j0, doub
 }
 
 size_t apply_q_work_elems(long long m, long long ncols) {
-    return (size_t)m * WY_NB + 2 * WY_NB * WY_NB + 2 * (size_t)WY_NB * ncols;
+    return (size_t)round_up(m, 32) * WY_NB + 2 * WY_NB * WY_NB + 2 * (size_t)WY_NB * ncols;
+}
+
+// C <- H C with H = H_0 ... H_{kb-1} (trans = 0) or H^T (trans = 1) for ONE
+// panel of kb <= WY_NB reflectors stored below the diagonal of P (rows
+// `rows`, ld ldp; reflector i has its unit at row i).
+static int apply_panel(const double* P, long long ldp, long long rows, int kb, const double* tau, double* C,
+                       long long ldc, long long ncols, int trans, double* work, cudaStream_t st) {
+    const long long ldw = round_up(rows, 32);
+    double* Vp = work;                                  // rows x WY_NB (ld ldw)
+    double* S = Vp + (size_t)ldw * WY_NB;               // WY_NB x WY_NB
+    double* T = S + WY_NB * WY_NB;
+    double* W1 = T + WY_NB * WY_NB;                     // WY_NB x ncols
+    double* W2 = W1 + (size_t)WY_NB * ncols;
+    int gx = (int)ceil_div(rows, 256);
+    if (gx > 128) gx = 128;
+    k_make_panel<<<dim3(gx, WY_NB), 256, 0, st>>>(P, ldp, rows, 0, kb, Vp, ldw);
+    MPJ_LAUNCHED();
+    int rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldw, Vp, ldw, 0.0, S, WY_NB, st);
+    if (rc) return rc;
+    k_larft<<<1, WY_NB, 0, st>>>(S, kb, tau, 0, T);
+    MPJ_LAUNCHED();
+    rc = gemm_f64(1, 0, WY_NB, ncols, rows, 1.0, Vp, ldw, C, ldc, 0.0, W1, WY_NB, st);
+    if (rc) return rc;
+    rc = gemm_f64(trans ? 1 : 0, 0, WY_NB, ncols, WY_NB, 1.0, T, WY_NB, W1, WY_NB, 0.0, W2, WY_NB, st);
+    if (rc) return rc;
+    rc = gemm_f64(0, 0, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, WY_NB, 1.0, C, ldc, st);
+    return rc;
 }
 
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
                long long ncols, double* work, cudaStream_t st) {
-    double* Vp = work;                                  // m x WY_NB (ld m)
-    double* S = Vp + (size_t)m * WY_NB;                 // WY_NB x WY_NB
-    double* T = S + WY_NB * WY_NB;
-    double* W1 = T + WY_NB * WY_NB;                     // WY_NB x ncols
-    double* W2 = W1 + (size_t)WY_NB * ncols;
     const int npan = (k + WY_NB - 1) / WY_NB;
     for (int pnl = npan - 1; pnl >= 0; --pnl) {
         const int j0 = pnl * WY_NB;
         const int kb = k - j0 < WY_NB ? k - j0 : WY_NB;
-        const long long rows = m - j0;
-        const long long ldp = m;
-        int gx = (int)ceil_div(rows, 256);
-        if (gx > 128) gx = 128;
-        k_make_panel<<<dim3(gx, WY_NB), 256, 0, st>>>(Vr, ldv, m, j0, kb, Vp, ldp);
-        MPJ_LAUNCHED();
-        int rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldp, Vp, ldp, 0.0, S, WY_NB, st);
+        int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, C + j0, ldc, ncols, 0, work, st);
         if (rc) return rc;
-        k_larft<<<1, WY_NB, 0, st>>>(S, kb, tau, j0, T);
-        MPJ_LAUNCHED();
-        rc = gemm_f64(1, 0, WY_NB, ncols, rows, 1.0, Vp, ldp, C + j0, ldc, 0.0, W1, WY_NB, st);
+    }
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// Blocked Householder QR (LAPACK xGEQRF structure): panels of WY_NB columns
+// factored by the cooperative unblocked kernel (one CTA per column), trailing
+// matrix updated with the panel's compact-WY form Q^T = I - V T^T V^T on the
+// DMMA GEMM.  Used for the tall QR and the LQ of R
+// (QR of R^T).  Same reflectors / R as the unblocked algorithm
+// up to rounding.
+int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st) {
+    for (int j0 = 0; j0 < n; j0 += WY_NB) {
+        const int kb = n - j0 < WY_NB ? n - j0 : WY_NB;
+        double* Pn = A + j0 + (long long)j0 * lda;
+        QrWork wp = w;
+        int grid = 0;
+        int rc = qr_coop_grid(m - j0, &grid);
         if (rc) return rc;
-        rc = gemm_f64(0, 0, WY_NB, ncols, WY_NB, 1.0, T, WY_NB, W1, WY_NB, 0.0, W2, WY_NB, st);
+        wp.grid = grid < kb ? grid : kb;
+        rc = qr_coop(Pn, lda, m - j0, kb, tau + j0, 0, wp, nullptr, st);
         if (rc) return rc;
-        rc = gemm_f64(0, 0, rows, ncols, WY_NB, -1.0, Vp, ldp, W2, WY_NB, 1.0, C + j0, ldc, st);
-        if (rc) return rc;
+        if (j0 + kb < n) {
+            rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)kb * lda, lda, n - j0 - kb, 1, work, st);
+            if (rc) return rc;
+        }
     }
     MPJ_CUDA_TRY(cudaGetLastError());
     return 0;

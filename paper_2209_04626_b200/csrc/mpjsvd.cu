@@ -38,7 +38,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -283,6 +283,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_TRY(ensure(h, S_SCAL, sizeof(double) * 8));
     MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m_pad, n)));
     if (m > n) MPJ_TRY(ensure(h, S_UBIG, sizeof(double) * (size_t)m_pad * n));
+    MPJ_TRY(ensure(h, S_GEMMWS, sizeof(double) * (size_t)8 * 64 * n_pad + sizeof(double) * 64 * 64 * 64));
+    gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
 
     double* dA = P<double>(h, S_A);
     double* dA1 = P<double>(h, S_A1);
@@ -313,7 +315,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (m > n) {
         MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
         PROF_B("qr_coop_tall");
-        MPJ_TRY(qr_coop(dA, m_pad, (int)m, (int)n, P<double>(h, S_TAU_T0), 0, qw, nullptr, st));
+        MPJ_TRY(qr_blocked(dA, m_pad, (int)m, (int)n, P<double>(h, S_TAU_T0), qw, P<double>(h, S_WY), st));
         PROF_E("qr_coop_tall");
         MPJ_TRY(upper_of(dA, m_pad, dA1, n_pad, (int)n, n_pad, st));
     } else {
@@ -332,7 +334,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (o.x_from_lq) {
         MPJ_TRY(transpose_upper(dA1L, n_pad, dRt, n_pad, (int)n, n_pad, st));
         PROF_B("lq_coop");
-        MPJ_TRY(qr_coop(dRt, n_pad, (int)n, (int)n, P<double>(h, S_TAU_T), 0, qw, nullptr, st));
+        MPJ_TRY(qr_blocked(dRt, n_pad, (int)n, (int)n, P<double>(h, S_TAU_T), qw, P<double>(h, S_WY), st));
         PROF_E("lq_coop");
         MPJ_TRY(lower_from_rt(dRt, n_pad, dX, n_pad, (int)n, n_pad, st));
     } else {
@@ -651,6 +653,8 @@ int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_
 int mpjsvd_gemm_f64(mpjsvd_handle h, int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t K, double alpha,
                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (!h || !A || !B || !C) return MPJSVD_ERR_INVALID_ARG;
+    MPJ_TRY(ensure(h, S_GEMMWS, sizeof(double) * (size_t)(M > 0 ? M : 1) * (N > 0 ? N : 1) * 16));
+    gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
     int rc = gemm_f64(transa, transb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h->stream);
     if (rc) return rc;
     return cudaStreamSynchronize(h->stream) == cudaSuccess ? 0 : MPJSVD_ERR_CUDA;
@@ -688,6 +692,7 @@ int mpjsvd_block_jacobi_f32(mpjsvd_handle h, float* X, int64_t m, int64_t n, int
 int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, double* tau, int32_t* perm,
               int32_t pivot) {
     if (!h || !A || !tau || m < n || n < 1 || lda < m) return MPJSVD_ERR_INVALID_ARG;
+    gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32);
     MPJ_TRY(ensure(h, S_TMP1, sizeof(double) * (size_t)m_pad * n));
@@ -700,7 +705,15 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
     QrWork qw;
     MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
     int* phys = P<int>(h, S_IOTA);
-    MPJ_TRY(qr_coop(Aw, m_pad, (int)m, (int)n, tau, pivot ? 1 : 0, qw, phys, st));
+    if (pivot) {
+        MPJ_TRY(qr_coop(Aw, m_pad, (int)m, (int)n, tau, 1, qw, phys, st));
+    } else {
+        MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m_pad, n)));
+        MPJ_TRY(qr_blocked(Aw, m_pad, (int)m, (int)n, tau, qw, P<double>(h, S_WY), st));
+        std::vector<int> iota(n);
+        for (int i = 0; i < n; ++i) iota[i] = i;
+        MPJ_CUDA_TRY(cudaMemcpyAsync(phys, iota.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    }
     double* out = Aw;
     if (pivot) {
         MPJ_TRY(gather_cols(Aw, m_pad, phys, P<double>(h, S_TMP2), m_pad, m_pad, (int)n, st));
@@ -715,6 +728,7 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
 
 int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq) {
     if (!h || !V32 || !Q || n < 1 || ldv32 < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
+    gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long n_pad = round_up(n, 32);
     MPJ_TRY(ensure(h, S_TMP1, sizeof(float) * (size_t)n_pad * n));
@@ -743,6 +757,7 @@ int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, dou
 int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv, const double* tau, double* C,
                    int64_t ldc, int64_t ncols) {
     if (!h || !Vr || !tau || !C || k > m || ldv < m || ldc < m) return MPJSVD_ERR_INVALID_ARG;
+    gemm_set_workspace(nullptr, 0);
     MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m, ncols)));
     MPJ_TRY(apply_q_wy(Vr, m, (int)k, ldv, tau, C, ldc, ncols, P<double>(h, S_WY), h->stream));
     MPJ_CUDA_TRY(cudaStreamSynchronize(h->stream));
