@@ -282,9 +282,10 @@ def inner_solve(G, tol_in: float, max_inner: int = 30, handle: Handle | None = N
             handle.close()
 
 
-def qr(A, pivot: bool = True, handle: Handle | None = None):
-    """Step-level: (pivoted) Householder QR in place on a device fp64 tensor.
-    Returns (packed, tau, perm)."""
+def qr(A, pivot: int = 1, handle: Handle | None = None):
+    """Step-level: Householder QR on a copy of a device fp64 tensor.
+    pivot = 1: column-pivoted (lazy cooperative kernel of the path), 2: the
+    unblocked pivoted kernel, 0: blocked unpivoted QR.  Returns (packed, tau, perm)."""
     import torch
     own = handle is None
     if own:

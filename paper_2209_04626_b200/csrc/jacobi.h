@@ -57,6 +57,12 @@ struct QrWork {
 int qr_coop(double* A, long long lda, int m, int n, double* tau, int pivot, QrWork& w,
             int* phys_out, cudaStream_t st);
 int qr_coop_grid(int m, int* grid);  // cooperative grid size for this m
+// Column-pivoted QR with xLAQPS-style lazy panel updates (k_qrp.cu); same
+// outputs as qr_coop(pivot = 1).  work >= qrp_lazy_work_doubles(n, grid).
+int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, int* phys_out,
+             cudaStream_t st);
+int qrp_lazy_grid(int m, int n, int* grid, int* nown);
+size_t qrp_lazy_work_doubles(int n, int grid);
 // out[:, k] = A[:, perm[k]] for k < n (rows m_pad)
 int gather_cols(const double* A, long long lda, const int* perm, double* out, long long ldo,
                 long long rows, int n, cudaStream_t st);

@@ -129,10 +129,10 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_coop(QrArgs a) {
             double bv = -1.0;
             int bp = 0x7fffffff, bc = -1;
             for (int g = tid; g < G; g += QR_NT) {
-                int pc = a.w.cand_col[buf * G + g];
+                int pc = __ldcg(a.w.cand_col + buf * G + g);
                 if (pc < 0) continue;
-                double v = a.w.cand_val[buf * G + g];
-                int ps = a.w.cand_pos[buf * G + g];
+                double v = __ldcg(a.w.cand_val + buf * G + g);
+                int ps = __ldcg(a.w.cand_pos + buf * G + g);
                 if (v > bv || (v == bv && ps < bp)) { bv = v; bp = ps; bc = pc; }
             }
             bc = block_argmax(bv, bp, bc, red);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_coop(QrArgs a) {
                 __shared__ double s_rkp;
                 if (tid == 0) s_rkp = y[0];       // row k lives in thread 0, j = 0
                 __syncthreads();
-                double v1 = a.w.vn1[p], v2 = a.w.vn2[p];
+                double v1 = __ldcg(a.w.vn1 + p), v2 = __ldcg(a.w.vn2 + p);
                 bool recompute = false;
                 if (v1 != 0.0) {
                     double r = fabs(s_rkp) / v1;

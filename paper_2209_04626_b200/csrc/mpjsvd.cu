@@ -38,7 +38,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -325,7 +325,12 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- stage 1: column-pivoted QR  A1 P = Q_p R
     MPJ_TRY(ensure_qr_work(h, (int)n, (int)n, qw));
     PROF_B("qrp_coop");
-    MPJ_TRY(qr_coop(dA1, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), 1, qw, P<int>(h, S_PERM), st));
+    {
+        int g = 0, no = 0;
+        MPJ_TRY(qrp_lazy_grid((int)n, (int)n, &g, &no));
+        MPJ_TRY(ensure(h, S_QRPW, sizeof(double) * qrp_lazy_work_doubles((int)n, g)));
+        MPJ_TRY(qrp_lazy(dA1, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), qw, P<double>(h, S_QRPW), P<int>(h, S_PERM), st));
+    }
     PROF_E("qrp_coop");
     MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
     MPJ_TRY(diag_stats(dA1L, n_pad, (int)n, scal + 1, flags + 1, st));
@@ -705,8 +710,13 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
     QrWork qw;
     MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
     int* phys = P<int>(h, S_IOTA);
-    if (pivot) {
+    if (pivot == 2) {                 // unblocked reference kernel (tests)
         MPJ_TRY(qr_coop(Aw, m_pad, (int)m, (int)n, tau, 1, qw, phys, st));
+    } else if (pivot) {
+        int g = 0, no = 0;
+        MPJ_TRY(qrp_lazy_grid((int)m, (int)n, &g, &no));
+        MPJ_TRY(ensure(h, S_QRPW, sizeof(double) * qrp_lazy_work_doubles((int)n, g)));
+        MPJ_TRY(qrp_lazy(Aw, m_pad, (int)m, (int)n, tau, qw, P<double>(h, S_QRPW), phys, st));
     } else {
         MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m_pad, n)));
         MPJ_TRY(qr_blocked(Aw, m_pad, (int)m, (int)n, tau, qw, P<double>(h, S_WY), st));

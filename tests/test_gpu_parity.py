@@ -124,8 +124,11 @@ def test_block_jacobi_f32_vs_oracle(mp, n, b):
     assert orth(V) < 1e-4
 
 
-@pytest.mark.parametrize("m,n,pivot", [(300, 300, True), (257, 100, True), (1000, 77, False), (64, 64, False)])
+@pytest.mark.parametrize("m,n,pivot", [(300, 300, 1), (257, 100, 1), (1000, 77, 0), (64, 64, 0), (300, 300, 2),
+                                       (700, 700, 1), (2100, 700, 0)])
 def test_qr_vs_oracle(mp, m, n, pivot):
+    """pivot 1: lazy (xLAQPS-style) cooperative QRP used by the path;
+    pivot 2: the unblocked cooperative kernel; pivot 0: blocked Householder QR."""
     rng = np.random.default_rng(m + n)
     a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
     packed, tau, perm = mp.qr(dev(a), pivot=pivot)
@@ -140,6 +143,28 @@ def test_qr_vs_oracle(mp, m, n, pivot):
     assert np.abs(r - r_o).max() <= 1e-12 * np.abs(r_o).max()
     assert np.abs(tau - tau_o).max() <= 1e-12
     q = oracle.form_q(packed, tau, n)
+    assert orth(q) < 1e-13
+    assert np.abs(q @ r - a[:, perm]).max() <= 1e-13 * np.abs(a).max()
+
+
+def test_qrp_recompute_path(mp):
+    """Strongly decaying partial norms (sigma 1 -> 1e-14) force the partial-norm
+    recomputation (xLAQP2 rule) on many columns: pivots and R must still match."""
+    n = 400
+    a = np.asfortranarray((testmat.haar(n, n, 11) * testmat.geom(n, 1e-14)) @ testmat.haar(n, n, 12).T)
+    packed, tau, perm = mp.qr(dev(a), pivot=1)
+    packed, tau, perm = host(packed), host(tau), host(perm)
+    p_o, perm_o, tau_o, _ = oracle.qrp(a)
+    r, r_o = np.triu(packed), np.triu(p_o)
+    d, d_o = np.diag(r), np.diag(r_o)
+    # QR is normwise backward stable: R_kk agree to ~u ||A|| absolutely; pivots are
+    # identical while the diagonal is well above that level
+    assert np.abs(d - d_o).max() <= 64 * n * U64 * d_o[0]
+    ok = d_o > 1e-8 * d_o[0]
+    kmax = int(np.argmin(ok)) if not ok.all() else n
+    assert kmax > 100
+    assert np.array_equal(perm[:kmax], perm_o[:kmax])
+    q = oracle.form_q(packed, tau)
     assert orth(q) < 1e-13
     assert np.abs(q @ r - a[:, perm]).max() <= 1e-13 * np.abs(a).max()
 
