@@ -38,6 +38,8 @@ struct ProfHook {
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook = nullptr);
 template <typename T>
+int gram_ctas_per_sm(int W);
+template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
 
 // ---- QR (k_qr.cu) --------------------------------------------------------

@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(64) k_pair_update(JacobiRound<T> a) {
 }
 
 
+
 // ========================================================================
 // FP64 tensor-pipe (DMMA) versions: mma.sync.aligned.m8n8k4.row.col.f64.
 // B200 has no tcgen05 kind::f64; DMMA runs on the FP64 pipe (measured 36.9
@@ -601,6 +602,123 @@ __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
     }
 }
 static size_t gram_dmma_smem(int W) { return sizeof(double) * (size_t)GRAM_STAGES * W * GRAM_S + sizeof(long long) * W; }
+
+// ------------------------------------------------------------------------
+// k_pair_gram_f32t: fp32 Gram (W = 64) on the FFMA pipe, symmetric at 16 x 16
+// block granularity.  The lower triangle of the 4 x 4 grid of 16 x 16 blocks
+// (6 off-diagonal + 4 diagonal blocks) is cut into 40 uniform 8 x 8 tiles
+// (90 % of the products are needed, no lane divergence: every thread runs the
+// same 8 x 8 outer product on its own columns).  Grid (nsplit, npairs), 160
+// threads = 4 row groups x 40 tiles; the CTA's row slab streams through a
+// 3-stage cp.async pipeline of 32-row k-tiles and row group g takes the
+// 4-row chunks 2g, 2g+1 of every k-tile (float4 fragments).  The row groups'
+// partial tiles are summed in shared memory; the lower triangle is written.
+// Shared layout: 16-byte chunk (column c, rows 4rc..4rc+3) at chunk index
+// 8c + (rc ^ (c >> 3)): the column groups of one LDS.128 hit distinct banks.
+// ------------------------------------------------------------------------
+constexpr int G32_KT = 32, G32_ST = 6, G32_NT = 160;
+
+__device__ __forceinline__ int g32_chunk(int c, int rc) { return 8 * c + (rc ^ ((c >> 3) & 7)); }
+
+__global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float> a) {
+    constexpr int W = 64;
+    extern __shared__ __align__(16) unsigned char g32_smem[];
+    float4* Ws = reinterpret_cast<float4*>(g32_smem);            // [ST][W*8] chunks
+    float* red = reinterpret_cast<float*>(g32_smem);               // [W*W] partial sums (aliases the stages)
+    __shared__ long long colofs[W];
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x;
+    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
+    const int w = pc.wI + pc.wJ;
+    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * a.ldx : -1;
+    __syncthreads();
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg) / G32_KT);
+    // tile of this thread: 16x16 block (BI >= BJ), 8x8 sub-tile (sa, sb)
+    const int tile = tid % 40, rg = tid / 40;
+    int BI, BJ, sa, sb;
+    if (tile < 24) {                                   // off-diagonal blocks (1,0),(2,0),(2,1),(3,0),(3,1),(3,2)
+        const int blk = tile >> 2;
+        BI = blk < 1 ? 1 : (blk < 3 ? 2 : 3);
+        BJ = blk - (BI * (BI - 1)) / 2;
+        sa = (tile >> 1) & 1; sb = tile & 1;
+    } else {                                           // diagonal blocks, full squares
+        const int t2 = tile - 24;
+        BI = BJ = t2 >> 2;
+        sa = (t2 >> 1) & 1; sb = t2 & 1;
+    }
+    const int ca = 16 * BI + 8 * sa, cb = 16 * BJ + 8 * sb;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    auto load_tile = [&](int t, int st) {
+        const long long r0 = rbeg + (long long)t * G32_KT;
+        float4* dst = Ws + st * W * 8;
+        for (int v = tid; v < W * 8; v += G32_NT) {
+            const int c = v >> 3, rc = v & 7;
+            float4* d = dst + g32_chunk(c, rc);
+            if (colofs[c] >= 0) cp_async16(d, a.X + colofs[c] + r0 + rc * 4);
+            else *d = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < G32_ST - 1; ++s0) {
+        if (s0 < ntile) load_tile(s0, s0);
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+        cp_async_wait<G32_ST - 2>();
+        __syncthreads();
+        if (t + G32_ST - 1 < ntile) load_tile(t + G32_ST - 1, (t + G32_ST - 1) % G32_ST);
+        cp_async_commit();
+        const float4* ws = Ws + (t % G32_ST) * W * 8;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rc = 2 * rg + h;
+            const float4* wa = ws + 8 * ca + (rc ^ (ca >> 3));
+            const float4* wb = ws + 8 * cb + (rc ^ (cb >> 3));
+            float4 fa[8], fb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                fa[u] = wa[8 * u];
+                fb[u] = wb[8 * u];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    acc[i][j] = fmaf(fa[i].x, fb[j].x, acc[i][j]);
+                    acc[i][j] = fmaf(fa[i].y, fb[j].y, acc[i][j]);
+                    acc[i][j] = fmaf(fa[i].z, fb[j].z, acc[i][j]);
+                    acc[i][j] = fmaf(fa[i].w, fb[j].w, acc[i][j]);
+                }
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();                                   // staging buffers become the reduction buffer
+    // ---- sum the four row groups' partial tiles (fixed order) and write the lower triangle
+    for (int g = 0; g < 4; ++g) {
+        __syncthreads();
+        if (rg == g) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float* d = &red[(ca + i) * W + cb + j];
+                    *d = g == 0 ? acc[i][j] : *d + acc[i][j];
+                }
+        }
+    }
+    __syncthreads();
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (W * W);
+    for (int e = tid; e < W * W; e += G32_NT) {
+        const int p = e / W, q = e % W;
+        if (p >= q) out[e] = red[e];
+    }
+}
 
 // ------------------------------------------------------------------------
 // k_pair_update_dmma: grid (row chunks of 128, npairs, 2 [X, V]), 256
@@ -811,6 +929,14 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
             attr_g = true;
         }
         k_pair_gram_dmma<W><<<dim3(a.nsplit, a.npairs), 128, gram_dmma_smem(W), st>>>(a);
+    } else if constexpr (W == 64) {
+        const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
+        static bool attr_t = false;
+        if (!attr_t) {
+            cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
+            attr_t = true;
+        }
+        k_pair_gram_f32t<<<dim3(a.nsplit, a.npairs), G32_NT, g32, st>>>(a);
     } else {
         k_pair_gram<T, W><<<dim3(a.nsplit, a.npairs), 64, 0, st>>>(a);
     }
@@ -862,6 +988,39 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
     }
     return 0;
 }
+
+// resident CTAs per SM of the Gram kernel used for (T, W) (for the split choice)
+template <typename T>
+int gram_ctas_per_sm(int W) {
+    int per = 1;
+    if constexpr (sizeof(T) == 8) {
+        const size_t smem = gram_dmma_smem(W);
+        if (W == 64) {
+            cudaFuncSetAttribute(k_pair_gram_dmma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_dmma<64>, 128, smem);
+        } else if (W == 32) {
+            cudaFuncSetAttribute(k_pair_gram_dmma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_dmma<32>, 128, smem);
+        } else {
+            cudaFuncSetAttribute(k_pair_gram_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_dmma<16>, 128, smem);
+        }
+    } else {
+        if (W == 64) {
+            const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
+            cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_f32t, G32_NT, g32);
+        } else if (W == 32) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram<float, 32>, 64, 0);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram<float, 16>, 64, 0);
+        }
+    }
+    cudaGetLastError();
+    return per < 1 ? 1 : per;
+}
+template int gram_ctas_per_sm<float>(int);
+template int gram_ctas_per_sm<double>(int);
 
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook) {

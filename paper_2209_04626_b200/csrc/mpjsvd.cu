@@ -7,6 +7,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <new>
 #include <string>
@@ -152,10 +153,18 @@ int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int 
     const int npairs = M / 2;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
-    long long target = (long long)dev_sms * 6;
-    long long nsplit = ceil_div(target, npairs);
-    if (nsplit < 1) nsplit = 1;
-    if (nsplit > m_pad / 32) nsplit = m_pad / 32;
+    // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
+    // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
+    const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W);
+    const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
+    long long nsplit = 1;
+    double best = 1e30;
+    for (long long ns = 1; ns <= maxsplit; ++ns) {
+        const long long rps_ = round_up(ceil_div(m_pad, ns), 32);
+        const long long ns_eff = ceil_div(m_pad, rps_);
+        const double cost = (double)ceil_div(npairs * ns_eff, slots) * (rps_ + 96) + 16.0 * ns_eff;
+        if (cost < best - 1e-9) { best = cost; nsplit = ns_eff; }
+    }
     long long rps = round_up(ceil_div(m_pad, nsplit), 32);
     nsplit = ceil_div(m_pad, rps);
     MPJ_TRY(ensure(h, S_PART, sizeof(T) * (size_t)npairs * nsplit * W * W));
