@@ -9,10 +9,13 @@ refinement, assembly) of BASELINE.json's config on inputs resident in HBM.
 Metric (BASELINE.json): "fp64 SVD time at n=4096 and 8192 (1/2/4/8 B200);
 sweep HBM GB/s vs peak" -> value = seconds per SVD (lower is better).
 
-Rank 0 prints ONE JSON line.  Multi-GPU (torchrun, N > 1): every rank runs
-its own replica SVD of the config on its GPU (the column-block sharded
-solver is not in this build), the timed region is
-bracketed by barrier + synchronize and the max over ranks is reported.
+Rank 0 prints ONE JSON line.  Multi-GPU (torchrun, N > 1): one SVD of the
+config per step, sharded over the N GPUs: rank 0 holds A and
+the outputs and runs preconditioning / lift / assembly, both Jacobi stages
+run column-block sharded with the per-round block exchange over NCCL
+(ncclSend/ncclRecv inside libmpjsvd.so).  Total work is fixed as N grows
+("scaling": "strong"); the timed region is bracketed by barrier +
+synchronize and the max over ranks is reported.
 """
 from __future__ import annotations
 
@@ -201,7 +204,7 @@ def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks:
             "traffic": None, "launches": launches}
 
 
-def algorithmic_work(stats_list, n: int, b: int):
+def algorithmic_work(stats_list, n: int, b: int, world: int = 1):
     """Algorithmic flops/bytes of the Jacobi kernels summed over the timed steps
     (DESIGN.md sec. 8).  Gram of a pair (w = 2b columns, n rows): the
     symmetric half incl. the diagonal, n w (w+1) flops, reading W once
@@ -209,7 +212,7 @@ def algorithmic_work(stats_list, n: int, b: int):
     and again for V per updated pair, bytes 2 x (read + write of n x w) x s."""
     flops, byts = {}, {}
     nblk = -(-n // b)
-    M = nblk + (nblk & 1)
+    M = nblk + (nblk & 1) if world == 1 else -(-nblk // (2 * world)) * (2 * world)
     npairs = M // 2
     rounds = M - 1
     for st in stats_list:
@@ -223,7 +226,8 @@ def algorithmic_work(stats_list, n: int, b: int):
             byts[g] = byts.get(g, 0.0) + sweeps * rounds * float(n) * n * s
             flops[u] = flops.get(u, 0.0) + upd * 16.0 * n * b * b
             byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * 2.0 * n * 2 * b * s
-    return {"flops": flops, "bytes": byts}
+    # per rank: the sharded engine spreads the pairs of every round over the ranks
+    return {"flops": {k: v / world for k, v in flops.items()}, "bytes": {k: v / world for k, v in byts.items()}}
 
 
 def main():
@@ -242,6 +246,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    root = rank == 0
 
     def barrier():
         if world > 1:
@@ -255,14 +260,19 @@ def main():
         return float(t.item())
 
     m, n, _ = testmat.CONFIGS[args.config]
-    a = testmat.cached_config(args.config)
-    A = torch.from_numpy(np.ascontiguousarray(a.T)).t().cuda()     # column-major, resident in HBM
+    device = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     h = mp.Handle(stream=stream.cuda_stream, block_cols=args.block_cols)
-    U = mp.empty_col_major(m, n, torch.float64, A.device)
-    V = mp.empty_col_major(n, n, torch.float64, A.device)
-    S = torch.empty(n, dtype=torch.float64, device=A.device)
-    l2_flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=A.device)
+    if world > 1:
+        h.comm_init_torch()          # NCCL communicator inside libmpjsvd.so (rank 0's id via torch.distributed)
+    a = A = U = V = S = None
+    if root:
+        a = testmat.cached_config(args.config)
+        A = torch.from_numpy(np.ascontiguousarray(a.T)).t().to(device)   # column-major, resident in HBM
+        U = mp.empty_col_major(m, n, torch.float64, device)
+        V = mp.empty_col_major(n, n, torch.float64, device)
+        S = torch.empty(n, dtype=torch.float64, device=device)
+    l2_flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
 
     def step():
         rc, st = mp.mpjsvd_factor(h, A, U, S, V, m, n, m, m, n)
@@ -296,23 +306,28 @@ def main():
     launches = int(sum(s["kernel_launches"] for s in stats))
 
     # ---------------- result check (plumbing: torch on the device)
-    Ud, Sd, Vd = U, S, V
-    eye = torch.eye(n, dtype=torch.float64, device=A.device)
-    orth_u = float((Ud.T @ Ud - eye).abs().max())
-    orth_v = float((Vd.T @ Vd - eye).abs().max())
-    res = float(torch.linalg.norm(A - (Ud * Sd) @ Vd.T) / torch.linalg.norm(A))
+    orth_u = orth_v = res = None
+    if root:
+        eye = torch.eye(n, dtype=torch.float64, device=device)
+        orth_u = float((U.T @ U - eye).abs().max())
+        orth_v = float((V.T @ V - eye).abs().max())
+        res = float(torch.linalg.norm(A - (U * S) @ V.T) / torch.linalg.norm(A))
+        del eye
 
     # ---------------- e2e: host buffers through the same C-ABI call
     e2e = None
     if not args.no_e2e:
-        Ah = torch.from_numpy(np.ascontiguousarray(a.T)).t().pin_memory()
-        Uh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
-        Vh = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
-        Sh = torch.empty(n, dtype=torch.float64).pin_memory()
+        Ah = Uh = Vh = Sh = None
+        if root:
+            Ah = torch.from_numpy(np.ascontiguousarray(a.T)).t().pin_memory()
+            Uh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+            Vh = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
+            Sh = torch.empty(n, dtype=torch.float64).pin_memory()
         e2e_ms = []
         for i in range(max(1, args.steps)):
             l2_flush.zero_()
             torch.cuda.synchronize()
+            barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             rc, _ = mp.mpjsvd_factor(h, Ah, Uh, Sh, Vh, m, n, m, m, n)
@@ -327,7 +342,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel
     peaks = load_peaks()
-    work = algorithmic_work(stats, n, args.block_cols)
+    work = algorithmic_work(stats, n, args.block_cols, world)
     try:
         work["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
@@ -355,10 +370,11 @@ def main():
     out = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic",
         "config": {"workload": args.config, "m": m, "n": n, "block_cols": args.block_cols,
-                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "parallelism": f"column-block sharded x{world} (NCCL block exchange)" if world > 1
+                   else "single-gpu",
                    "l2": "inputs (A 8n^2 B) and working set > L2; 512 MiB L2 flush between timed steps",
                    "recipe": testmat.CONFIGS[args.config][2]},
         "roofline": roof,

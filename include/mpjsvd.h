@@ -47,7 +47,8 @@
 extern "C" {
 #endif
 
-#define MPJSVD_VERSION 100
+#define MPJSVD_VERSION 110
+#define MPJSVD_COMM_ID_BYTES 128
 
 /* return codes */
 #define MPJSVD_OK 0
@@ -56,9 +57,9 @@ extern "C" {
 #define MPJSVD_ERR_NONFINITE (-2)     /* A contains NaN or Inf */
 #define MPJSVD_ERR_RANK_DEFICIENT (-3)/* zero R diagonal / zero column / singular V^T V */
 #define MPJSVD_ERR_CUDA (-4)          /* CUDA runtime error (see mpjsvd_last_cuda_error) */
-#define MPJSVD_ERR_NCCL (-5)
+#define MPJSVD_ERR_NCCL (-5)          /* NCCL missing or failed (see mpjsvd_last_cuda_error) */
 #define MPJSVD_ERR_OUT_OF_MEMORY (-6)
-#define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1 in this build, block_cols unsupported */
+#define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1, block_cols unsupported, n > 16384 */
 
 /* path (Alg. 3 gates; reading c-15) */
 #define MPJSVD_PATH_FORCE_MIXED 0     /* always run the fp32 Jacobi stage (default) */
@@ -68,7 +69,7 @@ extern "C" {
 typedef struct mpjsvd_handle_s* mpjsvd_handle;
 
 typedef struct {
-    int32_t num_gpus;          /* 1 in this build */
+    int32_t num_gpus;          /* must be 1: one handle per process/GPU; multi-GPU via mpjsvd_comm_init */
     int32_t device_id;         /* CUDA device ordinal (default: current device) */
     int32_t block_cols;        /* b, columns per Jacobi block: 8, 16 or 32 (default 32) */
     double tol_mult32;         /* eps_tol32 = tol_mult32 * sqrt(n) * 2^-24 (default 4) */
@@ -81,6 +82,12 @@ typedef struct {
     int32_t x_from_lq;         /* 1 (default): X = L; 0: X = R (ablation) */
     int32_t compute_gates;     /* 1 (default): report orth / tail / cond measures */
     void* stream;              /* cudaStream_t on device_id, or NULL */
+    int32_t virtual_shards;    /* G >= 1 (default 1): run the sharded Jacobi engine with G shards
+                                  emulated on this one GPU -- shard buffers, per-round block
+                                  exchange as device copies, one kernel over all shards' pairs
+                                  (the multi-GPU data path, testable on one device) */
+    int32_t split_rows;        /* > 0: rows per Gram row-split (fixes the fp summation order across
+                                  shard counts); 0 (default): chosen per launch for SM fill */
 } mpjsvd_options;
 
 typedef struct {
@@ -119,6 +126,50 @@ const char* mpjsvd_strerror(int code);
 const char* mpjsvd_last_cuda_error(void);
 
 int mpjsvd_version(void);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: one process per GPU,
+ * each with its own handle.  Rank 0 calls mpjsvd_comm_unique_id and hands
+ * the MPJSVD_COMM_ID_BYTES bytes to every rank (e.g. a torch.distributed
+ * broadcast); every rank then calls mpjsvd_comm_init with its rank and the
+ * world size (this creates the handle's NCCL communicator; NCCL is loaded
+ * with dlopen, MPJSVD_ERR_NCCL if unavailable).  Afterwards every rank calls
+ * mpjsvd_factor with the same m and n (checked: MPJSVD_ERR_INVALID_ARG on all
+ * ranks otherwise): rank 0 passes A, U, S, V; the others may pass NULL for
+ * all four (their ld arguments are ignored).  Preconditioning, lift and
+ * assembly run on rank 0; both Jacobi stages run sharded: rank g holds the
+ * column blocks of k = M/(2G) pairs and exchanges <= 2 blocks with its
+ * neighbours after every round (ncclSend/ncclRecv), with one max/sum
+ * all-reduce of the convergence counters per sweep.  The block count M is
+ * padded to a multiple of 2G with empty blocks.  Outputs are written on
+ * rank 0 only; the sweep statistics on every rank.  Collective: every rank
+ * must make the same sequence of calls.
+ * ------------------------------------------------------------------------ */
+int mpjsvd_comm_unique_id(uint8_t* id /* MPJSVD_COMM_ID_BYTES */);
+int mpjsvd_comm_init(mpjsvd_handle h, int32_t rank, int32_t world, const uint8_t* id);
+/* rank / world size of the handle (0 / 1 without a communicator) */
+int mpjsvd_comm_info(mpjsvd_handle h, int32_t* rank, int32_t* world);
+
+/* The shard plan (host only, no GPU needed): the schedule and the block
+ * exchanges the sharded engine performs, exported so that tests can drive
+ * the same exchange logic over another transport.  nblk column blocks over
+ * `world` ranks (world = 1: the single-GPU layout, buffer j = block j).
+ *   plan_info:    M positions (padded), k pairs per rank, nbuf buffers per rank
+ *   plan_pairs:   out[4t..4t+3] = (buf0, buf1, blk0, blk1) of rank's local
+ *                 pair t in the current round (blk0 < blk1; blk >= nblk is
+ *                 an empty bye block); returns k
+ *   plan_advance: apply one round's shift; writes up to cap inter-rank moves
+ *                 (blk, src_rank, src_buf, dst_rank, dst_buf), 5 int32 each,
+ *                 in the canonical order every rank posts them; returns the
+ *                 move count
+ *   plan_locate:  current (rank, buffer) of block blk                     */
+typedef struct mpjsvd_plan_s* mpjsvd_plan;
+int mpjsvd_plan_create(mpjsvd_plan* plan, int32_t nblk, int32_t world);
+int mpjsvd_plan_info(mpjsvd_plan plan, int32_t* M, int32_t* k, int32_t* nbuf);
+int mpjsvd_plan_pairs(mpjsvd_plan plan, int32_t rank, int32_t* out);
+int mpjsvd_plan_advance(mpjsvd_plan plan, int32_t* moves, int32_t cap);
+int mpjsvd_plan_locate(mpjsvd_plan plan, int32_t blk, int32_t* rank, int32_t* buf);
+int mpjsvd_plan_destroy(mpjsvd_plan plan);
 
 /* Per-kernel timing for benchmarking.  mpjsvd_set_profiling(h, 1) clears the
    accumulators and brackets every subsequent kernel launch of the Jacobi

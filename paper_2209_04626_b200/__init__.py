@@ -37,7 +37,7 @@ class Options(C.Structure):
                 ("tol_mult32", C.c_double), ("tol_mult64", C.c_double), ("inner_tol_div", C.c_int32),
                 ("max_sweeps32", C.c_int32), ("max_sweeps64", C.c_int32), ("max_inner", C.c_int32),
                 ("path", C.c_int32), ("x_from_lq", C.c_int32), ("compute_gates", C.c_int32),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("virtual_shards", C.c_int32), ("split_rows", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -73,8 +73,11 @@ EXPORTS = [
     "mpjsvd_default_options", "mpjsvd_create", "mpjsvd_factor", "mpjsvd_destroy", "mpjsvd_strerror",
     "mpjsvd_last_cuda_error", "mpjsvd_version", "mpjsvd_block_jacobi_f64", "mpjsvd_block_jacobi_f32",
     "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
-    "mpjsvd_set_profiling", "mpjsvd_get_profile",
+    "mpjsvd_set_profiling", "mpjsvd_get_profile", "mpjsvd_comm_unique_id", "mpjsvd_comm_init",
+    "mpjsvd_comm_info", "mpjsvd_plan_create", "mpjsvd_plan_info", "mpjsvd_plan_pairs", "mpjsvd_plan_advance",
+    "mpjsvd_plan_locate", "mpjsvd_plan_destroy",
 ]
+COMM_ID_BYTES = 128
 
 
 def lib():
@@ -106,6 +109,15 @@ def lib():
         L.mpjsvd_gemm_f64.argtypes = [vp, i32, i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]
         L.mpjsvd_set_profiling.argtypes = [vp, i32]
         L.mpjsvd_get_profile.argtypes = [vp, i32, C.c_char_p, i32, C.POINTER(dbl), C.POINTER(i64)]
+        L.mpjsvd_comm_unique_id.argtypes = [vp]
+        L.mpjsvd_comm_init.argtypes = [vp, i32, i32, vp]
+        L.mpjsvd_comm_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+        L.mpjsvd_plan_create.argtypes = [C.POINTER(vp), i32, i32]
+        L.mpjsvd_plan_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+        L.mpjsvd_plan_pairs.argtypes = [vp, i32, vp]
+        L.mpjsvd_plan_advance.argtypes = [vp, vp, i32]
+        L.mpjsvd_plan_locate.argtypes = [vp, i32, C.POINTER(i32), C.POINTER(i32)]
+        L.mpjsvd_plan_destroy.argtypes = [vp]
         _lib = L
         return L
 
@@ -158,6 +170,28 @@ class Handle:
     def ptr(self):
         return self._h
 
+    def comm_init(self, rank: int, world: int, uid: bytes):
+        """Attach an NCCL communicator (multi-GPU, one process per GPU).  uid
+        is comm_unique_id() of rank 0, distributed by the caller."""
+        if len(uid) != COMM_ID_BYTES:
+            raise ValueError("unique id must be 128 bytes")
+        buf = C.create_string_buffer(uid, COMM_ID_BYTES)
+        _check(lib().mpjsvd_comm_init(self._h, rank, world, buf), "mpjsvd_comm_init")
+
+    def comm_info(self):
+        r, w = C.c_int32(), C.c_int32()
+        _check(lib().mpjsvd_comm_info(self._h, C.byref(r), C.byref(w)))
+        return r.value, w.value
+
+    def comm_init_torch(self, group=None):
+        """comm_init over an initialised torch.distributed group (rank 0's
+        NCCL unique id is broadcast with broadcast_object_list)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.comm_init(rank, world, obj[0])
+
     def set_profiling(self, on: bool = True):
         _check(lib().mpjsvd_set_profiling(self._h, int(on)), "mpjsvd_set_profiling")
 
@@ -173,6 +207,54 @@ class Handle:
             L.mpjsvd_get_profile(self._h, i, buf, 64, C.byref(ms), C.byref(cnt))
             out[buf.value.decode()] = (ms.value, cnt.value)
         return out
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id (rank 0) for Handle.comm_init."""
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    _check(lib().mpjsvd_comm_unique_id(buf), "mpjsvd_comm_unique_id")
+    return buf.raw
+
+
+class ShardPlan:
+    """The library's host-side shard plan (include/mpjsvd.h mpjsvd_plan_*):
+    the round-robin schedule over `world` ranks and the block moves of every
+    round.  Host only (no GPU)."""
+
+    def __init__(self, nblk: int, world: int):
+        self._p = C.c_void_p()
+        _check(lib().mpjsvd_plan_create(C.byref(self._p), nblk, world), "mpjsvd_plan_create")
+        M, k, nb = C.c_int32(), C.c_int32(), C.c_int32()
+        lib().mpjsvd_plan_info(self._p, C.byref(M), C.byref(k), C.byref(nb))
+        self.nblk, self.world, self.M, self.k, self.nbuf = nblk, world, M.value, k.value, nb.value
+
+    def pairs(self, rank: int):
+        """[(buf0, buf1, blk0, blk1)] of the rank's k local pairs this round."""
+        out = (C.c_int32 * (4 * self.k))()
+        _check(lib().mpjsvd_plan_pairs(self._p, rank, out), "mpjsvd_plan_pairs")
+        return [tuple(out[4 * t:4 * t + 4]) for t in range(self.k)]
+
+    def advance(self):
+        """Apply one round's shift; [(blk, src_rank, src_buf, dst_rank, dst_buf)]."""
+        cap = 4 * self.world + 8
+        out = (C.c_int32 * (5 * cap))()
+        cnt = lib().mpjsvd_plan_advance(self._p, out, cap)
+        _check(cnt, "mpjsvd_plan_advance")
+        assert cnt <= cap
+        return [tuple(out[5 * i:5 * i + 5]) for i in range(cnt)]
+
+    def locate(self, blk: int):
+        r, b = C.c_int32(), C.c_int32()
+        _check(lib().mpjsvd_plan_locate(self._p, blk, C.byref(r), C.byref(b)), "mpjsvd_plan_locate")
+        return r.value, b.value
+
+    def __del__(self):
+        try:
+            if self._p:
+                lib().mpjsvd_plan_destroy(self._p)
+                self._p = C.c_void_p()
+        except Exception:
+            pass
 
 
 def _col_major(t):
@@ -193,11 +275,15 @@ def empty_col_major(rows: int, cols: int, dtype, device):
     return torch.empty((cols, rows), dtype=dtype, device=device).t()
 
 
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p()
+
+
 def mpjsvd_factor(handle: Handle, A, U, S, V, m: int, n: int, lda: int, ldu: int, ldv: int):
-    """Raw C-ABI call on pointers (device tensors or host tensors).  Returns (rc, stats)."""
+    """Raw C-ABI call on pointers (device tensors or host tensors; None for
+    the non-root ranks of a multi-GPU handle).  Returns (rc, stats)."""
     st = Stats()
-    rc = lib().mpjsvd_factor(handle.ptr, C.c_void_p(A.data_ptr()), m, n, lda, C.c_void_p(U.data_ptr()), ldu,
-                             C.c_void_p(S.data_ptr()), C.c_void_p(V.data_ptr()), ldv, C.byref(st))
+    rc = lib().mpjsvd_factor(handle.ptr, _ptr(A), m, n, lda, _ptr(U), ldu, _ptr(S), _ptr(V), ldv, C.byref(st))
     return rc, st
 
 

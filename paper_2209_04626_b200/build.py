@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libmpjsvd.so")
-SOURCES = ["mpjsvd.cu", "k_jacobi.cu", "k_qr.cu", "k_qrp.cu", "k_linalg.cu", "k_misc.cu"]
-HEADERS = ["common.cuh", "jacobi.h"]
+SOURCES = ["mpjsvd.cu", "k_jacobi.cu", "k_qr.cu", "k_qrp.cu", "k_linalg.cu", "k_misc.cu", "comm.cpp"]
+HEADERS = ["common.cuh", "jacobi.h", "shard.h", "comm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         cmd = [NVCC] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc build of libmpjsvd.so failed")
     tmp = SO + f".{os.getpid()}.tmp"
-    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"])
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-ldl"])
     os.replace(tmp, SO)
     return SO
 

@@ -6,17 +6,33 @@
 
 namespace mpj {
 
+// One block pair (I, J), I < J (block ids), of a Jacobi round: base pointers
+// of the two column slabs of X (rows m_pad, ld ldx) and V (rows nv_pad, ld
+// ldv) and their widths (0 for a bye block).  Pair-local column c is column c
+// of slab 0 for c < w0, else column c - w0 of slab 1 (W = [X_I X_J]).  The
+// slabs may live anywhere (the matrix itself on one GPU, shard buffers on
+// many: DESIGN.md "Multi-GPU").
+template <typename T>
+struct PairDesc {
+    T* x0;
+    T* x1;
+    T* v0;
+    T* v1;
+    int w0, w1;
+    int pad_[2];
+};
+
 // Arguments of one block round-robin Jacobi round (k_jacobi.cu).
 template <typename T>
 struct JacobiRound {
-    T* X;               // m_pad x n, column-major, rows >= m zero
+    const PairDesc<T>* pd;   // device: npairs descriptors of this round
     long long ldx;
     long long m_pad;    // multiple of 32
     int n;
-    T* V;               // nv_pad x n or nullptr
+    bool has_v;         // V slabs present
     long long ldv;
     long long nv_pad;   // multiple of 32
-    int b, nblk, M, round, npairs;
+    int b, npairs;
     int nsplit;
     long long rows_per_split;   // multiple of 32
     T* partial;         // npairs * nsplit * W * W

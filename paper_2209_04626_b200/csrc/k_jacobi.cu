@@ -26,23 +26,10 @@ template <> struct RealTraits<double> {
     static constexpr double rsqrt_u = 94906265.62425156;   // 1/sqrt(2^-53)
 };
 
-struct PairCols {
-    int I, J, wI, wJ;
-};
-
-__device__ __forceinline__ PairCols pair_cols(int r, int i, int M, int nblk, int b, int n) {
-    int a = rr_slot(r, i, M), c = rr_slot(r, M - 1 - i, M);
-    PairCols pc;
-    pc.I = min(a, c);
-    pc.J = max(a, c);
-    pc.wI = pc.I < nblk ? min(b, n - pc.I * b) : 0;
-    pc.wJ = pc.J < nblk ? min(b, n - pc.J * b) : 0;
-    return pc;
-}
-
-// global column of pair-local column c (c < wI + wJ)
-__device__ __forceinline__ int pair_gcol(const PairCols& pc, int c, int b) {
-    return c < pc.wI ? pc.I * b + c : pc.J * b + (c - pc.wI);
+// pointer to pair-local column c (c < w0 + w1) of X (v = false) or V (v = true)
+template <typename T>
+__device__ __forceinline__ T* pair_col(const PairDesc<T>& d, int c, bool v, long long ld) {
+    return c < d.w0 ? (v ? d.v0 : d.x0) + (long long)c * ld : (v ? d.v1 : d.x1) + (long long)(c - d.w0) * ld;
 }
 
 // ------------------------------------------------------------------------
@@ -57,13 +44,13 @@ __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
     constexpr int S = KT + VEC;               // padded column stride (conflict-free)
     constexpr int TP = W / 8;
     __shared__ __align__(16) T Ws[2][W * S];
-    __shared__ long long colofs[W];
+    __shared__ const T* colp[W];
 
     const int pair = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * a.ldx : -1;
+    const PairDesc<T> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, false, a.ldx) : nullptr;
     __syncthreads();
 
     const long long rbeg = (long long)split * a.rows_per_split;
@@ -86,9 +73,9 @@ __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
             if (v < W * VPC) {
                 int c = v / VPC, ch = v % VPC;
                 T* dst = &Ws[stage][c * S + ch * VEC];
-                long long off = colofs[c];
-                if (off >= 0 && r0 + ch * VEC < rend) {
-                    const T* src = a.X + off + r0 + ch * VEC;
+                const T* cp = colp[c];
+                if (cp != nullptr && r0 + ch * VEC < rend) {
+                    const T* src = cp + r0 + ch * VEC;
                     unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(src));
                 } else {
@@ -355,8 +342,7 @@ __global__ void __launch_bounds__(INNER_NT) k_pair_solve(JacobiRound<T> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
     const int pair = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
+    const int w = a.pd[pair].w0 + a.pd[pair].w1;
     // fixed-order reduction over row slabs (deterministic)
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
     for (int e = tid; e < W * W; e += nt) {
@@ -414,19 +400,18 @@ __global__ void __launch_bounds__(64) k_pair_update(JacobiRound<T> a) {
     extern __shared__ __align__(16) unsigned char upd_smem[];
     T* Ws = reinterpret_cast<T*>(upd_smem);              // W * SW
     T* Es = Ws + W * SW;                                   // W * SE
-    long long* colofs = reinterpret_cast<long long*>(Es + W * SE);
+    T** colp = reinterpret_cast<T**>(Es + W * SE);
     const int pair = blockIdx.y, which = blockIdx.z;
     if (!a.flag[pair]) return;
-    T* Mx = which ? a.V : a.X;
-    if (Mx == nullptr) return;
+    if (which && !a.has_v) return;
     const long long ld = which ? a.ldv : a.ldx;
     const long long rows_pad = which ? a.nv_pad : a.m_pad;
     const long long row0 = (long long)blockIdx.x * RC;
     if (row0 >= rows_pad) return;
     const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * ld : -1;
+    const PairDesc<T> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, which != 0, ld) : nullptr;
     const T* Eg = a.E + (long long)pair * (W * W);
     for (int e = tid; e < W * W; e += 64) {
         const int k = e / W, j = e - (e / W) * W;
@@ -438,8 +423,8 @@ __global__ void __launch_bounds__(64) k_pair_update(JacobiRound<T> a) {
     for (int v = tid; v < W * VPC; v += 64) {
         const int k = v / VPC, ch = v % VPC;
         T* dst = &Ws[k * SW + ch * VEC];
-        if (colofs[k] >= 0 && ch * VEC < nrow)
-            *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(Mx + colofs[k] + row0 + ch * VEC);
+        if (colp[k] != nullptr && ch * VEC < nrow)
+            *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(colp[k] + row0 + ch * VEC);
         else
             *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -472,7 +457,7 @@ __global__ void __launch_bounds__(64) k_pair_update(JacobiRound<T> a) {
     for (int j = 0; j < TP; ++j) {
         const int col = tx * TP + j;
         if (col >= w) continue;
-        T* dstc = Mx + colofs[col] + row0 + ty * 8;
+        T* dstc = colp[col] + row0 + ty * 8;
         if (ty * 8 >= nrow) continue;
 #pragma unroll
         for (int i = 0; i < 8; ++i) dstc[i] = Ws[col * SW + ty * 8 + i] + acc[i][j];
@@ -514,7 +499,7 @@ constexpr int GRAM_KT = 32, GRAM_S = GRAM_KT + 4, GRAM_STAGES = 3, GRAM_NWARP = 
 
 // The k-loop of one warp with a compile-time tile list (tiles WARP, WARP+4, ...)
 template <int W, int WARP>
-__device__ __forceinline__ void gram_warp(const double* __restrict__ X, const long long* colofs, double* Wsm,
+__device__ __forceinline__ void gram_warp(const double* const* colp, double* Wsm,
                                           long long rbeg, int ntile, double* out) {
     constexpr int KT = GRAM_KT, S = GRAM_S, STAGES = GRAM_STAGES, NTI = W / 8;
     constexpr int NTILE = NTI * (NTI + 1) / 2;
@@ -530,8 +515,8 @@ __device__ __forceinline__ void gram_warp(const double* __restrict__ X, const lo
         for (int v = tid; v < W * CH; v += 128) {
             const int c = v / CH, ch = v % CH;
             double* dst = &ws[c * S + ch * 2];
-            const long long off = colofs[c];
-            if (off >= 0) cp_async16(dst, X + off + r0 + ch * 2);
+            const double* cp = colp[c];
+            if (cp != nullptr) cp_async16(dst, cp + r0 + ch * 2);
             else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
         }
     };
@@ -583,22 +568,22 @@ template <int W>
 __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
     extern __shared__ __align__(16) unsigned char gram_smem[];
     double* Wsm = reinterpret_cast<double*>(gram_smem);
-    long long* colofs = reinterpret_cast<long long*>(Wsm + GRAM_STAGES * W * GRAM_S);
+    const double** colp = reinterpret_cast<const double**>(Wsm + GRAM_STAGES * W * GRAM_S);
     const int pair = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * a.ldx : -1;
+    const PairDesc<double> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, false, a.ldx) : nullptr;
     __syncthreads();
     const long long rbeg = (long long)split * a.rows_per_split;
     const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
     const int ntile = (int)((rend - rbeg) / GRAM_KT);
     double* out = a.partial + ((long long)pair * a.nsplit + split) * (W * W);
     switch (warp) {
-        case 0: gram_warp<W, 0>(a.X, colofs, Wsm, rbeg, ntile, out); break;
-        case 1: gram_warp<W, 1>(a.X, colofs, Wsm, rbeg, ntile, out); break;
-        case 2: gram_warp<W, 2>(a.X, colofs, Wsm, rbeg, ntile, out); break;
-        default: gram_warp<W, 3>(a.X, colofs, Wsm, rbeg, ntile, out); break;
+        case 0: gram_warp<W, 0>(colp, Wsm, rbeg, ntile, out); break;
+        case 1: gram_warp<W, 1>(colp, Wsm, rbeg, ntile, out); break;
+        case 2: gram_warp<W, 2>(colp, Wsm, rbeg, ntile, out); break;
+        default: gram_warp<W, 3>(colp, Wsm, rbeg, ntile, out); break;
     }
 }
 static size_t gram_dmma_smem(int W) { return sizeof(double) * (size_t)GRAM_STAGES * W * GRAM_S + sizeof(long long) * W; }
@@ -625,12 +610,12 @@ __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float>
     extern __shared__ __align__(16) unsigned char g32_smem[];
     float4* Ws = reinterpret_cast<float4*>(g32_smem);            // [ST][W*8] chunks
     float* red = reinterpret_cast<float*>(g32_smem);               // [W*W] partial sums (aliases the stages)
-    __shared__ long long colofs[W];
+    __shared__ const float* colp[W];
     const int pair = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * a.ldx : -1;
+    const PairDesc<float> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, false, a.ldx) : nullptr;
     __syncthreads();
     const long long rbeg = (long long)split * a.rows_per_split;
     const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
@@ -660,7 +645,7 @@ __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float>
         for (int v = tid; v < W * 8; v += G32_NT) {
             const int c = v >> 3, rc = v & 7;
             float4* d = dst + g32_chunk(c, rc);
-            if (colofs[c] >= 0) cp_async16(d, a.X + colofs[c] + r0 + rc * 4);
+            if (colp[c] != nullptr) cp_async16(d, colp[c] + r0 + rc * 4);
             else *d = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
@@ -736,26 +721,25 @@ __global__ void __launch_bounds__(256) k_pair_update_dmma(JacobiRound<double> a)
     extern __shared__ __align__(16) unsigned char upd_smem[];
     double* Ws = reinterpret_cast<double*>(upd_smem);      // [W][SW]  (column k, row rho)
     double* Et = Ws + W * SW;                                // [W][SE]  (Et[j][k] = E[k][j])
-    long long* colofs = reinterpret_cast<long long*>(Et + W * SE);
+    double** colp = reinterpret_cast<double**>(Et + W * SE);
     const int pair = blockIdx.y, which = blockIdx.z;
     if (!a.flag[pair]) return;
-    double* Mx = which ? a.V : a.X;
-    if (Mx == nullptr) return;
+    if (which && !a.has_v) return;
     const long long ld = which ? a.ldv : a.ldx;
     const long long rows_pad = which ? a.nv_pad : a.m_pad;
     const long long row0 = (long long)blockIdx.x * RC;
     if (row0 >= rows_pad) return;
     const int nrow = (int)min((long long)RC, rows_pad - row0);    // multiple of 32
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * ld : -1;
+    const auto pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, which != 0, ld) : nullptr;
     __syncthreads();
     // stage the slab (cp.async) and E^T
     for (int v = tid; v < W * (RC / 2); v += 256) {
         const int c = v / (RC / 2), ch = v % (RC / 2);
         double* dst = &Ws[c * SW + ch * 2];
-        if (colofs[c] >= 0 && ch * 2 < nrow) cp_async16(dst, Mx + colofs[c] + row0 + ch * 2);
+        if (colp[c] != nullptr && ch * 2 < nrow) cp_async16(dst, colp[c] + row0 + ch * 2);
         else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -799,7 +783,7 @@ __global__ void __launch_bounds__(256) k_pair_update_dmma(JacobiRound<double> a)
     for (int v = tid; v < W * (RC / 2); v += 256) {
         const int c = v / (RC / 2), ch = v % (RC / 2);
         if (c < w && ch * 2 < nrow)
-            *reinterpret_cast<double2*>(Mx + colofs[c] + row0 + ch * 2) =
+            *reinterpret_cast<double2*>(colp[c] + row0 + ch * 2) =
                 *reinterpret_cast<const double2*>(&Ws[c * SW + ch * 2]);
     }
 }
@@ -818,25 +802,24 @@ __global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
     extern __shared__ __align__(16) unsigned char upd_smem[];
     float* Ws = reinterpret_cast<float*>(upd_smem);     // [W][SW]  (column k, row rho)
     float* Es = Ws + W * SW;                            // [W][SE]  (Es[k][j] = E[k][j])
-    long long* colofs = reinterpret_cast<long long*>(Es + W * SE);
+    float** colp = reinterpret_cast<float**>(Es + W * SE);
     const int pair = blockIdx.y, which = blockIdx.z;
     if (!a.flag[pair]) return;
-    float* Mx = which ? a.V : a.X;
-    if (Mx == nullptr) return;
+    if (which && !a.has_v) return;
     const long long ld = which ? a.ldv : a.ldx;
     const long long rows_pad = which ? a.nv_pad : a.m_pad;
     const long long row0 = (long long)blockIdx.x * RC;
     if (row0 >= rows_pad) return;
     const int nrow = (int)min((long long)RC, rows_pad - row0);
     const int tid = threadIdx.x;
-    PairCols pc = pair_cols(a.round, pair, a.M, a.nblk, a.b, a.n);
-    const int w = pc.wI + pc.wJ;
-    if (tid < W) colofs[tid] = tid < w ? (long long)pair_gcol(pc, tid, a.b) * ld : -1;
+    const auto pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, which != 0, ld) : nullptr;
     __syncthreads();
     for (int v = tid; v < W * (RC / 4); v += 256) {
         const int c = v / (RC / 4), ch = v % (RC / 4);
         float* dst = &Ws[c * SW + ch * 4];
-        if (colofs[c] >= 0 && ch * 4 < nrow) cp_async16(dst, Mx + colofs[c] + row0 + ch * 4);
+        if (colp[c] != nullptr && ch * 4 < nrow) cp_async16(dst, colp[c] + row0 + ch * 4);
         else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     cp_async_commit();
@@ -878,7 +861,7 @@ __global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
     for (int v = tid; v < W * (RC / 4); v += 256) {
         const int c = v / (RC / 4), ch = v % (RC / 4);
         if (c < w && ch * 4 < nrow)
-            *reinterpret_cast<float4*>(Mx + colofs[c] + row0 + ch * 4) =
+            *reinterpret_cast<float4*>(colp[c] + row0 + ch * 4) =
                 *reinterpret_cast<const float4*>(&Ws[c * SW + ch * 4]);
     }
 }
@@ -968,7 +951,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
             cudaFuncSetAttribute(k_pair_update_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
             attr_d = true;
         }
-        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.V ? 2 : 1), 256, dsm, st>>>(a);
+        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.has_v ? 2 : 1), 256, dsm, st>>>(a);
     } else {
         const size_t fsm = sizeof(float) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
         static bool attr_f = false;
@@ -977,7 +960,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
             attr_f = true;
         }
         (void)usm;
-        k_pair_update_f32<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.V ? 2 : 1), 256, fsm, st>>>(a);
+        k_pair_update_f32<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.has_v ? 2 : 1), 256, fsm, st>>>(a);
     }
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::update);

@@ -15,7 +15,9 @@
 
 #include "../../include/mpjsvd.h"
 #include "common.cuh"
+#include "comm.h"
 #include "jacobi.h"
+#include "shard.h"
 
 thread_local int64_t g_mpj_launches = 0;
 static thread_local char g_last_cuda_err[512] = "no error";
@@ -39,7 +41,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -102,7 +104,10 @@ struct mpjsvd_handle_s {
     void* buf[S_COUNT] = {};
     size_t cap[S_COUNT] = {};
     void* host_pinned = nullptr;   // sweep read-back
+    void* pinned_tab = nullptr;    // staging of the per-sweep pair-descriptor table
+    size_t pinned_cap = 0;
     cudaEvent_t ev[10] = {};
+    Comm comm;                     // NCCL (multi-process sharding), inactive by default
 };
 
 namespace {
@@ -125,6 +130,21 @@ int ensure(mpjsvd_handle h, Slot s, size_t bytes) {
 template <typename T>
 T* P(mpjsvd_handle h, Slot s) { return reinterpret_cast<T*>(h->buf[s]); }
 
+int ensure_pinned(mpjsvd_handle h, size_t bytes) {
+    if (h->pinned_cap >= bytes) return 0;
+    if (h->pinned_tab) cudaFreeHost(h->pinned_tab);
+    h->pinned_tab = nullptr;
+    h->pinned_cap = 0;
+    cudaError_t e = cudaMallocHost(&h->pinned_tab, bytes);
+    if (e != cudaSuccess) {
+        mpj_record_cuda_error(e, "cudaMallocHost", __FILE__, __LINE__);
+        cudaGetLastError();
+        return MPJSVD_ERR_OUT_OF_MEMORY;
+    }
+    h->pinned_cap = bytes;
+    return 0;
+}
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes at;
     cudaError_t e = cudaPointerGetAttributes(&at, p);
@@ -139,31 +159,112 @@ struct JacobiResult {
     int upd[64] = {};
 };
 
-// Block round-robin Jacobi stage (fp32 or fp64) on padded device buffers.
+// Where the X / V column slabs of one Jacobi stage live (shard.h): the
+// matrix itself (one GPU: buffer j = block j, nothing moves), or per-rank
+// shard buffers of nbuf slabs (m_pad x b, ld m_pad), all ranks in this
+// process (virtual shards on one GPU) or only `me` (NCCL, one process/GPU).
 template <typename T>
-int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int n, T* V, long long ldv,
-                     long long nv_pad, int b, T tol, T tol_in, int max_sweeps, int max_inner, bool stagnation,
-                     JacobiResult& res) {
+struct JStore {
+    ShardPlan plan;
+    int me = -1;                       // NCCL rank of this process; -1: every rank is local
+    std::vector<T*> xs, vs;            // per rank: base of buffer 0 (nullptr if not local)
+    long long slab_x = 0, slab_v = 0;  // elements between consecutive buffers
+    bool local(int g) const { return me < 0 || g == me; }
+    T* bx(int g, int j) const { return xs[g] + (long long)j * slab_x; }
+    T* bv(int g, int j) const { return vs[g] ? vs[g] + (long long)j * slab_v : nullptr; }
+};
+
+// One sweep's schedule for the local ranks: descriptor table per round and
+// the inter-rank moves after each round (plan advanced M-1 times).
+template <typename T>
+void build_sweep(JStore<T>& S, int b, int n, std::vector<PairDesc<T>>& table,
+                 std::vector<std::vector<ShardPlan::Move>>& moves) {
+    ShardPlan& pl = S.plan;
+    const int R = pl.M - 1;
+    table.clear();
+    moves.assign(R, {});
+    for (int r = 0; r < R; ++r) {
+        for (int g = 0; g < pl.G; ++g) {
+            if (!S.local(g)) continue;
+            for (int t = 0; t < pl.k; ++t) {
+                const ShardPlan::Pair p = pl.pair(g, t);
+                PairDesc<T> d;
+                d.x0 = S.bx(g, p.buf0);
+                d.x1 = S.bx(g, p.buf1);
+                d.v0 = S.bv(g, p.buf0);
+                d.v1 = S.bv(g, p.buf1);
+                d.w0 = pl.width(p.blk0, b, n);
+                d.w1 = pl.width(p.blk1, b, n);
+                d.pad_[0] = p.blk0;
+                d.pad_[1] = p.blk1;
+                table.push_back(d);
+            }
+        }
+        pl.advance(&moves[r]);
+    }
+}
+
+// Transfers of one round's inter-rank moves (bye blocks carry no data).
+template <typename T>
+int exchange(mpjsvd_handle h, JStore<T>& S, const std::vector<ShardPlan::Move>& mv, size_t bytes_x,
+             size_t bytes_v, cudaStream_t st) {
+    if (mv.empty()) return 0;
+    const bool nccl = h->comm.active();
+    if (nccl) MPJ_TRY(h->comm.group_start());
+    int rc = 0;
+    for (const auto& m : mv) {
+        if (m.blk >= S.plan.nblk) continue;
+        const bool sl = S.local(m.src_rank), dl = S.local(m.dst_rank);
+        if (sl && dl) {
+            MPJ_CUDA_TRY(cudaMemcpyAsync(S.bx(m.dst_rank, m.dst_buf), S.bx(m.src_rank, m.src_buf), bytes_x,
+                                         cudaMemcpyDeviceToDevice, st));
+            if (bytes_v)
+                MPJ_CUDA_TRY(cudaMemcpyAsync(S.bv(m.dst_rank, m.dst_buf), S.bv(m.src_rank, m.src_buf), bytes_v,
+                                             cudaMemcpyDeviceToDevice, st));
+        } else if (sl) {
+            if (!rc) rc = h->comm.send(S.bx(m.src_rank, m.src_buf), bytes_x, m.dst_rank, st);
+            if (!rc && bytes_v) rc = h->comm.send(S.bv(m.src_rank, m.src_buf), bytes_v, m.dst_rank, st);
+        } else if (dl) {
+            if (!rc) rc = h->comm.recv(S.bx(m.dst_rank, m.dst_buf), bytes_x, m.src_rank, st);
+            if (!rc && bytes_v) rc = h->comm.recv(S.bv(m.dst_rank, m.dst_buf), bytes_v, m.src_rank, st);
+        }
+    }
+    if (nccl) {
+        const int rc2 = h->comm.group_end();
+        if (!rc) rc = rc2;
+    }
+    return rc;
+}
+
+// Block round-robin Jacobi stage (fp32 or fp64) over the slabs of S.
+template <typename T>
+int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_pad, int n, bool has_v,
+                     long long ldv, long long nv_pad, int b, T tol, T tol_in, int max_sweeps, int max_inner,
+                     bool stagnation, JacobiResult& res) {
     cudaStream_t st = h->stream;
     const int W = 2 * b;
     if (W != 16 && W != 32 && W != 64) return MPJSVD_ERR_NOT_SUPPORTED;
-    const int nblk = (int)ceil_div(n, b);
-    int M = nblk + (nblk & 1);
-    if (nblk == 1) M = 2;
-    const int npairs = M / 2;
+    int nlocal = 0;
+    for (int g = 0; g < S.plan.G; ++g) nlocal += S.local(g) ? 1 : 0;
+    const int npairs = nlocal * S.plan.k;
+    const int R = S.plan.M - 1;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
-    // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
-    // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
-    const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W);
-    const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
     long long nsplit = 1;
-    double best = 1e30;
-    for (long long ns = 1; ns <= maxsplit; ++ns) {
-        const long long rps_ = round_up(ceil_div(m_pad, ns), 32);
-        const long long ns_eff = ceil_div(m_pad, rps_);
-        const double cost = (double)ceil_div(npairs * ns_eff, slots) * (rps_ + 96) + 16.0 * ns_eff;
-        if (cost < best - 1e-9) { best = cost; nsplit = ns_eff; }
+    if (h->opts.split_rows > 0) {
+        nsplit = ceil_div(m_pad, round_up(h->opts.split_rows, 32));
+    } else {
+        // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
+        // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
+        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W);
+        const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
+        double best = 1e30;
+        for (long long ns = 1; ns <= maxsplit; ++ns) {
+            const long long rps_ = round_up(ceil_div(m_pad, ns), 32);
+            const long long ns_eff = ceil_div(m_pad, rps_);
+            const double cost = (double)ceil_div(npairs * ns_eff, slots) * (rps_ + 96) + 16.0 * ns_eff;
+            if (cost < best - 1e-9) { best = cost; nsplit = ns_eff; }
+        }
     }
     long long rps = round_up(ceil_div(m_pad, nsplit), 32);
     nsplit = ceil_div(m_pad, rps);
@@ -171,14 +272,18 @@ int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int 
     MPJ_TRY(ensure(h, S_E, sizeof(T) * (size_t)npairs * W * W));
     MPJ_TRY(ensure(h, S_JFLAG, sizeof(int) * (size_t)npairs));
     MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + sizeof(int))));
+    MPJ_TRY(ensure(h, S_PTAB, sizeof(PairDesc<T>) * (size_t)R * npairs));
+    MPJ_TRY(ensure_pinned(h, sizeof(PairDesc<T>) * (size_t)R * npairs));
     double* d_off = P<double>(h, S_SWEEP);
     int* d_upd = reinterpret_cast<int*>(d_off + 64);
     MPJ_CUDA_TRY(cudaMemsetAsync(d_off, 0, 64 * (sizeof(double) + sizeof(int)), st));
+    PairDesc<T>* d_tab = P<PairDesc<T>>(h, S_PTAB);
+    const size_t bytes_x = sizeof(T) * (size_t)S.slab_x, bytes_v = has_v ? sizeof(T) * (size_t)S.slab_v : 0;
 
     JacobiRound<T> a;
-    a.X = X; a.ldx = ldx; a.m_pad = m_pad; a.n = n;
-    a.V = V; a.ldv = ldv; a.nv_pad = V ? nv_pad : 0;
-    a.b = b; a.nblk = nblk; a.M = M; a.npairs = npairs;
+    a.ldx = ldx; a.m_pad = m_pad; a.n = n;
+    a.has_v = has_v; a.ldv = ldv; a.nv_pad = has_v ? nv_pad : 0;
+    a.b = b; a.npairs = npairs;
     a.nsplit = (int)nsplit; a.rows_per_split = rps;
     a.partial = P<T>(h, S_PART); a.E = P<T>(h, S_E); a.flag = P<int>(h, S_JFLAG);
     a.tol = tol; a.tol_in = tol_in; a.max_inner = max_inner;
@@ -186,13 +291,28 @@ int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
     double prev = -1.0;
     res = JacobiResult();
+    std::vector<PairDesc<T>> table;
+    std::vector<std::vector<ShardPlan::Move>> moves;
     for (int sw = 1; sw <= max_sweeps && sw <= 64; ++sw) {
+        build_sweep<T>(S, b, n, table, moves);
+        memcpy(h->pinned_tab, table.data(), sizeof(PairDesc<T>) * table.size());
+        MPJ_CUDA_TRY(cudaMemcpyAsync(d_tab, h->pinned_tab, sizeof(PairDesc<T>) * table.size(),
+                                     cudaMemcpyHostToDevice, st));
         a.sweep_off = d_off + (sw - 1);
         a.sweep_upd = d_upd + (sw - 1);
         ProfHook hook{&h->prof, &Profiler::hb, &Profiler::he};
-        for (int r = 0; r < M - 1; ++r) {
-            a.round = r;
+        for (int r = 0; r < R; ++r) {
+            a.pd = d_tab + (size_t)r * npairs;
             MPJ_TRY(launch_jacobi_round<T>(a, W, st, h->prof.on ? &hook : nullptr));
+            if (!moves[r].empty()) {
+                if (h->prof.on) h->prof.begin("exchange");
+                MPJ_TRY(exchange<T>(h, S, moves[r], bytes_x, bytes_v, st));
+                if (h->prof.on) h->prof.end("exchange");
+            }
+        }
+        if (h->comm.active()) {
+            MPJ_TRY(h->comm.allreduce_max_f64(d_off + (sw - 1), 1, st));
+            MPJ_TRY(h->comm.allreduce_sum_i32(d_upd + (sw - 1), 1, st));
         }
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -210,6 +330,123 @@ int run_block_jacobi(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int 
         prev = off;
     }
     return 0;
+}
+
+// Contiguous store over the matrix itself (one GPU, one rank).
+template <typename T>
+int contiguous_store(JStore<T>& S, T* X, long long ldx, T* V, long long ldv, int n, int b) {
+    if (S.plan.init((int)ceil_div(n, b), 1, true)) return MPJSVD_ERR_INVALID_ARG;
+    S.me = -1;
+    S.xs = {X};
+    S.vs = {V};
+    S.slab_x = (long long)b * ldx;
+    S.slab_v = (long long)b * ldv;
+    return 0;
+}
+
+// Sharded store over G ranks: shard buffers for the local ranks, filled from
+// the full matrices Xf (m_pad x n, ld m_pad) / Vf (nv_pad x n) -- which must
+// hold the data on every rank that has local shards.
+template <typename T>
+int sharded_store_in(mpjsvd_handle h, JStore<T>& S, int G, const T* Xf, long long m_pad, const T* Vf,
+                     long long nv_pad, int n, int b) {
+    cudaStream_t st = h->stream;
+    if (S.plan.init((int)ceil_div(n, b), G, false)) return MPJSVD_ERR_INVALID_ARG;
+    S.me = h->comm.active() ? h->comm.rank : -1;
+    const int nlocal = S.me < 0 ? G : 1;
+    S.slab_x = m_pad * b;
+    S.slab_v = Vf ? nv_pad * b : 0;
+    MPJ_TRY(ensure(h, S_SHX, sizeof(T) * (size_t)nlocal * S.plan.nbuf * S.slab_x));
+    if (Vf) MPJ_TRY(ensure(h, S_SHV, sizeof(T) * (size_t)nlocal * S.plan.nbuf * S.slab_v));
+    S.xs.assign(G, nullptr);
+    S.vs.assign(G, nullptr);
+    int li = 0;
+    for (int g = 0; g < G; ++g) {
+        if (!S.local(g)) continue;
+        S.xs[g] = P<T>(h, S_SHX) + (size_t)li * S.plan.nbuf * S.slab_x;
+        if (Vf) S.vs[g] = P<T>(h, S_SHV) + (size_t)li * S.plan.nbuf * S.slab_v;
+        ++li;
+        for (int l = 0; l < 2 * S.plan.k; ++l) {
+            const int buf = S.plan.buf_at(g, l), blk = S.plan.blk_of(g, buf);
+            const int w = S.plan.width(blk, b, n);
+            if (w == 0) continue;
+            MPJ_CUDA_TRY(cudaMemcpyAsync(S.bx(g, buf), Xf + (size_t)blk * b * m_pad, sizeof(T) * (size_t)w * m_pad,
+                                         cudaMemcpyDeviceToDevice, st));
+            if (Vf)
+                MPJ_CUDA_TRY(cudaMemcpyAsync(S.bv(g, buf), Vf + (size_t)blk * b * nv_pad,
+                                             sizeof(T) * (size_t)w * nv_pad, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return 0;
+}
+
+// Gather every block back into the full matrices on rank 0.  Virtual shards:
+// device copies.  NCCL: each rank sends its whole shard storage (nbuf
+// consecutive slabs, one message for X and one for V) to rank 0, which
+// receives into a staging area and copies every block to its columns.
+template <typename T>
+int sharded_store_out(mpjsvd_handle h, JStore<T>& S, T* Xf, long long m_pad, T* Vf, long long nv_pad, int n,
+                      int b) {
+    cudaStream_t st = h->stream;
+    const bool nccl = h->comm.active();
+    const int me = nccl ? h->comm.rank : 0;
+    const int G = S.plan.G;
+    const size_t shard_x = (size_t)S.plan.nbuf * S.slab_x, shard_v = (size_t)S.plan.nbuf * S.slab_v;
+    std::vector<T*> srcx(G, nullptr), srcv(G, nullptr);    // where rank g's buffer 0 is readable
+    for (int g = 0; g < G; ++g)
+        if (S.local(g)) { srcx[g] = S.xs[g]; srcv[g] = S.vs[g]; }
+    if (nccl) {
+        if (me != 0) {
+            MPJ_TRY(h->comm.group_start());
+            int rc = h->comm.send(S.xs[me], sizeof(T) * shard_x, 0, st);
+            if (!rc && Vf) rc = h->comm.send(S.vs[me], sizeof(T) * shard_v, 0, st);
+            const int rc2 = h->comm.group_end();
+            return rc ? rc : rc2;
+        }
+        MPJ_TRY(ensure(h, S_STAGE, sizeof(T) * (size_t)G * (shard_x + shard_v)));
+        T* stage = P<T>(h, S_STAGE);
+        MPJ_TRY(h->comm.group_start());
+        int rc = 0;
+        for (int g = 1; g < G; ++g) {
+            srcx[g] = stage + (size_t)g * (shard_x + shard_v);
+            srcv[g] = Vf ? srcx[g] + shard_x : nullptr;
+            if (!rc) rc = h->comm.recv(srcx[g], sizeof(T) * shard_x, g, st);
+            if (!rc && Vf) rc = h->comm.recv(srcv[g], sizeof(T) * shard_v, g, st);
+        }
+        const int rc2 = h->comm.group_end();
+        if (rc || rc2) return rc ? rc : rc2;
+    }
+    for (int blk = 0; blk < S.plan.nblk; ++blk) {
+        int g = 0, buf = 0;
+        if (!S.plan.locate(blk, g, buf)) return MPJSVD_ERR_INVALID_ARG;
+        const int w = S.plan.width(blk, b, n);
+        MPJ_CUDA_TRY(cudaMemcpyAsync(Xf + (size_t)blk * b * m_pad, srcx[g] + (size_t)buf * S.slab_x,
+                                     sizeof(T) * (size_t)w * m_pad, cudaMemcpyDeviceToDevice, st));
+        if (Vf)
+            MPJ_CUDA_TRY(cudaMemcpyAsync(Vf + (size_t)blk * b * nv_pad, srcv[g] + (size_t)buf * S.slab_v,
+                                         sizeof(T) * (size_t)w * nv_pad, cudaMemcpyDeviceToDevice, st));
+    }
+    return 0;
+}
+
+// One Jacobi stage on full matrices X (m_pad x n, ld ldx) / V: contiguous on
+// one rank, else scattered to shards, run, and gathered back to rank 0.
+template <typename T>
+int jacobi_stage(mpjsvd_handle h, T* X, long long ldx, long long m_pad, int n, T* V, long long ldv,
+                 long long nv_pad, int b, T tol, T tol_in, int max_sweeps, int max_inner, bool stagnation,
+                 JacobiResult& res) {
+    const int G = h->comm.active() ? h->comm.world : std::max(1, (int)h->opts.virtual_shards);
+    JStore<T> S;
+    if (G == 1) {
+        MPJ_TRY(contiguous_store<T>(S, X, ldx, V, ldv, n, b));
+        return run_block_jacobi<T>(h, S, ldx, m_pad, n, V != nullptr, ldv, nv_pad, b, tol, tol_in, max_sweeps,
+                                   max_inner, stagnation, res);
+    }
+    if (ldx != m_pad || (V && ldv != nv_pad)) return MPJSVD_ERR_INVALID_ARG;
+    MPJ_TRY(sharded_store_in<T>(h, S, G, X, m_pad, V, nv_pad, n, b));
+    MPJ_TRY(run_block_jacobi<T>(h, S, m_pad, m_pad, n, V != nullptr, nv_pad, nv_pad, b, tol, tol_in, max_sweeps,
+                                max_inner, stagnation, res));
+    return sharded_store_out<T>(h, S, X, m_pad, V, nv_pad, n, b);
 }
 
 int ensure_qr_work(mpjsvd_handle h, int m, int n, QrWork& w) {
@@ -261,8 +498,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     h->prof.st = h->stream;
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32), n_pad = round_up(n, 32);
-    const bool a_dev = is_device_ptr(A), u_dev = is_device_ptr(U), s_dev = is_device_ptr(S),
-               v_dev = is_device_ptr(V);
+    const bool a_dev = A && is_device_ptr(A), u_dev = U && is_device_ptr(U), s_dev = S && is_device_ptr(S),
+               v_dev = V && is_device_ptr(V);
     mpjsvd_stats local;
     mpjsvd_stats& s = stats ? *stats : local;
     memset(&s, 0, sizeof(s));
@@ -311,8 +548,41 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     double* scal = P<double>(h, S_SCAL);  // [0] maxabs [1..2] diag stats [3] orth
     cudaEvent_t* ev = h->ev;
 
+    const bool dist = h->comm.active();
+    const bool root = !dist || h->comm.rank == 0;
+    MPJ_TRY(ensure(h, S_HDR, sizeof(long long) * 8));
+    long long* d_hdr = P<long long>(h, S_HDR);
+    long long* h_hdr = reinterpret_cast<long long*>(h->host_pinned);
+    if (dist) {
+        // every rank must factor the same (m, n): max-allreduce of (m, n, -m, -n)
+        h_hdr[0] = m; h_hdr[1] = n; h_hdr[2] = -m; h_hdr[3] = -n;
+        MPJ_CUDA_TRY(cudaMemcpyAsync(d_hdr, h_hdr, 4 * sizeof(long long), cudaMemcpyHostToDevice, st));
+        MPJ_TRY(h->comm.allreduce_max_i64(d_hdr, 4, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr, d_hdr, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h_hdr[0] != -h_hdr[2] || h_hdr[1] != -h_hdr[3]) return MPJSVD_ERR_INVALID_ARG;
+    }
+    // root's error flags -> every rank (NCCL), so that all ranks leave together
+    auto agree_status = [&](int code_if_flag0, int code_if_flag12) -> int {
+        if (!dist) return 0;
+        int hf[8] = {0};
+        if (root) {
+            MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr + 4, flags, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+            MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+            memcpy(hf, h_hdr + 4, sizeof(hf));
+        }
+        h_hdr[0] = hf[0] ? code_if_flag0 : ((hf[1] || hf[2]) ? code_if_flag12 : 0);
+        MPJ_CUDA_TRY(cudaMemcpyAsync(d_hdr, h_hdr, sizeof(long long), cudaMemcpyHostToDevice, st));
+        MPJ_TRY(h->comm.bcast(d_hdr, sizeof(long long), 0, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr, d_hdr, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        return (int)h_hdr[0];
+    };
     MPJ_CUDA_TRY(cudaEventRecord(ev[0], st));
     MPJ_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * 8, st));
+    QrWork qw;
+    std::vector<double> xnorms;
+    if (root) {
     // ---- input -> padded device copy (host memory is staged here: e2e path)
     MPJ_CUDA_TRY(cudaMemsetAsync(dA, 0, sizeof(double) * (size_t)m_pad * n, st));
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(dA, sizeof(double) * m_pad, A, sizeof(double) * lda, sizeof(double) * m, n,
@@ -320,7 +590,6 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_TRY(check_finite(dA, m_pad, m, n, flags + 0, st));
 
     // ---- stage 0: tall QR  A = Q_tall R1
-    QrWork qw;
     if (m > n) {
         MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
         PROF_B("qr_coop_tall");
@@ -356,7 +625,6 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[3], st));
     // ---- stage 3: gate measures, report only
-    std::vector<double> xnorms;
     if (o.compute_gates) {
         PROF_B("gates_orth");
         MPJ_TRY(gates_orth(dX, n_pad, n_pad, (int)n, dX32, n_pad, scal + 3, st));
@@ -365,17 +633,30 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         xnorms.resize(n);
         MPJ_CUDA_TRY(cudaMemcpyAsync(xnorms.data(), P<double>(h, S_KEYS), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     }
+    }  // root
     MPJ_CUDA_TRY(cudaEventRecord(ev[4], st));
+    {
+        const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
+        if (rc) return rc;
+    }
     // ---- stage 4: fp32 block Jacobi
     JacobiResult r32, r64;
     if (o.path != MPJSVD_PATH_FORCE_FP64) {
-        MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
-        MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
+        if (root) {
+            MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
+            MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
+        }
         MPJ_TRY(set_identity<float>(dV32, n_pad, n_pad, n, st));
+        if (dist) {
+            PROF_B("bcast");
+            MPJ_TRY(h->comm.bcast(dX32, sizeof(float) * nn, 0, st));
+            PROF_E("bcast");
+        }
         const float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         const float tol32_in = tol32 / (float)o.inner_tol_div;
-        MPJ_TRY(run_block_jacobi<float>(h, dX32, n_pad, n_pad, (int)n, dV32, n_pad, n_pad, o.block_cols, tol32,
-                                        tol32_in, o.max_sweeps32, o.max_inner, true, r32));
+        MPJ_TRY(jacobi_stage<float>(h, dX32, n_pad, n_pad, (int)n, dV32, n_pad, n_pad, o.block_cols, tol32,
+                                    tol32_in, o.max_sweeps32, o.max_inner, true, r32));
+        if (root) {
         // sort by sigma32 (descending, stable) and upcast V32 -> Q
         MPJ_TRY(col_norms<float>(dX32, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 0, st));
         MPJ_TRY(rank_desc(P<double>(h, S_KEYS), (int)n, P<int>(h, S_RANK), st));
@@ -388,21 +669,60 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         PROF_B("rv_gemm");
         MPJ_TRY(gemm_f64(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, st));
         PROF_E("rv_gemm");
+        } else {
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+        }
         s.path_taken = MPJSVD_PATH_FORCE_MIXED;
     } else {
         MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
-        MPJ_TRY(set_identity<double>(dQ, n_pad, n_pad, n, st));
-        MPJ_TRY(copy_matrix(dX, n_pad, dY, n_pad, n_pad, n, st));
+        if (root) {
+            MPJ_TRY(set_identity<double>(dQ, n_pad, n_pad, n, st));
+            MPJ_TRY(copy_matrix(dX, n_pad, dY, n_pad, n_pad, n, st));
+        }
         s.path_taken = MPJSVD_PATH_FORCE_FP64;
+    }
+    {
+        const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
+        if (rc) return rc;
+    }
+    if (dist) {
+        PROF_B("bcast");
+        MPJ_TRY(h->comm.bcast(dY, sizeof(double) * nn, 0, st));
+        MPJ_TRY(h->comm.bcast(dQ, sizeof(double) * nn, 0, st));
+        PROF_E("bcast");
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[6], st));
     // ---- stage 6: fp64 refinement with V := Q
     {
         const double tol64 = o.tol_mult64 * sqrt((double)n) * U64;
-        MPJ_TRY(run_block_jacobi<double>(h, dY, n_pad, n_pad, (int)n, dQ, n_pad, n_pad, o.block_cols, tol64,
-                                         tol64 / o.inner_tol_div, o.max_sweeps64, o.max_inner, false, r64));
+        MPJ_TRY(jacobi_stage<double>(h, dY, n_pad, n_pad, (int)n, dQ, n_pad, n_pad, o.block_cols, tol64,
+                                     tol64 / o.inner_tol_div, o.max_sweeps64, o.max_inner, false, r64));
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[7], st));
+    auto fill_sweep_stats = [&]() {
+        s.sweeps32 = r32.sweeps;
+        s.sweeps64 = r64.sweeps;
+        s.converged = r64.converged ? 1 : 0;
+        for (int i = 0; i < 32; ++i) {
+            s.off_trace32[i] = r32.off[i]; s.upd_trace32[i] = r32.upd[i];
+            s.off_trace64[i] = r64.off[i]; s.upd_trace64[i] = r64.upd[i];
+        }
+        s.final_off32 = r32.sweeps ? r32.off[r32.sweeps - 1] : 0.0;
+        s.final_off64 = r64.sweeps ? r64.off[r64.sweeps - 1] : 0.0;
+    };
+    if (!root) {
+        // non-root ranks end after the sharded refinement (outputs live on rank 0)
+        MPJ_CUDA_TRY(cudaEventRecord(ev[9], st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h->prof.on) h->prof.resolve();
+        fill_sweep_stats();
+        s.stage_ms[4] = elapsed(ev[4], ev[5]);
+        s.stage_ms[5] = elapsed(ev[5], ev[6]);
+        s.stage_ms[6] = elapsed(ev[6], ev[7]);
+        s.total_ms = elapsed(ev[0], ev[9]);
+        s.kernel_launches = g_mpj_launches;
+        return r64.converged ? MPJSVD_OK : MPJSVD_WARN_NOT_CONVERGED;
+    }
     // ---- stage 7: sigma, U_X, sort; U = Q_tall Q_p U_X; V = P Q_t V_X
     MPJ_TRY(col_norms<double>(dY, n_pad, n_pad, (int)n, P<double>(h, S_SOUT), 1, st));
     MPJ_TRY(rank_desc(P<double>(h, S_SOUT), (int)n, P<int>(h, S_RANK), st));
@@ -443,15 +763,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (hflags[0]) return MPJSVD_ERR_NONFINITE;
     if (hflags[1] || hflags[2]) return MPJSVD_ERR_RANK_DEFICIENT;
 
-    s.sweeps32 = r32.sweeps;
-    s.sweeps64 = r64.sweeps;
-    s.converged = r64.converged ? 1 : 0;
-    for (int i = 0; i < 32; ++i) {
-        s.off_trace32[i] = r32.off[i]; s.upd_trace32[i] = r32.upd[i];
-        s.off_trace64[i] = r64.off[i]; s.upd_trace64[i] = r64.upd[i];
-    }
-    s.final_off32 = r32.sweeps ? r32.off[r32.sweeps - 1] : 0.0;
-    s.final_off64 = r64.sweeps ? r64.off[r64.sweeps - 1] : 0.0;
+    fill_sweep_stats();
     s.cond_estimate = hscal[2] > 0 ? hscal[1] / hscal[2] : INFINITY;
     s.orth_measure = o.compute_gates ? hscal[3] : NAN;
     s.tail_fraction = NAN;
@@ -508,8 +820,8 @@ static int jacobi_entry(mpjsvd_handle h, T* X, int64_t m, int64_t n, int64_t ldx
     }
     JacobiResult r;
     g_mpj_launches = 0;
-    MPJ_TRY(run_block_jacobi<T>(h, Xw, m_pad, m_pad, (int)n, Vw, nv_pad, nv_pad, h->opts.block_cols, tol, tol_in,
-                                max_sweeps, h->opts.max_inner, stagnation, r));
+    MPJ_TRY(jacobi_stage<T>(h, Xw, m_pad, m_pad, (int)n, Vw, nv_pad, nv_pad, h->opts.block_cols, tol, tol_in,
+                            max_sweeps, h->opts.max_inner, stagnation, r));
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(X, sizeof(T) * ldx, Xw, sizeof(T) * m_pad, sizeof(T) * m, n, cudaMemcpyDefault, st));
     if (V)
         MPJ_CUDA_TRY(cudaMemcpy2DAsync(V, sizeof(T) * ldv, Vw, sizeof(T) * nv_pad, sizeof(T) * nv, n, cudaMemcpyDefault, st));
@@ -546,6 +858,8 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->x_from_lq = 1;
     o->compute_gates = 1;
     o->stream = nullptr;
+    o->virtual_shards = 1;
+    o->split_rows = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -553,7 +867,8 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     *out = nullptr;
     mpjsvd_options o;
     if (opts) o = *opts; else mpjsvd_default_options(&o);
-    if (o.num_gpus != 1) return MPJSVD_ERR_NOT_SUPPORTED;
+    if (o.num_gpus != 1) return MPJSVD_ERR_NOT_SUPPORTED;   // multi-GPU: one handle per process + mpjsvd_comm_init
+    if (o.virtual_shards < 1 || o.virtual_shards > 64 || o.split_rows < 0) return MPJSVD_ERR_INVALID_ARG;
     if (o.block_cols != 8 && o.block_cols != 16 && o.block_cols != 32) return MPJSVD_ERR_NOT_SUPPORTED;
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || (o.path != 0 && o.path != 2))
@@ -601,6 +916,8 @@ int mpjsvd_destroy(mpjsvd_handle h) {
         if (e) cudaEventDestroy(e);
     for (auto& e : h->prof.pool) cudaEventDestroy(e);
     if (h->host_pinned) cudaFreeHost(h->host_pinned);
+    if (h->pinned_tab) cudaFreeHost(h->pinned_tab);
+    h->comm.destroy();
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     cudaGetLastError();
@@ -615,7 +932,7 @@ const char* mpjsvd_strerror(int code) {
         case MPJSVD_ERR_NONFINITE: return "input contains NaN or Inf";
         case MPJSVD_ERR_RANK_DEFICIENT: return "rank deficient input (zero R diagonal or zero column)";
         case MPJSVD_ERR_CUDA: return "CUDA error (see mpjsvd_last_cuda_error)";
-        case MPJSVD_ERR_NCCL: return "NCCL error";
+        case MPJSVD_ERR_NCCL: return "NCCL error (see mpjsvd_last_cuda_error)";
         case MPJSVD_ERR_OUT_OF_MEMORY: return "out of device memory";
         case MPJSVD_ERR_NOT_SUPPORTED: return "not supported in this build";
         default: return "unknown error code";
@@ -623,6 +940,88 @@ const char* mpjsvd_strerror(int code) {
 }
 
 const char* mpjsvd_last_cuda_error(void) { return g_last_cuda_err; }
+
+int mpjsvd_comm_unique_id(uint8_t* id) {
+    if (!id) return MPJSVD_ERR_INVALID_ARG;
+    const int rc = nccl_unique_id(id);
+    if (rc) snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "%s", nccl_last_error());
+    return rc;
+}
+
+int mpjsvd_comm_init(mpjsvd_handle h, int32_t rank, int32_t world, const uint8_t* id) {
+    if (!h || !id || world < 1 || rank < 0 || rank >= world) return MPJSVD_ERR_INVALID_ARG;
+    if (h->opts.virtual_shards > 1) return MPJSVD_ERR_INVALID_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); return MPJSVD_ERR_CUDA; }
+    const int rc = h->comm.init(rank, world, id);
+    if (rc) snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "%s", nccl_last_error());
+    return rc;
+}
+
+int mpjsvd_comm_info(mpjsvd_handle h, int32_t* rank, int32_t* world) {
+    if (!h) return MPJSVD_ERR_INVALID_ARG;
+    if (rank) *rank = h->comm.active() ? h->comm.rank : 0;
+    if (world) *world = h->comm.active() ? h->comm.world : 1;
+    return 0;
+}
+
+// ---- shard plan (host only; shard.h) ----
+struct mpjsvd_plan_s {
+    ShardPlan p;
+};
+
+int mpjsvd_plan_create(mpjsvd_plan* out, int32_t nblk, int32_t world) {
+    if (!out) return MPJSVD_ERR_INVALID_ARG;
+    *out = nullptr;
+    mpjsvd_plan pl = new (std::nothrow) mpjsvd_plan_s();
+    if (!pl) return MPJSVD_ERR_OUT_OF_MEMORY;
+    if (pl->p.init(nblk, world, world == 1)) { delete pl; return MPJSVD_ERR_INVALID_ARG; }
+    *out = pl;
+    return 0;
+}
+
+int mpjsvd_plan_info(mpjsvd_plan pl, int32_t* M, int32_t* k, int32_t* nbuf) {
+    if (!pl) return MPJSVD_ERR_INVALID_ARG;
+    if (M) *M = pl->p.M;
+    if (k) *k = pl->p.k;
+    if (nbuf) *nbuf = pl->p.nbuf;
+    return 0;
+}
+
+int mpjsvd_plan_pairs(mpjsvd_plan pl, int32_t rank, int32_t* out) {
+    if (!pl || !out || rank < 0 || rank >= pl->p.G) return MPJSVD_ERR_INVALID_ARG;
+    for (int t = 0; t < pl->p.k; ++t) {
+        const ShardPlan::Pair q = pl->p.pair(rank, t);
+        out[4 * t + 0] = q.buf0; out[4 * t + 1] = q.buf1;
+        out[4 * t + 2] = q.blk0; out[4 * t + 3] = q.blk1;
+    }
+    return pl->p.k;
+}
+
+int mpjsvd_plan_advance(mpjsvd_plan pl, int32_t* moves, int32_t cap) {
+    if (!pl || (cap > 0 && !moves)) return MPJSVD_ERR_INVALID_ARG;
+    std::vector<ShardPlan::Move> mv;
+    pl->p.advance(&mv);
+    const int cnt = (int)mv.size();
+    for (int i = 0; i < cnt && i < cap; ++i) {
+        moves[5 * i + 0] = mv[i].blk; moves[5 * i + 1] = mv[i].src_rank; moves[5 * i + 2] = mv[i].src_buf;
+        moves[5 * i + 3] = mv[i].dst_rank; moves[5 * i + 4] = mv[i].dst_buf;
+    }
+    return cnt;
+}
+
+int mpjsvd_plan_locate(mpjsvd_plan pl, int32_t blk, int32_t* rank, int32_t* buf) {
+    if (!pl) return MPJSVD_ERR_INVALID_ARG;
+    int g = 0, b = 0;
+    if (!pl->p.locate(blk, g, b)) return MPJSVD_ERR_INVALID_ARG;
+    if (rank) *rank = g;
+    if (buf) *buf = b;
+    return 0;
+}
+
+int mpjsvd_plan_destroy(mpjsvd_plan pl) {
+    delete pl;
+    return 0;
+}
 
 int mpjsvd_version(void) { return MPJSVD_VERSION; }
 
@@ -655,8 +1054,10 @@ int mpjsvd_get_profile(mpjsvd_handle h, int32_t idx, char* name, int32_t name_le
 
 int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, double* U, int64_t ldu,
                   double* S, double* V, int64_t ldv, mpjsvd_stats* stats) {
-    if (!h || !A || !U || !S || !V) return MPJSVD_ERR_INVALID_ARG;
-    if (n < 2 || m < n || lda < m || ldu < m || ldv < n) return MPJSVD_ERR_INVALID_ARG;
+    if (!h) return MPJSVD_ERR_INVALID_ARG;
+    const bool root = !h->comm.active() || h->comm.rank == 0;
+    if (root && (!A || !U || !S || !V)) return MPJSVD_ERR_INVALID_ARG;
+    if (n < 2 || m < n || (root && (lda < m || ldu < m || ldv < n))) return MPJSVD_ERR_INVALID_ARG;
     if (m > 16384 || n > 16384) return MPJSVD_ERR_NOT_SUPPORTED;
     if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); return MPJSVD_ERR_CUDA; }
     int rc = factor_impl(h, A, m, n, lda, U, ldu, S, V, ldv, stats);

@@ -40,7 +40,8 @@ def test_strerror_and_defaults():
     o = mp.default_options()
     assert o.block_cols == 32 and o.tol_mult64 == 4.0 and o.inner_tol_div == 8
     assert o.max_sweeps32 == 20 and o.max_sweeps64 == 30 and o.x_from_lq == 1
-    assert mp.lib().mpjsvd_version() == 100
+    assert mp.lib().mpjsvd_version() == 110
+    assert o.virtual_shards == 1 and o.split_rows == 0
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -83,3 +84,17 @@ def test_create_without_gpu_fails_cleanly():
     h = C.c_void_p()
     rc = mp.lib().mpjsvd_create(C.byref(h), None)
     assert rc < 0 and not h.value
+
+
+def test_comm_entry_points_without_gpu():
+    """NCCL is dlopen'd lazily: the unique id is produced (or MPJSVD_ERR_NCCL is
+    returned cleanly) without a GPU, and bad arguments are rejected."""
+    L = mp.lib()
+    buf = C.create_string_buffer(mp.COMM_ID_BYTES)
+    rc = L.mpjsvd_comm_unique_id(buf)
+    assert rc in (0, -5)
+    assert L.mpjsvd_comm_unique_id(None) == -1
+    assert L.mpjsvd_comm_init(None, 0, 1, buf) == -1
+    o = mp.default_options(virtual_shards=0)
+    h = C.c_void_p()
+    assert L.mpjsvd_create(C.byref(h), C.byref(o)) == -1
