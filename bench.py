@@ -384,6 +384,8 @@ def main():
         "clocks": clk,
         "sweeps32": st0["sweeps32"], "sweeps64": st0["sweeps64"],
         "upd_trace32": st0["upd_trace32"], "upd_trace64": st0["upd_trace64"],
+        "inner_max_trace32": st0["inner_max_trace32"], "inner_max_trace64": st0["inner_max_trace64"],
+        "inner_sum_trace32": st0["inner_sum_trace32"], "inner_sum_trace64": st0["inner_sum_trace64"],
         "stage_ms": st0["stage_ms"],
         "check": {"orth_u": orth_u, "orth_v": orth_v, "residual": res},
         "kernels": kernels, "jacobi_roofline": jacobi,

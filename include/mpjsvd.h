@@ -102,6 +102,8 @@ typedef struct {
     double off_trace32[32], off_trace64[32];   /* per-sweep max normalised off-diagonal */
     int32_t upd_trace32[32], upd_trace64[32];  /* per-sweep number of updated block pairs */
     int64_t kernel_launches;   /* kernels launched by this call */
+    int32_t inner_max_trace32[32], inner_max_trace64[32];  /* per sweep: most inner sweeps of one pair */
+    int32_t inner_sum_trace32[32], inner_sum_trace64[32];  /* per sweep: inner sweeps summed over pairs */
 } mpjsvd_stats;
 
 /* Fill *opts with the defaults above. */

@@ -47,7 +47,9 @@ class Stats(C.Structure):
                 ("cond_estimate", C.c_double), ("final_off32", C.c_double), ("final_off64", C.c_double),
                 ("off_trace32", C.c_double * 32), ("off_trace64", C.c_double * 32),
                 ("upd_trace32", C.c_int32 * 32), ("upd_trace64", C.c_int32 * 32),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64),
+                ("inner_max_trace32", C.c_int32 * 32), ("inner_max_trace64", C.c_int32 * 32),
+                ("inner_sum_trace32", C.c_int32 * 32), ("inner_sum_trace64", C.c_int32 * 32)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -63,6 +65,10 @@ class Stats(C.Structure):
             "upd_trace32": list(self.upd_trace32[:min(s32, 32)]),
             "upd_trace64": list(self.upd_trace64[:min(s64, 32)]),
             "kernel_launches": int(self.kernel_launches),
+            "inner_max_trace32": list(self.inner_max_trace32[:min(s32, 32)]),
+            "inner_max_trace64": list(self.inner_max_trace64[:min(s64, 32)]),
+            "inner_sum_trace32": list(self.inner_sum_trace32[:min(s32, 32)]),
+            "inner_sum_trace64": list(self.inner_sum_trace64[:min(s64, 32)]),
         }
 
 

@@ -42,6 +42,7 @@ struct JacobiRound {
     int max_inner;
     double* sweep_off;  // device scalar, atomic max (this sweep)
     int* sweep_upd;     // device scalar, atomic add (this sweep)
+    int* sweep_inner;   // device [2]: max inner sweeps of a pair, summed inner sweeps (this sweep)
 };
 
 // Optional per-launch timing hook (bench profiling): begin/end bracket one launch.

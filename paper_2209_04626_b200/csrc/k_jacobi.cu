@@ -131,7 +131,22 @@ __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
 // pairs carry the identity (c, s) = (1, 0).  See inner_solve_dev for the
 // thread organisation.
 // ------------------------------------------------------------------------
-constexpr int INNER_NT = 256;
+// Inner-solve thread layout (see inner_solve_dev): NB_MAX pair-pair blocks of
+// G, W/2 pairs x W/8 eight-row chunks of E, and one warp for the rotations.
+template <int W>
+constexpr int inner_nb_max() { return (W / 2) * (W / 2 + 1) / 2; }
+template <int W>
+constexpr int inner_g_threads() { return (inner_nb_max<W>() + 31) / 32 * 32; }
+template <int W>
+constexpr int inner_e_items() { return (W / 2) * (W / 8); }
+template <int W>
+constexpr int inner_nt() { return inner_g_threads<W>() + (inner_e_items<W>() + 31) / 32 * 32 + 32; }
+
+// rotation of one pair: (c, s), c - 1 and an active flag, read with one vector load
+template <typename T>
+struct __align__(4 * sizeof(T)) Rot4 {
+    T c, s, cm1, act;
+};
 
 template <typename T, int W>
 struct InnerSmem {
@@ -139,10 +154,9 @@ struct InnerSmem {
     static constexpr int R = W - 1;                    // max rounds per inner sweep
     T G[W * (W + 1)];
     T E[W * (W + 1)];
-    T rc[2][W / 2], rs[2][W / 2], rt[2][W / 2], rm[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];
-    int act[2][W / 2];
-    unsigned char sp[R][W / 2], sq[R][W / 2];          // pair k of round r (p < q; q may be the bye)
-    unsigned char spk[R][W], spart[R][W];              // pair index / partner of index x in round r
+    Rot4<T> rot[2][W / 2];                             // current / next round
+    T rt[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];   // exact 2x2 diagonal update
+    unsigned short spq[R][W / 2];                      // pair k of round r: p | q << 8 (p < q; q may be the bye)
     int nrot[2];
     T red[32];
 };
@@ -170,166 +184,210 @@ __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k,
     // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||
     if (q < w && gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq)) {
         // closest-to-identity rotation (reading c-3)
-        T zeta = (gqq - gpp) / (T(2) * gpq);
-        if (fabs(zeta) > RealTraits<T>::rsqrt_u) {
-            t = T(1) / (T(2) * zeta);
+        if constexpr (sizeof(T) == 4) {
+            // fp32 stage (an initial guess refined in fp64): MUFU rsqrt / fast
+            // division, a few ulp from the IEEE formulas (DESIGN.md c-14)
+            const float zeta = __fdividef(gqq - gpp, 2.0f * gpq);
+            if (fabsf(zeta) > RealTraits<float>::rsqrt_u) {
+                t = __fdividef(0.5f, zeta);
+            } else {
+                const float r1 = fmaf(zeta, zeta, 1.0f);
+                const float sq = r1 * rsqrtf(r1);
+                t = __fdividef(zeta >= 0.0f ? 1.0f : -1.0f, fabsf(zeta) + sq);
+            }
+            const float r2 = fmaf(t, t, 1.0f);
+            c = rsqrtf(r2);
+            sn = t * c;
+            cm1 = -__fdividef(t * t * c, 1.0f + r2 * c);
         } else {
-            T sg = zeta >= T(0) ? T(1) : T(-1);
-            t = sg / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
+            T zeta = (gqq - gpp) / (T(2) * gpq);
+            if (fabs(zeta) > RealTraits<T>::rsqrt_u) {
+                t = T(1) / (T(2) * zeta);
+            } else {
+                T sg = zeta >= T(0) ? T(1) : T(-1);
+                t = sg / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
+            }
+            T rt = sqrt(T(1) + t * t);
+            c = T(1) / rt;
+            sn = t * c;
+            cm1 = -(t * t * c) / (T(1) + rt);
         }
-        T rt = sqrt(T(1) + t * t);
-        c = T(1) / rt;
-        sn = t * c;
-        cm1 = -(t * t * c) / (T(1) + rt);
         active = 1;
     }
-    sm.rc[buf][k] = c;
-    sm.rs[buf][k] = sn;
+    Rot4<T> r4;
+    r4.c = c;
+    r4.s = sn;
+    r4.cm1 = cm1;
+    r4.act = active ? T(1) : T(0);
+    sm.rot[buf][k] = r4;
     sm.rt[buf][k] = t;
-    sm.rm[buf][k] = cm1;
     sm.rg[buf][k] = gpq;
     sm.rpp[buf][k] = gpp;
     sm.rqq[buf][k] = gqq;
-    sm.act[buf][k] = active;
     return active;
 }
 
-// G'[x][x] after the current round (pair kx of index x, parameter buffer buf)
-template <typename T, int W>
-__device__ __forceinline__ T diag_after(const InnerSmem<T, W>& sm, int buf, int kx, int x, int px) {
-    constexpr int GS = InnerSmem<T, W>::GS;
-    if (!sm.act[buf][kx]) return sm.G[x * GS + x];
-    const T t = sm.rt[buf][kx], g = sm.rg[buf][kx];
-    return x == px ? fma_rn(-t, g, sm.rpp[buf][kx]) : fma_rn(t, g, sm.rqq[buf][kx]);
-}
-
-constexpr int INNER_TPP = 8;   // threads owning one rotation pair (INNER_NT / (W/2) at W = 64)
-
-// Row-owner inner solve: INNER_TPP threads own pair A = (p_A, q_A) of the
-// current round and rewrite rows p_A, q_A of G (blocks G[{p_A,q_A}][{p_B,q_B}]
-// <- R_A^T X R_B for every pair B, higher pair index rotated first so that
-// the two owners of a block and its mirror perform identical operations and
-// G stays exactly symmetric) and columns p_A, q_A of E.  The owner of row x
-// then computes the rotation of x's next-round pair (x, y), x < y, from its
-// fresh row and pair(y)'s published parameters; one barrier per inner round.
+// Inner solve, two phases per round of the circle method on the w2 indices
+// (pairs k = 0..P-1 of round r are (sp[r][k], sq[r][k]), p < q, q = w the bye
+// when w is odd).  G is kept as its upper triangle G[min][max] (+ diagonal):
+//   phase A  thread t < NB = P(P+1)/2 owns the pair-pair block (kA, kB),
+//            kA <= kB (fixed for the whole solve): the 2 x 2 block
+//            G[{p_A,q_A}][{p_B,q_B}] <- R_A^T G R_B (B's column rotation first,
+//            then A's row rotation; kA == kB: the exact 2 x 2 diagonal update).
+//            Every element of G is written by exactly one thread.
+//   barrier
+//   phase B  the last warp: lane kn computes the rotation of pair kn of the
+//            next round from the fresh G (reading c-3); the threads between
+//            NB and the last warp apply the current rotations to E's columns
+//            (E <- (I + E) J - I, delta form).
+//   barrier (OR-reduced at the end of an inner sweep: stop when no rotation)
+// Rotations of one round act on disjoint index pairs, so the result is that
+// of the oracle's sequential loop up to the rounding order of the two
+// rotations applied to an off-diagonal block (reading c-5).
 template <typename T, int W>
 __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used) {
     constexpr int GS = InnerSmem<T, W>::GS;
+    constexpr int NG = inner_g_threads<W>();
+    constexpr int NCH = W / 8;                          // eight-row chunks of E per pair
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31;
     const int w2 = w + (w & 1);
     const int P = w2 / 2, NR = w2 - 1;
-    const int tpp = nt / (W / 2);                      // threads per pair (8 at W = 64, 256 threads)
-    const int grp = tid / tpp, gl = tid - (tid / tpp) * tpp;
+    const int NB = P * (P + 1) / 2;
+    const int pwarp0 = nt - 32;                         // first thread of the rotation warp
     for (int e = tid; e < NR * P; e += nt) {
         const int r = e / P, k = e - (e / P) * P;
         const int x = rr_slot(r, k, w2), y = rr_slot(r, w2 - 1 - k, w2);
-        const int p = min(x, y), q = max(x, y);
-        sm.sp[r][k] = (unsigned char)p;
-        sm.sq[r][k] = (unsigned char)q;
-        sm.spk[r][p] = (unsigned char)k;
-        sm.spk[r][q] = (unsigned char)k;
-        sm.spart[r][p] = (unsigned char)q;
-        sm.spart[r][q] = (unsigned char)p;
+        sm.spq[r][k] = (unsigned short)(min(x, y) | (max(x, y) << 8));
     }
     for (int i = tid; i < W * GS; i += nt) sm.E[i] = T(0);
     if (tid < 2) sm.nrot[tid] = 0;
+    // fixed roles: pair-pair block (kA, kB) of G, or (pair kE, rows 8 cE ..) of E
+    int kA = -1, kB = -1, kE = -1, r0E = 0;
+    if (tid < NB) {
+        int rem = tid, row = 0;
+        while (rem >= P - row) { rem -= P - row; ++row; }
+        kA = row;
+        kB = row + rem;
+    } else if (tid >= NG && tid < NG + P * NCH) {
+        kE = (tid - NG) / NCH;
+        r0E = 8 * ((tid - NG) % NCH);
+        if (r0E >= w) kE = -1;
+    }
     __syncthreads();
     if (max_inner < 1) { if (sweeps_used) *sweeps_used = 0; return 0; }
-    if (tid < P) {
-        const int p = sm.sp[0][tid], q = sm.sq[0][tid];
+    int f_cur = 0, f_next = 0, my_cnt = 0;
+    if (tid >= pwarp0 && lane < P) {
+        const unsigned pq = sm.spq[0][lane];
+        const int p = pq & 255, q = pq >> 8;
         const T gpp = sm.G[p * GS + p];
         const T gqq = q < w ? sm.G[q * GS + q] : T(0);
         const T gpq = q < w ? sm.G[p * GS + q] : T(0);
-        if (set_rotation<T, W>(sm, 0, tid, q, w, gpp, gqq, gpq, tol_in)) atomicAdd(&sm.nrot[0], 1);
+        f_cur = set_rotation<T, W>(sm, 0, lane, q, w, gpp, gqq, gpq, tol_in);
     }
     __syncthreads();
-    int total = 0, sweep = 0, r = 0, buf = 0;
+    int sweep = 0, r = 0, buf = 0;
     while (true) {
         const bool last = (r == NR - 1);
         const int rn = last ? 0 : r + 1;
-        const int sn = last ? sweep + 1 : sweep;
-        if (grp < P) {
-            const int k = grp;
-            const int pa = sm.sp[r][k], qa = sm.sq[r][k], aA = sm.act[buf][k];
-            const bool qav = qa < w;
-            const T cA = sm.rc[buf][k], sA = sm.rs[buf][k];
-            for (int B = gl; B < P; B += tpp) {
-                if (B == k) {
-                    if (aA) {
-                        const T t = sm.rt[buf][k], g = sm.rg[buf][k];
-                        sm.G[pa * GS + pa] = fma_rn(-t, g, sm.rpp[buf][k]);
-                        sm.G[qa * GS + qa] = fma_rn(t, g, sm.rqq[buf][k]);
-                        sm.G[pa * GS + qa] = T(0);
-                        sm.G[qa * GS + pa] = T(0);
-                    }
-                    continue;
+        // ---------------- phase A: G blocks (upper triangle G[min][max])
+        if (kA >= 0) {
+            const Rot4<T> RA = sm.rot[buf][kA];
+            const unsigned pqa = sm.spq[r][kA];
+            const int pa = pqa & 255, qa = pqa >> 8;
+            if (kA == kB) {
+                if (RA.act != T(0)) {
+                    const T t = sm.rt[buf][kA], g = sm.rg[buf][kA];
+                    sm.G[pa * GS + pa] = fma_rn(-t, g, sm.rpp[buf][kA]);
+                    sm.G[qa * GS + qa] = fma_rn(t, g, sm.rqq[buf][kA]);
+                    sm.G[pa * GS + qa] = T(0);
+                    ++my_cnt;
                 }
-                const int aB = sm.act[buf][B];
-                if (!aA && !aB) continue;
-                const int pb = sm.sp[r][B], qb = sm.sq[r][B];
-                const bool qbv = qb < w;
-                T x00 = sm.G[pa * GS + pb];
-                T x01 = qbv ? sm.G[pa * GS + qb] : T(0);
-                T x10 = qav ? sm.G[qa * GS + pb] : T(0);
-                T x11 = (qav && qbv) ? sm.G[qa * GS + qb] : T(0);
-                const T cB = sm.rc[buf][B], sB = sm.rs[buf][B];
-                if (B > k) {        // higher pair B first (column op), then own rows
-                    rot2(cB, sB, x00, x01); rot2(cB, sB, x10, x11);
-                    rot2(cA, sA, x00, x10); rot2(cA, sA, x01, x11);
-                } else {            // own pair is the higher one: own rows first, then B's columns
-                    rot2(cA, sA, x00, x10); rot2(cA, sA, x01, x11);
-                    rot2(cB, sB, x00, x01); rot2(cB, sB, x10, x11);
-                }
-                sm.G[pa * GS + pb] = x00;
-                if (qbv) sm.G[pa * GS + qb] = x01;
-                if (qav) sm.G[qa * GS + pb] = x10;
-                if (qav && qbv) sm.G[qa * GS + qb] = x11;
-            }
-            if (aA) {
-                const T cm1 = sm.rm[buf][k];
-                for (int rho = gl; rho < w; rho += tpp) {
-                    T ep = sm.E[rho * GS + pa], eq = sm.E[rho * GS + qa];
-                    rot2(cA, sA, ep, eq);
-                    if (rho == pa) { ep += cm1; eq += sA; }
-                    if (rho == qa) { ep -= sA; eq += cm1; }
-                    sm.E[rho * GS + pa] = ep;
-                    sm.E[rho * GS + qa] = eq;
-                }
-            }
-        }
-        __syncwarp();
-        // parameters of the next round: the owner of the lower index x of each next pair (x, y)
-        if (grp < P && gl < 2) {
-            const int x = gl == 0 ? sm.sp[r][grp] : sm.sq[r][grp];
-            if (x < w) {
-                const int y = sm.spart[rn][x];
-                if (x < y) {
-                    const int kn = sm.spk[rn][x];
-                    T gxx = sm.G[x * GS + x];
-                    T gxy = y < w ? sm.G[x * GS + y] : T(0);
-                    T gyy = T(0);
-                    if (y < w) {
-                        const int B = sm.spk[r][y];
-                        gyy = B == grp ? sm.G[y * GS + y] : diag_after<T, W>(sm, buf, B, y, sm.sp[r][B]);
-                    }
-                    if (set_rotation<T, W>(sm, buf ^ 1, kn, y, w, gxx, gyy, gxy, tol_in))
-                        atomicAdd(&sm.nrot[sn & 1], 1);
+            } else {
+                const Rot4<T> RB = sm.rot[buf][kB];
+                if (RA.act != T(0) || RB.act != T(0)) {
+                    const unsigned pqb = sm.spq[r][kB];
+                    const int pb = pqb & 255, qb = pqb >> 8;
+                    const bool qav = qa < w, qbv = qb < w;
+                    // p_A < q_A and p_B < q_B; the block's canonical positions
+                    const int i00 = pa < pb ? pa * GS + pb : pb * GS + pa;
+                    const int i01 = pa < qb ? pa * GS + qb : qb * GS + pa;
+                    const int i10 = qa < pb ? qa * GS + pb : pb * GS + qa;
+                    const int i11 = qa < qb ? qa * GS + qb : qb * GS + qa;
+                    T x00 = sm.G[i00];
+                    T x01 = qbv ? sm.G[i01] : T(0);
+                    T x10 = qav ? sm.G[i10] : T(0);
+                    T x11 = (qav && qbv) ? sm.G[i11] : T(0);
+                    rot2(RB.c, RB.s, x00, x01); rot2(RB.c, RB.s, x10, x11);     // columns (p_B, q_B)
+                    rot2(RA.c, RA.s, x00, x10); rot2(RA.c, RA.s, x01, x11);     // rows (p_A, q_A)
+                    sm.G[i00] = x00;
+                    if (qbv) sm.G[i01] = x01;
+                    if (qav) sm.G[i10] = x10;
+                    if (qav && qbv) sm.G[i11] = x11;
                 }
             }
         }
         __syncthreads();
+        // ---------------- phase B: next-round rotations | E <- (I + E) J - I
+        if (tid >= pwarp0) {
+            if (lane < P) {
+                const unsigned pq = sm.spq[rn][lane];
+                const int x = pq & 255, y = pq >> 8;
+                const T gxx = sm.G[x * GS + x];
+                const T gyy = y < w ? sm.G[y * GS + y] : T(0);
+                const T gxy = y < w ? sm.G[x * GS + y] : T(0);
+                const int act = set_rotation<T, W>(sm, buf ^ 1, lane, y, w, gxx, gyy, gxy, tol_in);
+                if (last) f_next |= act; else f_cur |= act;
+            }
+        } else if (kE >= 0) {
+            const Rot4<T> R4 = sm.rot[buf][kE];
+            if (R4.act != T(0)) {
+                const unsigned pq = sm.spq[r][kE];
+                const int pa = pq & 255, qa = pq >> 8;
+                T ep[8], eq[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    ep[u] = sm.E[(r0E + u) * GS + pa];
+                    eq[u] = sm.E[(r0E + u) * GS + qa];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) rot2(R4.c, R4.s, ep[u], eq[u]);
+                const int up = pa - r0E, uq = qa - r0E;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (u == up) { ep[u] += R4.cm1; eq[u] += R4.s; }
+                    if (u == uq) { ep[u] -= R4.s; eq[u] += R4.cm1; }
+                    if (r0E + u < w) {
+                        sm.E[(r0E + u) * GS + pa] = ep[u];
+                        sm.E[(r0E + u) * GS + qa] = eq[u];
+                    }
+                }
+            }
+        }
         if (last) {
-            const int nr = sm.nrot[sweep & 1];
-            total += nr;
+            const int any = __syncthreads_or(f_cur);
+            f_cur = f_next;
+            f_next = 0;
+            if (!any || sweep + 1 >= max_inner) break;
+            ++sweep;
+        } else {
             __syncthreads();
-            if (tid == 0) sm.nrot[sweep & 1] = 0;
-            if (nr == 0 || sweep + 1 >= max_inner) break;
         }
         r = rn;
-        sweep = sn;
         buf ^= 1;
     }
     if (sweeps_used) *sweeps_used = sweep + 1;
+    // mirror the upper triangle (callers read G as a full symmetric matrix)
+    for (int e = tid; e < w * w; e += nt) {
+        const int x = e / w, y = e - (e / w) * w;
+        if (x > y) sm.G[x * GS + y] = sm.G[y * GS + x];
+    }
+    // total rotations: warp sums, then one shared atomic per warp
+    const int wsum = __reduce_add_sync(0xffffffffu, (unsigned)my_cnt);
+    if (lane == 0) atomicAdd(&sm.nrot[0], wsum);
+    __syncthreads();
+    const int total = sm.nrot[0];
+    __syncthreads();
     return total;
 }
 
@@ -337,7 +395,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
 // k_pair_solve: one CTA per pair.
 // ------------------------------------------------------------------------
 template <typename T, int W>
-__global__ void __launch_bounds__(INNER_NT) k_pair_solve(JacobiRound<T> a) {
+__global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -378,7 +436,12 @@ __global__ void __launch_bounds__(INNER_NT) k_pair_solve(JacobiRound<T> a) {
         a.flag[pair] = rotate ? 1 : 0;
     }
     if (!rotate) return;
-    inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, nullptr);
+    int used = 0;
+    inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
+    if (tid == 0) {
+        atomicMax(a.sweep_inner, used);
+        atomicAdd(a.sweep_inner + 1, used);
+    }
     T* E = a.E + (long long)pair * (W * W);
     for (int e = tid; e < W * W; e += nt) {
         const int k = e / W, j = e - (e / W) * W;
@@ -870,7 +933,7 @@ __global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
 // k_inner_solve_batch: test entry (mpjsvd_inner_solve): count matrices.
 // ------------------------------------------------------------------------
 template <typename T, int W>
-__global__ void __launch_bounds__(INNER_NT) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
+__global__ void __launch_bounds__(inner_nt<W>()) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -932,7 +995,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
         attr_set = true;
     }
     if (hook) hook->begin(hook->ctx, KName<T>::solve);
-    k_pair_solve<T, W><<<a.npairs, INNER_NT, sms, st>>>(a);
+    k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::solve);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
@@ -1021,7 +1084,7 @@ template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     const size_t sms = sizeof(InnerSmem<T, W>);
     cudaFuncSetAttribute(k_inner_solve_batch<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-    k_inner_solve_batch<T, W><<<count, INNER_NT, sms, st>>>(G, E, w, tol_in, max_inner, rot);
+    k_inner_solve_batch<T, W><<<count, inner_nt<W>(), sms, st>>>(G, E, w, tol_in, max_inner, rot);
     MPJ_LAUNCHED();
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }

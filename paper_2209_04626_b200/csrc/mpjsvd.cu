@@ -157,6 +157,8 @@ struct JacobiResult {
     bool converged = false;
     double off[64] = {};
     int upd[64] = {};
+    int inner_max[64] = {};      // max inner sweeps of a pair, per outer sweep
+    int inner_sum[64] = {};      // summed inner sweeps over the updated pairs, per outer sweep
 };
 
 // Where the X / V column slabs of one Jacobi stage live (shard.h): the
@@ -271,12 +273,13 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     MPJ_TRY(ensure(h, S_PART, sizeof(T) * (size_t)npairs * nsplit * W * W));
     MPJ_TRY(ensure(h, S_E, sizeof(T) * (size_t)npairs * W * W));
     MPJ_TRY(ensure(h, S_JFLAG, sizeof(int) * (size_t)npairs));
-    MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + sizeof(int))));
+    MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + 3 * sizeof(int))));
     MPJ_TRY(ensure(h, S_PTAB, sizeof(PairDesc<T>) * (size_t)R * npairs));
     MPJ_TRY(ensure_pinned(h, sizeof(PairDesc<T>) * (size_t)R * npairs));
     double* d_off = P<double>(h, S_SWEEP);
     int* d_upd = reinterpret_cast<int*>(d_off + 64);
-    MPJ_CUDA_TRY(cudaMemsetAsync(d_off, 0, 64 * (sizeof(double) + sizeof(int)), st));
+    int* d_inner = d_upd + 64;     // [64][2]
+    MPJ_CUDA_TRY(cudaMemsetAsync(d_off, 0, 64 * (sizeof(double) + 3 * sizeof(int)), st));
     PairDesc<T>* d_tab = P<PairDesc<T>>(h, S_PTAB);
     const size_t bytes_x = sizeof(T) * (size_t)S.slab_x, bytes_v = has_v ? sizeof(T) * (size_t)S.slab_v : 0;
 
@@ -300,6 +303,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
                                      cudaMemcpyHostToDevice, st));
         a.sweep_off = d_off + (sw - 1);
         a.sweep_upd = d_upd + (sw - 1);
+        a.sweep_inner = d_inner + 2 * (sw - 1);
         ProfHook hook{&h->prof, &Profiler::hb, &Profiler::he};
         for (int r = 0; r < R; ++r) {
             a.pd = d_tab + (size_t)r * npairs;
@@ -314,6 +318,8 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             MPJ_TRY(h->comm.allreduce_max_f64(d_off + (sw - 1), 1, st));
             MPJ_TRY(h->comm.allreduce_sum_i32(d_upd + (sw - 1), 1, st));
         }
+        MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 2), d_inner + 2 * (sw - 1), 2 * sizeof(int),
+                                     cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
@@ -324,6 +330,8 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         res.sweeps = sw;
         res.off[sw - 1] = off;
         res.upd[sw - 1] = upd;
+        memcpy(&res.inner_max[sw - 1], reinterpret_cast<int*>(hp + 2), sizeof(int));
+        memcpy(&res.inner_sum[sw - 1], reinterpret_cast<int*>(hp + 2) + 1, sizeof(int));
         if (upd == 0) { res.converged = true; break; }
         // fp32 stagnation exit (reading c-10)
         if (stagnation && sw >= 3 && off <= 1e-4 && prev >= 0 && off > 0.25 * prev) { res.converged = true; break; }
@@ -706,6 +714,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         for (int i = 0; i < 32; ++i) {
             s.off_trace32[i] = r32.off[i]; s.upd_trace32[i] = r32.upd[i];
             s.off_trace64[i] = r64.off[i]; s.upd_trace64[i] = r64.upd[i];
+            s.inner_max_trace32[i] = r32.inner_max[i]; s.inner_sum_trace32[i] = r32.inner_sum[i];
+            s.inner_max_trace64[i] = r64.inner_max[i]; s.inner_sum_trace64[i] = r64.inner_sum[i];
         }
         s.final_off32 = r32.sweeps ? r32.off[r32.sweeps - 1] : 0.0;
         s.final_off64 = r64.sweeps ? r64.off[r64.sweeps - 1] : 0.0;
@@ -830,8 +840,13 @@ static int jacobi_entry(mpjsvd_handle h, T* X, int64_t m, int64_t n, int64_t ldx
     if (stats) {
         memset(stats, 0, sizeof(*stats));
         for (int i = 0; i < 32; ++i) {
-            if (is64) { stats->off_trace64[i] = r.off[i]; stats->upd_trace64[i] = r.upd[i]; }
-            else { stats->off_trace32[i] = r.off[i]; stats->upd_trace32[i] = r.upd[i]; }
+            if (is64) {
+                stats->off_trace64[i] = r.off[i]; stats->upd_trace64[i] = r.upd[i];
+                stats->inner_max_trace64[i] = r.inner_max[i]; stats->inner_sum_trace64[i] = r.inner_sum[i];
+            } else {
+                stats->off_trace32[i] = r.off[i]; stats->upd_trace32[i] = r.upd[i];
+                stats->inner_max_trace32[i] = r.inner_max[i]; stats->inner_sum_trace32[i] = r.inner_sum[i];
+            }
         }
         if (is64) stats->sweeps64 = r.sweeps; else stats->sweeps32 = r.sweeps;
         stats->converged = r.converged;

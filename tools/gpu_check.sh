@@ -18,3 +18,10 @@ for w in $WHAT; do
             python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?" ;;
   esac
 done
+# ncu --set full of the Jacobi kernels on C3 (one launch each, round 11 of sweep 1)
+if [[ " $WHAT " == *" ncufull "* ]]; then
+  timeout 600 python bench.py --config C3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/plain_C3.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_pair_(solve|update|gram)" -s 30 -c 3 \
+     -o $OUT/prof_C3 python bench.py --config C3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
+  echo "ncu full rc=$?"
+fi
