@@ -88,6 +88,9 @@ typedef struct {
                                   (the multi-GPU data path, testable on one device) */
     int32_t split_rows;        /* > 0: rows per Gram row-split (fixes the fp summation order across
                                   shard counts); 0 (default): chosen per launch for SM fill */
+    int32_t fp32_tensor_cores; /* 1 (default): the fp32 stage's Gram and update products (b = 32) run on
+                                  the tcgen05 TF32 tensor cores with a hi/lo split (~2^-21 relative per
+                                  product, fp32 accumulation; reading c-20); 0: FFMA SIMT */
 } mpjsvd_options;
 
 typedef struct {

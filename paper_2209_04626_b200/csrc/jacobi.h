@@ -43,6 +43,7 @@ struct JacobiRound {
     double* sweep_off;  // device scalar, atomic max (this sweep)
     int* sweep_upd;     // device scalar, atomic add (this sweep)
     int* sweep_inner;   // device [2]: max inner sweeps of a pair, summed inner sweeps (this sweep)
+    int use_tc;         // fp32, W = 64: tcgen05 TF32 (hi/lo split) Gram and update (k_tc.cu)
 };
 
 // Optional per-launch timing hook (bench profiling): begin/end bracket one launch.
@@ -55,7 +56,11 @@ struct ProfHook {
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook = nullptr);
 template <typename T>
-int gram_ctas_per_sm(int W);
+int gram_ctas_per_sm(int W, int use_tc);
+// tcgen05 fp32 kernels (k_tc.cu)
+int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
+int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);
+int gram_tc_ctas_per_sm();
 template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
 

@@ -976,6 +976,11 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
         }
         k_pair_gram_dmma<W><<<dim3(a.nsplit, a.npairs), 128, gram_dmma_smem(W), st>>>(a);
     } else if constexpr (W == 64) {
+        if (a.use_tc) {
+            launch_gram_tc(a, st);
+            if (hook) hook->end(hook->ctx, KName<T>::gram);
+            goto solve;
+        }
         const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
         static bool attr_t = false;
         if (!attr_t) {
@@ -988,6 +993,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
     }
     MPJ_LAUNCHED();
     if (hook) hook->end(hook->ctx, KName<T>::gram);
+solve:
     const size_t sms = sizeof(InnerSmem<T, W>);
     static bool attr_set = false;
     if (!attr_set) {
@@ -1015,6 +1021,8 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
             attr_d = true;
         }
         k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.has_v ? 2 : 1), 256, dsm, st>>>(a);
+    } else if (W == 64 && a.use_tc) {
+        if constexpr (sizeof(T) == 4) launch_update_tc(a, st);
     } else {
         const size_t fsm = sizeof(float) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
         static bool attr_f = false;
@@ -1037,7 +1045,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
 
 // resident CTAs per SM of the Gram kernel used for (T, W) (for the split choice)
 template <typename T>
-int gram_ctas_per_sm(int W) {
+int gram_ctas_per_sm(int W, int use_tc) {
     int per = 1;
     if constexpr (sizeof(T) == 8) {
         const size_t smem = gram_dmma_smem(W);
@@ -1052,7 +1060,9 @@ int gram_ctas_per_sm(int W) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_dmma<16>, 128, smem);
         }
     } else {
-        if (W == 64) {
+        if (W == 64 && use_tc) {
+            per = gram_tc_ctas_per_sm();
+        } else if (W == 64) {
             const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
             cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pair_gram_f32t, G32_NT, g32);
@@ -1065,8 +1075,8 @@ int gram_ctas_per_sm(int W) {
     cudaGetLastError();
     return per < 1 ? 1 : per;
 }
-template int gram_ctas_per_sm<float>(int);
-template int gram_ctas_per_sm<double>(int);
+template int gram_ctas_per_sm<float>(int, int);
+template int gram_ctas_per_sm<double>(int, int);
 
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook) {

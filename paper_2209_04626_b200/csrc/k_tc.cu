@@ -1,0 +1,458 @@
+// k_tc.cu -- tcgen05 (5th-generation tensor core) kernels of the fp32 Jacobi
+// stage (reading c-20).
+//
+// The fp32 block Jacobi's two dense contractions run on the TF32 tensor cores
+// with fp32 operands split as x = hi + lo (hi = x with the low 13 mantissa
+// bits cleared, i.e. exactly representable in tf32; lo = x - hi exactly),
+// accumulating in TMEM in fp32:
+//   k_pair_gram_tc    G = W^T W of a row slab of W = [X_I X_J] (n x 64):
+//                     A = [W_hi^T ; W_lo^T] (128 x K), B_hi = W_hi^T, B_lo = W_lo^T,
+//                     D = A B_hi^T + A B_lo^T (M = 128, N = 64), so that
+//                     G = D[0:64] + D[64:128] = (hi + lo)^T (hi + lo);
+//   k_pair_update_tc  out = W + W E on 128-row tiles:
+//                     D = W_hi E_hi + W_lo E_hi + W_hi E_lo (3 passes, K = 64).
+// Per-product error ~2^-21 relative (the lo parts are tf32-truncated by the
+// MMA), against 2^-24 for FFMA: the fp32 stage only produces the initial
+// guess the fp64 refinement corrects (reading c-20).
+//
+// Operands are staged by the threads into shared memory in the canonical
+// K-major SWIZZLE_NONE layout (core matrices of 8 rows x 16 B; LBO = 128 B
+// between the two k-halves of a K = 8 step, SBO between 8-row groups); one
+// elected thread issues tcgen05.mma, completion is signalled through
+// tcgen05.commit -> mbarrier, and the epilogue reads TMEM with tcgen05.ld
+// (warp w owns TMEM lanes 32w..32w+31).  Validated by tools/tc_probe.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+#include "jacobi.h"
+
+namespace mpj {
+
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// shared-memory matrix descriptor: SWIZZLE_NONE, version 1 (sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor kind::tf32, fp32 accumulate, both operands K-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(mbar)));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(mbar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(smem_u32(mbar)), "r"(parity));
+    }
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n"); }
+
+template <int NCOL>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst) {   // one full warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)), "n"(NCOL));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+template <int NCOL>
+__device__ __forceinline__ void tmem_free(uint32_t base) {     // the allocating warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "n"(NCOL));
+}
+// 32 lanes x 16 columns of fp32 (thread = lane, v[j] = column c0 + j)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+__device__ __forceinline__ float hi_part(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ float4 hi4(float4 v) { return make_float4(hi_part(v.x), hi_part(v.y), hi_part(v.z), hi_part(v.w)); }
+__device__ __forceinline__ float4 lo4(float4 v, float4 h) { return make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w); }
+
+// byte offset of element (r, k) in a K-major SWIZZLE_NONE operand with KK columns
+__device__ __forceinline__ uint32_t koff(int r, int k, int KK) {
+    return (uint32_t)(((r >> 3) * (KK >> 2) + (k >> 2)) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+// 4 x 4 transpose inside each quad of lanes: lane i holds row i of a 4 x 4
+// block in v (v.x = column 0 ...) and ends with column i (two butterfly
+// stages; each swaps the elements whose index bit differs from the lane's).
+__device__ __forceinline__ float4 quad_transpose(float4 v, int lane) {
+    const bool b0 = lane & 1, b1 = (lane >> 1) & 1;
+    float x = b0 ? v.x : v.y, y = b0 ? v.z : v.w;
+    float rx = __shfl_xor_sync(0xffffffffu, x, 1), ry = __shfl_xor_sync(0xffffffffu, y, 1);
+    if (b0) { v.x = rx; v.z = ry; } else { v.y = rx; v.w = ry; }
+    x = b1 ? v.x : v.z;
+    y = b1 ? v.y : v.w;
+    rx = __shfl_xor_sync(0xffffffffu, x, 2);
+    ry = __shfl_xor_sync(0xffffffffu, y, 2);
+    if (b1) { v.x = rx; v.y = ry; } else { v.z = rx; v.w = ry; }
+    return v;
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------------
+// k_pair_gram_tc: grid (nsplit, npairs), 128 threads.  The CTA's row slab
+// streams through GT_ST shared stages of 32 rows.  A stage holds the operand
+// A = [W^T ; W_lo^T] (128 x 32, K-major): rows 0..63 are the raw fp32 W
+// chunks, copied straight from global memory with cp.async (the tensor core
+// truncates them to tf32, which is exactly the hi part), rows 64..127 the lo
+// parts x - trunc(x) written by the thread that copied the chunk.
+// Epilogue: D rows 64..127 (warps 2, 3) through shared memory into rows
+// 0..63 (warps 0, 1); the full 64 x 64 partial Gram is written row-major.
+// ------------------------------------------------------------------------
+constexpr int GT_KT = 32, GT_ST = 6, GT_NT = 128;
+constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;        // 16 KB
+constexpr size_t gram_tc_smem() { return (size_t)GT_ST * GT_STAGE_BYTES + 1024; }
+
+__device__ __forceinline__ void cp16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a) {
+    extern __shared__ __align__(1024) unsigned char gt_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gt_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t mbar[GT_ST + 1];
+    __shared__ uint32_t tmem_base;
+    __shared__ const float* colp[64];
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    if (tid < 64) colp[tid] = tid < w ? (tid < pd.w0 ? pd.x0 + (long long)tid * a.ldx : pd.x1 + (long long)(tid - pd.w0) * a.ldx) : nullptr;
+    if (warp == 0) tc::tmem_alloc<64>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s <= GT_ST; ++s) tc::mbar_init(&mbar[s]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg) / GT_KT);
+    constexpr uint32_t SBO = (GT_KT / 4) * 128;         // 1024 B between 8-row groups
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    const uint32_t sbase = tc::smem_u32(sm);
+    // this thread's 4 chunks f = tid + 128 u: column c = 8 (f >> 6) + (f & 7), rows 4 ((f >> 3) & 7) .. + 3
+    const float* src[4];
+    uint32_t soff[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int f = tid + 128 * u;
+        const int c = 8 * (f >> 6) + (f & 7), k4 = (f >> 3) & 7;
+        src[u] = colp[c] ? colp[c] + 4 * k4 : nullptr;
+        soff[u] = (uint32_t)(((f >> 6) * (GT_KT / 4) + k4) * 128 + (f & 7) * 16);
+    }
+    auto issue = [&](int t) {               // raw chunks of tile t -> stage t % GT_ST (rows 0..63)
+        unsigned char* st = sm + (size_t)(t % GT_ST) * GT_STAGE_BYTES;
+        const long long r0 = rbeg + (long long)t * GT_KT;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (src[u]) cp16(sbase + (uint32_t)((t % GT_ST) * GT_STAGE_BYTES) + soff[u], src[u] + r0);
+            else *reinterpret_cast<float4*>(st + soff[u]) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+#pragma unroll
+    for (int t = 0; t < GT_ST - 1; ++t) {
+        if (t < ntile) issue(t);
+        cp_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+        const int s = t % GT_ST;
+        unsigned char* st = sm + (size_t)s * GT_STAGE_BYTES;
+        cp_wait<GT_ST - 2>();                           // this thread's chunks of tile t have landed
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 x = *reinterpret_cast<const float4*>(st + soff[u]);
+            *reinterpret_cast<float4*>(st + soff[u] + 8 * SBO) = tc::lo4(x, tc::hi4(x));
+        }
+        tc::fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t base = sbase + (uint32_t)(s * GT_STAGE_BYTES);
+#pragma unroll
+            for (int ks = 0; ks < GT_KT / 8; ++ks) {
+                const uint64_t ad = tc::sdesc(base + ks * 256, 128, SBO);
+                const uint64_t bl = tc::sdesc(base + 8 * SBO + ks * 256, 128, SBO);
+                tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);   // B = rows 0..63 = W^T (hi)
+                tc::mma(tmem, ad, bl, idesc, 1u);                               // B = W_lo^T
+            }
+            tc::commit(&mbar[s]);
+        }
+        // refill: tile t + GT_ST - 1 goes to the stage of tile t - 1 once its MMAs are done
+        const int tn = t + GT_ST - 1;
+        if (tn < ntile) {
+            if (t >= 1) tc::mbar_wait(&mbar[(t - 1) % GT_ST], (uint32_t)(((t - 1) / GT_ST) & 1));
+            issue(tn);
+        }
+        cp_commit();
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);           // 64 x 65 floats (stages are free after the last MMA)
+    cp_wait<0>();
+    if (ntile > 0) {
+        if (tid == 0) tc::commit(&mbar[GT_ST]);
+        tc::mbar_wait(&mbar[GT_ST], 0);
+        tc::fence_after();
+        if (warp >= 2) {
+            const int row = 32 * (warp - 2) + (tid & 31);
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[row * 65 + c0 + j] = v[j];
+            }
+        }
+        __syncthreads();
+        if (warp < 2) {
+            const int row = 32 * warp + (tid & 31);
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[row * 65 + c0 + j] += v[j];
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = red[(e >> 6) * 65 + (e & 63)];
+    } else {
+        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
+// ------------------------------------------------------------------------
+// k_pair_update_tc: grid (tile groups, npairs, 2 [X, V]), 256 threads;
+// out = W + W E on 128-row tiles, two tiles in flight:
+//   tile t:   loads (issued during tile t-1) -> 4 x 4 quad transposes (thread
+//             row = tid % 128, columns 32 (tid / 128) .. + 31) -> A_hi / A_lo
+//             (K-major, buffer t % 2) and the exact W row into TMEM
+//             accumulator t % 2 (tcgen05.st) -> MMAs D += W_hi E_hi + W_lo E_hi
+//             + W_hi E_lo (thread 0, commit -> mbar[t % 2]);
+//   meanwhile the epilogue of tile t - 1 drains accumulator (t-1) % 2
+//             (tcgen05.ld; one coalesced 128-byte store per warp and column).
+// E^T is staged once per CTA (hi / lo, K-major B operand).
+// ------------------------------------------------------------------------
+constexpr int UT_NT = 256, UT_TM = 128;
+constexpr size_t update_tc_smem() { return (size_t)2 * 64 * 64 * 4 + (size_t)4 * UT_TM * 64 * 4 + 1024; }
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])));
+}
+
+__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> a, int tiles_per_cta) {
+    extern __shared__ __align__(1024) unsigned char ut_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ut_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* Bh = sm;                       // E^T hi: 64 x 64 K-major (16 KB)
+    unsigned char* Bl = sm + 16384;               // E^T lo
+    unsigned char* Abuf = sm + 32768;             // [2][hi 32 KB | lo 32 KB]: W tile, 128 x 64 K-major
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float* colp[64];
+    const int pair = blockIdx.y, which = blockIdx.z;
+    if (!a.flag[pair]) return;
+    if (which && !a.has_v) return;
+    const long long ld = which ? a.ldv : a.ldx;
+    const long long rows_pad = which ? a.nv_pad : a.m_pad;
+    const long long row_lo = (long long)blockIdx.x * tiles_per_cta * UT_TM;
+    if (row_lo >= rows_pad) return;
+    const long long row_hi = min(rows_pad, row_lo + (long long)tiles_per_cta * UT_TM);
+    const int ntile = (int)((row_hi - row_lo + UT_TM - 1) / UT_TM);
+    const int tid = threadIdx.x, warp = tid >> 5, qi = tid & 3;
+    const int trow = tid & 127, half = tid >> 7;  // tile row (= TMEM lane) and column half of this thread
+    const PairDesc<float> pd = a.pd[pair];
+    const int w = pd.w0 + pd.w1;
+    float* const s0 = which ? pd.v0 : pd.x0;
+    float* const s1 = which ? pd.v1 : pd.x1;
+    if (tid < 64) colp[tid] = tid < w ? (tid < pd.w0 ? s0 + (long long)tid * ld : s1 + (long long)(tid - pd.w0) * ld) : nullptr;
+    if (warp == 0) tc::tmem_alloc<128>(&tmem_base);
+    if (tid == 0) {
+        tc::mbar_init(&mbar[0]);
+        tc::mbar_init(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    // B = E^T: B[n][k] = E[k][n]; item (n, k4): float4 over k
+    const float* Eg = a.E + (long long)pair * (64 * 64);
+    for (int it = tid; it < 64 * 16; it += UT_NT) {
+        const int n = it & 63, k4 = it >> 6;
+        float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
+                               Eg[(4 * k4 + 3) * 64 + n]);
+        const uint32_t o = tc::koff(n, 4 * k4, 64);
+        const float4 h = tc::hi4(v);
+        *reinterpret_cast<float4*>(Bh + o) = h;
+        *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    constexpr uint32_t SBO = 16 * 128;                  // 64 columns: 2048 B between 8-row groups
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    // this thread loads, for u < 8: rows r0 + 4 (trow / 4) .. + 3 of column 32 half + 4u + qi
+    float4 v[8];
+    auto load = [&](int t) {
+        const long long rr = row_lo + (long long)t * UT_TM + 4 * (trow >> 2);
+        const bool rok = rr < rows_pad;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float* p = colp[32 * half + 4 * u + qi];
+            v[u] = (p && rok) ? __ldg(reinterpret_cast<const float4*>(p + rr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto epilogue = [&](int t) {
+        const long long row = row_lo + (long long)t * UT_TM + trow;
+        const bool rok = row < rows_pad;
+        const uint32_t acc = tmem + (uint32_t)(64 * (t & 1));
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += 16) {
+            float d[16];
+            tc::tmem_ld16(acc + lane_base + (uint32_t)(32 * half + c0), d);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c = 32 * half + c0 + j;
+                if (rok && c < w) {
+                    float* p = c < pd.w0 ? s0 + (long long)c * ld : s1 + (long long)(c - pd.w0) * ld;
+                    p[row] = d[j];
+                }
+            }
+        }
+    };
+    load(0);
+    for (int t = 0; t < ntile; ++t) {
+        const int b = t & 1;
+        unsigned char* Ah = Abuf + (size_t)b * 65536;
+        unsigned char* Al = Ah + 32768;
+        // ---- stage tile t: transpose, split, W row -> TMEM accumulator b
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {           // 16 columns at a time
+            float wv[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int u = 4 * g + q;
+                const float4 x = tc::quad_transpose(v[u], qi);
+                wv[4 * q] = x.x; wv[4 * q + 1] = x.y; wv[4 * q + 2] = x.z; wv[4 * q + 3] = x.w;
+                const uint32_t o = tc::koff(trow, 32 * half + 4 * u, 64);
+                const float4 h = tc::hi4(x);
+                *reinterpret_cast<float4*>(Ah + o) = h;
+                *reinterpret_cast<float4*>(Al + o) = tc::lo4(x, h);
+            }
+            tmem_st16(tmem + (uint32_t)(64 * b) + lane_base + (uint32_t)(32 * half + 16 * g), wv);
+        }
+        if (t + 1 < ntile) load(t + 1);          // in flight during the MMAs and the epilogue below
+        asm volatile("tcgen05.wait::st.sync.aligned;\n");
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t ah = tc::smem_u32(Ah), al = tc::smem_u32(Al), bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
+            const uint32_t acc = tmem + (uint32_t)(64 * b);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                tc::mma(acc, tc::sdesc(ah + ks * 256, 128, SBO), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                tc::mma(acc, tc::sdesc(al + ks * 256, 128, SBO), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                tc::mma(acc, tc::sdesc(ah + ks * 256, 128, SBO), tc::sdesc(bl + ks * 256, 128, SBO), idesc, 1u);
+            tc::commit(&mbar[b]);
+        }
+        // ---- epilogue of tile t - 1 (its MMAs were issued one iteration ago)
+        if (t >= 1) {
+            tc::mbar_wait(&mbar[b ^ 1], (uint32_t)(((t - 1) >> 1) & 1));
+            tc::fence_after();
+            epilogue(t - 1);
+        }
+        // buffers b ^ 1 (A and accumulator) are free for tile t + 1 after this barrier
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (ntile >= 1) {
+        const int t = ntile - 1;
+        tc::mbar_wait(&mbar[t & 1], (uint32_t)((t >> 1) & 1));
+        tc::fence_after();
+        epilogue(t);
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<128>(tmem);
+}
+
+// ------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------
+int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pair_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem());
+        attr = true;
+    }
+    k_pair_gram_tc<<<dim3(a.nsplit, a.npairs), GT_NT, gram_tc_smem(), st>>>(a);
+    MPJ_LAUNCHED();
+    return 0;
+}
+
+int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pair_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
+        attr = true;
+    }
+    const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
+    const long long tiles = (rows_pad + UT_TM - 1) / UT_TM;
+    const int tpc = tiles >= 16 ? 16 : (int)tiles;
+    const unsigned gx = (unsigned)((tiles + tpc - 1) / tpc);
+    k_pair_update_tc<<<dim3(gx, a.npairs, a.has_v ? 2 : 1), UT_NT, update_tc_smem(), st>>>(a, tpc);
+    MPJ_LAUNCHED();
+    return 0;
+}
+
+int gram_tc_ctas_per_sm() {
+    // shared memory bound: (GT_ST stages + alignment + static) per CTA of 228 KB per SM
+    const int per = (int)((228 * 1024) / (gram_tc_smem() + 2048));
+    return per < 2 ? per : 2;                       // __launch_bounds__(GT_NT, 2)
+}
+
+}  // namespace mpj

@@ -252,13 +252,14 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     const int R = S.plan.M - 1;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
+    const int use_tc = (sizeof(T) == 4 && W == 64 && h->opts.fp32_tensor_cores) ? 1 : 0;
     long long nsplit = 1;
     if (h->opts.split_rows > 0) {
         nsplit = ceil_div(m_pad, round_up(h->opts.split_rows, 32));
     } else {
         // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
         // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
-        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W);
+        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc);
         const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
         double best = 1e30;
         for (long long ns = 1; ns <= maxsplit; ++ns) {
@@ -290,6 +291,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.nsplit = (int)nsplit; a.rows_per_split = rps;
     a.partial = P<T>(h, S_PART); a.E = P<T>(h, S_E); a.flag = P<int>(h, S_JFLAG);
     a.tol = tol; a.tol_in = tol_in; a.max_inner = max_inner;
+    a.use_tc = use_tc;
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
     double prev = -1.0;
@@ -875,6 +877,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->stream = nullptr;
     o->virtual_shards = 1;
     o->split_rows = 0;
+    o->fp32_tensor_cores = 1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {

@@ -124,3 +124,22 @@ def test_nccl_communicator_world1_equals_plain(mp):
     U2, S2, V2, st2 = mp.factor(dev(a), handle=h)
     assert torch.equal(S1, S2) and torch.equal(U1, U2) and torch.equal(V1, V2)
     assert st1["sweeps64"] == st2["sweeps64"]
+
+
+@pytest.mark.parametrize("n", [256, 1000])
+def test_fp32_tensor_core_stage_vs_simt_and_oracle(mp, n):
+    """The fp32 stage on tcgen05 TF32 (hi/lo split, reading c-20) against the
+    FFMA path and the oracle: same sweeps +-1, and the final SVD within the
+    parity bar either way."""
+    a = testmat.config_matrix("C5", n)
+    U1, S1, V1, st1 = mp.factor(dev(a), fp32_tensor_cores=1)
+    U0, S0, V0, st0 = mp.factor(dev(a), fp32_tensor_cores=0)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a)
+    for (U, S, V, st) in ((U1, S1, V1, st1), (U0, S0, V0, st0)):
+        U, S, V = host(U), host(S), host(V)
+        assert orth(U) <= 1e-13 and orth(V) <= 1e-13
+        assert np.linalg.norm(a - (U * S) @ V.T) / np.linalg.norm(a) <= 1e-13
+        k = so[0] / so[-1]
+        assert np.all(np.abs(S - so) / so <= tiered(so, k))
+        assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
+        assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
