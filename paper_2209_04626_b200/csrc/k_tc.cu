@@ -117,16 +117,17 @@ __device__ __forceinline__ float4 quad_transpose(float4 v, int lane) {
 
 // ------------------------------------------------------------------------
 // k_pair_gram_tc: grid (nsplit, npairs), 128 threads.  The CTA's row slab
-// streams through GT_ST shared stages of 32 rows.  A stage holds the operand
-// A = [W^T ; W_lo^T] (128 x 32, K-major): rows 0..63 are the raw fp32 W
-// chunks, copied straight from global memory with cp.async (the tensor core
-// truncates them to tf32, which is exactly the hi part), rows 64..127 the lo
-// parts x - trunc(x) written by the thread that copied the chunk.
-// Epilogue: D rows 64..127 (warps 2, 3) through shared memory into rows
-// 0..63 (warps 0, 1); the full 64 x 64 partial Gram is written row-major.
+// streams through GT_ST shared stages of GT_KT rows.  A stage holds the
+// operand A = [H^T ; L^T] (128 x GT_KT, K-major): rows 0..63 are the raw fp32
+// W chunks, copied from global memory with cp.async (the tensor core
+// truncates them to tf32: exactly the hi part H), rows 64..127 the lo parts
+// L = W - H written by the thread that copied the chunk.  One MMA per K = 8
+// step, D = A H (M = 128, N = 64), gives D[0:64] = H^T H and D[64:128] = L^T H,
+// and G = H^T H + L^T H + (L^T H)^T (the lo x lo term, ~2^-22, is dropped).
 // ------------------------------------------------------------------------
-constexpr int GT_KT = 32, GT_ST = 6, GT_NT = 128;
-constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;        // 16 KB
+constexpr int GT_KT = 64, GT_ST = 3, GT_NT = 128;
+constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;        // 32 KB
+constexpr int GT_CHUNKS = 64 * (GT_KT / 4) / GT_NT;   // 16-byte chunks per thread per tile (8)
 constexpr size_t gram_tc_smem() { return (size_t)GT_ST * GT_STAGE_BYTES + 1024; }
 
 __device__ __forceinline__ void cp16(uint32_t saddr, const void* g) {
@@ -158,26 +159,29 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
     const uint32_t tmem = tmem_base;
     const long long rbeg = (long long)split * a.rows_per_split;
     const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
-    const int ntile = (int)((rend - rbeg) / GT_KT);
-    constexpr uint32_t SBO = (GT_KT / 4) * 128;         // 1024 B between 8-row groups
+    const int ntile = (int)((rend - rbeg + GT_KT - 1) / GT_KT);
+    constexpr uint32_t SBO = (GT_KT / 4) * 128;         // 2048 B between 8-row groups
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
     const uint32_t sbase = tc::smem_u32(sm);
-    // this thread's 4 chunks f = tid + 128 u: column c = 8 (f >> 6) + (f & 7), rows 4 ((f >> 3) & 7) .. + 3
-    const float* src[4];
-    uint32_t soff[4];
+    // chunk f = tid + 128 u: column c = 8 (f / (8 KT/4)) + (f & 7), rows 4 k4 .. + 3, k4 = (f >> 3) % (KT/4)
+    const float* src[GT_CHUNKS];
+    uint32_t soff[GT_CHUNKS];
+    int krow[GT_CHUNKS];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int f = tid + 128 * u;
-        const int c = 8 * (f >> 6) + (f & 7), k4 = (f >> 3) & 7;
+    for (int u = 0; u < GT_CHUNKS; ++u) {
+        const int f = tid + GT_NT * u;
+        const int cg = f / (8 * (GT_KT / 4)), k4 = (f >> 3) % (GT_KT / 4), c8 = f & 7;
+        const int c = 8 * cg + c8;
         src[u] = colp[c] ? colp[c] + 4 * k4 : nullptr;
-        soff[u] = (uint32_t)(((f >> 6) * (GT_KT / 4) + k4) * 128 + (f & 7) * 16);
+        krow[u] = 4 * k4;
+        soff[u] = (uint32_t)((cg * (GT_KT / 4) + k4) * 128 + c8 * 16);
     }
     auto issue = [&](int t) {               // raw chunks of tile t -> stage t % GT_ST (rows 0..63)
         unsigned char* st = sm + (size_t)(t % GT_ST) * GT_STAGE_BYTES;
         const long long r0 = rbeg + (long long)t * GT_KT;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (src[u]) cp16(sbase + (uint32_t)((t % GT_ST) * GT_STAGE_BYTES) + soff[u], src[u] + r0);
+        for (int u = 0; u < GT_CHUNKS; ++u) {
+            if (src[u] && r0 + krow[u] < rend) cp16(sbase + (uint32_t)((t % GT_ST) * GT_STAGE_BYTES) + soff[u], src[u] + r0);
             else *reinterpret_cast<float4*>(st + soff[u]) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
         unsigned char* st = sm + (size_t)s * GT_STAGE_BYTES;
         cp_wait<GT_ST - 2>();                           // this thread's chunks of tile t have landed
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < GT_CHUNKS; ++u) {
             const float4 x = *reinterpret_cast<const float4*>(st + soff[u]);
             *reinterpret_cast<float4*>(st + soff[u] + 8 * SBO) = tc::lo4(x, tc::hi4(x));
         }
@@ -203,9 +207,7 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
 #pragma unroll
             for (int ks = 0; ks < GT_KT / 8; ++ks) {
                 const uint64_t ad = tc::sdesc(base + ks * 256, 128, SBO);
-                const uint64_t bl = tc::sdesc(base + 8 * SBO + ks * 256, 128, SBO);
-                tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);   // B = rows 0..63 = W^T (hi)
-                tc::mma(tmem, ad, bl, idesc, 1u);                               // B = W_lo^T
+                tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);   // B = rows 0..63 = H^T
             }
             tc::commit(&mbar[s]);
         }
@@ -218,35 +220,26 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
         cp_commit();
     }
     float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
-    float* red = reinterpret_cast<float*>(sm);           // 64 x 65 floats (stages are free after the last MMA)
+    float* red = reinterpret_cast<float*>(sm);           // 2 x 64 x 65 floats (stages are free after the last MMA)
     cp_wait<0>();
     if (ntile > 0) {
         if (tid == 0) tc::commit(&mbar[GT_ST]);
         tc::mbar_wait(&mbar[GT_ST], 0);
         tc::fence_after();
-        if (warp >= 2) {
-            const int row = 32 * (warp - 2) + (tid & 31);
+        // every thread: TMEM lane tid (row tid of D) -> red[tid / 64][tid % 64][:]
 #pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                float v[16];
-                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) red[row * 65 + c0 + j] = v[j];
-            }
+            for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
         }
         __syncthreads();
-        if (warp < 2) {
-            const int row = 32 * warp + (tid & 31);
-#pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                float v[16];
-                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) red[row * 65 + c0 + j] += v[j];
-            }
+        // G[p][q] = (H^T H)[p][q] + (L^T H)[p][q] + (L^T H)[q][p]
+        for (int e = tid; e < 64 * 64; e += GT_NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
         }
-        __syncthreads();
-        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = red[(e >> 6) * 65 + (e & 63)];
     } else {
         for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
     }
@@ -257,18 +250,21 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
 
 // ------------------------------------------------------------------------
 // k_pair_update_tc: grid (tile groups, npairs, 2 [X, V]), 256 threads;
-// out = W + W E on 128-row tiles, two tiles in flight:
-//   tile t:   loads (issued during tile t-1) -> 4 x 4 quad transposes (thread
-//             row = tid % 128, columns 32 (tid / 128) .. + 31) -> A_hi / A_lo
-//             (K-major, buffer t % 2) and the exact W row into TMEM
-//             accumulator t % 2 (tcgen05.st) -> MMAs D += W_hi E_hi + W_lo E_hi
-//             + W_hi E_lo (thread 0, commit -> mbar[t % 2]);
-//   meanwhile the epilogue of tile t - 1 drains accumulator (t-1) % 2
-//             (tcgen05.ld; one coalesced 128-byte store per warp and column).
-// E^T is staged once per CTA (hi / lo, K-major B operand).
+// out = W + W E on 128-row tiles.  Raw tiles (column-major 128 x 64 fp32)
+// stream into a UT_NR-deep cp.async ring; per tile the threads transpose
+// from shared memory (thread: row tid % 128, columns 32 (tid / 128) .. + 31;
+// a warp reads 32 consecutive rows of a column: conflict-free), split into
+// A_hi / A_lo (K-major) and write the exact W row into TMEM accumulator
+// t % 2 (tcgen05.st); thread 0 issues D += W_hi E_hi + W_lo E_hi + W_hi E_lo
+// (24 MMAs, commit -> mbar[t % 2]); the epilogue of tile t - 1 then drains
+// accumulator (t-1) % 2 (tcgen05.ld, one coalesced 128-byte store per warp and
+// column) while the MMAs of tile t run.  E^T is staged once per CTA.
 // ------------------------------------------------------------------------
-constexpr int UT_NT = 256, UT_TM = 128;
-constexpr size_t update_tc_smem() { return (size_t)2 * 64 * 64 * 4 + (size_t)4 * UT_TM * 64 * 4 + 1024; }
+constexpr int UT_NT = 256, UT_TM = 128, UT_NR = 4;
+constexpr int UT_RAW_BYTES = UT_TM * 64 * 4;          // 32 KB
+constexpr size_t update_tc_smem() {
+    return (size_t)2 * 64 * 64 * 4 + (size_t)2 * UT_TM * 64 * 4 + (size_t)UT_NR * UT_RAW_BYTES + 1024;
+}
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
     asm volatile(
@@ -284,7 +280,9 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ut_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char* Bh = sm;                       // E^T hi: 64 x 64 K-major (16 KB)
     unsigned char* Bl = sm + 16384;               // E^T lo
-    unsigned char* Abuf = sm + 32768;             // [2][hi 32 KB | lo 32 KB]: W tile, 128 x 64 K-major
+    unsigned char* Ah = sm + 32768;               // W tile hi: 128 x 64 K-major (32 KB)
+    unsigned char* Al = sm + 65536;               // W tile lo
+    float* ring = reinterpret_cast<float*>(sm + 98304);   // UT_NR raw tiles [64 cols][128 rows]
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ uint32_t tmem_base;
     __shared__ float* colp[64];
@@ -297,7 +295,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
     if (row_lo >= rows_pad) return;
     const long long row_hi = min(rows_pad, row_lo + (long long)tiles_per_cta * UT_TM);
     const int ntile = (int)((row_hi - row_lo + UT_TM - 1) / UT_TM);
-    const int tid = threadIdx.x, warp = tid >> 5, qi = tid & 3;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int trow = tid & 127, half = tid >> 7;  // tile row (= TMEM lane) and column half of this thread
     const PairDesc<float> pd = a.pd[pair];
     const int w = pd.w0 + pd.w1;
@@ -309,6 +307,27 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
         tc::mbar_init(&mbar[0]);
         tc::mbar_init(&mbar[1]);
         asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    __syncthreads();                              // colp visible
+    // raw tile t: 64 columns x 32 chunks of 4 rows; thread: 8 chunks (c = (tid + 256 u) / 32, rows 4 ((tid + 256 u) % 32))
+    const uint32_t rbase = tc::smem_u32(ring);
+    auto issue = [&](int t) {
+        const int slot = t % UT_NR;
+        const long long r0 = row_lo + (long long)t * UT_TM;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int f = tid + UT_NT * u;
+            const int c = f >> 5, r4 = 4 * (f & 31);
+            const float* p = colp[c];
+            float* dst = ring + (size_t)slot * (UT_TM * 64) + c * UT_TM + r4;
+            if (p && r0 + r4 < rows_pad) cp16(rbase + (uint32_t)(((size_t)slot * (UT_TM * 64) + c * UT_TM + r4) * 4), p + r0 + r4);
+            else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+#pragma unroll
+    for (int t = 0; t < UT_NR - 1; ++t) {
+        if (t < ntile) issue(t);
+        cp_commit();
     }
     // B = E^T: B[n][k] = E[k][n]; item (n, k4): float4 over k
     const float* Eg = a.E + (long long)pair * (64 * 64);
@@ -328,17 +347,6 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     constexpr uint32_t SBO = 16 * 128;                  // 64 columns: 2048 B between 8-row groups
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
-    // this thread loads, for u < 8: rows r0 + 4 (trow / 4) .. + 3 of column 32 half + 4u + qi
-    float4 v[8];
-    auto load = [&](int t) {
-        const long long rr = row_lo + (long long)t * UT_TM + 4 * (trow >> 2);
-        const bool rok = rr < rows_pad;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const float* p = colp[32 * half + 4 * u + qi];
-            v[u] = (p && rok) ? __ldg(reinterpret_cast<const float4*>(p + rr)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
     auto epilogue = [&](int t) {
         const long long row = row_lo + (long long)t * UT_TM + trow;
         const bool rok = row < rows_pad;
@@ -357,32 +365,36 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
             }
         }
     };
-    load(0);
     for (int t = 0; t < ntile; ++t) {
         const int b = t & 1;
-        unsigned char* Ah = Abuf + (size_t)b * 65536;
-        unsigned char* Al = Ah + 32768;
-        // ---- stage tile t: transpose, split, W row -> TMEM accumulator b
+        cp_wait<UT_NR - 2>();                      // this thread's chunks of tile t
+        __syncthreads();                           // everyone's chunks of tile t
+        if (t >= 1) tc::mbar_wait(&mbar[b ^ 1], (uint32_t)(((t - 1) >> 1) & 1));   // MMAs of t - 1 done: A free
+        tc::fence_after();
+        // ---- transpose from the raw tile, split, W row -> TMEM accumulator b
+        const float* raw = ring + (size_t)(t % UT_NR) * (UT_TM * 64);
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {           // 16 columns at a time
+        for (int g = 0; g < 2; ++g) {              // 16 columns at a time
             float wv[16];
 #pragma unroll
+            for (int j = 0; j < 16; ++j) wv[j] = raw[(32 * half + 16 * g + j) * UT_TM + trow];
+#pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int u = 4 * g + q;
-                const float4 x = tc::quad_transpose(v[u], qi);
-                wv[4 * q] = x.x; wv[4 * q + 1] = x.y; wv[4 * q + 2] = x.z; wv[4 * q + 3] = x.w;
-                const uint32_t o = tc::koff(trow, 32 * half + 4 * u, 64);
+                const float4 x = make_float4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+                const uint32_t o = tc::koff(trow, 32 * half + 16 * g + 4 * q, 64);
                 const float4 h = tc::hi4(x);
                 *reinterpret_cast<float4*>(Ah + o) = h;
                 *reinterpret_cast<float4*>(Al + o) = tc::lo4(x, h);
             }
             tmem_st16(tmem + (uint32_t)(64 * b) + lane_base + (uint32_t)(32 * half + 16 * g), wv);
         }
-        if (t + 1 < ntile) load(t + 1);          // in flight during the MMAs and the epilogue below
         asm volatile("tcgen05.wait::st.sync.aligned;\n");
         tc::fence_async_smem();
         tc::fence_before();
-        __syncthreads();
+        __syncthreads();                           // A, TMEM b written; raw slot t % NR consumed
+        // refill the ring: tile t + NR - 1 -> slot (t - 1) % NR (consumed last iteration)
+        if (t + UT_NR - 1 < ntile) issue(t + UT_NR - 1);
+        cp_commit();
         if (tid == 0) {
             tc::fence_after();
             const uint32_t ah = tc::smem_u32(Ah), al = tc::smem_u32(Al), bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
@@ -398,17 +410,11 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
                 tc::mma(acc, tc::sdesc(ah + ks * 256, 128, SBO), tc::sdesc(bl + ks * 256, 128, SBO), idesc, 1u);
             tc::commit(&mbar[b]);
         }
-        // ---- epilogue of tile t - 1 (its MMAs were issued one iteration ago)
-        if (t >= 1) {
-            tc::mbar_wait(&mbar[b ^ 1], (uint32_t)(((t - 1) >> 1) & 1));
-            tc::fence_after();
-            epilogue(t - 1);
-        }
-        // buffers b ^ 1 (A and accumulator) are free for tile t + 1 after this barrier
+        // ---- epilogue of tile t - 1 (accumulator b ^ 1) while the MMAs of tile t run
+        if (t >= 1) epilogue(t - 1);
         tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
     }
+    cp_wait<0>();
     if (ntile >= 1) {
         const int t = ntile - 1;
         tc::mbar_wait(&mbar[t & 1], (uint32_t)((t >> 1) & 1));
