@@ -769,88 +769,107 @@ __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float>
 }
 
 // ------------------------------------------------------------------------
-// k_pair_update_dmma: grid (row chunks of 128, npairs, 2 [X, V]), 256
-// threads (8 warps).  out = W + W E on a 128-row slab: the slab and E are
-// staged in shared memory (W column stride 132, E^T stride W+4: conflict-free
-// fragment loads), each warp owns (128/WR) x (W/WC) of the output and runs
-// K = w/4 DMMA k-steps; the result is added in place into the staged slab
-// and stored back with coalesced 16-byte stores.
+// k_pair_update_dmma: grid (tile groups, npairs, 2 [X, V]), 512 threads (16
+// warps); out = W + W E on 128-row tiles, UD_TPC tiles per CTA.  E^T is
+// staged once per CTA (column stride W+4: conflict-free fragment loads); the
+// tiles are double-buffered (cp.async of tile t+1 overlaps the DMMAs of tile
+// t; column stride 132).  Each warp owns (128/8) x (W/2) of the output and
+// runs K = w/4 DMMA k-steps; the result is added in place into the staged
+// tile and stored back with coalesced 16-byte stores.
 // ------------------------------------------------------------------------
+constexpr int UD_NT = 512, UD_RC = 128, UD_TPC = 8;
 template <int W>
-__global__ void __launch_bounds__(256) k_pair_update_dmma(JacobiRound<double> a) {
-    constexpr int RC = 128, SW = RC + 4, SE = W + 4;
-    constexpr int WC = W >= 64 ? 2 : 1, WR = 8 / WC;
+constexpr size_t update_dmma_smem() {
+    return sizeof(double) * ((size_t)2 * W * (UD_RC + 4) + (size_t)W * (W + 4)) + sizeof(double*) * W;
+}
+
+template <int W>
+__global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma(JacobiRound<double> a) {
+    constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
+    constexpr int WC = W >= 64 ? 2 : 1, WR = 16 / WC;
     constexpr int TM = RC / WR / 8, TN = W / WC / 8;
     extern __shared__ __align__(16) unsigned char upd_smem[];
-    double* Ws = reinterpret_cast<double*>(upd_smem);      // [W][SW]  (column k, row rho)
-    double* Et = Ws + W * SW;                                // [W][SE]  (Et[j][k] = E[k][j])
+    double* Wbuf = reinterpret_cast<double*>(upd_smem);     // [2][W][SW]  (column k, row rho)
+    double* Et = Wbuf + 2 * W * SW;                          // [W][SE]     (Et[j][k] = E[k][j])
     double** colp = reinterpret_cast<double**>(Et + W * SE);
     const int pair = blockIdx.y, which = blockIdx.z;
     if (!a.flag[pair]) return;
     if (which && !a.has_v) return;
     const long long ld = which ? a.ldv : a.ldx;
     const long long rows_pad = which ? a.nv_pad : a.m_pad;
-    const long long row0 = (long long)blockIdx.x * RC;
-    if (row0 >= rows_pad) return;
-    const int nrow = (int)min((long long)RC, rows_pad - row0);    // multiple of 32
+    const long long row_lo = (long long)blockIdx.x * UD_TPC * RC;
+    if (row_lo >= rows_pad) return;
+    const long long row_hi = min(rows_pad, row_lo + (long long)UD_TPC * RC);
+    const int ntile = (int)((row_hi - row_lo + RC - 1) / RC);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const auto pd = a.pd[pair];
     const int w = pd.w0 + pd.w1;
     if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, which != 0, ld) : nullptr;
     __syncthreads();
-    // stage the slab (cp.async) and E^T
-    for (int v = tid; v < W * (RC / 2); v += 256) {
-        const int c = v / (RC / 2), ch = v % (RC / 2);
-        double* dst = &Ws[c * SW + ch * 2];
-        if (colp[c] != nullptr && ch * 2 < nrow) cp_async16(dst, colp[c] + row0 + ch * 2);
-        else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
-    }
-    cp_async_commit();
+    auto issue = [&](int t) {
+        double* Ws = Wbuf + (t & 1) * (W * SW);
+        const long long row0 = row_lo + (long long)t * RC;
+        const int nrow = (int)min((long long)RC, rows_pad - row0);    // multiple of 32
+        for (int v = tid; v < W * (RC / 2); v += UD_NT) {
+            const int c = v / (RC / 2), ch = v % (RC / 2);
+            double* dst = &Ws[c * SW + ch * 2];
+            if (colp[c] != nullptr && ch * 2 < nrow) cp_async16(dst, colp[c] + row0 + ch * 2);
+            else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        }
+        cp_async_commit();
+    };
+    issue(0);
     const double* Eg = a.E + (long long)pair * (W * W);
-    for (int e = tid; e < W * W; e += 256) {
+    for (int e = tid; e < W * W; e += UD_NT) {
         const int k = e / W, j = e - (e / W) * W;
         Et[j * SE + k] = Eg[e];
     }
-    cp_async_wait<0>();
-    __syncthreads();
     const int wr = warp / WC, wc = warp % WC;
     const int rb = wr * (RC / WR), cb = wc * (W / WC);
-    double acc[TM][TN][2];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int kend = (w + 3) & ~3;
-    for (int k0 = 0; k0 < kend; k0 += 4) {
-        double fa[TM], fb[TN];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) fa[i] = Ws[(k0 + (lane & 3)) * SW + rb + 8 * i + (lane >> 2)];
-#pragma unroll
-        for (int j = 0; j < TN; ++j) fb[j] = Et[(cb + 8 * j + (lane >> 2)) * SE + k0 + (lane & 3)];
+    for (int t = 0; t < ntile; ++t) {
+        if (t + 1 < ntile) { issue(t + 1); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();                                      // tile t (and E) visible
+        double* Ws = Wbuf + (t & 1) * (W * SW);
+        double acc[TM][TN][2];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-    }
-    __syncthreads();   // all fragment reads done before the in-place add
+            for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int k0 = 0; k0 < kend; k0 += 4) {
+            double fa[TM], fb[TN];
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+            for (int i = 0; i < TM; ++i) fa[i] = Ws[(k0 + (lane & 3)) * SW + rb + 8 * i + (lane >> 2)];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) {
-            const int rho = rb + 8 * i + (lane >> 2);
-            const int col = cb + 8 * j + 2 * (lane & 3);
-            Ws[col * SW + rho] += acc[i][j][0];
-            Ws[(col + 1) * SW + rho] += acc[i][j][1];
+            for (int j = 0; j < TN; ++j) fb[j] = Et[(cb + 8 * j + (lane >> 2)) * SE + k0 + (lane & 3)];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
         }
-    __syncthreads();
-    for (int v = tid; v < W * (RC / 2); v += 256) {
-        const int c = v / (RC / 2), ch = v % (RC / 2);
-        if (c < w && ch * 2 < nrow)
-            *reinterpret_cast<double2*>(colp[c] + row0 + ch * 2) =
-                *reinterpret_cast<const double2*>(&Ws[c * SW + ch * 2]);
+        __syncthreads();                                      // all fragment reads done before the in-place add
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int rho = rb + 8 * i + (lane >> 2);
+                const int col = cb + 8 * j + 2 * (lane & 3);
+                Ws[col * SW + rho] += acc[i][j][0];
+                Ws[(col + 1) * SW + rho] += acc[i][j][1];
+            }
+        __syncthreads();
+        const long long row0 = row_lo + (long long)t * RC;
+        const int nrow = (int)min((long long)RC, rows_pad - row0);
+        for (int v = tid; v < W * (RC / 2); v += UD_NT) {
+            const int c = v / (RC / 2), ch = v % (RC / 2);
+            if (c < w && ch * 2 < nrow)
+                *reinterpret_cast<double2*>(colp[c] + row0 + ch * 2) =
+                    *reinterpret_cast<const double2*>(&Ws[c * SW + ch * 2]);
+        }
+        __syncthreads();                                      // buffer t & 1 free for tile t + 2
     }
 }
-
 
 // ------------------------------------------------------------------------
 // k_pair_update_f32: fp32 SIMT version of the update (FFMA pipe).  Grid
@@ -1014,13 +1033,14 @@ solve:
     }
     if (hook) hook->begin(hook->ctx, KName<T>::update);
     if constexpr (sizeof(T) == 8) {
-        const size_t dsm = sizeof(double) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
+        const size_t dsm = update_dmma_smem<W>();
         static bool attr_d = false;
         if (!attr_d) {
             cudaFuncSetAttribute(k_pair_update_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
             attr_d = true;
         }
-        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.has_v ? 2 : 1), 256, dsm, st>>>(a);
+        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, (long long)UD_RC * UD_TPC), a.npairs, a.has_v ? 2 : 1),
+                                UD_NT, dsm, st>>>(a);
     } else if (W == 64 && a.use_tc) {
         if constexpr (sizeof(T) == 4) launch_update_tc(a, st);
     } else {
