@@ -244,6 +244,22 @@ __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k,
 // Rotations of one round act on disjoint index pairs, so the result is that
 // of the oracle's sequential loop up to the rounding order of the two
 // rotations applied to an off-diagonal block (reading c-5).
+// Does any pair (p < q < w) pass the rotation guard of set_rotation (reading
+// c-3)?  Upper-triangle storage; this thread's share of the pairs.
+template <typename T, int W>
+__device__ __forceinline__ int any_pair_above(const InnerSmem<T, W>& sm, int w, T tol_in) {
+    constexpr int GS = InnerSmem<T, W>::GS;
+    int f = 0;
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+        const int p = e / w, q = e - (e / w) * w;
+        if (p < q) {
+            const T gpp = sm.G[p * GS + p], gqq = sm.G[q * GS + q], gpq = sm.G[p * GS + q];
+            f |= (gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq)) ? 1 : 0;
+        }
+    }
+    return f;
+}
+
 template <typename T, int W>
 __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used) {
     constexpr int GS = InnerSmem<T, W>::GS;
@@ -287,6 +303,10 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
     }
     __syncthreads();
     int sweep = 0, r = 0, buf = 0;
+    if (!__syncthreads_or(any_pair_above<T, W>(sm, w, tol_in))) {   // already converged: the check sweep only
+        if (sweeps_used) *sweeps_used = 1;
+        return 0;
+    }
     while (true) {
         const bool last = (r == NR - 1);
         const int rn = last ? 0 : r + 1;
@@ -370,6 +390,10 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
             f_next = 0;
             if (!any || sweep + 1 >= max_inner) break;
             ++sweep;
+            // A sweep without rotations leaves G unchanged, so its rounds would take exactly the
+            // decisions of one parallel pass over all pairs now: if none exceeds the threshold,
+            // that (check) sweep is counted and skipped.
+            if (!__syncthreads_or(any_pair_above<T, W>(sm, w, tol_in))) break;
         } else {
             __syncthreads();
         }
