@@ -176,58 +176,78 @@ def load_peaks():
 
 
 def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks: dict, n: int, b: int):
-    """Roofline entry for the dominant kernel from algorithmic work (DESIGN.md
-    "Algorithmic work per unit")."""
-    hbm = (peaks["measured"] or {}).get("hbm_gbs", 6650.0)
+    """Roofline entry of one kernel from its algorithmic work (DESIGN.md sec. 8
+    "Algorithmic work per unit"), its summed CUDA-event time over the timed
+    steps and the measured peaks (MEASURED_PEAKS.json copy bandwidth;
+    profiles/peaks.json DFMA/DMMA/FFMA microbenchmarks)."""
+    hbm = (peaks["measured"] or {}).get("hbm_gbs") or 6650.0
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (copy)" if (peaks["measured"] or {}).get("hbm_gbs") else "fallback 6.65 TB/s"
     micro = peaks["micro"] or {}
     sec = ms_total / 1e3
-    if kernel.startswith("pair_") and ("gram" in kernel or "update" in kernel):
-        is64 = kernel.endswith("f64")
-        flops = work["flops"].get(kernel, 0.0)
-        byts = work["bytes"].get(kernel, 0.0)
-        ach_f = flops / sec / 1e12
-        if is64:
-            peak = micro.get("dfma_tflops") or (148 * 64 * 2 * 1.965e9 / 1e12)
-            src = "measured DFMA microbenchmark (profiles/peaks.json)" if micro.get("dfma_tflops") else \
-                "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
-        else:
-            peak = micro.get("ffma_tflops") or (148 * 128 * 2 * 1.965e9 / 1e12)
-            src = "measured FFMA microbenchmark (profiles/peaks.json)" if micro.get("ffma_tflops") else \
-                "derived: 148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz"
-        return {"kernel": kernel, "bound": "alu", "achieved": ach_f, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach_f / peak, "traffic": work.get("traffic", {}).get(kernel),
-                "algorithmic_bytes_per_launch": byts / max(launches, 1),
-                "algorithmic_flops_per_launch": flops / max(launches, 1),
-                "hbm_gbs_achieved": byts / sec / 1e9, "hbm_frac": byts / sec / 1e9 / hbm,
-                "peak_source": src, "launches": launches, "avg_launch_us": ms_total * 1e3 / max(launches, 1)}
-    return {"kernel": kernel, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-            "traffic": None, "launches": launches}
+    flops = work["flops"].get(kernel)
+    byts = work["bytes"].get(kernel)
+    base = {"kernel": kernel, "launches": launches, "avg_launch_us": ms_total * 1e3 / max(launches, 1),
+            "traffic": work.get("traffic", {}).get(kernel)}
+    if byts is not None:
+        base["algorithmic_bytes_per_launch"] = byts / max(launches, 1)
+        base["hbm_gbs_achieved"] = byts / sec / 1e9
+        base["hbm_frac"] = byts / sec / 1e9 / hbm
+    if flops is not None:
+        base["algorithmic_flops_per_launch"] = flops / max(launches, 1)
+    bound = work["bound"].get(kernel)
+    if bound == "hbm" and byts is not None:
+        ach = byts / sec / 1e9
+        base.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "peak_source": hbm_src})
+    elif bound == "alu64" and flops is not None:
+        ach = flops / sec / 1e12
+        peak = micro.get("dmma_tflops") or micro.get("dfma_tflops") or (148 * 64 * 2 * 1.965e9 / 1e12)
+        base.update({"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "peak_source": "measured DMMA (mma.sync f64) microbenchmark, profiles/peaks.json"})
+    elif bound == "alu32" and flops is not None:
+        ach = flops / sec / 1e12
+        peak = micro.get("ffma_tflops") or (148 * 128 * 2 * 1.965e9 / 1e12)
+        base.update({"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "peak_source": "measured FFMA microbenchmark, profiles/peaks.json"})
+    else:
+        base.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
+    return base
 
 
-def algorithmic_work(stats_list, n: int, b: int, world: int = 1):
-    """Algorithmic flops/bytes of the Jacobi kernels summed over the timed steps
-    (DESIGN.md sec. 8).  Gram of a pair (w = 2b columns, n rows): the
-    symmetric half incl. the diagonal, n w (w+1) flops, reading W once
-    (n w s bytes; per round the whole X: n^2 s); update: 2 n w^2 flops for X
-    and again for V per updated pair, bytes 2 x (read + write of n x w) x s."""
-    flops, byts = {}, {}
+def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None = None, tensor32: bool = True):
+    """Algorithmic flops / HBM bytes of the path's kernels summed over the timed
+    steps, per rank.  Gram of a pair (w = 2b columns, n
+    rows): symmetric half incl. the diagonal, n w (w+1) flops, reading W once
+    (per round the whole X: n^2 s bytes); update: 2 n w^2 flops for X and
+    again for V per updated pair, bytes 2 x (read + write of n x w) x s; QRP:
+    the lazy GEMV reads the (n-k)^2 trailing matrix at every step k (8 n^3 / 3
+    bytes in fp64)."""
+    flops, byts, bound = {}, {}, {}
     nblk = -(-n // b)
     M = nblk + (nblk & 1) if world == 1 else -(-nblk // (2 * world)) * (2 * world)
     npairs = M // 2
     rounds = M - 1
+    w = 2 * b
     for st in stats_list:
         for tag, s, key in (("f32", 4, "32"), ("f64", 8, "64")):
             sweeps = st["sweeps" + key]
             upd = sum(st["upd_trace" + key])
-            g = f"pair_gram_{tag}"
-            u = f"pair_update_{tag}"
-            w = 2 * b
+            g, u = f"pair_gram_{tag}", f"pair_update_{tag}"
             flops[g] = flops.get(g, 0.0) + sweeps * rounds * npairs * float(n) * w * (w + 1)
             byts[g] = byts.get(g, 0.0) + sweeps * rounds * float(n) * n * s
-            flops[u] = flops.get(u, 0.0) + upd * 16.0 * n * b * b
-            byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * 2.0 * n * 2 * b * s
-    # per rank: the sharded engine spreads the pairs of every round over the ranks
-    return {"flops": {k: v / world for k, v in flops.items()}, "bytes": {k: v / world for k, v in byts.items()}}
+            flops[u] = flops.get(u, 0.0) + upd * 2 * 2.0 * n * w * w
+            byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * float(n) * w * s
+        flops["qrp_coop"] = flops.get("qrp_coop", 0.0) + 4.0 * n ** 3 / 3
+        byts["qrp_coop"] = byts.get("qrp_coop", 0.0) + 8.0 * n ** 3 / 3
+    # fp32 Gram/update are HBM-bound on the tensor cores (tcgen05) and ALU-bound on FFMA
+    for k in ("pair_gram_f32", "pair_update_f32"):
+        bound[k] = "hbm" if tensor32 else "alu32"
+    bound["pair_gram_f64"] = "alu64"
+    bound["pair_update_f64"] = "alu64"
+    bound["qrp_coop"] = "hbm"
+    return {"flops": {k: v / world for k, v in flops.items() if not k.startswith("qrp") or world == 1},
+            "bytes": {k: v / world for k, v in byts.items() if not k.startswith("qrp") or world == 1},
+            "bound": bound}
 
 
 def main():
@@ -342,7 +362,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel
     peaks = load_peaks()
-    work = algorithmic_work(stats, n, args.block_cols, world)
+    work = algorithmic_work(stats, n, args.block_cols, world, m, tensor32=True)
     try:
         work["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
@@ -353,10 +373,11 @@ def main():
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                    "share": v[0] / max(1e-9, sum(x[0] for x in prof.values()))} for k, v in prof.items()}
     jacobi = {}
-    for k in ("pair_gram_f64", "pair_update_f64", "pair_gram_f32", "pair_update_f32"):
+    for k in ("pair_gram_f64", "pair_update_f64", "pair_gram_f32", "pair_update_f32", "qrp_coop"):
         if k in prof:
             r = roofline_for(k, prof[k][0], prof[k][1], work, peaks, n, args.block_cols)
-            jacobi[k] = {kk: r[kk] for kk in ("achieved", "peak", "frac", "hbm_gbs_achieved", "hbm_frac")}
+            jacobi[k] = {kk: r.get(kk) for kk in ("bound", "achieved", "peak", "unit", "frac", "hbm_gbs_achieved",
+                                                  "hbm_frac", "avg_launch_us")}
 
     if rank != 0:
         if world > 1:
