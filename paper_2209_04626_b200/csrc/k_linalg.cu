@@ -412,11 +412,14 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     if (rc) return rc;
     k_larft<<<1, WY_NB, 0, st>>>(S, kb, tau, 0, T);
     MPJ_LAUNCHED();
-    rc = gemm_f64(1, 0, WY_NB, ncols, rows, 1.0, Vp, ldw, C, ldc, 0.0, W1, WY_NB, st);
+    // transposed products keep the long dimension (ncols) in the GEMM's M: W1^T = C^T Vp,
+    // W2^T = W1^T T^(T) (T^T for trans), C -= Vp W2 = Vp (W2^T)^T
+    const long long ldt = ncols;
+    rc = gemm_f64(1, 0, ncols, WY_NB, rows, 1.0, C, ldc, Vp, ldw, 0.0, W1, ldt, st);
     if (rc) return rc;
-    rc = gemm_f64(trans ? 1 : 0, 0, WY_NB, ncols, WY_NB, 1.0, T, WY_NB, W1, WY_NB, 0.0, W2, WY_NB, st);
+    rc = gemm_f64(0, trans ? 0 : 1, ncols, WY_NB, WY_NB, 1.0, W1, ldt, T, WY_NB, 0.0, W2, ldt, st);
     if (rc) return rc;
-    rc = gemm_f64(0, 0, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, WY_NB, 1.0, C, ldc, st);
+    rc = gemm_f64(0, 1, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, ldt, 1.0, C, ldc, st);
     return rc;
 }
 
