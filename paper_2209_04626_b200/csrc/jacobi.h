@@ -97,6 +97,11 @@ void gemm_set_workspace(double* ws, size_t elems);
 int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A,
              long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
              cudaStream_t st);
+// shape bit 0: compute only the upper triangle of C (tiles below the diagonal are skipped);
+// bit 1: op(A) is lower triangular (the K loop of a row tile stops at its last row)
+int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A,
+                long long lda, const double* B, long long ldb, double beta, double* C, long long ldc, int shape,
+                cudaStream_t st);
 // Cholesky of the n x n SPD matrix G (upper, in place): G = R^T R.  *bad set
 // (device int) if a pivot is not positive.
 int potrf_upper(double* G, long long ldg, int n, int* bad, cudaStream_t st);

@@ -75,13 +75,17 @@ __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, l
                                                   double alpha, const double* __restrict__ A, long long lda,
                                                   const double* __restrict__ B, long long ldb, double beta,
                                                   double* __restrict__ C, long long ldc, int vec_a, int vec_b,
-                                                  long long kchunk, double* __restrict__ part) {
+                                                  long long kchunk, double* __restrict__ part, int shape) {
     extern __shared__ __align__(16) unsigned char gm_smem[];
     double* As = reinterpret_cast<double*>(gm_smem);                  // [ST][BK][SA]
     double* Bs = As + GM_ST * GM_BK * GM_SA;                          // [ST][BK][SB]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;                          // 4 x 2 warps
     const long long i0 = (long long)blockIdx.x * GM_BM, j0 = (long long)blockIdx.y * GM_BN;
+    // shape bit 0: only the upper triangle of C is wanted -> skip tiles strictly below the diagonal
+    if ((shape & 1) && j0 + GM_BN <= i0) return;
+    // shape bit 1: op(A) is lower triangular -> op(A)(i, k) = 0 for k > i: K range ends at the tile's last row
+    if ((shape & 2) && kchunk == 0 && K > i0 + GM_BM) K = i0 + GM_BM;
     // split-K: this CTA covers k in [kb, kb + kchunk) of op(A)/op(B); partial results go to part
     const long long kb = (long long)blockIdx.z * kchunk;
     if (kchunk > 0) {
@@ -169,8 +173,8 @@ void gemm_set_workspace(double* ws, size_t elems) {
     g_gemm_ws_elems = elems;
 }
 
-int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
-             const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t st) {
+int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
+                const double* B, long long ldb, double beta, double* C, long long ldc, int shape, cudaStream_t st) {
     if (M <= 0 || N <= 0) return 0;
     static bool attr = false;
     const size_t smem = sizeof(double) * (size_t)GM_ST * GM_BK * (GM_SA + GM_SB);
@@ -184,7 +188,7 @@ int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha
     // split K when the output tiles cannot fill the GPU (skinny WY / Gram products)
     const long long tiles = (long long)grid.x * grid.y;
     long long nsplit = 1;
-    if (tiles < 148 && K >= 1024 && g_gemm_ws) {
+    if (tiles < 148 && K >= 1024 && g_gemm_ws && shape == 0) {
         nsplit = ceil_div(2 * 148, tiles);
         nsplit = min(nsplit, K / 256);
         nsplit = min(nsplit, (long long)(g_gemm_ws_elems / (size_t)(M * N)));
@@ -195,7 +199,7 @@ int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha
         nsplit = ceil_div(K, kchunk);
         grid.z = (unsigned)nsplit;
         k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
-                                            kchunk, g_gemm_ws);
+                                            kchunk, g_gemm_ws, 0);
         MPJ_LAUNCHED();
         long long gr = ceil_div(M * N, 256);
         if (gr > 4096) gr = 4096;
@@ -203,11 +207,16 @@ int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha
         MPJ_LAUNCHED();
     } else {
         k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
-                                            0, nullptr);
+                                            0, nullptr, shape);
         MPJ_LAUNCHED();
     }
     MPJ_CUDA_TRY(cudaGetLastError());
     return 0;
+}
+
+int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
+             const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t st) {
+    return gemm_f64_ex(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0, st);
 }
 
 // ------------------------------------------------------------------------
@@ -284,7 +293,7 @@ int potrf_upper(double* G, long long ldg, int n, int* bad, cudaStream_t st) {
             MPJ_LAUNCHED();
             const double* U12 = G + k0 + (long long)(k0 + kb) * ldg;
             double* A22 = G + (k0 + kb) + (long long)(k0 + kb) * ldg;
-            int rc = gemm_f64(1, 0, rest, rest, kb, -1.0, U12, ldg, U12, ldg, 1.0, A22, ldg, st);
+            int rc = gemm_f64_ex(1, 0, rest, rest, kb, -1.0, U12, ldg, U12, ldg, 1.0, A22, ldg, 1, st);   // upper only
             if (rc) return rc;
         }
     }

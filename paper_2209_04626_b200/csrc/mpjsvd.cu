@@ -487,7 +487,7 @@ int lift_inplace(mpjsvd_handle h, double* Q, long long ldq, int n, int* bad) {
     const long long n_pad = round_up(n, 32);
     MPJ_TRY(ensure(h, S_G, sizeof(double) * (size_t)n_pad * n));
     double* G = P<double>(h, S_G);
-    MPJ_TRY(gemm_f64(1, 0, n, n, n, 1.0, Q, ldq, Q, ldq, 0.0, G, n_pad, st));
+    MPJ_TRY(gemm_f64_ex(1, 0, n, n, n, 1.0, Q, ldq, Q, ldq, 0.0, G, n_pad, 1, st));   // upper triangle of Q^T Q
     MPJ_TRY(potrf_upper(G, n_pad, n, bad, st));
     MPJ_TRY(trsm_right_upper(G, n_pad, Q, ldq, n, n, st));
     return 0;
@@ -677,7 +677,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(lift_inplace(h, dQ, n_pad, (int)n, flags + 2));
         PROF_E("lift_cholqr");
         PROF_B("rv_gemm");
-        MPJ_TRY(gemm_f64(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, st));
+        // X lower triangular (X = L, reading c-7): K range of a row tile ends at its last row
+        MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
         PROF_E("rv_gemm");
         } else {
             MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
