@@ -44,7 +44,29 @@ struct JacobiRound {
     int* sweep_upd;     // device scalar, atomic add (this sweep)
     int* sweep_inner;   // device [2]: max inner sweeps of a pair, summed inner sweeps (this sweep)
     int use_tc;         // fp32, W = 64: tcgen05 TF32 (hi/lo split) Gram and update (k_tc.cu)
+    // completion-ordered publication of solved pairs (overlapped update):
+    // dlist[npairs] (-1 = not yet), dctr[0] = publication tail, dctr[1] = update work counter,
+    // dctr[2] = error flag (a consumer timed out); reset by the round's Gram kernel
+    int* dlist;
+    int* dctr;
+    int pdl;            // 1: the update is launched as a programmatic dependent of the solve
 };
+
+// reset of the publication list by the first CTA of the round's Gram kernel
+template <typename T>
+__device__ __forceinline__ void reset_publication(const JacobiRound<T>& a) {
+    if (a.dlist == nullptr || blockIdx.x != 0 || blockIdx.y != 0) return;
+    for (int i = threadIdx.x; i < a.npairs; i += blockDim.x) a.dlist[i] = -1;
+    if (threadIdx.x == 0) { a.dctr[0] = 0; a.dctr[1] = 0; }
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 
 // Optional per-launch timing hook (bench profiling): begin/end bracket one launch.
 struct ProfHook {
@@ -60,6 +82,8 @@ int gram_ctas_per_sm(int W, int use_tc);
 // tcgen05 fp32 kernels (k_tc.cu)
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);
+// persistent overlapped variant: drains pairs in the order the solve publishes them (a.pdl)
+int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st);
 int gram_tc_ctas_per_sm();
 template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);

@@ -39,6 +39,7 @@ __device__ __forceinline__ T* pair_col(const PairDesc<T>& d, int c, bool v, long
 // ------------------------------------------------------------------------
 template <typename T, int W>
 __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
+    reset_publication(a);
     constexpr int KT = 32;
     constexpr int VEC = 16 / sizeof(T);       // elements per 16-byte vector
     constexpr int S = KT + VEC;               // padded column stride (conflict-free)
@@ -424,6 +425,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
     const int pair = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    if (a.pdl) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // the update may start
     const int w = a.pd[pair].w0 + a.pd[pair].w1;
     // fixed-order reduction over row slabs (deterministic)
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
@@ -459,17 +461,26 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
         if (rotate) atomicAdd(a.sweep_upd, 1);
         a.flag[pair] = rotate ? 1 : 0;
     }
-    if (!rotate) return;
-    int used = 0;
-    inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
-    if (tid == 0) {
-        atomicMax(a.sweep_inner, used);
-        atomicAdd(a.sweep_inner + 1, used);
+    if (rotate) {
+        int used = 0;
+        inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
+        if (tid == 0) {
+            atomicMax(a.sweep_inner, used);
+            atomicAdd(a.sweep_inner + 1, used);
+        }
+        T* E = a.E + (long long)pair * (W * W);
+        for (int e = tid; e < W * W; e += nt) {
+            const int k = e / W, j = e - (e / W) * W;
+            E[e] = (k < w && j < w) ? sm.E[k * GS + j] : T(0);   // E[k][j] row-major
+        }
     }
-    T* E = a.E + (long long)pair * (W * W);
-    for (int e = tid; e < W * W; e += nt) {
-        const int k = e / W, j = e - (e / W) * W;
-        E[e] = (k < w && j < w) ? sm.E[k * GS + j] : T(0);   // E[k][j] row-major
+    if (a.dlist) {                 // publish: E and flag of this pair are complete
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const int pos = atomicAdd(a.dctr, 1);
+            st_release_gpu(a.dlist + pos, pair);
+        }
     }
 }
 
@@ -653,6 +664,7 @@ __device__ __forceinline__ void gram_warp(const double* const* colp, double* Wsm
 // ------------------------------------------------------------------------
 template <int W>
 __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
+    reset_publication(a);
     extern __shared__ __align__(16) unsigned char gram_smem[];
     double* Wsm = reinterpret_cast<double*>(gram_smem);
     const double** colp = reinterpret_cast<const double**>(Wsm + GRAM_STAGES * W * GRAM_S);
@@ -693,6 +705,7 @@ constexpr int G32_KT = 32, G32_ST = 6, G32_NT = 160;
 __device__ __forceinline__ int g32_chunk(int c, int rc) { return 8 * c + (rc ^ ((c >> 3) & 7)); }
 
 __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float> a) {
+    reset_publication(a);
     constexpr int W = 64;
     extern __shared__ __align__(16) unsigned char g32_smem[];
     float4* Ws = reinterpret_cast<float4*>(g32_smem);            // [ST][W*8] chunks
@@ -1043,9 +1056,25 @@ solve:
         cudaFuncSetAttribute(k_pair_solve<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
         attr_set = true;
     }
-    if (hook) hook->begin(hook->ctx, KName<T>::solve);
+    // overlapped update (fp32 tcgen05 with programmatic dependent launch): no event may sit
+    // between the solve and the update, so one bracket covers both
+    const bool overlap = sizeof(T) == 4 && W == 64 && a.use_tc && a.pdl;
+    if (hook) hook->begin(hook->ctx, overlap ? "pair_solve_update_f32" : KName<T>::solve);
     k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
     MPJ_LAUNCHED();
+    if (overlap) {
+        if constexpr (sizeof(T) == 4) {
+            const int rc = launch_update_tc_pdl(a, st);
+            if (rc) return rc;
+        }
+        if (hook) hook->end(hook->ctx, "pair_solve_update_f32");
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            mpj_record_cuda_error(e, "jacobi round launch", __FILE__, __LINE__);
+            return -4;
+        }
+        return 0;
+    }
     if (hook) hook->end(hook->ctx, KName<T>::solve);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
     constexpr int VEC = 16 / sizeof(T);

@@ -138,6 +138,7 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a) {
+    reset_publication(a);
     extern __shared__ __align__(1024) unsigned char gt_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gt_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t mbar[GT_ST + 1];
@@ -427,6 +428,194 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
 }
 
 // ------------------------------------------------------------------------
+// k_pair_update_tc_pdl: the update of k_pair_update_tc as a persistent
+// kernel (one CTA per SM) launched as a programmatic dependent of the round's
+// solve, so that it starts while slow pairs are still solving.  Work items
+// (completion position p, X or V, group of UT_TPC tiles) are taken from a
+// global counter in completion order; item p waits (acquire) until the p-th
+// solved pair is published (k_pair_solve: E and flag written, then release),
+// skips pairs that did not rotate, and runs the same pipeline as
+// k_pair_update_tc on its rows.  mbarrier phases are tracked per CTA across
+// items.  A consumer that waits too long sets dctr[2] and gives up (no hang).
+// ------------------------------------------------------------------------
+constexpr int UT_TPC = 16;
+
+__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<float> a, int ngroups) {
+    extern __shared__ __align__(1024) unsigned char ut_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ut_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* Bh = sm;
+    unsigned char* Bl = sm + 16384;
+    unsigned char* Ah = sm + 32768;
+    unsigned char* Al = sm + 65536;
+    float* ring = reinterpret_cast<float*>(sm + 98304);
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float* colp[64];
+    __shared__ int item[3];                     // pair, which, group (pair < 0: stop)
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int trow = tid & 127, half = tid >> 7;
+    if (warp == 0) tc::tmem_alloc<128>(&tmem_base);
+    if (tid == 0) {
+        tc::mbar_init(&mbar[0]);
+        tc::mbar_init(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    constexpr uint32_t SBO = 16 * 128;
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    const uint32_t rbase = tc::smem_u32(ring);
+    const long long total = (long long)a.npairs * 2 * ngroups;
+    uint32_t ph[2] = {0u, 0u};                  // completed waits per accumulator barrier
+    while (true) {
+        if (tid == 0) {
+            int pair = -1, which = 0, grp = 0;
+            while (true) {
+                const long long wk = atomicAdd(a.dctr + 1, 1);
+                if (wk >= total) break;
+                const int p = (int)(wk / (2 * ngroups)), rem = (int)(wk % (2 * ngroups));
+                which = rem / ngroups;
+                grp = rem % ngroups;
+                int pr = ld_acquire_gpu(a.dlist + p);
+                long long spins = 0;
+                while (pr < 0) {
+                    __nanosleep(256);
+                    pr = ld_acquire_gpu(a.dlist + p);
+                    if (++spins > (1LL << 24)) { atomicExch(a.dctr + 2, 1); break; }
+                }
+                if (pr < 0) { pair = -1; break; }
+                if (!a.flag[pr] || (which && !a.has_v)) continue;
+                const long long rows_pad = which ? a.nv_pad : a.m_pad;
+                if ((long long)grp * UT_TPC * UT_TM >= rows_pad) continue;
+                pair = pr;
+                break;
+            }
+            item[0] = pair; item[1] = which; item[2] = grp;
+        }
+        __syncthreads();
+        const int pair = item[0], which = item[1], grp = item[2];
+        if (pair < 0) break;
+        const long long ld = which ? a.ldv : a.ldx;
+        const long long rows_pad = which ? a.nv_pad : a.m_pad;
+        const long long row_lo = (long long)grp * UT_TPC * UT_TM;
+        const long long row_hi = min(rows_pad, row_lo + (long long)UT_TPC * UT_TM);
+        const int ntile = (int)((row_hi - row_lo + UT_TM - 1) / UT_TM);
+        const PairDesc<float> pd = a.pd[pair];
+        const int w = pd.w0 + pd.w1;
+        float* const s0 = which ? pd.v0 : pd.x0;
+        float* const s1 = which ? pd.v1 : pd.x1;
+        if (tid < 64) colp[tid] = tid < w ? (tid < pd.w0 ? s0 + (long long)tid * ld : s1 + (long long)(tid - pd.w0) * ld) : nullptr;
+        __syncthreads();
+        auto issue = [&](int t) {
+            const int slot = t % UT_NR;
+            const long long r0 = row_lo + (long long)t * UT_TM;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int f = tid + UT_NT * u;
+                const int c = f >> 5, r4 = 4 * (f & 31);
+                const float* p = colp[c];
+                float* dst = ring + (size_t)slot * (UT_TM * 64) + c * UT_TM + r4;
+                if (p && r0 + r4 < rows_pad) cp16(rbase + (uint32_t)(((size_t)slot * (UT_TM * 64) + c * UT_TM + r4) * 4), p + r0 + r4);
+                else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+#pragma unroll
+        for (int t = 0; t < UT_NR - 1; ++t) {
+            if (t < ntile) issue(t);
+            cp_commit();
+        }
+        const float* Eg = a.E + (long long)pair * (64 * 64);
+        for (int it = tid; it < 64 * 16; it += UT_NT) {
+            const int n = it & 63, k4 = it >> 6;
+            float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
+                                   Eg[(4 * k4 + 3) * 64 + n]);
+            const uint32_t o = tc::koff(n, 4 * k4, 64);
+            const float4 h = tc::hi4(v);
+            *reinterpret_cast<float4*>(Bh + o) = h;
+            *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
+        }
+        auto epilogue = [&](int t) {
+            const long long row = row_lo + (long long)t * UT_TM + trow;
+            const bool rok = row < rows_pad;
+            const uint32_t acc = tmem + (uint32_t)(64 * (t & 1));
+#pragma unroll
+            for (int c0 = 0; c0 < 32; c0 += 16) {
+                float d[16];
+                tc::tmem_ld16(acc + lane_base + (uint32_t)(32 * half + c0), d);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int c = 32 * half + c0 + j;
+                    if (rok && c < w) {
+                        float* p = c < pd.w0 ? s0 + (long long)c * ld : s1 + (long long)(c - pd.w0) * ld;
+                        p[row] = d[j];
+                    }
+                }
+            }
+        };
+        for (int t = 0; t < ntile; ++t) {
+            const int b = t & 1;
+            cp_wait<UT_NR - 2>();
+            tc::fence_before();
+            __syncthreads();
+            if (t >= 1) { tc::mbar_wait(&mbar[b ^ 1], ph[b ^ 1] & 1u); ++ph[b ^ 1]; }
+            tc::fence_after();
+            const float* raw = ring + (size_t)(t % UT_NR) * (UT_TM * 64);
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                float wv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) wv[j] = raw[(32 * half + 16 * g + j) * UT_TM + trow];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 x = make_float4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+                    const uint32_t o = tc::koff(trow, 32 * half + 16 * g + 4 * q, 64);
+                    const float4 h = tc::hi4(x);
+                    *reinterpret_cast<float4*>(Ah + o) = h;
+                    *reinterpret_cast<float4*>(Al + o) = tc::lo4(x, h);
+                }
+                tmem_st16(tmem + (uint32_t)(64 * b) + lane_base + (uint32_t)(32 * half + 16 * g), wv);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n");
+            tc::fence_async_smem();
+            tc::fence_before();
+            __syncthreads();
+            if (t + UT_NR - 1 < ntile) issue(t + UT_NR - 1);
+            cp_commit();
+            if (tid == 0) {
+                tc::fence_after();
+                const uint32_t ah = tc::smem_u32(Ah), al = tc::smem_u32(Al), bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
+                const uint32_t acc = tmem + (uint32_t)(64 * b);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma(acc, tc::sdesc(ah + ks * 256, 128, SBO), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma(acc, tc::sdesc(al + ks * 256, 128, SBO), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma(acc, tc::sdesc(ah + ks * 256, 128, SBO), tc::sdesc(bl + ks * 256, 128, SBO), idesc, 1u);
+                tc::commit(&mbar[b]);
+            }
+            if (t >= 1) epilogue(t - 1);
+        }
+        cp_wait<0>();
+        if (ntile >= 1) {
+            const int t = ntile - 1;
+            tc::mbar_wait(&mbar[t & 1], ph[t & 1] & 1u);
+            ++ph[t & 1];
+            tc::fence_after();
+            epilogue(t);
+        }
+        tc::fence_before();
+        __syncthreads();                        // item done: smem, TMEM free for the next item
+    }
+    if (warp == 0) tc::tmem_free<128>(tmem);
+}
+
+// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
@@ -461,4 +650,38 @@ int gram_tc_ctas_per_sm() {
     return per < 2 ? per : 2;                       // __launch_bounds__(GT_NT, 2)
 }
 
+}  // namespace mpj
+
+namespace mpj {
+int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pair_update_tc_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
+        attr = true;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
+    const int ngroups = (int)((rows_pad + (long long)UT_TPC * UT_TM - 1) / ((long long)UT_TPC * UT_TM));
+    const long long items = (long long)a.npairs * 2 * ngroups;
+    const unsigned grid = (unsigned)(items < nsm ? items : nsm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(UT_NT);
+    cfg.dynamicSmemBytes = update_tc_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute attr1[1];
+    attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr1[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr1;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl, a, ngroups);
+    MPJ_LAUNCHED();
+    if (e != cudaSuccess) {
+        mpj_record_cuda_error(e, "cudaLaunchKernelEx(update pdl)", __FILE__, __LINE__);
+        return -4;
+    }
+    return 0;
+}
 }  // namespace mpj

@@ -41,7 +41,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -277,6 +277,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + 3 * sizeof(int))));
     MPJ_TRY(ensure(h, S_PTAB, sizeof(PairDesc<T>) * (size_t)R * npairs));
     MPJ_TRY(ensure_pinned(h, sizeof(PairDesc<T>) * (size_t)R * npairs));
+    MPJ_TRY(ensure(h, S_PUB, sizeof(int) * ((size_t)npairs + 4)));
     double* d_off = P<double>(h, S_SWEEP);
     int* d_upd = reinterpret_cast<int*>(d_off + 64);
     int* d_inner = d_upd + 64;     // [64][2]
@@ -292,6 +293,10 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.partial = P<T>(h, S_PART); a.E = P<T>(h, S_E); a.flag = P<int>(h, S_JFLAG);
     a.tol = tol; a.tol_in = tol_in; a.max_inner = max_inner;
     a.use_tc = use_tc;
+    a.dctr = P<int>(h, S_PUB);
+    a.dlist = a.dctr + 4;
+    a.pdl = (use_tc && h->opts.pdl_overlap) ? 1 : 0;
+    MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
     double prev = -1.0;
@@ -322,6 +327,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         }
         MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 2), d_inner + 2 * (sw - 1), 2 * sizeof(int),
                                      cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 3), a.dctr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
@@ -334,6 +340,12 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         res.upd[sw - 1] = upd;
         memcpy(&res.inner_max[sw - 1], reinterpret_cast<int*>(hp + 2), sizeof(int));
         memcpy(&res.inner_sum[sw - 1], reinterpret_cast<int*>(hp + 2) + 1, sizeof(int));
+        int pub_err = 0;
+        memcpy(&pub_err, reinterpret_cast<int*>(hp + 3), sizeof(int));
+        if (pub_err) {
+            snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "overlapped update: a consumer timed out waiting for a solved pair");
+            return MPJSVD_ERR_CUDA;
+        }
         if (upd == 0) { res.converged = true; break; }
         // fp32 stagnation exit (reading c-10)
         if (stagnation && sw >= 3 && off <= 1e-4 && prev >= 0 && off > 0.25 * prev) { res.converged = true; break; }
@@ -879,6 +891,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->virtual_shards = 1;
     o->split_rows = 0;
     o->fp32_tensor_cores = 1;
+    o->pdl_overlap = 1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
