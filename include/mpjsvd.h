@@ -91,7 +91,7 @@ typedef struct {
     int32_t fp32_tensor_cores; /* 1 (default): the fp32 stage's Gram and update products (b = 32) run on
                                   the tcgen05 TF32 tensor cores with a hi/lo split (~2^-21 relative per
                                   product, fp32 accumulation; reading c-20); 0: FFMA SIMT */
-    int32_t pdl_overlap;       /* 1 (default, with fp32_tensor_cores): the fp32 update is a persistent kernel
+    int32_t pdl_overlap;       /* 1 (default): the Jacobi update (fp64 DMMA; fp32 with fp32_tensor_cores) is a persistent kernel
                                   launched as a programmatic dependent of the inner solve and drains the
                                   pairs in the order their solves finish (overlaps the solve's tail) */
 } mpjsvd_options;

@@ -909,6 +909,161 @@ __global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma(JacobiRound<doubl
 }
 
 // ------------------------------------------------------------------------
+// k_pair_update_dmma_pdl: k_pair_update_dmma as a persistent kernel (one CTA
+// per SM) launched as a programmatic dependent of the round's solve: work
+// items (completion position p, X or V, group of UD_TPC tiles) come from a
+// global counter in completion order, item p waits (acquire) for the p-th
+// published pair (k_pair_solve) and skips pairs that did not rotate.
+// ------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma_pdl(JacobiRound<double> a, int ngroups) {
+    constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
+    constexpr int WC = W >= 64 ? 2 : 1, WR = 16 / WC;
+    constexpr int TM = RC / WR / 8, TN = W / WC / 8;
+    extern __shared__ __align__(16) unsigned char upd_smem[];
+    double* Wbuf = reinterpret_cast<double*>(upd_smem);
+    double* Et = Wbuf + 2 * W * SW;
+    double** colp = reinterpret_cast<double**>(Et + W * SE);
+    __shared__ int item[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp / WC, wc = warp % WC;
+    const int rb = wr * (RC / WR), cb = wc * (W / WC);
+    const long long total = (long long)a.npairs * 2 * ngroups;
+    while (true) {
+        if (tid == 0) {
+            int pair = -1, which = 0, grp = 0;
+            while (true) {
+                const long long wk = atomicAdd(a.dctr + 1, 1);
+                if (wk >= total) break;
+                const int p = (int)(wk / (2 * ngroups)), rem = (int)(wk % (2 * ngroups));
+                which = rem / ngroups;
+                grp = rem % ngroups;
+                int pr = ld_acquire_gpu(a.dlist + p);
+                long long spins = 0;
+                while (pr < 0) {
+                    __nanosleep(256);
+                    pr = ld_acquire_gpu(a.dlist + p);
+                    if (++spins > (1LL << 24)) { atomicExch(a.dctr + 2, 1); break; }
+                }
+                if (pr < 0) { pair = -1; break; }
+                if (!a.flag[pr] || (which && !a.has_v)) continue;
+                const long long rows_pad = which ? a.nv_pad : a.m_pad;
+                if ((long long)grp * UD_TPC * RC >= rows_pad) continue;
+                pair = pr;
+                break;
+            }
+            item[0] = pair; item[1] = which; item[2] = grp;
+        }
+        __syncthreads();
+        const int pair = item[0], which = item[1], grp = item[2];
+        if (pair < 0) break;
+        const long long ld = which ? a.ldv : a.ldx;
+        const long long rows_pad = which ? a.nv_pad : a.m_pad;
+        const long long row_lo = (long long)grp * UD_TPC * RC;
+        const long long row_hi = min(rows_pad, row_lo + (long long)UD_TPC * RC);
+        const int ntile = (int)((row_hi - row_lo + RC - 1) / RC);
+        const auto pd = a.pd[pair];
+        const int w = pd.w0 + pd.w1;
+        if (tid < W) colp[tid] = tid < w ? pair_col(pd, tid, which != 0, ld) : nullptr;
+        __syncthreads();
+        auto issue = [&](int t) {
+            double* Ws = Wbuf + (t & 1) * (W * SW);
+            const long long row0 = row_lo + (long long)t * RC;
+            const int nrow = (int)min((long long)RC, rows_pad - row0);
+            for (int v = tid; v < W * (RC / 2); v += UD_NT) {
+                const int c = v / (RC / 2), ch = v % (RC / 2);
+                double* dst = &Ws[c * SW + ch * 2];
+                if (colp[c] != nullptr && ch * 2 < nrow) cp_async16(dst, colp[c] + row0 + ch * 2);
+                else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+            }
+            cp_async_commit();
+        };
+        issue(0);
+        const double* Eg = a.E + (long long)pair * (W * W);
+        for (int e = tid; e < W * W; e += UD_NT) {
+            const int k = e / W, j = e - (e / W) * W;
+            Et[j * SE + k] = Eg[e];
+        }
+        const int kend = (w + 3) & ~3;
+        for (int t = 0; t < ntile; ++t) {
+            if (t + 1 < ntile) { issue(t + 1); cp_async_wait<1>(); }
+            else cp_async_wait<0>();
+            __syncthreads();
+            double* Ws = Wbuf + (t & 1) * (W * SW);
+            double acc[TM][TN][2];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            for (int k0 = 0; k0 < kend; k0 += 4) {
+                double fa[TM], fb[TN];
+#pragma unroll
+                for (int i = 0; i < TM; ++i) fa[i] = Ws[(k0 + (lane & 3)) * SW + rb + 8 * i + (lane >> 2)];
+#pragma unroll
+                for (int j = 0; j < TN; ++j) fb[j] = Et[(cb + 8 * j + (lane >> 2)) * SE + k0 + (lane & 3)];
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    const int rho = rb + 8 * i + (lane >> 2);
+                    const int col = cb + 8 * j + 2 * (lane & 3);
+                    Ws[col * SW + rho] += acc[i][j][0];
+                    Ws[(col + 1) * SW + rho] += acc[i][j][1];
+                }
+            __syncthreads();
+            const long long row0 = row_lo + (long long)t * RC;
+            const int nrow = (int)min((long long)RC, rows_pad - row0);
+            for (int v = tid; v < W * (RC / 2); v += UD_NT) {
+                const int c = v / (RC / 2), ch = v % (RC / 2);
+                if (c < w && ch * 2 < nrow)
+                    *reinterpret_cast<double2*>(colp[c] + row0 + ch * 2) =
+                        *reinterpret_cast<const double2*>(&Ws[c * SW + ch * 2]);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int W>
+static int launch_update_dmma_pdl(const JacobiRound<double>& a, cudaStream_t st) {
+    const size_t dsm = update_dmma_smem<W>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pair_update_dmma_pdl<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        attr = true;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
+    const int ngroups = (int)((rows_pad + (long long)UD_TPC * UD_RC - 1) / ((long long)UD_TPC * UD_RC));
+    const long long items = (long long)a.npairs * 2 * ngroups;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(items < nsm ? items : nsm));
+    cfg.blockDim = dim3(UD_NT);
+    cfg.dynamicSmemBytes = dsm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_update_dmma_pdl<W>, a, ngroups);
+    MPJ_LAUNCHED();
+    if (e != cudaSuccess) {
+        mpj_record_cuda_error(e, "cudaLaunchKernelEx(update dmma pdl)", __FILE__, __LINE__);
+        return -4;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------------
 // k_pair_update_f32: fp32 SIMT version of the update (FFMA pipe).  Grid
 // (row chunks of 128, npairs, 2), 256 threads; thread tile 8 rows x (W/16)
 // columns of out = W + W E; slab and E staged in shared memory (16-byte
@@ -1058,16 +1213,17 @@ solve:
     }
     // overlapped update (fp32 tcgen05 with programmatic dependent launch): no event may sit
     // between the solve and the update, so one bracket covers both
-    const bool overlap = sizeof(T) == 4 && W == 64 && a.use_tc && a.pdl;
-    if (hook) hook->begin(hook->ctx, overlap ? "pair_solve_update_f32" : KName<T>::solve);
+    const bool overlap = a.pdl && (sizeof(T) == 8 || (W == 64 && a.use_tc));
+    const char* both = sizeof(T) == 4 ? "pair_solve_update_f32" : "pair_solve_update_f64";
+    if (hook) hook->begin(hook->ctx, overlap ? both : KName<T>::solve);
     k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
     MPJ_LAUNCHED();
     if (overlap) {
-        if constexpr (sizeof(T) == 4) {
-            const int rc = launch_update_tc_pdl(a, st);
-            if (rc) return rc;
-        }
-        if (hook) hook->end(hook->ctx, "pair_solve_update_f32");
+        int rc = 0;
+        if constexpr (sizeof(T) == 4) rc = launch_update_tc_pdl(a, st);
+        else rc = launch_update_dmma_pdl<W>(a, st);
+        if (rc) return rc;
+        if (hook) hook->end(hook->ctx, both);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             mpj_record_cuda_error(e, "jacobi round launch", __FILE__, __LINE__);

@@ -295,7 +295,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.use_tc = use_tc;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
-    a.pdl = (use_tc && h->opts.pdl_overlap) ? 1 : 0;
+    a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
