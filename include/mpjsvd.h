@@ -94,6 +94,10 @@ typedef struct {
     int32_t pdl_overlap;       /* 1 (default): the Jacobi update (fp64 DMMA; fp32 with fp32_tensor_cores) is a persistent kernel
                                   launched as a programmatic dependent of the inner solve and drains the
                                   pairs in the order their solves finish (overlaps the solve's tail) */
+    int32_t mp_rrqr;           /* 1: mixed-precision RRQR (Alg. 4): the column permutation
+                                  from an fp32 QRP of fl32(A1 2^-e), then fp64 Householder QR of A1 P;
+                                  0 (default): fp64 column-pivoted QR (Businger-Golub).  On B200 the fp32
+                                  QRP costs about as much as the fp64 one (reading c-22) */
 } mpjsvd_options;
 
 typedef struct {
@@ -224,7 +228,9 @@ int mpjsvd_inner_solve(mpjsvd_handle h, int32_t is_f64, void* G, void* E, int32_
 /* Column-pivoted Householder QR A P = Q R in place (n x n or m x n, lda):
    on exit R in the upper triangle (diag >= 0), reflectors below, tau[n],
    perm[n] (0-based original column at position k).  pivot = 0: plain QR
-   (perm = identity).  PAPER.md:332-335 / 416-420. */
+   (perm = identity); 1: fp64 QRP (lazy cooperative kernel); 2: fp64 QRP
+   (unblocked kernel); 3: mixed-precision RRQR, Alg. 4 (fp32 QRP pivots of
+   fl32(A 2^-e), then fp64 QR of A P).  PAPER.md:332-335 / 416-420 / 496-512. */
 int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, double* tau,
               int32_t* perm, int32_t pivot);
 

@@ -47,7 +47,7 @@ class Opts(C.Structure):
     _fields_ = [("b", C.c_int32), ("tol_mult32", C.c_double), ("tol_mult64", C.c_double),
                 ("inner_tol_div", C.c_int32), ("max_sweeps32", C.c_int32),
                 ("max_sweeps64", C.c_int32), ("max_inner", C.c_int32), ("path", C.c_int32),
-                ("x_from_lq", C.c_int32), ("nthreads", C.c_int32)]
+                ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -87,6 +87,8 @@ def lib():
             L.om_house.restype = C.c_double
             L.om_qr.argtypes = [dp, i64, i64, i64, dp]
             L.om_qrp.argtypes = [dp, i64, i64, i64, ip, dp]
+            L.om_qrp_f32.argtypes = [fp, i64, i64, i64, ip, fp]
+            L.om_mprrqr.argtypes = [dp, i64, i64, i64, ip, dp]
             L.om_apply_q.argtypes = [dp, i64, i64, i64, dp, dp, i64, i64]
             L.om_inner_solve_f64.argtypes = [dp, C.c_int32, C.c_double, C.c_int32, dp, ip]
             L.om_inner_solve_f64.restype = C.c_int64
@@ -156,6 +158,26 @@ def qrp(a: np.ndarray):
     tau = np.zeros(n)
     perm = np.zeros(n, dtype=np.int32)
     rc = lib().om_qrp(_dp(a), m, n, m, _ip(perm), _dp(tau))
+    return a, perm, tau, rc
+
+
+def qrp_f32(a: np.ndarray):
+    """Businger-Golub QRP entirely in fp32 (Alg. 4 line 2)."""
+    a = np.array(a, dtype=np.float32, order="F")
+    m, n = a.shape
+    tau = np.zeros(n, dtype=np.float32)
+    perm = np.zeros(n, dtype=np.int32)
+    rc = lib().om_qrp_f32(_fp(a), m, n, m, _ip(perm), _fp(tau))
+    return a, perm, tau, rc
+
+
+def mprrqr(a: np.ndarray):
+    """Mixed-precision RRQR (Alg. 4): packed R / reflectors of A P, perm, tau."""
+    a = np.array(a, dtype=np.float64, order="F")
+    m, n = a.shape
+    tau = np.zeros(n)
+    perm = np.zeros(n, dtype=np.int32)
+    rc = lib().om_mprrqr(_dp(a), m, n, m, _ip(perm), _dp(tau))
     return a, perm, tau, rc
 
 

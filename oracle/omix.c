@@ -65,6 +65,7 @@ void om_default_opts(om_opts* o) {
     o->path = OM_PATH_FORCE_MIXED;
     o->x_from_lq = 1;
     o->nthreads = 0;
+    o->mp_rrqr = 0;
 }
 
 /* ---- Householder ------------------------------------------------------ */
@@ -170,6 +171,124 @@ int om_qrp(double* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, double* 
     free(vn1);
     free(vn2);
     free(tmp);
+    return rc;
+}
+
+/* ---- fp32 QRP (Alg. 4 line 2) ------------------------------------------
+   om_house / apply_h / plain_norm / om_qrp written out again in float: every
+   operation rounds to fp32; tol3z = sqrt(u32) (LAPACK xLAQP2 in single). */
+static float house_f32(float* x, int64_t len) {
+    float alpha = x[0];
+    float sigma = 0.0f;
+    for (int64_t i = 1; i < len; ++i) sigma += x[i] * x[i];
+    if (sigma == 0.0f) {
+        if (alpha >= 0.0f) return 0.0f;
+        x[0] = -alpha;
+        return 2.0f;
+    }
+    float mu = sqrtf(alpha * alpha + sigma);
+    float v0 = alpha <= 0.0f ? alpha - mu : -sigma / (alpha + mu);
+    float tau = 2.0f * v0 * v0 / (sigma + v0 * v0);
+    for (int64_t i = 1; i < len; ++i) x[i] /= v0;
+    x[0] = mu;
+    return tau;
+}
+
+static void apply_h_f32(const float* v, int64_t len, float tau, float* c) {
+    if (tau == 0.0f) return;
+    float w = c[0];
+    for (int64_t i = 1; i < len; ++i) w += v[i] * c[i];
+    w *= tau;
+    c[0] -= w;
+    for (int64_t i = 1; i < len; ++i) c[i] -= w * v[i];
+}
+
+static float plain_norm_f32(const float* x, int64_t len) {
+    float s = 0.0f;
+    for (int64_t i = 0; i < len; ++i) s += x[i] * x[i];
+    return sqrtf(s);
+}
+
+int om_qrp_f32(float* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, float* tau) {
+    const float tol3z = sqrtf((float)U32);
+    float* vn1 = (float*)malloc(sizeof(float) * (size_t)n);
+    float* vn2 = (float*)malloc(sizeof(float) * (size_t)n);
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)m);
+    int rc = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        perm[j] = (int32_t)j;
+        vn1[j] = plain_norm_f32(A + j * lda, m);
+        vn2[j] = vn1[j];
+    }
+    for (int64_t k = 0; k < n && k < m; ++k) {
+        int64_t pvt = k;
+        for (int64_t j = k + 1; j < n; ++j)
+            if (vn1[j] > vn1[pvt]) pvt = j;          /* ties -> lowest index */
+        if (pvt != k) {
+            memcpy(tmp, A + pvt * lda, sizeof(float) * (size_t)m);
+            memcpy(A + pvt * lda, A + k * lda, sizeof(float) * (size_t)m);
+            memcpy(A + k * lda, tmp, sizeof(float) * (size_t)m);
+            int32_t ip = perm[pvt]; perm[pvt] = perm[k]; perm[k] = ip;
+            vn1[pvt] = vn1[k];
+            vn2[pvt] = vn2[k];
+        }
+        float* ak = A + k * lda + k;
+        tau[k] = house_f32(ak, m - k);
+        if (ak[0] == 0.0f) rc = -3;
+#pragma omp parallel for schedule(static)
+        for (int64_t j = k + 1; j < n; ++j) {
+            float* aj = A + j * lda;
+            apply_h_f32(ak, m - k, tau[k], aj + k);
+            if (vn1[j] != 0.0f) {
+                float r = fabsf(aj[k]) / vn1[j];
+                float temp = 1.0f - r * r;
+                if (temp < 0.0f) temp = 0.0f;
+                float q = vn1[j] / vn2[j];
+                float temp2 = temp * q * q;
+                if (temp2 <= tol3z) {
+                    if (k + 1 < m) {
+                        vn1[j] = plain_norm_f32(aj + k + 1, m - k - 1);
+                        vn2[j] = vn1[j];
+                    } else {
+                        vn1[j] = 0.0f;
+                        vn2[j] = 0.0f;
+                    }
+                } else {
+                    vn1[j] *= sqrtf(temp);
+                }
+            }
+        }
+    }
+    free(vn1);
+    free(vn2);
+    free(tmp);
+    return rc;
+}
+
+/* Mixed-precision RRQR, PAPER.md:496-512 (Alg. 4):
+   line 1  A_low = lower(A)                 (fl32 of A 2^-e: exact power-of-two scale, c-9)
+   line 2  A_low P = Q_low R_low in fp32    (om_qrp_f32; only P is kept)
+   line 3  A <- A P
+   line 4  A = Q R in the working precision (om_qr, fp64 Householder). */
+int om_mprrqr(double* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, double* tau) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) { double v = fabs(A[i + j * lda]); if (v > mx) mx = v; }
+    int e = 0;
+    frexp(mx, &e);
+    const double scale = ldexp(1.0, -e);
+    float* A32 = (float*)malloc(sizeof(float) * (size_t)m * (size_t)n);
+    float* tau32 = (float*)malloc(sizeof(float) * (size_t)n);
+    double* Ap = (double*)malloc(sizeof(double) * (size_t)m * (size_t)n);
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) A32[i + j * m] = (float)(A[i + j * lda] * scale);
+    om_qrp_f32(A32, m, n, m, perm, tau32);
+    for (int64_t k = 0; k < n; ++k) memcpy(Ap + k * m, A + (int64_t)perm[k] * lda, sizeof(double) * (size_t)m);
+    for (int64_t k = 0; k < n; ++k) memcpy(A + k * lda, Ap + k * m, sizeof(double) * (size_t)m);
+    int rc = om_qr(A, m, n, lda, tau);
+    free(A32);
+    free(tau32);
+    free(Ap);
     return rc;
 }
 
@@ -301,8 +420,12 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         for (int64_t j = 0; j < n; ++j) memcpy(A1 + j * n, Aw + j * m, sizeof(double) * (size_t)n);
     }
 
-    /* step 3: RRQR A1 P = Q_p R */
-    if (om_qrp(A1, n, n, n, perm, tau_p) != 0) { rc = -3; goto done; }
+    /* step 3: RRQR A1 P = Q_p R, by the mixed-precision RRQR of
+       PAPER.md:494-495 ("We use this mixed precision algorithm ... in the preconditioning stage") */
+    if ((o.mp_rrqr ? om_mprrqr(A1, n, n, n, perm, tau_p) : om_qrp(A1, n, n, n, perm, tau_p)) != 0) {
+        rc = -3;
+        goto done;
+    }
 
     /* step 4: R = L Q2 via QR of R^T; X = L (F1) */
     if (o.x_from_lq) {

@@ -39,6 +39,7 @@ typedef struct {
     int32_t path;           /* OM_PATH_* */
     int32_t x_from_lq;      /* 1: X = L (default, F1); 0: X = R */
     int32_t nthreads;       /* OpenMP threads over disjoint pairs (0 = default) */
+    int32_t mp_rrqr;        /* 1: mixed-precision RRQR, Alg. 4; 0 (default): fp64 QRP (c-22) */
 } om_opts;
 
 typedef struct {
@@ -61,6 +62,11 @@ int om_qr(double* A, int64_t m, int64_t n, int64_t lda, double* tau);
 /* Businger-Golub column-pivoted QR (LAPACK xGEQP3 semantics, diag(R) >= 0,
    pivot = largest partial norm, ties -> lowest index).  PAPER.md:332-335. */
 int om_qrp(double* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, double* tau);
+/* The same Businger-Golub QRP carried out entirely in fp32 (Alg. 4 line 2, "RRQR in a lower precision"). */
+int om_qrp_f32(float* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, float* tau);
+/* Mixed-precision RRQR (Alg. 4) of the m x n A in place: P from om_qrp_f32 on
+   fl32(A 2^-e) (e = frexp exponent of max|A|, reading c-9), then om_qr of A P. Same outputs as om_qrp. */
+int om_mprrqr(double* A, int64_t m, int64_t n, int64_t lda, int32_t* perm, double* tau);
 /* C <- Q*C with Q = H_0 H_1 ... H_{k-1} stored as in om_qr (rows m). */
 void om_apply_q(const double* Vr, int64_t m, int64_t k, int64_t ldv, const double* tau,
                 double* C, int64_t ldc, int64_t ncols);

@@ -109,6 +109,10 @@ int qr_coop_grid(int m, int* grid);  // cooperative grid size for this m
 // outputs as qr_coop(pivot = 1).  work >= qrp_lazy_work_doubles(n, grid).
 int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, int* phys_out,
              cudaStream_t st);
+// fp32 instance (pivots of the mixed-precision RRQR, Alg. 4); work as for
+// qrp_lazy (sized in doubles), tau n floats
+int qrp_lazy_f32(float* A, long long lda, int m, int n, float* tau, QrWork& w, float* work, int* phys_out,
+                 cudaStream_t st);
 int qrp_lazy_grid(int m, int n, int* grid, int* nown);
 size_t qrp_lazy_work_doubles(int n, int grid);
 // out[:, k] = A[:, perm[k]] for k < n (rows m_pad)

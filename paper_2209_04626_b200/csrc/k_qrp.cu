@@ -37,25 +37,27 @@ namespace mpj {
 constexpr int QP_NT = 512;
 constexpr int QP_NB = 32;
 
+template <typename T>
 struct QrpArgs {
-    double* A;
+    T* A;
     long long lda;
     int m, n;
-    double* tau;
+    T* tau;
     QrWork w;
-    double* F;       // n x QP_NB (row p: pending panel coefficients of column p)
-    double* part;    // G x (QP_NB + 1)
-    double* v0g;     // n
-    double* mug;     // n
+    T* F;       // n x QP_NB (row p: pending panel coefficients of column p)
+    T* part;    // G x (QP_NB + 1)
+    T* v0g;     // n
+    T* mug;     // n
     int nown;        // max owned columns per CTA
     long long* dbg;  // optional phase timers (CTA 0), MPJSVD_QRP_TIMING=1
 };
 
-__device__ __forceinline__ int qp_argmax(double v, int p, int c, double* red) {
+template <typename T>
+__device__ __forceinline__ int qp_argmax(T v, int p, int c, T* red) {
     int* redi = reinterpret_cast<int*>(red + 16);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        T v2 = __shfl_xor_sync(0xffffffffu, v, o);
         int p2 = __shfl_xor_sync(0xffffffffu, p, o);
         int c2 = __shfl_xor_sync(0xffffffffu, c, o);
         if (c2 >= 0 && (c < 0 || v2 > v || (v2 == v && p2 < p))) { v = v2; p = p2; c = c2; }
@@ -70,7 +72,7 @@ __device__ __forceinline__ int qp_argmax(double v, int p, int c, double* red) {
         c = lane < nw ? redi[2 * lane + 1] : -1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+            T v2 = __shfl_xor_sync(0xffffffffu, v, o);
             int p2 = __shfl_xor_sync(0xffffffffu, p, o);
             int c2 = __shfl_xor_sync(0xffffffffu, c, o);
             if (c2 >= 0 && (c < 0 || v2 > v || (v2 == v && p2 < p))) { v = v2; p = p2; c = c2; }
@@ -84,8 +86,8 @@ __device__ __forceinline__ int qp_argmax(double v, int p, int c, double* red) {
 }
 
 // block-wide sums of NV values (fixed tree); red needs 32 * NV doubles
-template <int NV>
-__device__ __forceinline__ void block_sum_n(double (&v)[NV], double* red) {
+template <int NV, typename T>
+__device__ __forceinline__ void block_sum_n(T (&v)[NV], T* red) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
@@ -95,30 +97,31 @@ __device__ __forceinline__ void block_sum_n(double (&v)[NV], double* red) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-        double r = lane < nw ? red[q * 32 + lane] : 0.0;
+        T r = lane < nw ? red[q * 32 + lane] : 0.0;
         v[q] = warp_sum(r);
     }
     __syncthreads();
 }
 
-template <int RPT>
-__global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
+template <typename T, int RPT>
+__global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ double qsm[];
+    extern __shared__ __align__(16) unsigned char qsm_raw[];
+    T* qsm = reinterpret_cast<T*>(qsm_raw);
     const int m = a.m, n = a.n, nown = a.nown;
-    double* vs = qsm;                               // m: current reflector v (rows k..m-1)
-    double* Fown = vs + m;                          // nown x QP_NB
-    double* vn1s = Fown + (size_t)nown * QP_NB;     // nown
-    double* vn2s = vn1s + nown;                     // nown
-    double* red = vn2s + nown;                      // 33 * 32 (>= 32 * (QP_NB + 1))
-    double* auxv = red + 32 * (QP_NB + 1);          // QP_NB
-    double* vk = auxv + QP_NB;                      // QP_NB: v_t(k)
-    double* v0p = vk + QP_NB;                       // QP_NB: 1 / v0 of the panel reflectors
-    double* fpiv = v0p + QP_NB;                     // QP_NB: F(piv, :)
-    double* scal = fpiv + QP_NB;                    // 8 scalars
-    double* dsm = scal + 8;                         // nown: v^T a_p of the owned columns
-    double* ykp = dsm + nown;                       // nown: a(k, p) before the row update
-    double* dsm2 = ykp + nown;                      // 2 nown: per-half partial dots
+    T* vs = qsm;                               // m: current reflector v (rows k..m-1)
+    T* Fown = vs + m;                          // nown x QP_NB
+    T* vn1s = Fown + (size_t)nown * QP_NB;     // nown
+    T* vn2s = vn1s + nown;                     // nown
+    T* red = vn2s + nown;                      // 33 * 32 (>= 32 * (QP_NB + 1))
+    T* auxv = red + 32 * (QP_NB + 1);          // QP_NB
+    T* vk = auxv + QP_NB;                      // QP_NB: v_t(k)
+    T* v0p = vk + QP_NB;                       // QP_NB: 1 / v0 of the panel reflectors
+    T* fpiv = v0p + QP_NB;                     // QP_NB: F(piv, :)
+    T* scal = fpiv + QP_NB;                    // 8 scalars
+    T* dsm = scal + 8;                         // nown: v^T a_p of the owned columns
+    T* ykp = dsm + nown;                       // nown: a(k, p) before the row update
+    T* dsm2 = ykp + nown;                      // 2 nown: per-half partial dots
     int* pcol = reinterpret_cast<int*>(dsm2 + 2 * nown); // QP_NB
     int* rflag = pcol + QP_NB;                      // nown: recompute flags
     int* lpos = rflag + nown;                       // nown: logical position of owned column s
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
     const long long lda = a.lda;
     volatile int* phys = a.w.phys_all + (long long)cta * n;
     volatile int* pos = a.w.pos_all + (long long)cta * n;
-    const double tol3z = sqrt(1.1102230246251565e-16);
+    const T tol3z = sqrt(sizeof(T) == 8 ? T(1.1102230246251565e-16) : T(5.9604644775390625e-08));
 
     for (int j = tid; j < n; j += QP_NT) { phys[j] = j; pos[j] = j; }
     for (int e = tid; e < nown * QP_NB; e += QP_NT) Fown[e] = 0.0;
@@ -136,24 +139,24 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         lpos[sl] = p < n ? p : -1;                   // -1: no column in this slot
         rflag[sl] = 0;
     }
-    double best = -1.0;
+    T best = -1.0;
     int best_pos = 0x7fffffff, best_col = -1;
     for (int p = cta, s = 0; p < n; p += G, ++s) {
-        const double* col = a.A + (long long)p * lda;
-        double sq[1] = {0.0};
+        const T* col = a.A + (long long)p * lda;
+        T sq[1] = {0.0};
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             int i = tid + QP_NT * j;
-            if (i < m) { double x = __ldcg(col + i); sq[0] += x * x; }
+            if (i < m) { T x = __ldcg(col + i); sq[0] += x * x; }
         }
-        block_sum_n<1>(sq, red);
-        const double nrm = sqrt(sq[0]);
+        block_sum_n<1, T>(sq, red);
+        const T nrm = sqrt(sq[0]);
         if (tid == 0) { vn1s[s] = nrm; vn2s[s] = nrm; }
         if (nrm > best || (nrm == best && p < best_pos)) { best = nrm; best_pos = p; best_col = p; }
         for (int t = tid; t < QP_NB; t += QP_NT) a.F[(long long)p * QP_NB + t] = 0.0;
     }
     if (tid == 0) {
-        a.w.cand_val[cta] = best;
+        a.w.cand_val[cta] = (double)best;
         a.w.cand_pos[cta] = best_pos;
         a.w.cand_col[cta] = best_col;
     }
@@ -174,12 +177,12 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         const int jj = k % QP_NB;
         tmark(7);
         // ---------------- pivot (largest partial norm, ties -> lowest logical index)
-        double bv = -1.0;
+        T bv = -1.0;
         int bp = 0x7fffffff, bc = -1;
         for (int g = tid; g < G; g += QP_NT) {
             int pc = __ldcg(a.w.cand_col + buf * G + g);
             if (pc < 0) continue;
-            double v = __ldcg(a.w.cand_val + buf * G + g);
+            T v = (T)__ldcg(a.w.cand_val + buf * G + g);
             int ps = __ldcg(a.w.cand_pos + buf * G + g);
             if (v > bv || (v == bv && ps < bp)) { bv = v; bp = ps; bc = pc; }
         }
@@ -205,15 +208,15 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             const long long S = (rows + G - 1) / G;
             const long long r0 = k + (long long)cta * S, r1 = min((long long)m, r0 + S);
             const int lane = tid & 31, wid = tid >> 5;
-            double* pc = a.A + (long long)piv * lda;
-            const double* pcl = lane < jj ? a.A + (long long)pcol[lane] * lda : nullptr;
-            const double rvl = lane < jj ? v0p[lane] : 0.0, fl = lane < jj ? fpiv[lane] : 0.0;
-            double zl = 0.0, sx2 = 0.0;
+            T* pc = a.A + (long long)piv * lda;
+            const T* pcl = lane < jj ? a.A + (long long)pcol[lane] * lda : nullptr;
+            const T rvl = lane < jj ? v0p[lane] : 0.0, fl = lane < jj ? fpiv[lane] : 0.0;
+            T zl = 0.0, sx2 = 0.0;
             for (long long i = r0 + wid; i < r1; i += QP_NT / 32) {
-                const double vt = lane < jj ? __ldcg(pcl + i) * rvl : 0.0;
-                const double xi0 = __ldcg(pc + i);
-                const double upd = warp_sum(vt * fl);
-                const double x = xi0 - upd;
+                const T vt = lane < jj ? __ldcg(pcl + i) * rvl : 0.0;
+                const T xi0 = __ldcg(pc + i);
+                const T upd = warp_sum(vt * fl);
+                const T x = xi0 - upd;
                 if (lane == 0) pc[i] = x;
                 if (i > k) {
                     zl += vt * x;
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             if (lane == 0) red[wid * 33 + 32] = sx2;
             __syncthreads();
             if (tid <= QP_NB) {
-                double sacc = 0.0;
+                T sacc = 0.0;
                 for (int w = 0; w < QP_NT / 32; ++w) sacc += red[w * 33 + tid];
                 const int q = tid == 32 ? QP_NB : tid;
                 if (q < jj || q == QP_NB) a.part[(long long)cta * (QP_NB + 1) + q] = sacc;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             const int lane = tid & 31, wid = tid >> 5;
             for (int q = wid; q <= QP_NB; q += QP_NT / 32) {
                 if (q < jj || q == QP_NB) {
-                    double sacc = 0.0;
+                    T sacc = 0.0;
                     for (int g = lane; g < G; g += 32) sacc += __ldcg(a.part + (long long)g * (QP_NB + 1) + q);
                     sacc = warp_sum(sacc);
                     if (lane == 0) red[q] = sacc;
@@ -252,8 +255,8 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         if (tid == 0) scal[0] = __ldcg(a.A + (long long)piv * lda + k);   // alpha
         if (tid < jj) vk[tid] = __ldcg(a.A + (long long)pcol[tid] * lda + k) * v0p[tid];
         __syncthreads();
-        const double sig = red[QP_NB], alpha = scal[0];
-        double tau, v0, mu;
+        const T sig = red[QP_NB], alpha = scal[0];
+        T tau, v0, mu;
         if (sig == 0.0) {
             v0 = 1.0;
             if (alpha >= 0.0) { tau = 0.0; mu = alpha; } else { tau = 2.0; mu = -alpha; }
@@ -262,11 +265,11 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             v0 = alpha <= 0.0 ? alpha - mu : -sig / (alpha + mu);
             tau = 2.0 * v0 * v0 / (sig + v0 * v0);
         }
-        const double rv0 = 1.0 / v0;
+        const T rv0 = 1.0 / v0;
         if (tid < jj) auxv[tid] = -tau * (vk[tid] + red[tid] * rv0);
         if (cta == 0 && tid == 0) { a.tau[k] = tau; a.v0g[k] = v0; a.mug[k] = mu; }
         {
-            const double* pc = a.A + (long long)piv * lda;
+            const T* pc = a.A + (long long)piv * lda;
 #pragma unroll
             for (int j = 0; j < RPT; ++j) {
                 int i = k + 1 + tid + QP_NT * j;
@@ -288,20 +291,20 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             for (int it = wid; it < 2 * nown; it += QP_NT / 32) {
                 const int sl = it >> 1, h = it & 1;
                 if (lpos[sl] <= k) continue;
-                const double* col = a.A + (long long)(cta + G * sl) * lda;
+                const T* col = a.A + (long long)(cta + G * sl) * lda;
                 const long long rb = k + h * L, re = min((long long)m, rb + L);
-                double acc0 = 0.0, acc1 = 0.0;
+                T acc0 = 0.0, acc1 = 0.0;
                 long long i = rb + lane;
                 for (; i + 96 < re; i += 128) {
-                    const double y0v = __ldcg(col + i), y1v = __ldcg(col + i + 32);
-                    const double y2v = __ldcg(col + i + 64), y3v = __ldcg(col + i + 96);
+                    const T y0v = __ldcg(col + i), y1v = __ldcg(col + i + 32);
+                    const T y2v = __ldcg(col + i + 64), y3v = __ldcg(col + i + 96);
                     acc0 += vs[i] * y0v;
                     acc1 += vs[i + 32] * y1v;
                     acc0 += vs[i + 64] * y2v;
                     acc1 += vs[i + 96] * y3v;
                 }
                 for (; i < re; i += 32) acc0 += vs[i] * __ldcg(col + i);
-                const double dp = warp_sum(acc0 + acc1);
+                const T dp = warp_sum(acc0 + acc1);
                 if (lane == 0) {
                     dsm2[it] = dp;
                     if (h == 0) ykp[sl] = __ldcg(col + k);
@@ -312,28 +315,28 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         for (int sl = tid; sl < nown; sl += QP_NT) dsm[sl] = dsm2[2 * sl] + dsm2[2 * sl + 1];
         __syncthreads();
         // ---------------- pass 2b: one thread per owned column: F(p, jj), row k, norm downdate
-        double cbest = -1.0;
+        T cbest = -1.0;
         int cpos = 0x7fffffff, ccol = -1;
         for (int sl = tid; sl < nown; sl += QP_NT) {
             if (lpos[sl] <= k) continue;
             const int p = cta + G * sl;
-            double* Fs = Fown + (size_t)sl * QP_NB;
-            double f = tau * dsm[sl];
+            T* Fs = Fown + (size_t)sl * QP_NB;
+            T f = tau * dsm[sl];
             for (int t = 0; t < jj; ++t) f += Fs[t] * auxv[t];
-            double akp = ykp[sl];
+            T akp = ykp[sl];
             for (int t = 0; t < jj; ++t) akp -= vk[t] * Fs[t];
             akp -= f;
             a.A[(long long)p * lda + k] = akp;
             Fs[jj] = f;
             a.F[(long long)p * QP_NB + jj] = f;
             // partial-norm downdate (LAPACK xLAQP2)
-            const double v1 = vn1s[sl], v2 = vn2s[sl];
+            const T v1 = vn1s[sl], v2 = vn2s[sl];
             int rec = 0;
             if (v1 != 0.0) {
-                const double r = fabs(akp) / v1;
-                double temp = 1.0 - r * r;
+                const T r = fabs(akp) / v1;
+                T temp = 1.0 - r * r;
                 temp = temp < 0.0 ? 0.0 : temp;
-                const double q = v1 / v2;
+                const T q = v1 / v2;
                 if (temp * q * q <= tol3z) rec = 1;
                 else vn1s[sl] = v1 * sqrt(temp);
             }
@@ -345,21 +348,21 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         for (int sl = 0; sl < nown; ++sl) {
             if (!rflag[sl]) continue;                  // flags are only set for live columns
             const int p = cta + G * sl;
-            double* col = a.A + (long long)p * lda;
-            const double* Fs = Fown + (size_t)sl * QP_NB;
-            double sq[1] = {0.0};
+            T* col = a.A + (long long)p * lda;
+            const T* Fs = Fown + (size_t)sl * QP_NB;
+            T sq[1] = {0.0};
             for (long long i = k + 1 + tid; i < m; i += QP_NT) {
-                double yv = __ldcg(col + i);
+                T yv = __ldcg(col + i);
                 for (int t = 0; t <= jj; ++t) {
-                    const double vt = t == jj ? vs[i] : __ldcg(a.A + (long long)pcol[t] * lda + i) * v0p[t];
+                    const T vt = t == jj ? vs[i] : __ldcg(a.A + (long long)pcol[t] * lda + i) * v0p[t];
                     yv -= vt * Fs[t];
                 }
                 col[i] = yv;
                 sq[0] += yv * yv;
             }
-            block_sum_n<1>(sq, red);
+            block_sum_n<1, T>(sq, red);
             if (tid == 0) {
-                const double nv = k + 1 < m ? sqrt(sq[0]) : 0.0;
+                const T nv = k + 1 < m ? sqrt(sq[0]) : 0.0;
                 vn1s[sl] = nv;
                 vn2s[sl] = nv;
                 rflag[sl] = 0;
@@ -375,14 +378,14 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             for (long long i0 = k + 1; i0 < m; i0 += QP_NT) {
                 const long long i = i0 + tid;
                 if (i < m) {
-                    double vt[QP_NB];
+                    T vt[QP_NB];
 #pragma unroll
                     for (int t = 0; t < QP_NB; ++t) {
                         vt[t] = 0.0;
                         if (t <= jj) vt[t] = (t == jj) ? vs[i] : __ldcg(a.A + (long long)pcol[t] * lda + i) * v0p[t];
                     }
                     for (int s0 = 0; s0 < nown; s0 += 4) {
-                        double yv[4];
+                        T yv[4];
                         bool lv[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             if (!lv[u]) continue;
-                            const double* Fs = Fown + (size_t)(s0 + u) * QP_NB;
+                            const T* Fs = Fown + (size_t)(s0 + u) * QP_NB;
 #pragma unroll
                             for (int t = 0; t < QP_NB; ++t)
                                 if (t <= jj) yv[u] -= vt[t] * Fs[t];
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
         // ---------------- candidates for the next step (block argmax over owned columns)
         for (int sl = tid; sl < nown; sl += QP_NT) {
             if (lpos[sl] <= k) continue;
-            const double v1 = vn1s[sl];
+            const T v1 = vn1s[sl];
             const int ps = lpos[sl];
             if (v1 > cbest || (v1 == cbest && ps < cpos)) { cbest = v1; cpos = ps; ccol = cta + G * sl; }
         }
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
             if (tid == 0) {
                 const int nb = buf ^ 1;
                 const int wsl = wcol >= 0 ? (wcol - cta) / G : 0;
-                a.w.cand_val[nb * G + cta] = wcol >= 0 ? vn1s[wsl] : -1.0;
+                a.w.cand_val[nb * G + cta] = wcol >= 0 ? (double)vn1s[wsl] : -1.0;
                 a.w.cand_pos[nb * G + cta] = wcol >= 0 ? lpos[wsl] : 0x7fffffff;
                 a.w.cand_col[nb * G + cta] = wcol;
             }
@@ -436,43 +439,46 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs a) {
     // ---------------- normalise the stored reflectors, R_kk = mu
     for (int p = cta; p < n; p += G) {
         const int k = pos[p];
-        const double rv0 = 1.0 / __ldcg(a.v0g + k), mu = __ldcg(a.mug + k);
-        double* col = a.A + (long long)p * lda;
+        const T rv0 = 1.0 / __ldcg(a.v0g + k), mu = __ldcg(a.mug + k);
+        T* col = a.A + (long long)p * lda;
         for (long long i = k + 1 + tid; i < m; i += QP_NT) col[i] = col[i] * rv0;
         if (tid == 0) col[k] = mu;
     }
 }
 
-template <int RPT>
-static void* qrp_kernel_ptr() { return (void*)k_qrp_lazy<RPT>; }
+template <typename T, int RPT>
+static void* qrp_kernel_ptr() { return (void*)k_qrp_lazy<T, RPT>; }
 
+template <typename T>
 static void* qrp_kernel_for(int m) {
     int r = 1;
     while (r * QP_NT < m) r <<= 1;
     switch (r) {
-        case 1: return qrp_kernel_ptr<1>();
-        case 2: return qrp_kernel_ptr<2>();
-        case 4: return qrp_kernel_ptr<4>();
-        case 8: return qrp_kernel_ptr<8>();
-        case 16: return qrp_kernel_ptr<16>();
+        case 1: return qrp_kernel_ptr<T, 1>();
+        case 2: return qrp_kernel_ptr<T, 2>();
+        case 4: return qrp_kernel_ptr<T, 4>();
+        case 8: return qrp_kernel_ptr<T, 8>();
+        case 16: return qrp_kernel_ptr<T, 16>();
         default: return nullptr;
     }
 }
 
+template <typename T>
 static size_t qrp_smem(int m, int nown) {
-    return sizeof(double) * ((size_t)m + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
+    return sizeof(T) * ((size_t)m + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
            sizeof(int) * (QP_NB + 2 * (size_t)nown) + 64;
 }
 
-int qrp_lazy_grid(int m, int n, int* grid, int* nown) {
-    void* fn = qrp_kernel_for(m);
+template <typename T>
+static int qrp_lazy_grid_t(int m, int n, int* grid, int* nown) {
+    void* fn = qrp_kernel_for<T>(m);
     if (!fn) return -7;
     int dev = 0, nsm = 0, per = 0;
     MPJ_CUDA_TRY(cudaGetDevice(&dev));
     MPJ_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int g = nsm;
     int no = (n + g - 1) / g;
-    size_t smem = qrp_smem(m, no);
+    size_t smem = qrp_smem<T>(m, no);
     if (smem > 227 * 1024) return -7;
     MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MPJ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, QP_NT, smem));
@@ -482,17 +488,20 @@ int qrp_lazy_grid(int m, int n, int* grid, int* nown) {
     return 0;
 }
 
+int qrp_lazy_grid(int m, int n, int* grid, int* nown) { return qrp_lazy_grid_t<double>(m, n, grid, nown); }
+
 size_t qrp_lazy_work_doubles(int n, int grid) {
     return (size_t)n * QP_NB + (size_t)grid * (QP_NB + 1) + 2 * (size_t)n;
 }
 
-int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, int* phys_out,
-             cudaStream_t st) {
+template <typename T>
+static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* work, int* phys_out,
+                      cudaStream_t st) {
     int grid = 0, nown = 0;
-    int rc = qrp_lazy_grid(m, n, &grid, &nown);
+    int rc = qrp_lazy_grid_t<T>(m, n, &grid, &nown);
     if (rc) return rc;
-    void* fn = qrp_kernel_for(m);
-    QrpArgs args;
+    void* fn = qrp_kernel_for<T>(m);
+    QrpArgs<T> args;
     args.A = A;
     args.lda = lda;
     args.m = m;
@@ -513,7 +522,7 @@ int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, dou
         args.dbg = dbg;
     }
     void* params[] = {&args};
-    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem(m, nown), st));
+    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem<T>(m, nown), st));
     MPJ_LAUNCHED();
     if (phys_out)
         MPJ_CUDA_TRY(cudaMemcpyAsync(phys_out, w.phys_all, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
@@ -527,6 +536,15 @@ int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, dou
         fprintf(stderr, "\n");
     }
     return 0;
+}
+
+int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, int* phys_out,
+             cudaStream_t st) {
+    return qrp_lazy_t<double>(A, lda, m, n, tau, w, work, phys_out, st);
+}
+int qrp_lazy_f32(float* A, long long lda, int m, int n, float* tau, QrWork& w, float* work, int* phys_out,
+                 cudaStream_t st) {
+    return qrp_lazy_t<float>(A, lda, m, n, tau, w, work, phys_out, st);
 }
 
 }  // namespace mpj

@@ -624,6 +624,23 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_CUDA_TRY(cudaEventRecord(ev[1], st));
     // ---- stage 1: column-pivoted QR  A1 P = Q_p R
     MPJ_TRY(ensure_qr_work(h, (int)n, (int)n, qw));
+    if (o.mp_rrqr) {
+        // mixed-precision RRQR (Alg. 4): the permutation from an fp32 QRP of
+        // fl32(A1 2^-e) (exact power-of-two scale, reading c-9), then the fp64 QR of A1 P
+        PROF_B("qrp_coop");
+        int g = 0, no = 0;
+        MPJ_TRY(qrp_lazy_grid((int)n, (int)n, &g, &no));
+        MPJ_TRY(ensure(h, S_QRPW, sizeof(double) * qrp_lazy_work_doubles((int)n, g)));
+        MPJ_TRY(maxabs(dA1, n_pad, n_pad, n, scal + 4, st));
+        MPJ_TRY(downcast_scaled(dA1, n_pad, dX32, n_pad, n_pad, (int)n, scal + 4, st));
+        MPJ_TRY(qrp_lazy_f32(dX32, n_pad, (int)n, (int)n, reinterpret_cast<float*>(P<double>(h, S_TAU_T)), qw,
+                             reinterpret_cast<float*>(P<double>(h, S_QRPW)), P<int>(h, S_PERM), st));
+        PROF_E("qrp_coop");
+        MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
+        PROF_B("qr_ap");
+        MPJ_TRY(qr_blocked(dA1L, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), qw, P<double>(h, S_WY), st));
+        PROF_E("qr_ap");
+    } else {
     PROF_B("qrp_coop");
     {
         int g = 0, no = 0;
@@ -633,6 +650,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     PROF_E("qrp_coop");
     MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
+    }
     MPJ_TRY(diag_stats(dA1L, n_pad, (int)n, scal + 1, flags + 1, st));
     MPJ_CUDA_TRY(cudaEventRecord(ev[2], st));
     // ---- stage 2: R = L Q_2 via QR of R^T; X = L
@@ -892,6 +910,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->split_rows = 0;
     o->fp32_tensor_cores = 1;
     o->pdl_overlap = 1;
+    o->mp_rrqr = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1152,7 +1171,27 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
     QrWork qw;
     MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
     int* phys = P<int>(h, S_IOTA);
-    if (pivot == 2) {                 // unblocked reference kernel (tests)
+    if (pivot == 3) {                 // mixed-precision RRQR (Alg. 4): fp32 pivots, fp64 QR of A P
+        int g = 0, no = 0;
+        MPJ_TRY(qrp_lazy_grid((int)m, (int)n, &g, &no));
+        MPJ_TRY(ensure(h, S_QRPW, sizeof(double) * qrp_lazy_work_doubles((int)n, g)));
+        MPJ_TRY(ensure(h, S_X32, sizeof(float) * (size_t)m_pad * n));
+        MPJ_TRY(ensure(h, S_TAU_T, sizeof(double) * (size_t)n));
+        MPJ_TRY(ensure(h, S_SCAL, sizeof(double) * 8));
+        MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m_pad, n)));
+        double* sc = P<double>(h, S_SCAL);
+        MPJ_TRY(maxabs(Aw, m_pad, m_pad, n, sc + 4, st));
+        MPJ_TRY(downcast_scaled(Aw, m_pad, P<float>(h, S_X32), m_pad, m_pad, (int)n, sc + 4, st));
+        MPJ_TRY(qrp_lazy_f32(P<float>(h, S_X32), m_pad, (int)m, (int)n, reinterpret_cast<float*>(P<double>(h, S_TAU_T)),
+                             qw, reinterpret_cast<float*>(P<double>(h, S_QRPW)), phys, st));
+        MPJ_TRY(gather_cols(Aw, m_pad, phys, P<double>(h, S_TMP2), m_pad, m_pad, (int)n, st));
+        MPJ_TRY(qr_blocked(P<double>(h, S_TMP2), m_pad, (int)m, (int)n, tau, qw, P<double>(h, S_WY), st));
+        MPJ_CUDA_TRY(cudaMemcpy2DAsync(A, sizeof(double) * lda, P<double>(h, S_TMP2), sizeof(double) * m_pad,
+                                       sizeof(double) * m, n, cudaMemcpyDefault, st));
+        if (perm) MPJ_CUDA_TRY(cudaMemcpyAsync(perm, phys, sizeof(int) * n, cudaMemcpyDefault, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        return 0;
+    } else if (pivot == 2) {          // unblocked reference kernel (tests)
         MPJ_TRY(qr_coop(Aw, m_pad, (int)m, (int)n, tau, 1, qw, phys, st));
     } else if (pivot) {
         int g = 0, no = 0;

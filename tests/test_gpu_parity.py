@@ -125,15 +125,19 @@ def test_block_jacobi_f32_vs_oracle(mp, n, b):
 
 
 @pytest.mark.parametrize("m,n,pivot", [(300, 300, 1), (257, 100, 1), (1000, 77, 0), (64, 64, 0), (300, 300, 2),
-                                       (700, 700, 1), (2100, 700, 0)])
+                                       (700, 700, 1), (2100, 700, 0), (300, 300, 3), (700, 700, 3), (257, 100, 3)])
 def test_qr_vs_oracle(mp, m, n, pivot):
-    """pivot 1: lazy (xLAQPS-style) cooperative QRP used by the path;
-    pivot 2: the unblocked cooperative kernel; pivot 0: blocked Householder QR."""
+    """pivot 1: lazy (xLAQPS-style) cooperative QRP; pivot 2: the unblocked
+    cooperative kernel; pivot 0: blocked Householder QR; pivot 3: the path's
+    mixed-precision RRQR (Alg. 4: fp32 lazy QRP pivots, fp64 blocked QR of A P)
+    against the oracle's om_mprrqr."""
     rng = np.random.default_rng(m + n)
     a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
     packed, tau, perm = mp.qr(dev(a), pivot=pivot)
     packed, tau, perm = host(packed), host(tau), host(perm)
-    if pivot:
+    if pivot == 3:
+        p_o, perm_o, tau_o, _ = oracle.mprrqr(a)
+    elif pivot:
         p_o, perm_o, tau_o, _ = oracle.qrp(a)
     else:
         p_o, tau_o, _ = oracle.qr(a)
@@ -306,3 +310,18 @@ def test_errors(mp):
     # not converged: soft warning, outputs filled
     U, S, V, st = mp.factor(dev(a), max_sweeps64=1)
     assert st["rc"] == 1 and not st["converged"]
+
+
+@pytest.mark.parametrize("name,n", [("C3", 512), ("C2", 384), ("C4", 256)])
+def test_factor_mixed_precision_rrqr_vs_oracle(mp, name, n):
+    """The mixed-precision RRQR preconditioning (PAPER.md:496-512, Alg. 4;
+    option mp_rrqr = 1) end to end against the oracle run with the same option."""
+    a = testmat.config_matrix(name, n)
+    U, S, V, st = mp.factor(dev(a), mp_rrqr=1)
+    U, S, V = host(U), host(S), host(V)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, mp_rrqr=1)
+    assert rc == 0 and st["rc"] == 0
+    check_svd(a, U, S, V)
+    assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+    assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
+    assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1

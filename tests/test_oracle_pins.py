@@ -128,6 +128,46 @@ def test_qrp_against_lapack_dgeqp3():
         assert d[k] >= np.linalg.norm(r[k:, k + 1:], axis=0).max() * (1 - 1e-12)
 
 
+@pytest.mark.parametrize("m,n", [(60, 60), (120, 45)])
+def test_qrp_f32_against_lapack_sgeqp3(m, n):
+    """Alg. 4 line 2: the fp32 QRP is LAPACK's single-precision
+    Businger-Golub QRP -- same pivot sequence as sgeqp3, |R| within fp32 rounding."""
+    import scipy.linalg.lapack as la
+    rng = np.random.default_rng(m + n)
+    a = (rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-3, 3, n)).astype(np.float32)
+    packed, perm, tau, rc = oracle.qrp_f32(a)
+    qr_l, jpvt, tau_l, *_, info = la.sgeqp3(np.asfortranarray(a))
+    assert rc == 0 and info == 0
+    assert np.array_equal(perm, jpvt - 1)
+    r, r_l = np.triu(packed[:n]), np.triu(qr_l[:n])
+    np.testing.assert_allclose(np.abs(r), np.abs(r_l), rtol=0, atol=2e-5 * np.abs(r_l).max())
+
+
+def test_mprrqr_is_qr_of_permuted_matrix():
+    """Alg. 4: P from the fp32 QRP of lower(A) (power-of-two
+    scaled, c-9), then the fp64 QR of A P: R equals LAPACK dgeqrf of A P, the
+    factorisation reproduces A P to fp64 accuracy, and R is rank revealing up to
+    the fp32 pivoting (diagonal non-increasing within a u32-sized slack)."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(4)
+    n = 80
+    a = rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-3, 3, n)
+    packed, perm, tau, rc = oracle.mprrqr(a)
+    assert rc == 0
+    _, perm32, _, _ = oracle.qrp_f32((a * 2.0 ** -np.frexp(np.abs(a).max())[1]).astype(np.float32))
+    assert np.array_equal(perm, perm32)
+    r = np.triu(packed)
+    r_l = sl.qr(a[:, perm], mode="r")[0]
+    np.testing.assert_allclose(np.abs(r), np.abs(r_l), rtol=1e-12, atol=1e-12 * np.abs(r_l).max())
+    q = oracle.form_q(packed, tau)
+    assert np.abs(q @ r - a[:, perm]).max() < 1e-13 * np.abs(a).max()
+    d = np.diag(r)
+    assert np.all(d >= 0) and np.all(d[:-1] >= d[1:] * (1 - 1e-5))
+    # the fp32 pivots agree with the fp64 QRP's wherever the latter's choice is not a near tie
+    _, perm64, _, _ = oracle.qrp(a)
+    assert np.mean(perm == perm64) > 0.9
+
+
 def test_qrp_ties_lowest_index():
     a = np.asfortranarray(np.eye(6) * 2.0)
     packed, perm, tau, rc = oracle.qrp(a)
