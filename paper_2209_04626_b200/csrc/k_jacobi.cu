@@ -807,23 +807,23 @@ __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float>
 
 // ------------------------------------------------------------------------
 // k_pair_update_dmma: grid (tile groups, npairs, 2 [X, V]), 512 threads (16
-// warps); out = W + W E on 128-row tiles, UD_TPC tiles per CTA.  E^T is
+// warps); out = W + W E on UD_RC-row tiles, UD_TPC tiles per CTA.  E^T is
 // staged once per CTA (column stride W+4: conflict-free fragment loads); the
 // tiles are double-buffered (cp.async of tile t+1 overlaps the DMMAs of tile
 // t; column stride 132).  Each warp owns (128/8) x (W/2) of the output and
 // runs K = w/4 DMMA k-steps; the result is added in place into the staged
 // tile and stored back with coalesced 16-byte stores.
 // ------------------------------------------------------------------------
-constexpr int UD_NT = 512, UD_RC = 128, UD_TPC = 8;
+constexpr int UD_NT = 256, UD_RC = 64, UD_TPC = 16;   // 2 CTAs per SM (smem ~104 KB each)
 template <int W>
 constexpr size_t update_dmma_smem() {
     return sizeof(double) * ((size_t)2 * W * (UD_RC + 4) + (size_t)W * (W + 4)) + sizeof(double*) * W;
 }
 
 template <int W>
-__global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma(JacobiRound<double> a) {
+__global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma(JacobiRound<double> a) {
     constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
-    constexpr int WC = W >= 64 ? 2 : 1, WR = 16 / WC;
+    constexpr int WC = W >= 64 ? 2 : 1, WR = (UD_NT / 32) / WC;
     constexpr int TM = RC / WR / 8, TN = W / WC / 8;
     extern __shared__ __align__(16) unsigned char upd_smem[];
     double* Wbuf = reinterpret_cast<double*>(upd_smem);     // [2][W][SW]  (column k, row rho)
@@ -916,9 +916,9 @@ __global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma(JacobiRound<doubl
 // published pair (k_pair_solve) and skips pairs that did not rotate.
 // ------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(UD_NT, 1) k_pair_update_dmma_pdl(JacobiRound<double> a, int ngroups) {
+__global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma_pdl(JacobiRound<double> a, int ngroups) {
     constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
-    constexpr int WC = W >= 64 ? 2 : 1, WR = 16 / WC;
+    constexpr int WC = W >= 64 ? 2 : 1, WR = (UD_NT / 32) / WC;
     constexpr int TM = RC / WR / 8, TN = W / WC / 8;
     extern __shared__ __align__(16) unsigned char upd_smem[];
     double* Wbuf = reinterpret_cast<double*>(upd_smem);
@@ -1045,7 +1045,7 @@ static int launch_update_dmma_pdl(const JacobiRound<double>& a, cudaStream_t st)
     const int ngroups = (int)((rows_pad + (long long)UD_TPC * UD_RC - 1) / ((long long)UD_TPC * UD_RC));
     const long long items = (long long)a.npairs * 2 * ngroups;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(items < nsm ? items : nsm));
+    cfg.gridDim = dim3((unsigned)(items < 2 * nsm ? items : 2 * nsm));   // 2 CTAs per SM
     cfg.blockDim = dim3(UD_NT);
     cfg.dynamicSmemBytes = dsm;
     cfg.stream = st;
