@@ -145,6 +145,80 @@ __global__ void k_probe(const float* A, const float* B, float* D, int mode) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(64));
 }
 
+// M = 64 probe: A rows 0..63 only; read all 128 TMEM lanes x 64 columns
+__global__ void k_probe_m64(const float* A, const float* B, float* D) {
+    extern __shared__ __align__(1024) float dyn_raw[];
+    float* dyn = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_raw) + 1023) & ~(uintptr_t)1023);
+    float* As = dyn;
+    float* Bs = dyn + 64 * K;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    char* as = reinterpret_cast<char*>(As);
+    char* bs = reinterpret_cast<char*>(Bs);
+    for (int e = tid; e < 64 * K; e += blockDim.x) {
+        const int r = e / K, k = e % K;
+        *reinterpret_cast<float*>(as + off_kmajor(r, k, K)) = A[r * K + k];
+    }
+    for (int e = tid; e < N * K; e += blockDim.x) {
+        const int r = e / K, k = e % K;
+        *reinterpret_cast<float*>(bs + off_kmajor(r, k, K)) = B[r * K + k];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(64));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tbase = tmem_base;
+    // zero the accumulator region first (all 128 lanes) so untouched lanes read 0
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        const uint32_t taddr = tbase + ((uint32_t)(32 * warp) << 16) + c0;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(0u));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (tid == 0) {
+        const uint32_t idesc = idesc_tf32(64, N, 0, 0);
+        for (int ks = 0; ks < K / 8; ++ks) {
+            uint64_t ad = make_sdesc(smem_u32(as) + ks * 256, 128, (K / 4) * 128);
+            uint64_t bd = make_sdesc(smem_u32(bs) + ks * 256, 128, (K / 4) * 128);
+            mma_tf32(tbase, ad, bd, idesc, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar)));
+    }
+    {
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(done) : "r"(smem_u32(&mbar)), "r"(0));
+        }
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tbase + ((uint32_t)(32 * warp) << 16) + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        for (int j = 0; j < 16; ++j) D[tid * N + c0 + j] = __uint_as_float(v[j]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(64));
+}
+
 static float tf32_trunc(float x) {
     uint32_t u;
     memcpy(&u, &x, 4);
@@ -188,6 +262,32 @@ int main() {
         printf("mode %d layout %s-major: max|D-ref| = %.3e  max|D-ref(tf32-truncated)| = %.3e  (scale %.3f)  D[0]=%g D[last]=%g\n",
                mn, mn ? "MN" : "K", maxerr, maxerr_t, scale, D[0], D[M * N - 1]);
         if (!(maxerr_t < 1e-4 * scale)) ++fails;
+    }
+    // M = 64: where does row i of D land?
+    {
+        cudaMemset(dD, 0, D.size() * 4);
+        cudaFuncSetAttribute(k_probe_m64, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 + N) * K * 4 + 1024);
+        k_probe_m64<<<1, 128, (64 + N) * K * 4 + 1024>>>(dA, dB, dD);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("m64: CUDA error %s\n", cudaGetErrorString(e)); return 2; }
+        cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+        int found = 0;
+        for (int lane = 0; lane < 128; ++lane) {
+            // match lane's row against reference rows of A (tf32)
+            int match = -1;
+            for (int i = 0; i < 64 && match < 0; ++i) {
+                double err = 0, sc = 0;
+                for (int n = 0; n < N; ++n) {
+                    double ref = 0;
+                    for (int k = 0; k < K; ++k) ref += (double)tf32_trunc(A[i * K + k]) * tf32_trunc(B[n * K + k]);
+                    err = fmax(err, fabs(D[lane * N + n] - ref)); sc = fmax(sc, fabs(ref));
+                }
+                if (err < 1e-4 * sc) match = i;
+            }
+            if (match >= 0) ++found;
+            if (lane % 8 == 0 || match >= 0 && lane < 40) printf("m64 lane %3d -> row %d (D[0]=%g)\n", lane, match, D[lane * N]);
+        }
+        printf("m64: %d lanes matched a row\n", found);
     }
     printf(fails ? "PROBE FAILED\n" : "PROBE OK\n");
     return fails ? 1 : 0;
