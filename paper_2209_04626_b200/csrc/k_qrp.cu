@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     __syncthreads();
     grid.sync();
 
-    long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tlast = clock64();
     auto tmark = [&](int ph) {
         if (a.dbg && cta == 0 && tid == 0) {
@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             }
             __syncthreads();
         }
+        tmark(8);
         // ---------------- end of panel: apply the panel to the owned trailing columns
         if (panel_end) {
             for (long long i0 = k + 1; i0 < m; i0 += QP_NT) {
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         grid.sync();
     }
     if (a.dbg && cta == 0 && tid == 0)
-        for (int q = 0; q < 8; ++q) a.dbg[q] = tph[q];
+        for (int q = 0; q < 10; ++q) a.dbg[q] = tph[q];
     // ---------------- normalise the stored reflectors, R_kk = mu
     for (int p = cta; p < n; p += G) {
         const int k = pos[p];
@@ -518,7 +519,7 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
     static long long* dbg = nullptr;
     const char* env = getenv("MPJSVD_QRP_TIMING");
     if (env && env[0] == '1') {
-        if (!dbg) cudaMalloc(&dbg, 8 * sizeof(long long));
+        if (!dbg) cudaMalloc(&dbg, 10 * sizeof(long long));
         args.dbg = dbg;
     }
     void* params[] = {&args};
@@ -527,12 +528,12 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
     if (phys_out)
         MPJ_CUDA_TRY(cudaMemcpyAsync(phys_out, w.phys_all, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
     if (args.dbg) {
-        long long h[8];
+        long long h[10];
         cudaMemcpyAsync(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        const char* names[8] = {"pivot", "pass1", "sync1", "reflector", "pass2", "recompute+panel", "cand", "sync2"};
+        const char* names[10] = {"pivot", "pass1", "sync1", "reflector", "pass2", "panel", "cand", "sync2", "recompute", "?"};
         fprintf(stderr, "[qrp timing m=%d n=%d G=%d] ", m, n, grid);
-        for (int q = 0; q < 8; ++q) fprintf(stderr, "%s=%.1fms ", names[q], h[q] / 1.965e6);
+        for (int q = 0; q < 9; ++q) fprintf(stderr, "%s=%.1fms ", names[q], h[q] / 1.965e6);
         fprintf(stderr, "\n");
     }
     return 0;
