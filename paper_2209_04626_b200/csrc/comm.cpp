@@ -24,6 +24,7 @@ struct NcclApi {
     decltype(&ncclBroadcast) Broadcast = nullptr;
     decltype(&ncclAllReduce) AllReduce = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) GetAsyncError = nullptr;
 };
 
 NcclApi g_api;
@@ -57,6 +58,7 @@ void load_api() {
     MPJ_SYM(Broadcast, ncclBroadcast)
     MPJ_SYM(AllReduce, ncclAllReduce)
     MPJ_SYM(GetErrorString, ncclGetErrorString)
+    MPJ_SYM(GetAsyncError, ncclCommGetAsyncError)
 #undef MPJ_SYM
     g_api.ok = true;
 }
@@ -130,6 +132,14 @@ int Comm::allreduce_max_i64(long long* buf, size_t count, cudaStream_t st) {
     return check(g_api.AllReduce(buf, buf, count, ncclInt64, ncclMax, static_cast<ncclComm_t>(comm_), st),
                  "ncclAllReduce(max)");
 }
+int Comm::async_error() {
+    if (!comm_) return 0;
+    ncclResult_t ae = ncclSuccess;
+    int rc = check(g_api.GetAsyncError(static_cast<ncclComm_t>(comm_), &ae), "ncclCommGetAsyncError");
+    if (rc) return rc;
+    return check(ae, "NCCL asynchronous error");
+}
+
 int Comm::allreduce_sum_i32(int* buf, size_t count, cudaStream_t st) {
     return check(g_api.AllReduce(buf, buf, count, ncclInt32, ncclSum, static_cast<ncclComm_t>(comm_), st),
                  "ncclAllReduce(sum)");

@@ -26,6 +26,7 @@ public:
     int allreduce_max_f64(double* buf, size_t count, cudaStream_t st);
     int allreduce_max_i64(long long* buf, size_t count, cudaStream_t st);
     int allreduce_sum_i32(int* buf, size_t count, cudaStream_t st);
+    int async_error();   // ncclCommGetAsyncError, polled at the per-sweep synchronisation
 
 private:
     void* comm_ = nullptr;   // ncclComm_t

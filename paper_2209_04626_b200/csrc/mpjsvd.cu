@@ -331,6 +331,13 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h->comm.active()) {
+            const int rc = h->comm.async_error();
+            if (rc) {
+                snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "%s", nccl_last_error());
+                return rc;
+            }
+        }
         if (h->prof.on) h->prof.resolve();
         const double off = hp[0];
         int upd = 0;
