@@ -357,7 +357,8 @@ int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, l
 //   Vp explicit (unit diagonal), S = Vp^T Vp, T (LAPACK xLARFT 'F','C'),
 //   W1 = Vp^T C, W2 = T W1, C -= Vp W2.
 // ------------------------------------------------------------------------
-constexpr int WY_NB = 64;
+constexpr int WY_NB = 128;   // panel of the WY application / blocked QR
+constexpr int LT_NB = 64;    // block of the T formation (k_larft)
 
 __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j0, int kb, double* Vp,
                              long long ldp) {
@@ -373,33 +374,43 @@ __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j
     }
 }
 
+// T of the compact WY form (LAPACK xLARFT 'F','C'): column i of T is
+// -tau_i T[0:i, 0:i] S[0:i, i], T[i][i] = tau_i.  S (the strict upper part of
+// Vp^T Vp) and tau are staged in shared memory first, so the kb dependent
+// steps run on shared memory only.
 __global__ void k_larft(const double* S, int kb, const double* tau, int j0, double* T) {
-    // S, T: WY_NB x WY_NB column-major (ld WY_NB); T upper triangular
-    __shared__ double t[WY_NB][WY_NB + 1];
-    __shared__ double zs[WY_NB];
+    // S, T: LT_NB x LT_NB blocks of ld WY_NB matrices (column-major); T upper triangular
+    extern __shared__ double lsm[];
+    double* t = lsm;                                  // [LT_NB][LT_NB + 1]: t[r * (LT_NB + 1) + c]
+    double* sv = t + LT_NB * (LT_NB + 1);             // [LT_NB][LT_NB + 1]: S
+    double* ts = sv + LT_NB * (LT_NB + 1);            // tau
+    constexpr int LS = LT_NB + 1;
     const int r = threadIdx.x;
-    for (int e = r; e < WY_NB * WY_NB; e += blockDim.x) t[e % WY_NB][e / WY_NB] = 0.0;
+    for (int e = r; e < LT_NB * LT_NB; e += blockDim.x) {
+        const int a = e % LT_NB, c = e / LT_NB;
+        t[a * LS + c] = 0.0;
+        sv[a * LS + c] = S[a + (long long)c * WY_NB];
+    }
+    if (r < kb) ts[r] = tau[j0 + r];
     __syncthreads();
     for (int i = 0; i < kb; ++i) {
-        const double ti = tau[j0 + i];
-        if (r < i) zs[r] = S[r + i * WY_NB];
-        __syncthreads();
         double val = 0.0;
         if (r < i) {
             double s = 0.0;
-            for (int c = r; c < i; ++c) s += t[r][c] * zs[c];
-            val = -ti * s;
+            for (int c = r; c < i; ++c) s += t[r * LS + c] * sv[c * LS + i];
+            val = -ts[i] * s;
         }
         __syncthreads();
-        if (r < i) t[r][i] = val;
-        if (r == i) t[i][i] = ti;
+        if (r < i) t[r * LS + i] = val;
+        if (r == i) t[i * LS + i] = ts[i];
         __syncthreads();
     }
-    for (int e = r; e < WY_NB * WY_NB; e += blockDim.x) T[e] = t[e % WY_NB][e / WY_NB];
+    for (int e = r; e < LT_NB * LT_NB; e += blockDim.x) T[(e % LT_NB) + (long long)(e / LT_NB) * WY_NB] = t[(e % LT_NB) * LS + e / LT_NB];
 }
+static size_t larft_smem() { return sizeof(double) * (2 * (size_t)LT_NB * (LT_NB + 1) + LT_NB); }
 
 size_t apply_q_work_elems(long long m, long long ncols) {
-    return (size_t)round_up(m, 32) * WY_NB + 2 * WY_NB * WY_NB + 2 * (size_t)WY_NB * ncols;
+    return (size_t)round_up(m, 32) * WY_NB + 3 * WY_NB * WY_NB + 2 * (size_t)WY_NB * ncols;
 }
 
 // C <- H C with H = H_0 ... H_{kb-1} (trans = 0) or H^T (trans = 1) for ONE
@@ -411,7 +422,8 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     double* Vp = work;                                  // rows x WY_NB (ld ldw)
     double* S = Vp + (size_t)ldw * WY_NB;               // WY_NB x WY_NB
     double* T = S + WY_NB * WY_NB;
-    double* W1 = T + WY_NB * WY_NB;                     // WY_NB x ncols
+    double* T12w = T + WY_NB * WY_NB;                   // WY_NB x WY_NB scratch (recursive T)
+    double* W1 = T12w + WY_NB * WY_NB;                  // WY_NB x ncols
     double* W2 = W1 + (size_t)WY_NB * ncols;
     int gx = (int)ceil_div(rows, 256);
     if (gx > 128) gx = 128;
@@ -419,8 +431,28 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     MPJ_LAUNCHED();
     int rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldw, Vp, ldw, 0.0, S, WY_NB, st);
     if (rc) return rc;
-    k_larft<<<1, WY_NB, 0, st>>>(S, kb, tau, 0, T);
-    MPJ_LAUNCHED();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)larft_smem());
+        attr = true;
+    }
+    // T in LT_NB blocks: diagonal blocks by k_larft, then the recursive coupling
+    // T[0:a, a:b] = -T[0:a, 0:a] S[0:a, a:b] T[a:b, a:b] (LAPACK xLARFT, recursive form)
+    MPJ_CUDA_TRY(cudaMemsetAsync(T, 0, sizeof(double) * WY_NB * WY_NB, st));
+    for (int b0 = 0; b0 < kb; b0 += LT_NB) {
+        const int bk = kb - b0 < LT_NB ? kb - b0 : LT_NB;
+        k_larft<<<1, LT_NB, larft_smem(), st>>>(S + b0 + (long long)b0 * WY_NB, bk, tau, b0,
+                                                  T + b0 + (long long)b0 * WY_NB);
+        MPJ_LAUNCHED();
+        if (b0 > 0) {
+            // W = S[0:b0, b0:b0+bk] T22 ; T12 = -T11 W
+            rc = gemm_f64(0, 0, b0, bk, bk, 1.0, S + (long long)b0 * WY_NB, WY_NB, T + b0 + (long long)b0 * WY_NB,
+                          WY_NB, 0.0, T12w, WY_NB, st);
+            if (rc) return rc;
+            rc = gemm_f64(0, 0, b0, bk, b0, -1.0, T, WY_NB, T12w, WY_NB, 0.0, T + (long long)b0 * WY_NB, WY_NB, st);
+            if (rc) return rc;
+        }
+    }
     // transposed products keep the long dimension (ncols) in the GEMM's M: W1^T = C^T Vp,
     // W2^T = W1^T T^(T) (T^T for trans), C -= Vp W2 = Vp (W2^T)^T
     const long long ldt = ncols;
