@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -354,6 +355,8 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             return MPJSVD_ERR_CUDA;
         }
         if (upd == 0) { res.converged = true; break; }
+        // fp32 near-convergence exit (reading c-10): every pair of this sweep was within 2 eps_tol
+        if (stagnation && off <= 2.0 * (double)tol) { res.converged = true; break; }
         // fp32 stagnation exit (reading c-10)
         if (stagnation && sw >= 3 && off <= 1e-4 && prev >= 0 && off > 0.25 * prev) { res.converged = true; break; }
         prev = off;
@@ -701,8 +704,10 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         }
         const float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         const float tol32_in = tol32 / (float)o.inner_tol_div;
+        int max_inner32 = o.max_inner;
+        if (const char* ev = getenv("MPJSVD_MAX_INNER32")) max_inner32 = atoi(ev);   // experiment hook
         MPJ_TRY(jacobi_stage<float>(h, dX32, n_pad, n_pad, (int)n, dV32, n_pad, n_pad, o.block_cols, tol32,
-                                    tol32_in, o.max_sweeps32, o.max_inner, true, r32));
+                                    tol32_in, o.max_sweeps32, max_inner32, true, r32));
         if (root) {
         // sort by sigma32 (descending, stable) and upcast V32 -> Q
         MPJ_TRY(col_norms<float>(dX32, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 0, st));
