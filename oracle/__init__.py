@@ -47,7 +47,8 @@ class Opts(C.Structure):
     _fields_ = [("b", C.c_int32), ("tol_mult32", C.c_double), ("tol_mult64", C.c_double),
                 ("inner_tol_div", C.c_int32), ("max_sweeps32", C.c_int32),
                 ("max_sweeps64", C.c_int32), ("max_inner", C.c_int32), ("path", C.c_int32),
-                ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32)]
+                ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32),
+                ("max_inner32", C.c_int32)]
 
 
 class Stats(C.Structure):

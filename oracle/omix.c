@@ -66,6 +66,7 @@ void om_default_opts(om_opts* o) {
     o->x_from_lq = 1;
     o->nthreads = 0;
     o->mp_rrqr = 0;
+    o->max_inner32 = 2;
 }
 
 /* ---- Householder ------------------------------------------------------ */
@@ -493,7 +494,7 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         float tol32_in = tol32 / (float)o.inner_tol_div;
         int32_t sw32 = om_block_jacobi_f32(X32, n, n, n, V32, n, n, o.b, tol32, tol32_in, o.max_sweeps32,
-                                           o.max_inner, 1, st->off_trace32, st->upd_trace32, o.nthreads);
+                                           o.max_inner32, 1, st->off_trace32, st->upd_trace32, o.nthreads);
         st->sweeps32 = sw32 < 0 ? -sw32 : sw32;
         st->final_off32 = st->sweeps32 > 0 && st->sweeps32 <= 64 ? st->off_trace32[st->sweeps32 - 1] : 0;
 

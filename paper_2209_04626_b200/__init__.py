@@ -39,7 +39,7 @@ class Options(C.Structure):
                 ("path", C.c_int32), ("x_from_lq", C.c_int32), ("compute_gates", C.c_int32),
                 ("stream", C.c_void_p), ("virtual_shards", C.c_int32), ("split_rows", C.c_int32),
                 ("fp32_tensor_cores", C.c_int32), ("pdl_overlap", C.c_int32),
-                ("mp_rrqr", C.c_int32)]
+                ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32)]
 
 
 class Stats(C.Structure):

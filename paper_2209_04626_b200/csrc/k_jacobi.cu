@@ -13,6 +13,8 @@
 // Columns of X / V never move on one GPU: block ids index column slabs.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "jacobi.h"
 
@@ -154,12 +156,19 @@ struct InnerSmem {
     static constexpr int GS = W + 1;
     static constexpr int R = W - 1;                    // max rounds per inner sweep
     T G[W * (W + 1)];
-    T E[W * (W + 1)];
+    // fp32: E stored by columns (E[row][col] at E[col * ES + row]) and updated with 16-byte vectors;
+    // fp64: by rows (E[row * ES + col]), which measured faster for the 8-byte element
+    static constexpr bool ECOL = sizeof(T) == 4;
+    static constexpr int EV = 16 / sizeof(T);          // elements per 16-byte vector
+    static constexpr int ES = ECOL ? W + EV : W + 1;
+    alignas(16) T E[W * ES];
+    static __device__ __forceinline__ int eidx(int row, int col) { return ECOL ? col * ES + row : row * ES + col; }
     Rot4<T> rot[2][W / 2];                             // current / next round
     T rt[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];   // exact 2x2 diagonal update
     unsigned short spq[R][W / 2];                      // pair k of round r: p | q << 8 (p < q; q may be the bye)
     int nrot[2];
     T red[32];
+    long long dbg_t[2][32];                            // per-warp phase end clocks (debug timing only)
 };
 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -262,7 +271,8 @@ __device__ __forceinline__ int any_pair_above(const InnerSmem<T, W>& sm, int w, 
 }
 
 template <typename T, int W>
-__device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used) {
+__device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used,
+                               long long* dbg = nullptr) {
     constexpr int GS = InnerSmem<T, W>::GS;
     constexpr int NG = inner_g_threads<W>();
     constexpr int NCH = W / 8;                          // eight-row chunks of E per pair
@@ -277,9 +287,12 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         const int x = rr_slot(r, k, w2), y = rr_slot(r, w2 - 1 - k, w2);
         sm.spq[r][k] = (unsigned short)(min(x, y) | (max(x, y) << 8));
     }
-    for (int i = tid; i < W * GS; i += nt) sm.E[i] = T(0);
+    constexpr int EV = InnerSmem<T, W>::EV, ES = InnerSmem<T, W>::ES;
+    for (int i = tid; i < W * ES; i += nt) sm.E[i] = T(0);
     if (tid < 2) sm.nrot[tid] = 0;
-    // fixed roles: pair-pair block (kA, kB) of G, or (pair kE, rows 8 cE ..) of E
+    // fixed roles: pair-pair block (kA, kB) of G, or (pair kE, row chunk cE) of E: chunk c holds the
+    // rows (j NCH + c) EV .. + EV - 1, j < 8 / EV, so that the NCH lanes of a pair read a contiguous
+    // run of every column with 16-byte accesses
     int kA = -1, kB = -1, kE = -1, r0E = 0;
     if (tid < NB) {
         int rem = tid, row = 0;
@@ -288,8 +301,8 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         kB = row + rem;
     } else if (tid >= NG && tid < NG + P * NCH) {
         kE = (tid - NG) / NCH;
-        r0E = 8 * ((tid - NG) % NCH);
-        if (r0E >= w) kE = -1;
+        r0E = (tid - NG) % NCH;                        // chunk index c
+        if (!InnerSmem<T, W>::ECOL) r0E *= 8;          // row-major E: rows 8c .. 8c + 7
     }
     __syncthreads();
     if (max_inner < 1) { if (sweeps_used) *sweeps_used = 0; return 0; }
@@ -308,9 +321,12 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         if (sweeps_used) *sweeps_used = 1;
         return 0;
     }
+    long long t_start = 0;
+    const int warp = tid >> 5;
     while (true) {
         const bool last = (r == NR - 1);
         const int rn = last ? 0 : r + 1;
+        if (dbg && tid == 0) t_start = clock64();
         // ---------------- phase A: G blocks (upper triangle G[min][max])
         if (kA >= 0) {
             const Rot4<T> RA = sm.rot[buf][kA];
@@ -348,7 +364,10 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 }
             }
         }
+        if (dbg) { __syncwarp(); if (lane == 0) sm.dbg_t[0][warp] = clock64(); }
         __syncthreads();
+        long long t_b1 = 0;
+        if (dbg && tid == 0) t_b1 = clock64();
         // ---------------- phase B: next-round rotations | E <- (I + E) J - I
         if (tid >= pwarp0) {
             if (lane < P) {
@@ -365,25 +384,63 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
             if (R4.act != T(0)) {
                 const unsigned pq = sm.spq[r][kE];
                 const int pa = pq & 255, qa = pq >> 8;
-                T ep[8], eq[8];
+                if constexpr (InnerSmem<T, W>::ECOL) {
+                    T* cp = sm.E + pa * ES;
+                    T* cq = sm.E + qa * ES;
+                    T ep[8], eq[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    ep[u] = sm.E[(r0E + u) * GS + pa];
-                    eq[u] = sm.E[(r0E + u) * GS + qa];
-                }
+                    for (int j = 0; j < 8 / EV; ++j) {
+                        const int row0 = (j * NCH + r0E) * EV;
+                        *reinterpret_cast<float4*>(&ep[j * EV]) = *reinterpret_cast<const float4*>(cp + row0);
+                        *reinterpret_cast<float4*>(&eq[j * EV]) = *reinterpret_cast<const float4*>(cq + row0);
+                    }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) rot2(R4.c, R4.s, ep[u], eq[u]);
-                const int up = pa - r0E, uq = qa - r0E;
+                    for (int u = 0; u < 8; ++u) rot2(R4.c, R4.s, ep[u], eq[u]);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (u == up) { ep[u] += R4.cm1; eq[u] += R4.s; }
-                    if (u == uq) { ep[u] -= R4.s; eq[u] += R4.cm1; }
-                    if (r0E + u < w) {
-                        sm.E[(r0E + u) * GS + pa] = ep[u];
-                        sm.E[(r0E + u) * GS + qa] = eq[u];
+                    for (int u = 0; u < 8; ++u) {
+                        const int row = ((u / EV) * NCH + r0E) * EV + (u % EV);
+                        if (row == pa) { ep[u] += R4.cm1; eq[u] += R4.s; }
+                        if (row == qa) { ep[u] -= R4.s; eq[u] += R4.cm1; }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8 / EV; ++j) {
+                        const int row0 = (j * NCH + r0E) * EV;
+                        *reinterpret_cast<float4*>(cp + row0) = *reinterpret_cast<const float4*>(&ep[j * EV]);
+                        *reinterpret_cast<float4*>(cq + row0) = *reinterpret_cast<const float4*>(&eq[j * EV]);
+                    }
+                } else {
+                    T ep[8], eq[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        ep[u] = sm.E[(r0E + u) * ES + pa];
+                        eq[u] = sm.E[(r0E + u) * ES + qa];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) rot2(R4.c, R4.s, ep[u], eq[u]);
+                    const int up = pa - r0E, uq = qa - r0E;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (u == up) { ep[u] += R4.cm1; eq[u] += R4.s; }
+                        if (u == uq) { ep[u] -= R4.s; eq[u] += R4.cm1; }
+                        sm.E[(r0E + u) * ES + pa] = ep[u];
+                        sm.E[(r0E + u) * ES + qa] = eq[u];
                     }
                 }
             }
+        }
+        if (dbg) { __syncwarp(); if (lane == 0) sm.dbg_t[1][warp] = clock64(); }
+        if (dbg) __syncthreads();
+        if (dbg && tid == 0) {
+            // dbg[0] phase A (slowest G warp), [1] barrier 1, [2] rotation warp, [3] slowest E warp, [4] rounds
+            long long mA = 0, mE = 0;
+            for (int q = 0; q < (NG >> 5); ++q) mA = max(mA, sm.dbg_t[0][q]);
+            for (int q = NG >> 5; q < (nt >> 5) - 1; ++q) mE = max(mE, sm.dbg_t[1][q]);
+            const long long mR = sm.dbg_t[1][(nt >> 5) - 1];
+            dbg[0] += mA - t_start;
+            dbg[1] += t_b1 - mA;
+            dbg[2] += mR - t_b1;
+            dbg[3] += mE - t_b1;
+            dbg[4] += 1;
         }
         if (last) {
             const int any = __syncthreads_or(f_cur);
@@ -471,7 +528,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
         T* E = a.E + (long long)pair * (W * W);
         for (int e = tid; e < W * W; e += nt) {
             const int k = e / W, j = e - (e / W) * W;
-            E[e] = (k < w && j < w) ? sm.E[k * GS + j] : T(0);   // E[k][j] row-major
+            E[e] = (k < w && j < w) ? sm.E[InnerSmem<T, W>::eidx(k, j)] : T(0);   // E[k][j] row-major
         }
     }
     if (a.dlist) {                 // publish: E and flag of this pair are complete
@@ -1143,6 +1200,9 @@ __global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
 // ------------------------------------------------------------------------
 // k_inner_solve_batch: test entry (mpjsvd_inner_solve): count matrices.
 // ------------------------------------------------------------------------
+__device__ long long* g_inner_dbg_f = nullptr;   // phase timers of the batch kernel (MPJSVD_INNER_TIMING=1)
+__device__ long long* g_inner_dbg_d = nullptr;
+
 template <typename T, int W>
 __global__ void __launch_bounds__(inner_nt<W>()) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
     constexpr int GS = InnerSmem<T, W>::GS;
@@ -1152,10 +1212,11 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_inner_solve_batch(T* G, T* E,
     T* e = E + (long long)blockIdx.x * w * w;
     for (int i = threadIdx.x; i < w * w; i += blockDim.x) sm.G[(i % w) * GS + i / w] = g[i];
     __syncthreads();
-    int nr = inner_solve_dev<T, W>(sm, w, tol_in, max_inner, nullptr);
+    long long* dbgp = sizeof(T) == 4 ? g_inner_dbg_f : g_inner_dbg_d;
+    int nr = inner_solve_dev<T, W>(sm, w, tol_in, max_inner, nullptr, blockIdx.x == 0 ? dbgp : nullptr);
     for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
         g[i] = sm.G[(i % w) * GS + i / w];
-        e[i] = sm.E[(i % w) * GS + i / w];   // column-major out: e[row + col*w] = E[row][col]
+        e[i] = sm.E[InnerSmem<T, W>::eidx(i % w, i / w)];   // column-major out: e[row + col*w] = E[row][col]
     }
     if (threadIdx.x == 0) rot[blockIdx.x] = nr;
 }
@@ -1323,8 +1384,28 @@ template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     const size_t sms = sizeof(InnerSmem<T, W>);
     cudaFuncSetAttribute(k_inner_solve_batch<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
+    static long long* dbg = nullptr;
+    const char* env = getenv("MPJSVD_INNER_TIMING");
+    const bool timing = env && env[0] == '1';
+    if (timing) {
+        if (!dbg) cudaMalloc(&dbg, 8 * sizeof(long long));
+        cudaMemsetAsync(dbg, 0, 8 * sizeof(long long), st);
+        if (sizeof(T) == 4) cudaMemcpyToSymbolAsync(g_inner_dbg_f, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, st);
+        else cudaMemcpyToSymbolAsync(g_inner_dbg_d, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, st);
+    }
     k_inner_solve_batch<T, W><<<count, inner_nt<W>(), sms, st>>>(G, E, w, tol_in, max_inner, rot);
     MPJ_LAUNCHED();
+    if (timing) {
+        long long hv[8];
+        long long* zero = nullptr;
+        cudaMemcpyAsync(hv, dbg, sizeof(hv), cudaMemcpyDeviceToHost, st);
+        if (sizeof(T) == 4) cudaMemcpyToSymbolAsync(g_inner_dbg_f, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+        else cudaMemcpyToSymbolAsync(g_inner_dbg_d, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+        const double rounds = hv[4] > 0 ? (double)hv[4] : 1.0;
+        fprintf(stderr, "[inner timing %s w=%d] rounds=%lld per round (cycles): phaseA=%.0f barrier1=%.0f rotation=%.0f E=%.0f\n",
+                sizeof(T) == 4 ? "f32" : "f64", w, hv[4], hv[0] / rounds, hv[1] / rounds, hv[2] / rounds, hv[3] / rounds);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 

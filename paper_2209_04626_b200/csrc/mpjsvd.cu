@@ -704,10 +704,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         }
         const float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         const float tol32_in = tol32 / (float)o.inner_tol_div;
-        int max_inner32 = o.max_inner;
-        if (const char* ev = getenv("MPJSVD_MAX_INNER32")) max_inner32 = atoi(ev);   // experiment hook
         MPJ_TRY(jacobi_stage<float>(h, dX32, n_pad, n_pad, (int)n, dV32, n_pad, n_pad, o.block_cols, tol32,
-                                    tol32_in, o.max_sweeps32, max_inner32, true, r32));
+                                    tol32_in, o.max_sweeps32, o.max_inner32, true, r32));
         if (root) {
         // sort by sigma32 (descending, stable) and upcast V32 -> Q
         MPJ_TRY(col_norms<float>(dX32, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 0, st));
@@ -923,6 +921,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->fp32_tensor_cores = 1;
     o->pdl_overlap = 1;
     o->mp_rrqr = 0;
+    o->max_inner32 = 2;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -934,7 +933,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (o.virtual_shards < 1 || o.virtual_shards > 64 || o.split_rows < 0) return MPJSVD_ERR_INVALID_ARG;
     if (o.block_cols != 8 && o.block_cols != 16 && o.block_cols != 32) return MPJSVD_ERR_NOT_SUPPORTED;
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
-        o.max_sweeps64 < 1 || o.max_inner < 1 || (o.path != 0 && o.path != 2))
+        o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;
