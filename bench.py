@@ -282,7 +282,12 @@ def main():
     m, n, _ = testmat.CONFIGS[args.config]
     device = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    h = mp.Handle(stream=stream.cuda_stream, block_cols=args.block_cols)
+    # experiment hook: MPJSVD_BENCH_OPTS="pdl_overlap=0,max_inner32=1" (Handle option overrides)
+    extra = {}
+    for kv in filter(None, os.environ.get("MPJSVD_BENCH_OPTS", "").split(",")):
+        k, v = kv.split("=")
+        extra[k.strip()] = float(v) if "." in v else int(v)
+    h = mp.Handle(stream=stream.cuda_stream, block_cols=args.block_cols, **extra)
     if world > 1:
         h.comm_init_torch()          # NCCL communicator inside libmpjsvd.so (rank 0's id via torch.distributed)
     a = A = U = V = S = None

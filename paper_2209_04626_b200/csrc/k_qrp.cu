@@ -23,6 +23,7 @@
 // (the unblocked algorithm reads AND writes it every step).  Reflectors are
 // stored unnormalised (x) during the factorisation and scaled by 1/v0 at the
 // end (R_kk = mu >= 0, reading c-13).
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
@@ -36,6 +37,8 @@ namespace mpj {
 
 constexpr int QP_NT = 512;
 constexpr int QP_NB = 32;
+constexpr int QP_PART_PT = 12;
+constexpr int QP_CAND_PL = 6;    // candidates per lane of the pivot warp: G <= 32 QP_CAND_PL   // partials per thread in the reflector reduction: G (QP_NB + 1) <= QP_NT QP_PART_PT
 
 template <typename T>
 struct QrpArgs {
@@ -85,6 +88,18 @@ __device__ __forceinline__ int qp_argmax(T v, int p, int c, T* red) {
     return res;
 }
 
+// warp-wide argmax under the total order (value desc, logical position asc); c < 0: no candidate
+template <typename T>
+__device__ __forceinline__ void warp_argmax(T& v, int& p, int& c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+        int c2 = __shfl_xor_sync(0xffffffffu, c, o);
+        if (c2 >= 0 && (c < 0 || v2 > v || (v2 == v && p2 < p))) { v = v2; p = p2; c = c2; }
+    }
+}
+
 // block-wide sums of NV values (fixed tree); red needs 32 * NV doubles
 template <int NV, typename T>
 __device__ __forceinline__ void block_sum_n(T (&v)[NV], T* red) {
@@ -109,8 +124,10 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     extern __shared__ __align__(16) unsigned char qsm_raw[];
     T* qsm = reinterpret_cast<T*>(qsm_raw);
     const int m = a.m, n = a.n, nown = a.nown;
-    T* vs = qsm;                               // m: current reflector v (rows k..m-1)
-    T* Fown = vs + m;                          // nown x QP_NB
+    T* vs = qsm;                               // m: current reflector v (rows k..m-1); also the
+                                               // staging of the G x (QP_NB + 1) partials (vsz >= both)
+    const int vsz = max(m, (int)gridDim.x * (QP_NB + 1));
+    T* Fown = vs + vsz;                        // nown x QP_NB
     T* vn1s = Fown + (size_t)nown * QP_NB;     // nown
     T* vn2s = vn1s + nown;                     // nown
     T* red = vn2s + nown;                      // 33 * 32 (>= 32 * (QP_NB + 1))
@@ -125,14 +142,15 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     int* pcol = reinterpret_cast<int*>(dsm2 + 2 * nown); // QP_NB
     int* rflag = pcol + QP_NB;                      // nown: recompute flags
     int* lpos = rflag + nown;                       // nown: logical position of owned column s
-    __shared__ int s_piv;
+    int* phys = lpos + nown;                        // n: column at logical position (this CTA's copy)
+    int* pos = phys + n;                            // n: logical position of physical column
+    __shared__ int s_anyrec, s_piv;
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const long long lda = a.lda;
-    volatile int* phys = a.w.phys_all + (long long)cta * n;
-    volatile int* pos = a.w.pos_all + (long long)cta * n;
     const T tol3z = sqrt(sizeof(T) == 8 ? T(1.1102230246251565e-16) : T(5.9604644775390625e-08));
 
     for (int j = tid; j < n; j += QP_NT) { phys[j] = j; pos[j] = j; }
+    if (tid == 0) s_anyrec = 0;
     for (int e = tid; e < nown * QP_NB; e += QP_NT) Fown[e] = 0.0;
     for (int sl = tid; sl < nown; sl += QP_NT) {
         const int p = cta + G * sl;
@@ -166,7 +184,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     long long tph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tlast = clock64();
     auto tmark = [&](int ph) {
-        if (a.dbg && cta == 0 && tid == 0) {
+        if (a.dbg && tid == 0) {
             long long t = clock64();
             tph[ph] += t - tlast;
             tlast = t;
@@ -176,28 +194,40 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         const int buf = k & 1;
         const int jj = k % QP_NB;
         tmark(7);
-        // ---------------- pivot (largest partial norm, ties -> lowest logical index)
-        T bv = -1.0;
-        int bp = 0x7fffffff, bc = -1;
-        for (int g = tid; g < G; g += QP_NT) {
-            int pc = __ldcg(a.w.cand_col + buf * G + g);
-            if (pc < 0) continue;
-            T v = (T)__ldcg(a.w.cand_val + buf * G + g);
-            int ps = __ldcg(a.w.cand_pos + buf * G + g);
-            if (v > bv || (v == bv && ps < bp)) { bv = v; bp = ps; bc = pc; }
+        // ---------------- pivot (largest partial norm, ties -> lowest logical index): warp 0
+        if (tid < 32) {
+            T bv = -1.0;
+            int bp = 0x7fffffff, bc = -1;
+            int pcv[QP_CAND_PL], psv[QP_CAND_PL];
+            double vv[QP_CAND_PL];
+#pragma unroll
+            for (int j = 0; j < QP_CAND_PL; ++j) {       // every candidate load in flight at once
+                const int g = tid + 32 * j;
+                pcv[j] = g < G ? __ldcg(a.w.cand_col + buf * G + g) : -1;
+                vv[j] = g < G ? __ldcg(a.w.cand_val + buf * G + g) : -1.0;
+                psv[j] = g < G ? __ldcg(a.w.cand_pos + buf * G + g) : 0x7fffffff;
+            }
+#pragma unroll
+            for (int j = 0; j < QP_CAND_PL; ++j) {
+                if (pcv[j] < 0) continue;
+                const T v = (T)vv[j];
+                if (v > bv || (v == bv && psv[j] < bp)) { bv = v; bp = psv[j]; bc = pcv[j]; }
+            }
+            warp_argmax(bv, bp, bc);
+            const int pv = __shfl_sync(0xffffffffu, bc, 0);
+            if (tid < jj) fpiv[tid] = __ldcg(a.F + (long long)pv * QP_NB + tid);
+            if (tid == 0) {
+                s_piv = pv;
+                int pk = phys[k], pj = pos[pv];
+                phys[k] = pv; phys[pj] = pk;
+                pos[pv] = k; pos[pk] = pj;
+                pcol[jj] = pv;
+                if (pk % G == cta) lpos[pk / G] = pj;
+                if (pv % G == cta) lpos[pv / G] = k;
+            }
         }
-        bc = qp_argmax(bv, bp, bc, red);
-        const int piv = bc;
-        if (tid == 0) {
-            int pk = phys[k], pj = pos[piv];
-            phys[k] = piv; phys[pj] = pk;
-            pos[piv] = k; pos[pk] = pj;
-            pcol[jj] = piv;
-            if (pk % G == cta) lpos[pk / G] = pj;
-            if (piv % G == cta) lpos[piv / G] = k;
-        }
-        if (tid < jj) fpiv[tid] = __ldcg(a.F + (long long)piv * QP_NB + tid);
         __syncthreads();
+        const int piv = s_piv;
         tmark(0);
         // ---------------- pass 1: pivot column rows k..m-1 in row slices.
         // A warp takes one row at a time; lane t < jj holds v_t(i) (panel reflector t,
@@ -212,15 +242,26 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             const T* pcl = lane < jj ? a.A + (long long)pcol[lane] * lda : nullptr;
             const T rvl = lane < jj ? v0p[lane] : 0.0, fl = lane < jj ? fpiv[lane] : 0.0;
             T zl = 0.0, sx2 = 0.0;
-            for (long long i = r0 + wid; i < r1; i += QP_NT / 32) {
-                const T vt = lane < jj ? __ldcg(pcl + i) * rvl : 0.0;
-                const T xi0 = __ldcg(pc + i);
-                const T upd = warp_sum(vt * fl);
-                const T x = xi0 - upd;
-                if (lane == 0) pc[i] = x;
-                if (i > k) {
-                    zl += vt * x;
-                    sx2 += x * x;
+            constexpr int RS = QP_NT / 32;
+            for (long long ib = r0 + wid; ib < r1; ib += 4 * RS) {
+                T vtv[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const long long i = ib + u * RS;
+                    vtv[u] = (lane < jj && i < r1) ? __ldcg(pcl + i) * rvl : T(0);
+                    xv[u] = i < r1 ? __ldcg(pc + i) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const long long i = ib + u * RS;
+                    if (i >= r1) break;
+                    const T upd = warp_sum(vtv[u] * fl);
+                    const T x = xv[u] - upd;
+                    if (lane == 0) pc[i] = x;
+                    if (i > k) {
+                        zl += vtv[u] * x;
+                        sx2 += x * x;
+                    }
                 }
             }
             // lane t of every warp holds a partial z_t; sx2 identical in all lanes of a warp
@@ -239,21 +280,47 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         grid.sync();
         tmark(2);
         // ---------------- reflector (identical in every CTA)
+        T colv[RPT];                  // pivot column rows k+1.. (pass 1 output), loaded with the partials
+        T alpha_r = 0.0, vk_r = 0.0;
         {
-            // value q (z_t for t < jj, sigma at q = QP_NB) summed over the G CTAs:
-            // warp w handles q = w, w + 16, ...; lanes stride over g; fixed tree
+            // value q (z_t for t < jj, sigma at q = QP_NB) summed over the G CTAs: the G x (QP_NB + 1)
+            // partials are staged in shared memory (every load in flight at once), then warp w sums
+            // q = w, w + 16, ... with lanes striding over g (fixed tree)
             const int lane = tid & 31, wid = tid >> 5;
+            const int tot = G * (QP_NB + 1);
+            T pv[QP_PART_PT];
+#pragma unroll
+            for (int j = 0; j < QP_PART_PT; ++j) {
+                const int e = tid + QP_NT * j;
+                pv[j] = e < tot ? __ldcg(a.part + e) : T(0);
+            }
+            {
+                const T* pcp = a.A + (long long)piv * lda;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    const int i = k + 1 + tid + QP_NT * j;
+                    colv[j] = i < m ? __ldcg(pcp + i) : T(0);
+                }
+                if (tid == 0) alpha_r = __ldcg(pcp + k);
+                if (tid < jj) vk_r = __ldcg(a.A + (long long)pcol[tid] * lda + k);
+            }
+#pragma unroll
+            for (int j = 0; j < QP_PART_PT; ++j) {
+                const int e = tid + QP_NT * j;
+                if (e < tot) vs[e] = pv[j];
+            }
+            __syncthreads();
             for (int q = wid; q <= QP_NB; q += QP_NT / 32) {
                 if (q < jj || q == QP_NB) {
                     T sacc = 0.0;
-                    for (int g = lane; g < G; g += 32) sacc += __ldcg(a.part + (long long)g * (QP_NB + 1) + q);
+                    for (int g = lane; g < G; g += 32) sacc += vs[g * (QP_NB + 1) + q];
                     sacc = warp_sum(sacc);
                     if (lane == 0) red[q] = sacc;
                 }
             }
         }
-        if (tid == 0) scal[0] = __ldcg(a.A + (long long)piv * lda + k);   // alpha
-        if (tid < jj) vk[tid] = __ldcg(a.A + (long long)pcol[tid] * lda + k) * v0p[tid];
+        if (tid == 0) scal[0] = alpha_r;   // alpha
+        if (tid < jj) vk[tid] = vk_r * v0p[tid];
         __syncthreads();
         const T sig = red[QP_NB], alpha = scal[0];
         T tau, v0, mu;
@@ -269,11 +336,10 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         if (tid < jj) auxv[tid] = -tau * (vk[tid] + red[tid] * rv0);
         if (cta == 0 && tid == 0) { a.tau[k] = tau; a.v0g[k] = v0; a.mug[k] = mu; }
         {
-            const T* pc = a.A + (long long)piv * lda;
 #pragma unroll
             for (int j = 0; j < RPT; ++j) {
                 int i = k + 1 + tid + QP_NT * j;
-                if (i < m) vs[i] = __ldcg(pc + i) * rv0;
+                if (i < m) vs[i] = colv[j] * rv0;
             }
             if (tid == 0) vs[k] = 1.0;
         }
@@ -288,8 +354,11 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             const int lane = tid & 31, wid = tid >> 5;
             const long long rows = m - k;
             const long long L = (rows + 1) / 2;
+            // the sweep over the owned columns alternates direction from step to step, so the
+            // columns read last (still in L2) are read first by the next step
+            const bool rev = (k & 1) != 0;
             for (int it = wid; it < 2 * nown; it += QP_NT / 32) {
-                const int sl = it >> 1, h = it & 1;
+                const int sl = rev ? nown - 1 - (it >> 1) : (it >> 1), h = it & 1;
                 if (lpos[sl] <= k) continue;
                 const T* col = a.A + (long long)(cta + G * sl) * lda;
                 const long long rb = k + h * L, re = min((long long)m, rb + L);
@@ -306,7 +375,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 for (; i < re; i += 32) acc0 += vs[i] * __ldcg(col + i);
                 const T dp = warp_sum(acc0 + acc1);
                 if (lane == 0) {
-                    dsm2[it] = dp;
+                    dsm2[2 * sl + h] = dp;
                     if (h == 0) ykp[sl] = __ldcg(col + k);
                 }
             }
@@ -341,11 +410,13 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 else vn1s[sl] = v1 * sqrt(temp);
             }
             rflag[sl] = rec;
+            if (rec) s_anyrec = 1;
         }
         __syncthreads();
         tmark(4);
         // ---------------- eager recompute of flagged columns (rare)
-        for (int sl = 0; sl < nown; ++sl) {
+        const bool anyrec = s_anyrec != 0;
+        for (int sl = 0; anyrec && sl < nown; ++sl) {
             if (!rflag[sl]) continue;                  // flags are only set for live columns
             const int p = cta + G * sl;
             T* col = a.A + (long long)p * lda;
@@ -372,6 +443,10 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 a.F[(long long)p * QP_NB + t] = 0.0;
             }
             __syncthreads();
+        }
+        if (anyrec) {
+            __syncthreads();
+            if (tid == 0) s_anyrec = 0;
         }
         tmark(8);
         // ---------------- end of panel: apply the panel to the owned trailing columns
@@ -413,30 +488,33 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             }
         }
         tmark(5);
-        // ---------------- candidates for the next step (block argmax over owned columns)
-        for (int sl = tid; sl < nown; sl += QP_NT) {
-            if (lpos[sl] <= k) continue;
-            const T v1 = vn1s[sl];
-            const int ps = lpos[sl];
-            if (v1 > cbest || (v1 == cbest && ps < cpos)) { cbest = v1; cpos = ps; ccol = cta + G * sl; }
-        }
-        {
-            // value and logical position of the winner (every thread gets the column)
-            const int wcol = qp_argmax(cbest, cpos, ccol, red);
+        // ---------------- candidate for the next step (argmax over the owned columns): warp 0
+        if (tid < 32) {
+            for (int sl = tid; sl < nown; sl += 32) {
+                if (lpos[sl] <= k) continue;
+                const T v1 = vn1s[sl];
+                const int ps = lpos[sl];
+                if (v1 > cbest || (v1 == cbest && ps < cpos)) { cbest = v1; cpos = ps; ccol = cta + G * sl; }
+            }
+            warp_argmax(cbest, cpos, ccol);
             if (tid == 0) {
                 const int nb = buf ^ 1;
-                const int wsl = wcol >= 0 ? (wcol - cta) / G : 0;
-                a.w.cand_val[nb * G + cta] = wcol >= 0 ? (double)vn1s[wsl] : -1.0;
-                a.w.cand_pos[nb * G + cta] = wcol >= 0 ? lpos[wsl] : 0x7fffffff;
-                a.w.cand_col[nb * G + cta] = wcol;
+                a.w.cand_val[nb * G + cta] = ccol >= 0 ? (double)cbest : -1.0;
+                a.w.cand_pos[nb * G + cta] = ccol >= 0 ? cpos : 0x7fffffff;
+                a.w.cand_col[nb * G + cta] = ccol;
             }
         }
         __syncthreads();
         tmark(6);
         grid.sync();
     }
-    if (a.dbg && cta == 0 && tid == 0)
-        for (int q = 0; q < 10; ++q) a.dbg[q] = tph[q];
+    if (a.dbg && tid == 0)
+        for (int q = 0; q < 10; ++q) {
+            if (cta == 0) a.dbg[q] = tph[q];
+            a.dbg[16 + 10 * cta + q] = tph[q];
+        }
+    if (cta == 0)
+        for (int j = tid; j < n; j += QP_NT) a.w.phys_all[j] = phys[j];
     // ---------------- normalise the stored reflectors, R_kk = mu
     for (int p = cta; p < n; p += G) {
         const int k = pos[p];
@@ -465,9 +543,10 @@ static void* qrp_kernel_for(int m) {
 }
 
 template <typename T>
-static size_t qrp_smem(int m, int nown) {
-    return sizeof(T) * ((size_t)m + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
-           sizeof(int) * (QP_NB + 2 * (size_t)nown) + 64;
+static size_t qrp_smem(int m, int n, int nown, int grid) {
+    const size_t vsz = std::max((size_t)m, (size_t)grid * (QP_NB + 1));
+    return sizeof(T) * (vsz + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
+           sizeof(int) * (QP_NB + 2 * (size_t)nown + 2 * (size_t)n) + 64;
 }
 
 template <typename T>
@@ -479,7 +558,8 @@ static int qrp_lazy_grid_t(int m, int n, int* grid, int* nown) {
     MPJ_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int g = nsm;
     int no = (n + g - 1) / g;
-    size_t smem = qrp_smem<T>(m, no);
+    if (g * (QP_NB + 1) > QP_NT * QP_PART_PT || g > 32 * QP_CAND_PL) return -7;
+    size_t smem = qrp_smem<T>(m, n, no, g);
     if (smem > 227 * 1024) return -7;
     MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MPJ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, QP_NT, smem));
@@ -519,21 +599,30 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
     static long long* dbg = nullptr;
     const char* env = getenv("MPJSVD_QRP_TIMING");
     if (env && env[0] == '1') {
-        if (!dbg) cudaMalloc(&dbg, 10 * sizeof(long long));
+        if (!dbg) cudaMalloc(&dbg, (16 + 10 * 1024) * sizeof(long long));
         args.dbg = dbg;
     }
     void* params[] = {&args};
-    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem<T>(m, nown), st));
+    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem<T>(m, n, nown, grid), st));
     MPJ_LAUNCHED();
     if (phys_out)
         MPJ_CUDA_TRY(cudaMemcpyAsync(phys_out, w.phys_all, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
     if (args.dbg) {
-        long long h[10];
-        cudaMemcpyAsync(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+        static long long h[16 + 10 * 1024];
+        cudaMemcpyAsync(h, args.dbg, sizeof(long long) * (16 + 10 * grid), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         const char* names[10] = {"pivot", "pass1", "sync1", "reflector", "pass2", "panel", "cand", "sync2", "recompute", "?"};
         fprintf(stderr, "[qrp timing m=%d n=%d G=%d] ", m, n, grid);
         for (int q = 0; q < 9; ++q) fprintf(stderr, "%s=%.1fms ", names[q], h[q] / 1.965e6);
+        fprintf(stderr, "\n[qrp timing over CTAs min/mean/max ms] ");
+        for (int q = 0; q < 9; ++q) {
+            double mn = 1e30, mx = 0, sm = 0;
+            for (int g = 0; g < grid; ++g) {
+                const double v = h[16 + 10 * g + q] / 1.965e6;
+                mn = v < mn ? v : mn; mx = v > mx ? v : mx; sm += v;
+            }
+            fprintf(stderr, "%s=%.1f/%.1f/%.1f ", names[q], mn, sm / grid, mx);
+        }
         fprintf(stderr, "\n");
     }
     return 0;

@@ -23,6 +23,8 @@
 // (warp w owns TMEM lanes 32w..32w+31).  Validated by tools/tc_probe.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "jacobi.h"
 
@@ -125,10 +127,9 @@ __device__ __forceinline__ float4 quad_transpose(float4 v, int lane) {
 // step, D = A H (M = 128, N = 64), gives D[0:64] = H^T H and D[64:128] = L^T H,
 // and G = H^T H + L^T H + (L^T H)^T (the lo x lo term, ~2^-22, is dropped).
 // ------------------------------------------------------------------------
-constexpr int GT_KT = 64, GT_ST = 3, GT_NT = 128;
-constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;        // 32 KB
-constexpr int GT_CHUNKS = 64 * (GT_KT / 4) / GT_NT;   // 16-byte chunks per thread per tile (8)
-constexpr size_t gram_tc_smem() { return (size_t)GT_ST * GT_STAGE_BYTES + 1024; }
+constexpr int GT_NT = 128;
+template <int KT, int ST>
+constexpr size_t gram_tc_smem() { return (size_t)ST * (128 * KT * 4) + 1024; }
 
 __device__ __forceinline__ void cp16(uint32_t saddr, const void* g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
@@ -137,7 +138,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a) {
+__device__ long long* g_gram_dbg = nullptr;   // phase timers (MPJSVD_GRAM_TIMING=1, tools only)
+
+template <int GT_KT, int GT_ST, int MINB>
+__global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tc(JacobiRound<float> a) {
+    constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;
+    constexpr int GT_CHUNKS = 64 * (GT_KT / 4) / GT_NT;   // 16-byte chunks per thread per tile
     reset_publication(a);
     extern __shared__ __align__(1024) unsigned char gt_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gt_raw) + 1023) & ~(uintptr_t)1023);
@@ -191,17 +197,23 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
         if (t < ntile) issue(t);
         cp_commit();
     }
+    long long* dbg = g_gram_dbg;
+    long long tw[6] = {0, 0, 0, 0, 0, 0};
     for (int t = 0; t < ntile; ++t) {
         const int s = t % GT_ST;
         unsigned char* st = sm + (size_t)s * GT_STAGE_BYTES;
+        long long c0 = dbg ? clock64() : 0;
         cp_wait<GT_ST - 2>();                           // this thread's chunks of tile t have landed
+        long long c1 = dbg ? clock64() : 0;
 #pragma unroll
         for (int u = 0; u < GT_CHUNKS; ++u) {
             const float4 x = *reinterpret_cast<const float4*>(st + soff[u]);
             *reinterpret_cast<float4*>(st + soff[u] + 8 * SBO) = tc::lo4(x, tc::hi4(x));
         }
         tc::fence_async_smem();
+        long long c2 = dbg ? clock64() : 0;
         __syncthreads();
+        long long c3 = dbg ? clock64() : 0;
         if (tid == 0) {
             tc::fence_after();
             const uint32_t base = sbase + (uint32_t)(s * GT_STAGE_BYTES);
@@ -214,11 +226,21 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tc(JacobiRound<float> a)
         }
         // refill: tile t + GT_ST - 1 goes to the stage of tile t - 1 once its MMAs are done
         const int tn = t + GT_ST - 1;
+        long long c4 = dbg ? clock64() : 0, c5 = c4;
         if (tn < ntile) {
             if (t >= 1) tc::mbar_wait(&mbar[(t - 1) % GT_ST], (uint32_t)(((t - 1) / GT_ST) & 1));
+            c5 = dbg ? clock64() : 0;
             issue(tn);
         }
         cp_commit();
+        if (dbg) {
+            const long long c6 = clock64();
+            tw[0] += c1 - c0; tw[1] += c2 - c1; tw[2] += c3 - c2; tw[3] += c4 - c3; tw[4] += c5 - c4; tw[5] += c6 - c5;
+        }
+    }
+    if (dbg && tid == 32) {
+        for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)(dbg + i), (unsigned long long)tw[i]);
+        atomicAdd((unsigned long long*)(dbg + 6), (unsigned long long)ntile);
     }
     float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
     float* red = reinterpret_cast<float*>(sm);           // 2 x 64 x 65 floats (stages are free after the last MMA)
@@ -618,14 +640,54 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
 // ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
+// Gram variants (KT rows per stage, ST stages, CTAs per SM); MPJSVD_GRAM_VARIANT selects one (experiments)
+struct GramVariant {
+    void (*fn)(JacobiRound<float>);
+    size_t smem;
+    int per_sm;
+};
+static const GramVariant g_gram_variants[] = {
+    {k_pair_gram_tc<64, 3, 2>, gram_tc_smem<64, 3>(), 2},
+    {k_pair_gram_tc<64, 6, 1>, gram_tc_smem<64, 6>(), 1},
+    {k_pair_gram_tc<32, 6, 2>, gram_tc_smem<32, 6>(), 2},
+    {k_pair_gram_tc<128, 3, 1>, gram_tc_smem<128, 3>(), 1},
+    {k_pair_gram_tc<32, 4, 3>, gram_tc_smem<32, 4>(), 3},
+    {k_pair_gram_tc<64, 4, 1>, gram_tc_smem<64, 4>(), 1},
+};
+static const GramVariant& gram_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MPJSVD_GRAM_VARIANT");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v >= (int)(sizeof(g_gram_variants) / sizeof(g_gram_variants[0]))) v = 0;
+    }
+    return g_gram_variants[v];
+}
+
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    const GramVariant& gv = gram_variant();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_pair_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem());
+        cudaFuncSetAttribute(gv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gv.smem);
         attr = true;
     }
-    k_pair_gram_tc<<<dim3(a.nsplit, a.npairs), GT_NT, gram_tc_smem(), st>>>(a);
+    static long long* dbg = nullptr;
+    static long long calls = 0;
+    static const bool timing = getenv("MPJSVD_GRAM_TIMING") != nullptr;
+    if (timing && !dbg) {
+        cudaMalloc(&dbg, 8 * sizeof(long long));
+        cudaMemset(dbg, 0, 8 * sizeof(long long));
+        cudaMemcpyToSymbol(g_gram_dbg, &dbg, sizeof(dbg));
+    }
+    gv.fn<<<dim3(a.nsplit, a.npairs), GT_NT, gv.smem, st>>>(a);
     MPJ_LAUNCHED();
+    if (timing && ++calls % 500 == 0) {
+        long long hv[8];
+        cudaMemcpy(hv, dbg, sizeof(hv), cudaMemcpyDeviceToHost);
+        const double nt = hv[6] > 0 ? (double)hv[6] : 1.0;
+        fprintf(stderr, "[gram timing] tiles=%lld per tile (cycles, warp 1): cp_wait=%.0f lo=%.0f bar=%.0f mma_issue=%.0f mbar_wait=%.0f refill=%.0f\n",
+                hv[6], hv[0] / nt, hv[1] / nt, hv[2] / nt, hv[3] / nt, hv[4] / nt, hv[5] / nt);
+    }
     return 0;
 }
 
@@ -645,9 +707,10 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 }
 
 int gram_tc_ctas_per_sm() {
-    // shared memory bound: (GT_ST stages + alignment + static) per CTA of 228 KB per SM
-    const int per = (int)((228 * 1024) / (gram_tc_smem() + 2048));
-    return per < 2 ? per : 2;                       // __launch_bounds__(GT_NT, 2)
+    // shared memory bound: (stages + alignment + static) per CTA of 228 KB per SM
+    const GramVariant& gv = gram_variant();
+    const int per = (int)((228 * 1024) / (gv.smem + 2048));
+    return per < gv.per_sm ? per : gv.per_sm;
 }
 
 }  // namespace mpj
