@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define MPJSVD_VERSION 110
+#define MPJSVD_VERSION 120
 #define MPJSVD_COMM_ID_BYTES 128
 
 /* return codes */
@@ -100,6 +100,10 @@ typedef struct {
                                   QRP costs about as much as the fp64 one (reading c-22) */
     int32_t max_inner32;       /* inner sweeps cap of the fp32 stage's 2b x 2b solves (default 2; the fp64
                                   stage uses max_inner); reading c-5 */
+    int32_t switch_u;          /* 1 (default): U-route precision switch, the paper's Alg. 3 choice (PAPER.md:446-447,
+                                  542-545, 563-573): the fp32 stage does not accumulate V; Q = qr(X^T working(U_low))
+                                  by fp64 Householder QR (diag(R2) >= 0).  0: V-route, the fp32 stage accumulates V32
+                                  and Q = qr(fl64(V32)) by CholeskyQR (reading c-11) */
 } mpjsvd_options;
 
 typedef struct {
@@ -239,6 +243,15 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
 /* Precision lift: Q = V * Rv^-1, Rv = chol(V^T V),
    V = fl64(V32) (n x n, ldv32 / ldq). */
 int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq);
+
+/* U-route precision switch (Alg. 3 l.446-447): Z = X^T Ulow in fp64, Householder QR
+   Z = Q R2 with diag(R2) >= 0, Q = H_0 ... H_{n-1} I written to Q.  X, Ulow, Q are n x n column-major
+   fp64 (ldx, ldu, ldq >= n), device or host pointers (copied through handle workspaces; X and Ulow are
+   not modified).  x_lower != 0 declares X lower triangular (its upper part is then not read).  In exact
+   arithmetic Q = V_X when X = U_X S V_X^T and Ulow = U_X.  Errors: INVALID_ARG (null, n < 1, ld < n),
+   CUDA, OUT_OF_MEMORY. */
+int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
+                    double* Q, int64_t ldq, int32_t x_lower);
 
 /* C <- Q C with Q = H_0 ... H_{k-1} packed as returned by mpjsvd_qr (rows m). */
 int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv,

@@ -48,7 +48,7 @@ class Opts(C.Structure):
                 ("inner_tol_div", C.c_int32), ("max_sweeps32", C.c_int32),
                 ("max_sweeps64", C.c_int32), ("max_inner", C.c_int32), ("path", C.c_int32),
                 ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32),
-                ("max_inner32", C.c_int32)]
+                ("max_inner32", C.c_int32), ("switch_u", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -103,6 +103,7 @@ def lib():
                                               C.c_int32]
             L.om_block_jacobi_f32.restype = C.c_int32
             L.om_lift.argtypes = [fp, i64, i64, dp, i64]
+            L.om_switch_u.argtypes = [dp, i64, i64, dp, i64, dp, i64]
             L.om_mixed_svd.argtypes = [dp, i64, i64, i64, C.POINTER(Opts), dp, i64, dp, dp, i64,
                                        C.POINTER(Stats)]
             L.oc_cyclic_jacobi.argtypes = [dp, i64, i64, i64, dp, i64, C.c_double, C.c_int32,
@@ -239,6 +240,16 @@ def lift(v32: np.ndarray) -> tuple[np.ndarray, int]:
     n = v32.shape[0]
     q = np.zeros((n, n), order="F")
     rc = lib().om_lift(_fp(v32), n, n, _dp(q), n)
+    return q, rc
+
+
+def switch_u(x: np.ndarray, ulow: np.ndarray) -> tuple[np.ndarray, int]:
+    """U-route switch: Q of the Householder QR of X^T Ulow."""
+    x = np.asfortranarray(x, dtype=np.float64)
+    ulow = np.asfortranarray(ulow, dtype=np.float64)
+    n = x.shape[0]
+    q = np.zeros((n, n), order="F")
+    rc = lib().om_switch_u(_dp(x), n, n, _dp(ulow), n, _dp(q), n)
     return q, rc
 
 

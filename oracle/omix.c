@@ -67,6 +67,7 @@ void om_default_opts(om_opts* o) {
     o->nthreads = 0;
     o->mp_rrqr = 0;
     o->max_inner32 = 2;
+    o->switch_u = 1;
 }
 
 /* ---- Householder ------------------------------------------------------ */
@@ -349,6 +350,30 @@ int om_lift(const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq) 
     return rc;
 }
 
+/* ---- U-route precision switch (Alg. 3 l.446-447) --- */
+int om_switch_u(const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
+                double* Q, int64_t ldq) {
+    double* Z = (double*)malloc(sizeof(double) * (size_t)n * n);
+    double* tau = (double*)malloc(sizeof(double) * (size_t)n);
+    /* Z = X^T Ulow: z_ij = sum_r x_ri u_rj, ascending r */
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            double acc = 0.0;
+            for (int64_t r = 0; r < n; ++r) acc += X[r + i * ldx] * Ulow[r + j * ldu];
+            Z[i + j * n] = acc;
+        }
+    /* Z = Q R2, Householder, diag(R2) >= 0 */
+    int rc = om_qr(Z, n, n, n, tau);
+    /* Q = H_0 ... H_{n-1} I */
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) Q[i + j * ldq] = i == j ? 1.0 : 0.0;
+    om_apply_q(Z, n, n, n, tau, Q, ldq, n);
+    free(Z);
+    free(tau);
+    return rc;
+}
+
 /* overflow-safe two-pass norm: scale by max|x|, then sum squares */
 static double safe_norm(const double* x, int64_t len) {
     double mx = 0.0;
@@ -481,7 +506,7 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         memcpy(Y, X, sizeof(double) * (size_t)nn);
     } else {
         st->path_taken = OM_PATH_FORCE_MIXED;
-        /* step 6: X32 = fl32(X 2^-e), max|X| 2^-e in [0.5, 1) (c-9); V32 = I */
+        /* step 6: X32 = fl32(X 2^-e), max|X| 2^-e in [0.5, 1) (c-9); V32 = I (V-route only) */
         double mx = 0.0;
         for (int64_t i = 0; i < nn; ++i) if (fabs(X[i]) > mx) mx = fabs(X[i]);
         int e = 0;
@@ -490,26 +515,37 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         memset(V32, 0, sizeof(float) * (size_t)nn);
         for (int64_t j = 0; j < n; ++j) V32[j + j * n] = 1.0f;
 
-        /* step 7: fp32 block Jacobi (c-10) */
+        /* step 7: fp32 block Jacobi (c-10).  The U-route computes U_low only
+           (PAPER.md:542-545): no V accumulation */
         float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         float tol32_in = tol32 / (float)o.inner_tol_div;
-        int32_t sw32 = om_block_jacobi_f32(X32, n, n, n, V32, n, n, o.b, tol32, tol32_in, o.max_sweeps32,
-                                           o.max_inner32, 1, st->off_trace32, st->upd_trace32, o.nthreads);
+        int32_t sw32 = om_block_jacobi_f32(X32, n, n, n, o.switch_u ? NULL : V32, o.switch_u ? 0 : n, n, o.b,
+                                           tol32, tol32_in, o.max_sweeps32, o.max_inner32, 1, st->off_trace32,
+                                           st->upd_trace32, o.nthreads);
         st->sweeps32 = sw32 < 0 ? -sw32 : sw32;
         st->final_off32 = st->sweeps32 > 0 && st->sweeps32 <= 64 ? st->off_trace32[st->sweeps32 - 1] : 0;
 
-        /* step 8: sigma32 = column norms, stable descending sort, permute V32 (Alg. 1 l.309) */
+        /* step 8: sigma32 = column norms, stable descending sort (Alg. 1 l.309) */
         for (int64_t j = 0; j < n; ++j) {
             double s = 0.0;
             for (int64_t i = 0; i < n; ++i) s += (double)X32[i + j * n] * (double)X32[i + j * n];
             key[j] = sqrt(s);
         }
         argsort_desc(key, n, idx);
-        float* Vs = X32;  /* reuse: X32 no longer needed */
-        for (int64_t j = 0; j < n; ++j) memcpy(Vs + j * n, V32 + idx[j] * n, sizeof(float) * (size_t)n);
-
-        /* step 9: lift Q = qr(fl64(V32)) by CholeskyQR (c-11) */
-        if (om_lift(Vs, n, n, Q, n) != 0) { rc = -3; goto done; }
+        if (o.switch_u) {
+            /* step 9u: U_low = working(X32 Sigma32^-1), columns in sigma32-descending order;
+               Q = qr(X^T U_low) */
+            for (int64_t j = 0; j < n; ++j) {
+                if (!(key[idx[j]] > 0.0)) { rc = -3; goto done; }
+                for (int64_t i = 0; i < n; ++i) tmpm[i + j * n] = (double)X32[i + idx[j] * n] / key[idx[j]];
+            }
+            if (om_switch_u(X, n, n, tmpm, n, Q, n) != 0) { rc = -3; goto done; }
+        } else {
+            /* step 9: permute V32; lift Q = qr(fl64(V32)) by CholeskyQR (c-11) */
+            float* Vs = X32;  /* reuse: X32 no longer needed */
+            for (int64_t j = 0; j < n; ++j) memcpy(Vs + j * n, V32 + idx[j] * n, sizeof(float) * (size_t)n);
+            if (om_lift(Vs, n, n, Q, n) != 0) { rc = -3; goto done; }
+        }
 
         /* step 10: Y = X Q */
 #pragma omp parallel for schedule(static)

@@ -41,6 +41,8 @@ typedef struct {
     int32_t nthreads;       /* OpenMP threads over disjoint pairs (0 = default) */
     int32_t mp_rrqr;        /* 1: mixed-precision RRQR, Alg. 4; 0 (default): fp64 QRP (c-22) */
     int32_t max_inner32;    /* inner sweeps cap of the fp32 stage (c-5; default 2) */
+    int32_t switch_u;       /* 1: U-route switch (Alg. 3 l.446-447): the fp32 stage
+                               does not accumulate V; Q = qr(X^T U_low) (default); 0: V-route (c-11) */
 } om_opts;
 
 typedef struct {
@@ -92,6 +94,13 @@ int32_t om_block_jacobi_f32(float* X, int64_t m, int64_t n, int64_t ldx,
                             double* off_trace, int32_t* upd_trace, int32_t nthreads);
 /* Precision lift (c-11): Q = V * Rv^-1 with Rv = chol(V^T V), V = fl64(V32). */
 int om_lift(const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq);
+
+/* U-route precision switch (Alg. 3 l.446-447 "Q R2 = X^T working(U_low)"):
+   Z = X^T Ulow in fp64, Householder QR Z = Q R2 with diag(R2) >= 0 (c-13), Q formed explicitly
+   (Q = H_0 ... H_{n-1} I).  X, Ulow, Q n x n.  In exact arithmetic Q = V_X when X = U_X S V_X^T and
+   Ulow = U_X.  Returns -3 when a diagonal of R2 is zero. */
+int om_switch_u(const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
+                double* Q, int64_t ldq);
 
 /* --- the whole method ------------------------------------------------- */
 int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_opts* opts,

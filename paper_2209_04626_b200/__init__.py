@@ -39,7 +39,7 @@ class Options(C.Structure):
                 ("path", C.c_int32), ("x_from_lq", C.c_int32), ("compute_gates", C.c_int32),
                 ("stream", C.c_void_p), ("virtual_shards", C.c_int32), ("split_rows", C.c_int32),
                 ("fp32_tensor_cores", C.c_int32), ("pdl_overlap", C.c_int32),
-                ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32)]
+                ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32), ("switch_u", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -80,7 +80,7 @@ _lib = None
 EXPORTS = [
     "mpjsvd_default_options", "mpjsvd_create", "mpjsvd_factor", "mpjsvd_destroy", "mpjsvd_strerror",
     "mpjsvd_last_cuda_error", "mpjsvd_version", "mpjsvd_block_jacobi_f64", "mpjsvd_block_jacobi_f32",
-    "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
+    "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_switch_u", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
     "mpjsvd_set_profiling", "mpjsvd_get_profile", "mpjsvd_comm_unique_id", "mpjsvd_comm_init",
     "mpjsvd_comm_info", "mpjsvd_plan_create", "mpjsvd_plan_info", "mpjsvd_plan_pairs", "mpjsvd_plan_advance",
     "mpjsvd_plan_locate", "mpjsvd_plan_destroy",
@@ -113,6 +113,7 @@ def lib():
         L.mpjsvd_inner_solve.argtypes = [vp, i32, vp, vp, i32, i32, dbl, i32, vp]
         L.mpjsvd_qr.argtypes = [vp, vp, i64, i64, i64, vp, vp, i32]
         L.mpjsvd_lift.argtypes = [vp, vp, i64, i64, vp, i64]
+        L.mpjsvd_switch_u.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, i32]
         L.mpjsvd_apply_q.argtypes = [vp, vp, i64, i64, i64, vp, vp, i64, i64]
         L.mpjsvd_gemm_f64.argtypes = [vp, i32, i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]
         L.mpjsvd_set_profiling.argtypes = [vp, i32]
@@ -411,6 +412,27 @@ def lift(V32, handle: Handle | None = None):
         rc = lib().mpjsvd_lift(handle.ptr, C.c_void_p(Vc.data_ptr()), n, Vc.stride(1), C.c_void_p(Q.data_ptr()),
                                Q.stride(1))
         _check(rc, "mpjsvd_lift")
+        return Q
+    finally:
+        if own:
+            handle.close()
+
+
+def switch_u(X, Ulow, x_lower: bool = True, handle: Handle | None = None):
+    """Step-level: U-route switch Q = qr(X^T Ulow) on device."""
+    import torch
+    own = handle is None
+    if own:
+        handle = Handle(stream=torch.cuda.current_stream().cuda_stream)
+    try:
+        n = X.shape[0]
+        Xc = X.t().contiguous().t()
+        Uc = Ulow.t().contiguous().t()
+        Q = empty_col_major(n, n, torch.float64, X.device)
+        rc = lib().mpjsvd_switch_u(handle.ptr, C.c_void_p(Xc.data_ptr()), n, Xc.stride(1),
+                                   C.c_void_p(Uc.data_ptr()), Uc.stride(1), C.c_void_p(Q.data_ptr()), Q.stride(1),
+                                   int(x_lower))
+        _check(rc, "mpjsvd_switch_u")
         return Q
     finally:
         if own:

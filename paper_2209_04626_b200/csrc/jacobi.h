@@ -127,6 +127,7 @@ int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha
              cudaStream_t st);
 // shape bit 0: compute only the upper triangle of C (tiles below the diagonal are skipped);
 // bit 1: op(A) is lower triangular (the K loop of a row tile stops at its last row)
+// bit 2: op(A) is upper triangular (the K loop of a row tile starts at its first row)
 int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A,
                 long long lda, const double* B, long long ldb, double beta, double* C, long long ldc, int shape,
                 cudaStream_t st);
@@ -163,6 +164,8 @@ int col_norms(const T* X, long long ldx, long long rows, int n, double* out, int
 int rank_desc(const double* key, int n, int* rank, cudaStream_t st);
 int sort_upcast_v(const float* V32, long long ld32, const int* rank, double* V, long long ldv,
                   long long rows_pad, int n, cudaStream_t st);
+int sort_upcast_scale(const float* X32, long long ld32, const int* rank, const double* sig, double* U,
+                      long long ldu, long long rows_pad, int n, int* bad, cudaStream_t st);
 int finalize(const double* Y, long long ldy, const double* Q, long long ldq, const double* sig,
              const int* rank, double* UX, long long ldu, double* VX, long long ldvx, double* S,
              long long rows_pad, int n, cudaStream_t st);

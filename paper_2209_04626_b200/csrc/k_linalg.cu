@@ -86,6 +86,13 @@ __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, l
     if ((shape & 1) && j0 + GM_BN <= i0) return;
     // shape bit 1: op(A) is lower triangular -> op(A)(i, k) = 0 for k > i: K range ends at the tile's last row
     if ((shape & 2) && kchunk == 0 && K > i0 + GM_BM) K = i0 + GM_BM;
+    // shape bit 2: op(A) is upper triangular -> op(A)(i, k) = 0 for k < i: K range starts at the tile's first row
+    if ((shape & 4) && kchunk == 0) {
+        const long long k0 = min(K, (i0 / GM_BK) * GM_BK);
+        if (ta == 0) A += k0 * lda; else A += k0;
+        if (tb == 0) B += k0; else B += k0 * ldb;
+        K -= k0;
+    }
     // split-K: this CTA covers k in [kb, kb + kchunk) of op(A)/op(B); partial results go to part
     const long long kb = (long long)blockIdx.z * kchunk;
     if (kchunk > 0) {

@@ -235,6 +235,29 @@ int sort_upcast_v(const float* V32, long long ld32, const int* rank, double* V, 
     return 0;
 }
 
+// U-route: U_low[:, rank_j] = fl64(X32[:, j]) / sigma32_j (sigma32_j = ||X32[:, j]||, fp64);
+// a zero column sets *bad (rank deficient, reading c-18)
+__global__ void k_sort_upcast_scale(const float* X32, long long ld32, const int* rank, const double* sig,
+                                    double* U, long long ldu, long long rows_pad, int n, int* bad) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y) {
+        const long long dj = rank[j];
+        const double s = sig[j];
+        if (!(s > 0.0)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) *bad = 1;
+            continue;
+        }
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            U[i + dj * ldu] = (double)X32[i + j * ld32] / s;
+    }
+}
+int sort_upcast_scale(const float* X32, long long ld32, const int* rank, const double* sig, double* U, long long ldu,
+                      long long rows_pad, int n, int* bad, cudaStream_t st) {
+    k_sort_upcast_scale<<<grid2d(rows_pad, n), 256, 0, st>>>(X32, ld32, rank, sig, U, ldu, rows_pad, n, bad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // U_X[:, rank_j] = Y[:, j] / sigma_j ; V_X[:, rank_j] = Q[:, j] ; S[rank_j] = sigma_j
 __global__ void k_finalize(const double* Y, long long ldy, const double* Q, long long ldq, const double* sig,
                            const int* rank, double* UX, long long ldu, double* VX, long long ldvx, double* S,

@@ -42,7 +42,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -515,6 +515,19 @@ int lift_inplace(mpjsvd_handle h, double* Q, long long ldq, int n, int* bad) {
     return 0;
 }
 
+// U-route precision switch (Alg. 3 l.446-447): Z = X^T U_low (fp64; X lower
+// triangular when lower_x, so op(A) = X^T is upper), Householder QR Z = Q R2 (diag(R2) >= 0),
+// Q = H_0 ... H_{n-1} I.  Z is overwritten by the reflectors; Q (n_pad x n, zero padding rows).
+int switch_u_inplace(mpjsvd_handle h, const double* X, const double* Ulow, double* Z, double* Q, long long ld,
+                     int n, bool lower_x, QrWork& qw, cudaStream_t st) {
+    double* tau = P<double>(h, S_TAU_U);
+    MPJ_TRY(gemm_f64_ex(1, 0, n, n, n, 1.0, X, ld, Ulow, ld, 0.0, Z, ld, lower_x ? 4 : 0, st));
+    MPJ_TRY(qr_blocked(Z, ld, n, n, tau, qw, P<double>(h, S_WY), st));
+    MPJ_TRY(set_identity<double>(Q, ld, ld, n, st));
+    MPJ_TRY(apply_q_wy(Z, n, n, ld, tau, Q, ld, n, P<double>(h, S_WY), st));
+    return 0;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
@@ -553,6 +566,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_TRY(ensure(h, S_TAU_T0, sizeof(double) * n));
     MPJ_TRY(ensure(h, S_TAU_P, sizeof(double) * n));
     MPJ_TRY(ensure(h, S_TAU_T, sizeof(double) * n));
+    MPJ_TRY(ensure(h, S_TAU_U, sizeof(double) * n));
     MPJ_TRY(ensure(h, S_PERM, sizeof(int) * n));
     MPJ_TRY(ensure(h, S_RANK, sizeof(int) * n));
     MPJ_TRY(ensure(h, S_KEYS, sizeof(double) * n));
@@ -696,7 +710,8 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
             MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
         }
-        MPJ_TRY(set_identity<float>(dV32, n_pad, n_pad, n, st));
+        const bool uroute = o.switch_u != 0;       // U-route: the fp32 stage computes U_low only
+        if (!uroute) MPJ_TRY(set_identity<float>(dV32, n_pad, n_pad, n, st));
         if (dist) {
             PROF_B("bcast");
             MPJ_TRY(h->comm.bcast(dX32, sizeof(float) * nn, 0, st));
@@ -704,18 +719,32 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         }
         const float tol32 = (float)(o.tol_mult32 * sqrt((double)n) * U32);
         const float tol32_in = tol32 / (float)o.inner_tol_div;
-        MPJ_TRY(jacobi_stage<float>(h, dX32, n_pad, n_pad, (int)n, dV32, n_pad, n_pad, o.block_cols, tol32,
+        MPJ_TRY(jacobi_stage<float>(h, dX32, n_pad, n_pad, (int)n, uroute ? nullptr : dV32, n_pad, n_pad, o.block_cols, tol32,
                                     tol32_in, o.max_sweeps32, o.max_inner32, true, r32));
         if (root) {
         // sort by sigma32 (descending, stable) and upcast V32 -> Q
         MPJ_TRY(col_norms<float>(dX32, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 0, st));
         MPJ_TRY(rank_desc(P<double>(h, S_KEYS), (int)n, P<int>(h, S_RANK), st));
-        MPJ_TRY(sort_upcast_v(dV32, n_pad, P<int>(h, S_RANK), dQ, n_pad, n_pad, (int)n, st));
+        if (uroute) {
+            // U_low = working(X32 Sigma32^-1), sigma32-descending
+            MPJ_TRY(sort_upcast_scale(dX32, n_pad, P<int>(h, S_RANK), P<double>(h, S_KEYS), dUX, n_pad, n_pad,
+                                      (int)n, flags + 1, st));
+        } else {
+            MPJ_TRY(sort_upcast_v(dV32, n_pad, P<int>(h, S_RANK), dQ, n_pad, n_pad, (int)n, st));
+        }
         MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
-        // ---- stage 5: lift Q = qr(fl64(V32)), Y = X Q
-        PROF_B("lift_cholqr");
-        MPJ_TRY(lift_inplace(h, dQ, n_pad, (int)n, flags + 2));
-        PROF_E("lift_cholqr");
+        // ---- stage 5: switch precisions, Y = X Q
+        if (uroute) {
+            // Q = qr(X^T U_low) (U-route); dVX is free until the finalise step
+            PROF_B("switch_u");
+            MPJ_TRY(switch_u_inplace(h, dX, dUX, dVX, dQ, n_pad, (int)n, o.x_from_lq != 0, qw, st));
+            PROF_E("switch_u");
+        } else {
+            // Q = qr(fl64(V32)) by CholeskyQR (V-route, reading c-11)
+            PROF_B("lift_cholqr");
+            MPJ_TRY(lift_inplace(h, dQ, n_pad, (int)n, flags + 2));
+            PROF_E("lift_cholqr");
+        }
         PROF_B("rv_gemm");
         // X lower triangular (X = L, reading c-7): K range of a row tile ends at its last row
         MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
@@ -922,6 +951,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->pdl_overlap = 1;
     o->mp_rrqr = 0;
     o->max_inner32 = 2;
+    o->switch_u = 1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1254,6 +1284,35 @@ int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, dou
     MPJ_CUDA_TRY(cudaMemcpyAsync(bad, P<int>(h, S_FLAGS), sizeof(bad), cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaStreamSynchronize(st));
     return bad[2] ? MPJSVD_ERR_RANK_DEFICIENT : 0;
+}
+
+int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
+                    double* Q, int64_t ldq, int32_t x_lower) {
+    if (!h || !X || !Ulow || !Q || n < 1 || ldx < n || ldu < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
+    gemm_set_workspace(nullptr, 0);
+    cudaStream_t st = h->stream;
+    const long long n_pad = round_up(n, 32);
+    const size_t nn = (size_t)n_pad * n;
+    MPJ_TRY(ensure(h, S_TMP1, sizeof(double) * 3 * nn));
+    MPJ_TRY(ensure(h, S_TMP2, sizeof(double) * nn));
+    MPJ_TRY(ensure(h, S_TAU_U, sizeof(double) * n));
+    MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(n_pad, n)));
+    QrWork qw;
+    MPJ_TRY(ensure_qr_work(h, (int)n, (int)n, qw));
+    double* Xw = P<double>(h, S_TMP1);
+    double* Uw = Xw + nn;
+    double* Zw = Uw + nn;
+    double* Qw = P<double>(h, S_TMP2);
+    MPJ_CUDA_TRY(cudaMemsetAsync(Xw, 0, sizeof(double) * 2 * nn, st));
+    MPJ_CUDA_TRY(cudaMemcpy2DAsync(Xw, sizeof(double) * n_pad, X, sizeof(double) * ldx, sizeof(double) * n, n,
+                                   cudaMemcpyDefault, st));
+    MPJ_CUDA_TRY(cudaMemcpy2DAsync(Uw, sizeof(double) * n_pad, Ulow, sizeof(double) * ldu, sizeof(double) * n, n,
+                                   cudaMemcpyDefault, st));
+    MPJ_TRY(switch_u_inplace(h, Xw, Uw, Zw, Qw, n_pad, (int)n, x_lower != 0, qw, st));
+    MPJ_CUDA_TRY(cudaMemcpy2DAsync(Q, sizeof(double) * ldq, Qw, sizeof(double) * n_pad, sizeof(double) * n, n,
+                                   cudaMemcpyDefault, st));
+    MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
 }
 
 int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv, const double* tau, double* C,

@@ -198,6 +198,42 @@ def test_lift_vs_oracle(mp):
     assert np.abs(q - q_ref).max() < 1e-13
 
 
+@pytest.mark.parametrize("n,x_lower", [(200, True), (200, False), (97, True)])
+def test_switch_u_vs_oracle(mp, n, x_lower):
+    """U-route switch Q = qr(X^T U_low) on X = L and U_low from the fp32 stage,
+    GPU against the oracle's step; with x_lower the GEMM skips the zero triangle of X^T."""
+    a = testmat.config_matrix("C1", n)
+    x = np.asfortranarray(np.linalg.qr(a.T)[1].T)
+    e = np.frexp(np.abs(x).max())[1]
+    x32 = np.ldexp(x, -e).astype(np.float32)
+    t = np.float32(4 * np.sqrt(n) * 2.0 ** -24)
+    x32, _, _, _, _ = oracle.block_jacobi(x32, None, 32, t, t / 8, stagnation=True, dtype=np.float32)
+    s32 = np.linalg.norm(x32.astype(np.float64), axis=0)
+    order = np.argsort(-s32, kind="stable")
+    ul = np.asfortranarray(x32[:, order].astype(np.float64) / s32[order])
+    q_ref, rc = oracle.switch_u(x, ul)
+    q = host(mp.switch_u(dev(x), dev(ul), x_lower=x_lower))
+    assert rc == 0 and orth(q) < 1e-14
+    assert np.abs(q - q_ref).max() < 1e-11, np.abs(q - q_ref).max()
+    y = x @ q        # columns orthogonal to the level of u_low (PAPER.md:575-579)
+    g = y.T @ y
+    d = np.sqrt(np.diag(g))
+    assert np.abs(g / d[:, None] / d[None, :] - np.eye(n)).max() < 1e-4
+
+
+def test_switch_u_exact_factors(mp):
+    """Q = V_X exactly in exact arithmetic: exactly representable U, V."""
+    n = 256
+    rng = np.random.default_rng(11)
+    h = testmat.sylvester_hadamard(n) / 16.0
+    uu = rng.choice([-1.0, 1.0], n)[:, None] * h[rng.permutation(n)]
+    vv = rng.choice([-1.0, 1.0], n)[:, None] * h[rng.permutation(n)]
+    sigma = np.sort((1.0 + rng.integers(0, 1024, n) / 1024.0) * 2.0 ** -np.floor(13 * np.arange(n) / (n - 1)))[::-1]
+    a = (uu * sigma) @ vv.T
+    q = host(mp.switch_u(dev(a), dev(uu), x_lower=False))
+    assert np.abs(q - vv).max() < 50 * n * U64
+
+
 # ------------------------------------------------------------------- end to end
 def check_svd(a, U, S, V, tol_orth=1e-13, tol_res=1e-13):
     assert np.all(S[:-1] >= S[1:]) and np.all(S > 0)
@@ -207,13 +243,15 @@ def check_svd(a, U, S, V, tol_orth=1e-13, tol_res=1e-13):
     assert res <= tol_res, res
 
 
+@pytest.mark.parametrize("route", [1, 0])
 @pytest.mark.parametrize("name,n,kappa", [("C1", 256, 1e4), ("C2", 1024, 1e3), ("C3", 512, None),
                                           ("C4", 256, None), ("C5", 512, None)])
-def test_factor_vs_oracle(mp, name, n, kappa):
+def test_factor_vs_oracle(mp, name, n, kappa, route):
+    """route 1: U-route switch (default); 0: V-route (reading c-11)."""
     a = testmat.config_matrix(name, n)
-    U, S, V, st = mp.factor(dev(a))
+    U, S, V, st = mp.factor(dev(a), switch_u=route)
     U, S, V = host(U), host(S), host(V)
-    uo, so, vo, sto, rc = oracle.mixed_svd(a)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, switch_u=route)
     assert rc == 0 and st["rc"] == 0
     check_svd(a, U, S, V)
     k = kappa if kappa is not None else kappa_s(a)

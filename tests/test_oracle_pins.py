@@ -257,11 +257,83 @@ def test_lift_repairs_orthogonality():
     assert np.abs(q - v32).max() < 1e-4
 
 
+# ---------------------------------------------------------------- U-route switch
+def _exact_factors(n, emax=13, seed=None):
+    """A = U diag(sigma) V^T with U, V = S P H / sqrt(n) exactly representable (n = 4^k)."""
+    k = int(np.log2(n))
+    rng = np.random.default_rng(9000 + k if seed is None else seed)
+    kk = rng.integers(0, 1024, n)
+    ee = np.floor(float(emax) * np.arange(n) / max(n - 1, 1)).astype(int)
+    sigma = np.sort((1.0 + kk / 1024.0) * 2.0 ** (-ee))[::-1].copy()
+    h = testmat.sylvester_hadamard(n)
+    r = np.sqrt(n)
+    uu = rng.choice([-1.0, 1.0], n)[:, None] * h[rng.permutation(n)] / r
+    vv = rng.choice([-1.0, 1.0], n)[:, None] * h[rng.permutation(n)] / r
+    a = (uu * sigma) @ vv.T
+    return np.asfortranarray(a), uu, sigma, vv
+
+
+@pytest.mark.parametrize("n", [16, 64, 256])
+def test_switch_u_recovers_v_exactly_known(n):
+    """with U_low = U_X, qr(X^T U_X) gives Q = V_X "in exact arithmetic"
+    (X^T U_X = V_X Sigma, R2 = Sigma > 0 so no sign flips).  U, V are exactly representable
+    (entries +-2^-k), so Q must equal V to rounding; a transposed operand (X U) or a wrong
+    reflector sign fails this."""
+    a, uu, sigma, vv = _exact_factors(n)
+    q, rc = oracle.switch_u(a, uu)
+    assert rc == 0
+    assert np.abs(q - vv).max() < 50 * n * U
+    assert orth(q) < 20 * n * U
+
+
+def test_switch_u_column_scaling_bitwise():
+    """Householder QR is invariant to power-of-two column scaling (reflector vectors and tau are
+    scale-free), so Q(X, U_low 2^D) == Q(X, U_low) bitwise: the normalisation of U_low cannot
+    change the switch."""
+    a = testmat.config_matrix("C1", 64)
+    rng = np.random.default_rng(3)
+    ul = np.linalg.qr(rng.standard_normal((64, 64)))[0]
+    q1, _ = oracle.switch_u(a, ul)
+    q2, _ = oracle.switch_u(a, ul * 2.0 ** rng.integers(-30, 30, 64))
+    assert np.array_equal(q1, q2)
+
+
+def test_switch_u_is_qr_of_xtu_against_lapack():
+    """Q R2 = X^T U_low: the same Q as LAPACK dgeqrf/dorgqr after fixing diag(R2) >= 0 (c-13), and
+    Q^T (X^T U_low) upper triangular with a non-negative diagonal."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(5)
+    a = np.asfortranarray(rng.standard_normal((96, 96)))      # kappa(X^T U) ~ 1e2..1e3: Q fixed to ~u kappa
+    ul = np.linalg.qr(rng.standard_normal((96, 96)))[0]
+    q, rc = oracle.switch_u(a, ul)
+    z = a.T @ ul
+    ql, rl = sl.qr(z)
+    ql = ql * np.sign(np.diag(rl))
+    assert rc == 0 and np.abs(q - ql).max() < 1e-12
+    r2 = q.T @ z
+    assert np.abs(np.tril(r2, -1)).max() < 1e-12 * np.abs(z).max()
+    assert np.all(np.diag(r2) >= 0)
+
+
+@pytest.mark.parametrize("route", [0, 1])
+def test_routes_agree_on_structural_bounds(route):
+    """Both precision switches (V-route c-11 / U-route PAPER.md:563-573) give a valid SVD with
+    "typically three" refinement sweeps."""
+    a = testmat.config_matrix("C5", 256)
+    u, s, v, st, rc = oracle.mixed_svd(a, switch_u=route)
+    assert rc == 0 and orth(u) <= 1e-13 and orth(v) <= 1e-13
+    assert np.linalg.norm(a - (u * s) @ v.T) / np.linalg.norm(a) <= 1e-13
+    assert st["sweeps64"] <= GOLD["refinement_sweeps"]["max_with_slack"]
+    sr = oracle.mixed_svd(a, switch_u=1 - route)[1]
+    assert np.abs(s - sr).max() / s[0] <= 8 * np.sqrt(256) * U
+
+
 # ---------------------------------------------------------------- P2 exact sigma
 @pytest.mark.parametrize("n", [16, 64, 256])
-def test_exact_sigma(n):
+@pytest.mark.parametrize("route", [0, 1])
+def test_exact_sigma(n, route):
     a, sigma = testmat.exact_sigma_matrix(n)
-    u, s, v, st, rc = oracle.mixed_svd(a)
+    u, s, v, st, rc = oracle.mixed_svd(a, switch_u=route)
     assert rc == 0
     rel = np.abs(s - sigma) / sigma
     assert np.all(rel <= tiered_tol(sigma, sigma[0] / sigma[-1]))
