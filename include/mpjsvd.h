@@ -98,7 +98,7 @@ typedef struct {
                                   from an fp32 QRP of fl32(A1 2^-e), then fp64 Householder QR of A1 P;
                                   0 (default): fp64 column-pivoted QR (Businger-Golub).  On B200 the fp32
                                   QRP costs about as much as the fp64 one (reading c-22) */
-    int32_t max_inner32;       /* inner sweeps cap of the fp32 stage's 2b x 2b solves (default 2; the fp64
+    int32_t max_inner32;       /* inner sweeps cap of the fp32 stage's 2b x 2b solves (default 1; the fp64
                                   stage uses max_inner); reading c-5 */
     int32_t switch_u;          /* 1 (default): U-route precision switch, the paper's Alg. 3 choice (PAPER.md:446-447,
                                   542-545, 563-573): the fp32 stage does not accumulate V; Q = qr(X^T working(U_low))

@@ -66,7 +66,7 @@ void om_default_opts(om_opts* o) {
     o->x_from_lq = 1;
     o->nthreads = 0;
     o->mp_rrqr = 0;
-    o->max_inner32 = 2;
+    o->max_inner32 = 1;
     o->switch_u = 1;
 }
 

@@ -40,7 +40,7 @@ typedef struct {
     int32_t x_from_lq;      /* 1: X = L (default, F1); 0: X = R */
     int32_t nthreads;       /* OpenMP threads over disjoint pairs (0 = default) */
     int32_t mp_rrqr;        /* 1: mixed-precision RRQR, Alg. 4; 0 (default): fp64 QRP (c-22) */
-    int32_t max_inner32;    /* inner sweeps cap of the fp32 stage (c-5; default 2) */
+    int32_t max_inner32;    /* inner sweeps cap of the fp32 stage (c-5; default 1) */
     int32_t switch_u;       /* 1: U-route switch (Alg. 3 l.446-447): the fp32 stage
                                does not accumulate V; Q = qr(X^T U_low) (default); 0: V-route (c-11) */
 } om_opts;
