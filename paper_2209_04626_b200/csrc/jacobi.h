@@ -50,7 +50,6 @@ struct JacobiRound {
     int* dlist;
     int* dctr;
     int pdl;            // 1: the update is launched as a programmatic dependent of the solve
-    int ereg;           // 1: every pair has width 64 -> inner solve with E in registers (k_jacobi.cu)
 };
 
 // reset of the publication list by the first CTA of the round's Gram kernel

@@ -144,11 +144,6 @@ template <int W>
 constexpr int inner_e_items() { return (W / 2) * (W / 8); }
 template <int W>
 constexpr int inner_nt() { return inner_g_threads<W>() + (inner_e_items<W>() + 31) / 32 * 32 + 32; }
-// E-in-registers layout (W = 64, every pair of full width): 288 threads update G (two pair-pair blocks
-// each), 64 threads own one row of E each in registers, one warp computes the rotations
-constexpr int ER_G_THREADS = 288;
-template <int W, bool ER>
-constexpr int inner_threads() { return ER ? ER_G_THREADS + W + 32 : inner_nt<W>(); }
 
 // rotation of one pair: (c, s), c - 1 and an active flag, read with one vector load
 template <typename T>
@@ -171,8 +166,6 @@ struct InnerSmem {
     Rot4<T> rot[2][W / 2];                             // current / next round
     T rt[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];   // exact 2x2 diagonal update
     unsigned short spq[R][W / 2];                      // pair k of round r: p | q << 8 (p < q; q may be the bye)
-    unsigned char ssw[R][W / 2];                       // 1: position k of round r holds q (the larger index)
-    T sp[2][W / 2];                                    // s oriented by position (E-in-registers path)
     int nrot[2];
     T red[32];
     long long dbg_t[2][32];                            // per-warp phase end clocks (debug timing only)
@@ -195,7 +188,7 @@ __device__ __forceinline__ void rot2(T c, T s, T& x, T& y) {
 // rotation parameters of pair k (indices p < q) into buffer `buf`; returns active
 template <typename T, int W>
 __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k, int q, int w, T gpp, T gqq, T gpq,
-                                            T tol_in, bool swp = false) {
+                                            T tol_in) {
     int active = 0;
     T c = T(1), sn = T(0), t = T(0), cm1 = T(0);
     // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||
@@ -237,7 +230,6 @@ __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k,
     r4.cm1 = cm1;
     r4.act = active ? T(1) : T(0);
     sm.rot[buf][k] = r4;
-    sm.sp[buf][k] = swp ? -sn : sn;
     sm.rt[buf][k] = t;
     sm.rg[buf][k] = gpq;
     sm.rpp[buf][k] = gpp;
@@ -278,19 +270,11 @@ __device__ __forceinline__ int any_pair_above(const InnerSmem<T, W>& sm, int w, 
     return f;
 }
 
-// ER (E in registers; W = 64 and w = 64 only): thread NGT + i keeps row i of E in registers, in
-// position order (e[j] = E[i][index at position j of the current round], so that pair k of every round
-// is the register pair (k, 63 - k)); after each round the registers shift with the circle method
-// (position j -> j + 1 for j >= 1, 63 -> 1).  A full inner sweep returns every index to its position,
-// and the solve always ends at a sweep boundary.  The rotation acts on positions (a, b) = (k, 63 - k)
-// with s oriented by position (sp = -s when position k holds q), plus the delta-form identity terms
-// for the thread whose own index sits in the pair.  G threads handle two pair-pair blocks each.
-template <typename T, int W, bool ER = false>
+template <typename T, int W>
 __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inner, int* sweeps_used,
                                long long* dbg = nullptr) {
     constexpr int GS = InnerSmem<T, W>::GS;
-    static_assert(!ER || W == 64, "E-in-registers path is for W = 64");
-    constexpr int NG = ER ? ER_G_THREADS : inner_g_threads<W>();
+    constexpr int NG = inner_g_threads<W>();
     constexpr int NCH = W / 8;                          // eight-row chunks of E per pair
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31;
@@ -302,7 +286,6 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         const int r = e / P, k = e - (e / P) * P;
         const int x = rr_slot(r, k, w2), y = rr_slot(r, w2 - 1 - k, w2);
         sm.spq[r][k] = (unsigned short)(min(x, y) | (max(x, y) << 8));
-        sm.ssw[r][k] = (unsigned char)(x > y ? 1 : 0);
     }
     constexpr int EV = InnerSmem<T, W>::EV, ES = InnerSmem<T, W>::ES;
     for (int i = tid; i < W * ES; i += nt) sm.E[i] = T(0);
@@ -311,31 +294,16 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
     // rows (j NCH + c) EV .. + EV - 1, j < 8 / EV, so that the NCH lanes of a pair read a contiguous
     // run of every column with 16-byte accesses
     int kA = -1, kB = -1, kE = -1, r0E = 0;
-    int kA2 = -1, kB2 = -1;                             // ER: second pair-pair block
-    auto decode_blk = [&](int blk, int& ka, int& kb) {
-        int rem = blk, row = 0;
+    if (tid < NB) {
+        int rem = tid, row = 0;
         while (rem >= P - row) { rem -= P - row; ++row; }
-        ka = row;
-        kb = row + rem;
-    };
-    if (ER) {
-        if (tid < NG) {
-            if (tid < NB) decode_blk(tid, kA, kB);
-            if (tid + NG < NB) decode_blk(tid + NG, kA2, kB2);
-        }
-    } else if (tid < NB) {
-        decode_blk(tid, kA, kB);
+        kA = row;
+        kB = row + rem;
     } else if (tid >= NG && tid < NG + P * NCH) {
         kE = (tid - NG) / NCH;
         r0E = (tid - NG) % NCH;                        // chunk index c
         if (!InnerSmem<T, W>::ECOL) r0E *= 8;          // row-major E: rows 8c .. 8c + 7
     }
-    // ER: row eR of E in registers (position order), own position and pair/side
-    const int eR = (ER && tid >= NG && tid < NG + W) ? tid - NG : -1;
-    T ereg[ER ? W : 1];
-#pragma unroll
-    for (int j = 0; j < (ER ? W : 1); ++j) ereg[j] = T(0);
-    int epos = eR;                                      // round 0: index i sits at position i
     __syncthreads();
     if (max_inner < 1) { if (sweeps_used) *sweeps_used = 0; return 0; }
     int f_cur = 0, f_next = 0, my_cnt = 0;
@@ -345,7 +313,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         const T gpp = sm.G[p * GS + p];
         const T gqq = q < w ? sm.G[q * GS + q] : T(0);
         const T gpq = q < w ? sm.G[p * GS + q] : T(0);
-        f_cur = set_rotation<T, W>(sm, 0, lane, q, w, gpp, gqq, gpq, tol_in, sm.ssw[0][lane] != 0);
+        f_cur = set_rotation<T, W>(sm, 0, lane, q, w, gpp, gqq, gpq, tol_in);
     }
     __syncthreads();
     int sweep = 0, r = 0, buf = 0;
@@ -360,8 +328,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         const int rn = last ? 0 : r + 1;
         if (dbg && tid == 0) t_start = clock64();
         // ---------------- phase A: G blocks (upper triangle G[min][max])
-        auto g_block = [&](const int kA, const int kB) {
-
+        if (kA >= 0) {
             const Rot4<T> RA = sm.rot[buf][kA];
             const unsigned pqa = sm.spq[r][kA];
             const int pa = pqa & 255, qa = pqa >> 8;
@@ -396,9 +363,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                     if (qav && qbv) sm.G[i11] = x11;
                 }
             }
-        };
-        if (kA >= 0) g_block(kA, kB);
-        if (ER && kA2 >= 0) g_block(kA2, kB2);
+        }
         if (dbg) { __syncwarp(); if (lane == 0) sm.dbg_t[0][warp] = clock64(); }
         __syncthreads();
         long long t_b1 = 0;
@@ -411,33 +376,10 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 const T gxx = sm.G[x * GS + x];
                 const T gyy = y < w ? sm.G[y * GS + y] : T(0);
                 const T gxy = y < w ? sm.G[x * GS + y] : T(0);
-                const int act = set_rotation<T, W>(sm, buf ^ 1, lane, y, w, gxx, gyy, gxy, tol_in, sm.ssw[rn][lane] != 0);
+                const int act = set_rotation<T, W>(sm, buf ^ 1, lane, y, w, gxx, gyy, gxy, tol_in);
                 if (last) f_next |= act; else f_cur |= act;
             }
-        } else if (ER && eR >= 0) {
-            // E <- (I + E) J - I on row eR, registers in position order
-            const int my_k = epos < W / 2 ? epos : W - 1 - epos;
-            const bool my_b = epos >= W / 2;
-#pragma unroll
-            for (int k = 0; k < W / 2; ++k) {
-                const Rot4<T> R4 = sm.rot[buf][k];
-                const T sp = sm.sp[buf][k];
-                T xa = ereg[k], xb = ereg[W - 1 - k];
-                rot2(R4.c, sp, xa, xb);
-                if (k == my_k) {
-                    if (my_b) { xa -= sp; xb += R4.cm1; }
-                    else { xa += R4.cm1; xb += sp; }
-                }
-                ereg[k] = xa;
-                ereg[W - 1 - k] = xb;
-            }
-            // circle shift: position j -> j + 1 (j >= 1), W - 1 -> 1
-            const T t63 = ereg[W - 1];
-#pragma unroll
-            for (int j = W - 1; j >= 2; --j) ereg[j] = ereg[j - 1];
-            ereg[1] = t63;
-            epos = epos == 0 ? 0 : (epos == W - 1 ? 1 : epos + 1);
-        } else if (!ER && kE >= 0) {
+        } else if (kE >= 0) {
             const Rot4<T> R4 = sm.rot[buf][kE];
             if (R4.act != T(0)) {
                 const unsigned pq = sm.spq[r][kE];
@@ -490,7 +432,6 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         if (dbg) __syncthreads();
         if (dbg && tid == 0) {
             // dbg[0] phase A (slowest G warp), [1] barrier 1, [2] rotation warp, [3] slowest E warp, [4] rounds
-            // (G warps: NG >> 5; E warps: NG >> 5 .. nt / 32 - 2)
             long long mA = 0, mE = 0;
             for (int q = 0; q < (NG >> 5); ++q) mA = max(mA, sm.dbg_t[0][q]);
             for (int q = NG >> 5; q < (nt >> 5) - 1; ++q) mE = max(mE, sm.dbg_t[1][q]);
@@ -518,11 +459,6 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         buf ^= 1;
     }
     if (sweeps_used) *sweeps_used = sweep + 1;
-    if (ER && eR >= 0) {
-        // the solve ended at a sweep boundary: positions are the identity again
-#pragma unroll
-        for (int j = 0; j < W; ++j) sm.E[InnerSmem<T, W>::eidx(eR, j)] = ereg[j];
-    }
     // mirror the upper triangle (callers read G as a full symmetric matrix)
     for (int e = tid; e < w * w; e += nt) {
         const int x = e / w, y = e - (e / w) * w;
@@ -540,8 +476,8 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
 // ------------------------------------------------------------------------
 // k_pair_solve: one CTA per pair.
 // ------------------------------------------------------------------------
-template <typename T, int W, bool ER = false>
-__global__ void __launch_bounds__(inner_threads<W, ER>()) k_pair_solve(JacobiRound<T> a) {
+template <typename T, int W>
+__global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -584,7 +520,7 @@ __global__ void __launch_bounds__(inner_threads<W, ER>()) k_pair_solve(JacobiRou
     }
     if (rotate) {
         int used = 0;
-        inner_solve_dev<T, W, ER>(sm, w, a.tol_in, a.max_inner, &used);
+        inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
         if (tid == 0) {
             atomicMax(a.sweep_inner, used);
             atomicAdd(a.sweep_inner + 1, used);
@@ -1267,8 +1203,8 @@ __global__ void __launch_bounds__(256) k_pair_update_f32(JacobiRound<float> a) {
 __device__ long long* g_inner_dbg_f = nullptr;   // phase timers of the batch kernel (MPJSVD_INNER_TIMING=1)
 __device__ long long* g_inner_dbg_d = nullptr;
 
-template <typename T, int W, bool ER = false>
-__global__ void __launch_bounds__(inner_threads<W, ER>()) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
+template <typename T, int W>
+__global__ void __launch_bounds__(inner_nt<W>()) k_inner_solve_batch(T* G, T* E, int w, T tol_in, int max_inner, int* rot) {
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -1277,7 +1213,7 @@ __global__ void __launch_bounds__(inner_threads<W, ER>()) k_inner_solve_batch(T*
     for (int i = threadIdx.x; i < w * w; i += blockDim.x) sm.G[(i % w) * GS + i / w] = g[i];
     __syncthreads();
     long long* dbgp = sizeof(T) == 4 ? g_inner_dbg_f : g_inner_dbg_d;
-    int nr = inner_solve_dev<T, W, ER>(sm, w, tol_in, max_inner, nullptr, blockIdx.x == 0 ? dbgp : nullptr);
+    int nr = inner_solve_dev<T, W>(sm, w, tol_in, max_inner, nullptr, blockIdx.x == 0 ? dbgp : nullptr);
     for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
         g[i] = sm.G[(i % w) * GS + i / w];
         e[i] = sm.E[InnerSmem<T, W>::eidx(i % w, i / w)];   // column-major out: e[row + col*w] = E[row][col]
@@ -1334,8 +1270,6 @@ solve:
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_pair_solve<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-        if constexpr (W == 64)
-            cudaFuncSetAttribute(k_pair_solve<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
         attr_set = true;
     }
     // overlapped update (fp32 tcgen05 with programmatic dependent launch): no event may sit
@@ -1343,11 +1277,7 @@ solve:
     const bool overlap = a.pdl && (sizeof(T) == 8 || (W == 64 && a.use_tc));
     const char* both = sizeof(T) == 4 ? "pair_solve_update_f32" : "pair_solve_update_f64";
     if (hook) hook->begin(hook->ctx, overlap ? both : KName<T>::solve);
-    if (W == 64 && a.ereg) {
-        if constexpr (W == 64) k_pair_solve<T, W, true><<<a.npairs, inner_threads<W, true>(), sms, st>>>(a);
-    } else {
-        k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
-    }
+    k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
     MPJ_LAUNCHED();
     if (overlap) {
         int rc = 0;
@@ -1450,10 +1380,10 @@ int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const P
 template int launch_jacobi_round<float>(const JacobiRound<float>&, int, cudaStream_t, const ProfHook*);
 template int launch_jacobi_round<double>(const JacobiRound<double>&, int, cudaStream_t, const ProfHook*);
 
-template <typename T, int W, bool ER = false>
+template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     const size_t sms = sizeof(InnerSmem<T, W>);
-    cudaFuncSetAttribute(k_inner_solve_batch<T, W, ER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
+    cudaFuncSetAttribute(k_inner_solve_batch<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
     static long long* dbg = nullptr;
     const char* env = getenv("MPJSVD_INNER_TIMING");
     const bool timing = env && env[0] == '1';
@@ -1463,7 +1393,7 @@ static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, 
         if (sizeof(T) == 4) cudaMemcpyToSymbolAsync(g_inner_dbg_f, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, st);
         else cudaMemcpyToSymbolAsync(g_inner_dbg_d, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, st);
     }
-    k_inner_solve_batch<T, W, ER><<<count, inner_threads<W, ER>(), sms, st>>>(G, E, w, tol_in, max_inner, rot);
+    k_inner_solve_batch<T, W><<<count, inner_nt<W>(), sms, st>>>(G, E, w, tol_in, max_inner, rot);
     MPJ_LAUNCHED();
     if (timing) {
         long long hv[8];
@@ -1483,11 +1413,6 @@ template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     if (w <= 16) return inner_batch_w<T, 16>(G, E, w, tol_in, max_inner, count, rot, st);
     if (w <= 32) return inner_batch_w<T, 32>(G, E, w, tol_in, max_inner, count, rot, st);
-    if (w == 64) {
-        // E-in-registers solve unless MPJSVD_INNER_EREG=0 (comparison runs)
-        const char* env = getenv("MPJSVD_INNER_EREG");
-        if (!(env && env[0] == '0')) return inner_batch_w<T, 64, true>(G, E, w, tol_in, max_inner, count, rot, st);
-    }
     if (w <= 64) return inner_batch_w<T, 64>(G, E, w, tol_in, max_inner, count, rot, st);
     return -7;
 }
