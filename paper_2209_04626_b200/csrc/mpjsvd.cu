@@ -297,11 +297,6 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
-    // every pair of full width 2b = 64 (no ragged or bye block) -> E-in-registers inner solve
-    {
-        const char* env = getenv("MPJSVD_INNER_EREG");
-        a.ereg = (W == 64 && n % b == 0 && S.plan.M == (int)ceil_div(n, b) && !(env && env[0] == '0')) ? 1 : 0;
-    }
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
