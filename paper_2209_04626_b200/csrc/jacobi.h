@@ -50,6 +50,11 @@ struct JacobiRound {
     int* dlist;
     int* dctr;
     int pdl;            // 1: the update is launched as a programmatic dependent of the solve
+    // fp32 tcgen05 Gram with TMA loads (k_tc.cu): host pointer to a CUtensorMap over the matrix that holds
+    // every local slab (tbase, leading dimension tld), or nullptr (cp.async Gram)
+    const void* tmap;
+    const T* tbase;
+    long long tld;
 };
 
 // reset of the publication list by the first CTA of the round's Gram kernel
@@ -81,6 +86,9 @@ template <typename T>
 int gram_ctas_per_sm(int W, int use_tc);
 // tcgen05 fp32 kernels (k_tc.cu)
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
+// 4-D TMA view of the column-major fp32 matrix (rows_pad x cols, ld) whose boxes land in the canonical
+// K-major SWIZZLE_NONE operand layout of k_pair_gram_tma; out = 128-byte CUtensorMap.  0 on success.
+int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);
 // persistent overlapped variant: drains pairs in the order the solve publishes them (a.pdl)
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st);

@@ -21,6 +21,7 @@
 // elected thread issues tcgen05.mma, completion is signalled through
 // tcgen05.commit -> mbarrier, and the epilogue reads TMEM with tcgen05.ld
 // (warp w owns TMEM lanes 32w..32w+31).  Validated by tools/tc_probe.cu.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -269,6 +270,160 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tc(JacobiRound<float>
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
+// ------------------------------------------------------------------------
+// k_pair_gram_tma: k_pair_gram_tc with the raw W chunks loaded by TMA.  A
+// 4-D tensor view of X (r4 = 4 consecutive rows, c8 = 8 columns at stride ld,
+// kq = row groups of 4 at stride 16 B, cg = column groups of 8) makes one box
+// {4, 8, KT/4, 4} = 32 columns x KT rows land in shared memory exactly in the
+// canonical K-major SWIZZLE_NONE layout (core matrix (cg, kq) at cg SBO + kq
+// 128 B): X_I fills M-groups 0..3, X_J 4..7 of the stage, one elected thread
+// issues both boxes (mbarrier complete_tx), so no thread issues per-chunk
+// copies.  The 128 threads then write the lo parts (M-groups 8..15) from the
+// landed chunks, thread 0 issues the MMAs and refills the stage of tile t - 1
+// after its MMAs complete.  Rows past the matrix and columns past its last
+// column are zero-filled by the TMA unit.
+// ------------------------------------------------------------------------
+constexpr int GM_KT = 64, GM_ST = 3;
+constexpr size_t gram_tma_smem() { return (size_t)GM_ST * (128 * GM_KT * 4) + 1024; }
+
+__device__ __forceinline__ void tma_load_4d(uint32_t sdst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+        ::"r"(sdst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tc::smem_u32(mbar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tma(JacobiRound<float> a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int STAGE = 128 * GM_KT * 4;              // 32 KB: raw (16 KB) + lo (16 KB)
+    constexpr uint32_t SBO = (GM_KT / 4) * 128;         // 2048 B between 8-row (M) groups
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    reset_publication(a);
+    extern __shared__ __align__(1024) unsigned char gm_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gm_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], fin;
+    __shared__ uint32_t tmem_base;
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
+    const bool hasJ = pd.w1 > 0;
+    const uint32_t tx = hasJ ? 2u * 32u * GM_KT * 4u : 32u * GM_KT * 4u;
+    if (warp == 0) tc::tmem_alloc<64>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < GM_ST; ++s) { tc::mbar_init(&full[s]); tc::mbar_init(&done[s]); }
+        tc::mbar_init(&fin);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (!hasJ) {   // bye pair: M-groups 4..7 stay zero in every stage
+        for (int s = 0; s < GM_ST; ++s)
+            for (int i = tid; i < 4 * (int)SBO / 16; i += GT_NT)
+                reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4 * SBO)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tc::fence_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg + GM_KT - 1) / GM_KT);
+    const uint32_t sbase = tc::smem_u32(sm);
+    auto issue = [&](int t) {                // thread 0: both boxes of tile t -> stage t % GM_ST
+        const int s = t % GM_ST;
+        const int kq = (int)((rbeg + (long long)t * GM_KT) >> 2);
+        mbar_expect_tx(&full[s], tx);
+        tma_load_4d(sbase + (uint32_t)(s * STAGE), &tmap, 0, 0, kq, cI >> 3, &full[s]);
+        if (hasJ) tma_load_4d(sbase + (uint32_t)(s * STAGE) + 4 * SBO, &tmap, 0, 0, kq, cJ >> 3, &full[s]);
+    };
+    if (tid == 0)
+        for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
+    for (int t = 0; t < ntile; ++t) {
+        const int s = t % GM_ST;
+        unsigned char* st = sm + (size_t)s * STAGE;
+        tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
+        // lo parts of the landed raw chunks: 1024 16-byte chunks, 8 per thread, linear (conflict-free)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int f = tid + GT_NT * u;
+            const float4 x = reinterpret_cast<const float4*>(st)[f];
+            reinterpret_cast<float4*>(st + 8 * SBO)[f] = tc::lo4(x, tc::hi4(x));
+        }
+        tc::fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t base = sbase + (uint32_t)(s * STAGE);
+#pragma unroll
+            for (int ks = 0; ks < GM_KT / 8; ++ks) {
+                const uint64_t ad = tc::sdesc(base + ks * 256, 128, SBO);
+                tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);
+            }
+            tc::commit(&done[s]);
+            // refill the stage of tile t - 1 once its MMAs have read it
+            if (t >= 1 && t - 1 + GM_ST < ntile) {
+                const int sp = (t - 1) % GM_ST;
+                tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
+                issue(t - 1 + GM_ST);
+            }
+        }
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);
+    if (ntile > 0) {
+        if (tid == 0) tc::commit(&fin);
+        tc::mbar_wait(&fin, 0);
+        tc::fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += GT_NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
+        }
+    } else {
+        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
+int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    }
+    if (!fn || cols % 8 != 0 || rows_pad % 4 != 0 || ld % 4 != 0) return -1;
+    const cuuint64_t gdim[4] = {4, 8, (cuuint64_t)(rows_pad / 4), (cuuint64_t)(cols / 8)};
+    const cuuint64_t gstride[3] = {(cuuint64_t)ld * 4, 16, (cuuint64_t)ld * 4 * 8};
+    const cuuint32_t box[4] = {4, 8, GM_KT / 4, 4};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          const_cast<float*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
 }
 
 // ------------------------------------------------------------------------
@@ -665,6 +820,17 @@ static const GramVariant& gram_variant() {
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    if (a.tmap) {
+        static bool attr_m = false;
+        if (!attr_m) {
+            cudaFuncSetAttribute(k_pair_gram_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem());
+            attr_m = true;
+        }
+        k_pair_gram_tma<<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem(), st>>>(
+            a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
+        MPJ_LAUNCHED();
+        return 0;
+    }
     const GramVariant& gv = gram_variant();
     static bool attr = false;
     if (!attr) {

@@ -297,6 +297,33 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
+    // TMA-fed fp32 Gram: one tensor map over the matrix holding every local slab (the matrix itself on
+    // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
+    alignas(64) static thread_local unsigned char tmap_buf[128];
+    a.tmap = nullptr;
+    a.tbase = nullptr;
+    a.tld = 0;
+    if constexpr (sizeof(T) == 4) {
+        const char* env = getenv("MPJSVD_GRAM_TMA");
+        if (use_tc && !(env && env[0] == '0')) {
+            T* base = nullptr;
+            long long cols = 0;
+            for (int g = 0; g < S.plan.G; ++g)
+                if (S.local(g)) { base = S.xs[g]; break; }
+            int nlocal_ = 0;
+            for (int g = 0; g < S.plan.G; ++g) nlocal_ += S.local(g) ? 1 : 0;
+            // contiguous store: the n columns of X; shard store: nlocal * nbuf slabs of b columns
+            cols = S.plan.G == 1 && S.me < 0 && S.slab_x == (long long)b * ldx ? n : (long long)nlocal_ * S.plan.nbuf * b;
+            if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols) == 0) {
+                a.tmap = tmap_buf;
+                a.tbase = base;
+                a.tld = ldx;
+                // a TMA box covers 64 rows and only zero-fills past the matrix: row slabs must be whole boxes
+                a.rows_per_split = round_up(a.rows_per_split, 64LL);
+                a.nsplit = (int)ceil_div(m_pad, a.rows_per_split);
+            }
+        }
+    }
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);

@@ -363,3 +363,25 @@ def test_factor_mixed_precision_rrqr_vs_oracle(mp, name, n):
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
+
+
+def test_gram_tma_equals_cp_async_gram(mp, monkeypatch):
+    """The TMA-fed fp32 Gram (k_pair_gram_tma) lands the same operand layout and issues the same MMA
+    sequence as the cp.async Gram: with the same row slabs (split_rows = 128) the whole SVD is bitwise
+    equal; the default (automatic) slabs stay within the parity bar."""
+    a = testmat.config_matrix("C3", 512)
+    res = {}
+    for tma in ("1", "0"):
+        monkeypatch.setenv("MPJSVD_GRAM_TMA", tma)
+        U, S, V, st = mp.factor(dev(a), split_rows=128)
+        res[tma] = (host(U), host(S), host(V), st["sweeps32"], st["sweeps64"])
+    for x, y in zip(res["1"], res["0"]):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    # ragged n (last block narrower) and an odd block count (bye pairs) through the TMA Gram
+    monkeypatch.setenv("MPJSVD_GRAM_TMA", "1")
+    for n in (200, 352):
+        b = testmat.config_matrix("C1", n)
+        U, S, V, st = mp.factor(dev(b))
+        check_svd(b, host(U), host(S), host(V))
+        so = oracle.mixed_svd(b)[1]
+        assert np.max(np.abs(host(S) - so) / so) <= 1e-12
