@@ -302,7 +302,8 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
     } else if (tid >= NG && tid < NG + P * NCH) {
         kE = (tid - NG) / NCH;
         r0E = (tid - NG) % NCH;                        // chunk index c
-        if (!InnerSmem<T, W>::ECOL) r0E *= 8;          // row-major E: rows 8c .. 8c + 7
+        // row-major E: rows c, c + NCH, ..., c + 7 NCH (interleaved, so that the NCH lanes of a pair hit
+        // distinct banks; 8-row blocks put them only 0 or 8 double-words apart)
     }
     __syncthreads();
     if (max_inner < 1) { if (sweeps_used) *sweeps_used = 0; return 0; }
@@ -412,18 +413,18 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                     T ep[8], eq[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        ep[u] = sm.E[(r0E + u) * ES + pa];
-                        eq[u] = sm.E[(r0E + u) * ES + qa];
+                        ep[u] = sm.E[(r0E + NCH * u) * ES + pa];
+                        eq[u] = sm.E[(r0E + NCH * u) * ES + qa];
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) rot2(R4.c, R4.s, ep[u], eq[u]);
-                    const int up = pa - r0E, uq = qa - r0E;
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        if (u == up) { ep[u] += R4.cm1; eq[u] += R4.s; }
-                        if (u == uq) { ep[u] -= R4.s; eq[u] += R4.cm1; }
-                        sm.E[(r0E + u) * ES + pa] = ep[u];
-                        sm.E[(r0E + u) * ES + qa] = eq[u];
+                        const int row = r0E + NCH * u;
+                        if (row == pa) { ep[u] += R4.cm1; eq[u] += R4.s; }
+                        if (row == qa) { ep[u] -= R4.s; eq[u] += R4.cm1; }
+                        sm.E[row * ES + pa] = ep[u];
+                        sm.E[row * ES + qa] = eq[u];
                     }
                 }
             }
