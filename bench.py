@@ -232,9 +232,11 @@ def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None =
         for tag, s, key in (("f32", 4, "32"), ("f64", 8, "64")):
             sweeps = st["sweeps" + key]
             upd = sum(st["upd_trace" + key])
+            # pairs skipped as unchanged (exact skip) compute no Gram
+            evaluated = sweeps * rounds * npairs - sum(st.get("skip_trace" + key, []))
             g, u = f"pair_gram_{tag}", f"pair_update_{tag}"
-            flops[g] = flops.get(g, 0.0) + sweeps * rounds * npairs * float(n) * w * (w + 1)
-            byts[g] = byts.get(g, 0.0) + sweeps * rounds * float(n) * n * s
+            flops[g] = flops.get(g, 0.0) + evaluated * float(n) * w * (w + 1)
+            byts[g] = byts.get(g, 0.0) + evaluated * float(n) * w * s
             flops[u] = flops.get(u, 0.0) + upd * 2 * 2.0 * n * w * w
             byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * float(n) * w * s
         flops["qrp_coop"] = flops.get("qrp_coop", 0.0) + 4.0 * n ** 3 / 3
@@ -422,6 +424,7 @@ def main():
         "upd_trace32": st0["upd_trace32"], "upd_trace64": st0["upd_trace64"],
         "inner_max_trace32": st0["inner_max_trace32"], "inner_max_trace64": st0["inner_max_trace64"],
         "inner_sum_trace32": st0["inner_sum_trace32"], "inner_sum_trace64": st0["inner_sum_trace64"],
+        "skip_trace32": st0["skip_trace32"], "skip_trace64": st0["skip_trace64"],
         "stage_ms": st0["stage_ms"],
         "check": {"orth_u": orth_u, "orth_v": orth_v, "residual": res},
         "kernels": kernels, "jacobi_roofline": jacobi,

@@ -120,6 +120,9 @@ typedef struct {
     int64_t kernel_launches;   /* kernels launched by this call */
     int32_t inner_max_trace32[32], inner_max_trace64[32];  /* per sweep: most inner sweeps of one pair */
     int32_t inner_sum_trace32[32], inner_sum_trace64[32];  /* per sweep: inner sweeps summed over pairs */
+    int32_t skip_trace32[32], skip_trace64[32];  /* per sweep: pairs whose Gram and solve were skipped because
+                                                    neither block rotated since their previous evaluation
+                                                    (exact: same Gram, same metric, no rotation) */
 } mpjsvd_stats;
 
 /* Fill *opts with the defaults above. */

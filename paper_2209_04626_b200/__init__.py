@@ -51,7 +51,8 @@ class Stats(C.Structure):
                 ("upd_trace32", C.c_int32 * 32), ("upd_trace64", C.c_int32 * 32),
                 ("kernel_launches", C.c_int64),
                 ("inner_max_trace32", C.c_int32 * 32), ("inner_max_trace64", C.c_int32 * 32),
-                ("inner_sum_trace32", C.c_int32 * 32), ("inner_sum_trace64", C.c_int32 * 32)]
+                ("inner_sum_trace32", C.c_int32 * 32), ("inner_sum_trace64", C.c_int32 * 32),
+                ("skip_trace32", C.c_int32 * 32), ("skip_trace64", C.c_int32 * 32)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -71,6 +72,8 @@ class Stats(C.Structure):
             "inner_max_trace64": list(self.inner_max_trace64[:min(s64, 32)]),
             "inner_sum_trace32": list(self.inner_sum_trace32[:min(s32, 32)]),
             "inner_sum_trace64": list(self.inner_sum_trace64[:min(s64, 32)]),
+            "skip_trace32": list(self.skip_trace32[:min(s32, 32)]),
+            "skip_trace64": list(self.skip_trace64[:min(s64, 32)]),
         }
 
 

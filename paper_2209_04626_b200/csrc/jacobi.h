@@ -19,7 +19,7 @@ struct PairDesc {
     T* v0;
     T* v1;
     int w0, w1;
-    int pad_[2];
+    int b0, b1;         // block ids (schedule identity of the slabs; the bye block has id >= nblk)
 };
 
 // Arguments of one block round-robin Jacobi round (k_jacobi.cu).
@@ -43,6 +43,7 @@ struct JacobiRound {
     double* sweep_off;  // device scalar, atomic max (this sweep)
     int* sweep_upd;     // device scalar, atomic add (this sweep)
     int* sweep_inner;   // device [2]: max inner sweeps of a pair, summed inner sweeps (this sweep)
+    int* sweep_skip;    // device scalar, atomic add: pairs skipped as unchanged (this sweep)
     int use_tc;         // fp32, W = 64: tcgen05 TF32 (hi/lo split) Gram and update (k_tc.cu)
     // completion-ordered publication of solved pairs (overlapped update):
     // dlist[npairs] (-1 = not yet), dctr[0] = publication tail, dctr[1] = update work counter,
@@ -55,7 +56,23 @@ struct JacobiRound {
     const void* tmap;
     const T* tbase;
     long long tld;
+    // exact skip of unchanged pairs: last_mod[blk] = global round index (sweep * R + round) of the last
+    // rotation that touched block blk (-1: none); pair_off = this round's per-slot metric of the previous
+    // evaluation (written back every evaluation).  A pair whose two blocks were not rotated since its
+    // previous evaluation (global round gidx - R) has the same Gram, hence the same metric and no rotation:
+    // its Gram and solve are skipped (skip = 0 disables)
+    int* last_mod;
+    double* pair_off;
+    int gidx, R, skip;
 };
+
+// the pair's blocks are unchanged since its previous evaluation (exactly one sweep ago)
+template <typename T>
+__device__ __forceinline__ bool pair_unchanged(const JacobiRound<T>& a, const PairDesc<T>& pd) {
+    if (!a.skip) return false;
+    const int since = a.gidx - a.R;
+    return a.last_mod[pd.b0] < since && a.last_mod[pd.b1] < since;
+}
 
 // reset of the publication list by the first CTA of the round's Gram kernel
 template <typename T>
@@ -149,6 +166,9 @@ int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, l
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C,
                long long ldc, long long ncols, double* work, cudaStream_t st);
 size_t apply_q_work_elems(long long m, long long ncols);
+// Q = H_0 ... H_{k-1} formed in place on C (m x m, the identity on entry), trailing blocks only.
+int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
+              double* work, cudaStream_t st);
 // Blocked Householder QR (no pivoting) in place; work >= apply_q_work_elems(m, n).
 int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st);
 

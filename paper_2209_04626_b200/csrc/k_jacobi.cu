@@ -42,6 +42,7 @@ __device__ __forceinline__ T* pair_col(const PairDesc<T>& d, int c, bool v, long
 template <typename T, int W>
 __global__ void __launch_bounds__(64) k_pair_gram(JacobiRound<T> a) {
     reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     constexpr int KT = 32;
     constexpr int VEC = 16 / sizeof(T);       // elements per 16-byte vector
     constexpr int S = KT + VEC;               // padded column stride (conflict-free)
@@ -485,6 +486,20 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
     const int pair = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
     if (a.pdl) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // the update may start
     const int w = a.pd[pair].w0 + a.pd[pair].w1;
+    if (pair_unchanged(a, a.pd[pair])) {
+        // same Gram as one sweep ago: same metric, no rotation (exact skip)
+        if (tid == 0) {
+            atomic_max_nonneg(a.sweep_off, a.pair_off[pair]);
+            atomicAdd(a.sweep_skip, 1);
+            a.flag[pair] = 0;
+            if (a.dlist) {
+                __threadfence();
+                const int pos = atomicAdd(a.dctr, 1);
+                st_release_gpu(a.dlist + pos, pair);
+            }
+        }
+        return;
+    }
     // fixed-order reduction over row slabs (deterministic)
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
     for (int e = tid; e < W * W; e += nt) {
@@ -518,6 +533,13 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
         atomic_max_nonneg(a.sweep_off, (double)off);
         if (rotate) atomicAdd(a.sweep_upd, 1);
         a.flag[pair] = rotate ? 1 : 0;
+        if (a.skip) {
+            a.pair_off[pair] = (double)off;
+            if (rotate) {
+                a.last_mod[a.pd[pair].b0] = a.gidx;
+                a.last_mod[a.pd[pair].b1] = a.gidx;
+            }
+        }
     }
     if (rotate) {
         int used = 0;
@@ -723,6 +745,7 @@ __device__ __forceinline__ void gram_warp(const double* const* colp, double* Wsm
 template <int W>
 __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
     reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(16) unsigned char gram_smem[];
     double* Wsm = reinterpret_cast<double*>(gram_smem);
     const double** colp = reinterpret_cast<const double**>(Wsm + GRAM_STAGES * W * GRAM_S);
@@ -764,6 +787,7 @@ __device__ __forceinline__ int g32_chunk(int c, int rc) { return 8 * c + (rc ^ (
 
 __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float> a) {
     reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     constexpr int W = 64;
     extern __shared__ __align__(16) unsigned char g32_smem[];
     float4* Ws = reinterpret_cast<float4*>(g32_smem);            // [ST][W*8] chunks

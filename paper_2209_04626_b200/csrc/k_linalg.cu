@@ -484,6 +484,23 @@ int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double
     return 0;
 }
 
+// Q = H_0 ... H_{k-1} I formed in place on C (m x m, must hold the identity on entry; LAPACK xORGQR
+// order): panels are applied last to first, and before panel j0 is applied C is the identity outside
+// C[j0:, j0:], so the panel only touches that trailing block (4/3 m^3 instead of 2 m^3 flops).
+int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
+              double* work, cudaStream_t st) {
+    const int npan = (k + WY_NB - 1) / WY_NB;
+    for (int pnl = npan - 1; pnl >= 0; --pnl) {
+        const int j0 = pnl * WY_NB;
+        const int kb = k - j0 < WY_NB ? k - j0 : WY_NB;
+        int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, C + j0 + (long long)j0 * ldc,
+                             ldc, m - j0, 0, work, st);
+        if (rc) return rc;
+    }
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // Blocked Householder QR (LAPACK xGEQRF structure): panels of WY_NB columns
 // factored by the cooperative unblocked kernel (one CTA per column), trailing
 // matrix updated with the panel's compact-WY form Q^T = I - V T^T V^T on the

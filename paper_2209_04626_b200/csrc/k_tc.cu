@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tc(JacobiRound<float>
     constexpr int GT_STAGE_BYTES = 128 * GT_KT * 4;
     constexpr int GT_CHUNKS = 64 * (GT_KT / 4) / GT_NT;   // 16-byte chunks per thread per tile
     reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(1024) unsigned char gt_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gt_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t mbar[GT_ST + 1];
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tma(JacobiRound<float> a
     constexpr uint32_t SBO = (GM_KT / 4) * 128;         // 2048 B between 8-row (M) groups
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
     reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(1024) unsigned char gm_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gm_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], fin;

@@ -42,7 +42,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -160,6 +160,7 @@ struct JacobiResult {
     int upd[64] = {};
     int inner_max[64] = {};      // max inner sweeps of a pair, per outer sweep
     int inner_sum[64] = {};      // summed inner sweeps over the updated pairs, per outer sweep
+    int skipped[64] = {};        // pairs skipped as unchanged, per outer sweep
 };
 
 // Where the X / V column slabs of one Jacobi stage live (shard.h): the
@@ -198,8 +199,8 @@ void build_sweep(JStore<T>& S, int b, int n, std::vector<PairDesc<T>>& table,
                 d.v1 = S.bv(g, p.buf1);
                 d.w0 = pl.width(p.blk0, b, n);
                 d.w1 = pl.width(p.blk1, b, n);
-                d.pad_[0] = p.blk0;
-                d.pad_[1] = p.blk1;
+                d.b0 = p.blk0;
+                d.b1 = p.blk1;
                 table.push_back(d);
             }
         }
@@ -275,14 +276,15 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     MPJ_TRY(ensure(h, S_PART, sizeof(T) * (size_t)npairs * nsplit * W * W));
     MPJ_TRY(ensure(h, S_E, sizeof(T) * (size_t)npairs * W * W));
     MPJ_TRY(ensure(h, S_JFLAG, sizeof(int) * (size_t)npairs));
-    MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + 3 * sizeof(int))));
+    MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + 4 * sizeof(int))));
     MPJ_TRY(ensure(h, S_PTAB, sizeof(PairDesc<T>) * (size_t)R * npairs));
     MPJ_TRY(ensure_pinned(h, sizeof(PairDesc<T>) * (size_t)R * npairs));
     MPJ_TRY(ensure(h, S_PUB, sizeof(int) * ((size_t)npairs + 4)));
     double* d_off = P<double>(h, S_SWEEP);
     int* d_upd = reinterpret_cast<int*>(d_off + 64);
     int* d_inner = d_upd + 64;     // [64][2]
-    MPJ_CUDA_TRY(cudaMemsetAsync(d_off, 0, 64 * (sizeof(double) + 3 * sizeof(int)), st));
+    int* d_skip = d_inner + 128;   // [64]
+    MPJ_CUDA_TRY(cudaMemsetAsync(d_off, 0, 64 * (sizeof(double) + 4 * sizeof(int)), st));
     PairDesc<T>* d_tab = P<PairDesc<T>>(h, S_PTAB);
     const size_t bytes_x = sizeof(T) * (size_t)S.slab_x, bytes_v = has_v ? sizeof(T) * (size_t)S.slab_v : 0;
 
@@ -325,6 +327,16 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         }
     }
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
+    // exact skip of unchanged pairs (one process holds every block's history; NCCL ranks evaluate all)
+    MPJ_TRY(ensure(h, S_LMOD, sizeof(int) * (size_t)(S.plan.M + 8)));
+    MPJ_TRY(ensure(h, S_POFF, sizeof(double) * (size_t)R * npairs));
+    a.last_mod = P<int>(h, S_LMOD);
+    a.R = R;
+    {
+        const char* env = getenv("MPJSVD_SKIP_UNCHANGED");
+        a.skip = (S.me < 0 && !(env && env[0] == '0')) ? 1 : 0;
+    }
+    MPJ_CUDA_TRY(cudaMemsetAsync(a.last_mod, 0xff, sizeof(int) * (size_t)(S.plan.M + 8), st));   // -1
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
     double prev = -1.0;
@@ -339,9 +351,12 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         a.sweep_off = d_off + (sw - 1);
         a.sweep_upd = d_upd + (sw - 1);
         a.sweep_inner = d_inner + 2 * (sw - 1);
+        a.sweep_skip = d_skip + (sw - 1);
         ProfHook hook{&h->prof, &Profiler::hb, &Profiler::he};
         for (int r = 0; r < R; ++r) {
             a.pd = d_tab + (size_t)r * npairs;
+            a.pair_off = P<double>(h, S_POFF) + (size_t)r * npairs;
+            a.gidx = (sw - 1) * R + r;
             MPJ_TRY(launch_jacobi_round<T>(a, W, st, h->prof.on ? &hook : nullptr));
             if (!moves[r].empty()) {
                 if (h->prof.on) h->prof.begin("exchange");
@@ -358,6 +373,8 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 3), a.dctr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp, d_off + (sw - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(hp + 1, d_upd + (sw - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 4), d_skip + (sw - 1), sizeof(int),
+                                     cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
         if (h->comm.active()) {
             const int rc = h->comm.async_error();
@@ -375,6 +392,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         res.upd[sw - 1] = upd;
         memcpy(&res.inner_max[sw - 1], reinterpret_cast<int*>(hp + 2), sizeof(int));
         memcpy(&res.inner_sum[sw - 1], reinterpret_cast<int*>(hp + 2) + 1, sizeof(int));
+        memcpy(&res.skipped[sw - 1], reinterpret_cast<int*>(hp + 4), sizeof(int));
         int pub_err = 0;
         memcpy(&pub_err, reinterpret_cast<int*>(hp + 3), sizeof(int));
         if (pub_err) {
@@ -551,7 +569,7 @@ int switch_u_inplace(mpjsvd_handle h, const double* X, const double* Ulow, doubl
     MPJ_TRY(gemm_f64_ex(1, 0, n, n, n, 1.0, X, ld, Ulow, ld, 0.0, Z, ld, lower_x ? 4 : 0, st));
     MPJ_TRY(qr_blocked(Z, ld, n, n, tau, qw, P<double>(h, S_WY), st));
     MPJ_TRY(set_identity<double>(Q, ld, ld, n, st));
-    MPJ_TRY(apply_q_wy(Z, n, n, ld, tau, Q, ld, n, P<double>(h, S_WY), st));
+    MPJ_TRY(form_q_wy(Z, n, n, ld, tau, Q, ld, P<double>(h, S_WY), st));
     return 0;
 }
 
@@ -815,6 +833,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             s.off_trace64[i] = r64.off[i]; s.upd_trace64[i] = r64.upd[i];
             s.inner_max_trace32[i] = r32.inner_max[i]; s.inner_sum_trace32[i] = r32.inner_sum[i];
             s.inner_max_trace64[i] = r64.inner_max[i]; s.inner_sum_trace64[i] = r64.inner_sum[i];
+            s.skip_trace32[i] = r32.skipped[i]; s.skip_trace64[i] = r64.skipped[i];
         }
         s.final_off32 = r32.sweeps ? r32.off[r32.sweeps - 1] : 0.0;
         s.final_off64 = r64.sweeps ? r64.off[r64.sweeps - 1] : 0.0;
@@ -942,7 +961,9 @@ static int jacobi_entry(mpjsvd_handle h, T* X, int64_t m, int64_t n, int64_t ldx
             if (is64) {
                 stats->off_trace64[i] = r.off[i]; stats->upd_trace64[i] = r.upd[i];
                 stats->inner_max_trace64[i] = r.inner_max[i]; stats->inner_sum_trace64[i] = r.inner_sum[i];
+                stats->skip_trace64[i] = r.skipped[i];
             } else {
+                stats->skip_trace32[i] = r.skipped[i];
                 stats->off_trace32[i] = r.off[i]; stats->upd_trace32[i] = r.upd[i];
                 stats->inner_max_trace32[i] = r.inner_max[i]; stats->inner_sum_trace32[i] = r.inner_sum[i];
             }

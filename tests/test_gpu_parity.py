@@ -385,3 +385,24 @@ def test_gram_tma_equals_cp_async_gram(mp, monkeypatch):
         check_svd(b, host(U), host(S), host(V))
         so = oracle.mixed_svd(b)[1]
         assert np.max(np.abs(host(S) - so) / so) <= 1e-12
+
+
+@pytest.mark.parametrize("name,n,extra", [("C1", 256, {}), ("C3", 512, {"virtual_shards": 2}),
+                                          ("C2", 384, {"max_sweeps64": 30})])
+def test_skip_unchanged_pairs_is_exact(mp, monkeypatch, name, n, extra):
+    """Skipping the Gram and solve of a pair whose blocks did not rotate since its previous evaluation
+    (one sweep earlier) is exact: outputs and sweep counts are bitwise those of evaluating every pair."""
+    a = testmat.config_matrix(name, n)
+    res = {}
+    for sk in ("1", "0"):
+        monkeypatch.setenv("MPJSVD_SKIP_UNCHANGED", sk)
+        U, S, V, st = mp.factor(dev(a), **extra)
+        res[sk] = (host(U), host(S), host(V), st)
+    for x, y in zip(res["1"][:3], res["0"][:3]):
+        assert np.array_equal(x, y)
+    s1, s0 = res["1"][3], res["0"][3]
+    for k in ("sweeps32", "sweeps64", "upd_trace32", "upd_trace64", "off_trace32", "off_trace64"):
+        assert s1[k] == s0[k], k
+    assert sum(s0["skip_trace32"]) == 0 and sum(s0["skip_trace64"]) == 0
+    # the final check sweep follows a sweep with few rotations: some pairs are skipped
+    assert sum(s1["skip_trace32"]) + sum(s1["skip_trace64"]) > 0
