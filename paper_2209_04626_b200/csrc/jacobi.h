@@ -163,14 +163,21 @@ int potrf_upper(double* G, long long ldg, int n, int* bad, cudaStream_t st);
 int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, long long nrows, int n,
                      cudaStream_t st);
 // C <- Q C, Q = H_0 ... H_{k-1} packed in Vr (rows m, ld ldv), blocked WY.
+// tcache (optional): T factors of panels 0 .. ncached-1 as left by qr_blocked (skips their formation)
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C,
-               long long ldc, long long ncols, double* work, cudaStream_t st);
+               long long ldc, long long ncols, double* work, cudaStream_t st, const double* tcache = nullptr,
+               int ncached = 0);
 size_t apply_q_work_elems(long long m, long long ncols);
 // Q = H_0 ... H_{k-1} formed in place on C (m x m, the identity on entry), trailing blocks only.
 int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
-              double* work, cudaStream_t st);
+              double* work, cudaStream_t st, const double* tcache = nullptr, int ncached = 0);
+// number of WY panels of a k-reflector factorisation whose T qr_blocked leaves in its cache (all but the last)
+inline int wy_cached_panels(int k) { return (k + 127) / 128 - 1; }
+inline size_t wy_tcache_elems(int k) { return (size_t)((k + 127) / 128) * 128 * 128; }
 // Blocked Householder QR (no pivoting) in place; work >= apply_q_work_elems(m, n).
-int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st);
+// tcache (optional, wy_tcache_elems(n)): receives the T factor of every panel with a trailing update
+int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,
+               double* tcache = nullptr);
 
 // ---- misc (k_misc.cu) ----------------------------------------------------
 int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st);

@@ -424,7 +424,8 @@ size_t apply_q_work_elems(long long m, long long ncols) {
 // panel of kb <= WY_NB reflectors stored below the diagonal of P (rows
 // `rows`, ld ldp; reflector i has its unit at row i).
 static int apply_panel(const double* P, long long ldp, long long rows, int kb, const double* tau, double* C,
-                       long long ldc, long long ncols, int trans, double* work, cudaStream_t st) {
+                       long long ldc, long long ncols, int trans, double* work, cudaStream_t st,
+                       const double* t_in = nullptr, double* t_out = nullptr) {
     const long long ldw = round_up(rows, 32);
     double* Vp = work;                                  // rows x WY_NB (ld ldw)
     double* S = Vp + (size_t)ldw * WY_NB;               // WY_NB x WY_NB
@@ -436,7 +437,13 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     if (gx > 128) gx = 128;
     k_make_panel<<<dim3(gx, WY_NB), 256, 0, st>>>(P, ldp, rows, 0, kb, Vp, ldw);
     MPJ_LAUNCHED();
-    int rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldw, Vp, ldw, 0.0, S, WY_NB, st);
+    int rc = 0;
+    if (t_in) {
+        // T of this panel was formed by the factorisation that produced the reflectors
+        MPJ_CUDA_TRY(cudaMemcpyAsync(T, t_in, sizeof(double) * WY_NB * WY_NB, cudaMemcpyDeviceToDevice, st));
+        goto apply;
+    }
+    rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldw, Vp, ldw, 0.0, S, WY_NB, st);
     if (rc) return rc;
     static bool attr = false;
     if (!attr) {
@@ -460,24 +467,27 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
             if (rc) return rc;
         }
     }
+    if (t_out) MPJ_CUDA_TRY(cudaMemcpyAsync(t_out, T, sizeof(double) * WY_NB * WY_NB, cudaMemcpyDeviceToDevice, st));
+apply:
     // transposed products keep the long dimension (ncols) in the GEMM's M: W1^T = C^T Vp,
     // W2^T = W1^T T^(T) (T^T for trans), C -= Vp W2 = Vp (W2^T)^T
-    const long long ldt = ncols;
-    rc = gemm_f64(1, 0, ncols, WY_NB, rows, 1.0, C, ldc, Vp, ldw, 0.0, W1, ldt, st);
+    rc = gemm_f64(1, 0, ncols, WY_NB, rows, 1.0, C, ldc, Vp, ldw, 0.0, W1, ncols, st);
     if (rc) return rc;
-    rc = gemm_f64(0, trans ? 0 : 1, ncols, WY_NB, WY_NB, 1.0, W1, ldt, T, WY_NB, 0.0, W2, ldt, st);
+    rc = gemm_f64(0, trans ? 0 : 1, ncols, WY_NB, WY_NB, 1.0, W1, ncols, T, WY_NB, 0.0, W2, ncols, st);
     if (rc) return rc;
-    rc = gemm_f64(0, 1, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, ldt, 1.0, C, ldc, st);
+    rc = gemm_f64(0, 1, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, ncols, 1.0, C, ldc, st);
     return rc;
 }
 
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
-               long long ncols, double* work, cudaStream_t st) {
+               long long ncols, double* work, cudaStream_t st, const double* tcache, int ncached) {
     const int npan = (k + WY_NB - 1) / WY_NB;
     for (int pnl = npan - 1; pnl >= 0; --pnl) {
         const int j0 = pnl * WY_NB;
         const int kb = k - j0 < WY_NB ? k - j0 : WY_NB;
-        int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, C + j0, ldc, ncols, 0, work, st);
+        const double* tin = tcache && pnl < ncached ? tcache + (size_t)pnl * WY_NB * WY_NB : nullptr;
+        int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, C + j0, ldc, ncols, 0, work, st,
+                             tin);
         if (rc) return rc;
     }
     MPJ_CUDA_TRY(cudaGetLastError());
@@ -488,13 +498,14 @@ int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double
 // order): panels are applied last to first, and before panel j0 is applied C is the identity outside
 // C[j0:, j0:], so the panel only touches that trailing block (4/3 m^3 instead of 2 m^3 flops).
 int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
-              double* work, cudaStream_t st) {
+              double* work, cudaStream_t st, const double* tcache, int ncached) {
     const int npan = (k + WY_NB - 1) / WY_NB;
     for (int pnl = npan - 1; pnl >= 0; --pnl) {
         const int j0 = pnl * WY_NB;
         const int kb = k - j0 < WY_NB ? k - j0 : WY_NB;
+        const double* tin = tcache && pnl < ncached ? tcache + (size_t)pnl * WY_NB * WY_NB : nullptr;
         int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, C + j0 + (long long)j0 * ldc,
-                             ldc, m - j0, 0, work, st);
+                             ldc, m - j0, 0, work, st, tin);
         if (rc) return rc;
     }
     MPJ_CUDA_TRY(cudaGetLastError());
@@ -507,7 +518,8 @@ int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double*
 // DMMA GEMM.  Used for the tall QR and the LQ of R
 // (QR of R^T).  Same reflectors / R as the unblocked algorithm
 // up to rounding.
-int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st) {
+int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,
+               double* tcache) {
     for (int j0 = 0; j0 < n; j0 += WY_NB) {
         const int kb = n - j0 < WY_NB ? n - j0 : WY_NB;
         double* Pn = A + j0 + (long long)j0 * lda;
@@ -519,7 +531,8 @@ int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, d
         rc = qr_coop(Pn, lda, m - j0, kb, tau + j0, 0, wp, nullptr, st);
         if (rc) return rc;
         if (j0 + kb < n) {
-            rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)kb * lda, lda, n - j0 - kb, 1, work, st);
+            rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)kb * lda, lda, n - j0 - kb, 1, work, st,
+                             nullptr, tcache ? tcache + (size_t)(j0 / WY_NB) * WY_NB * WY_NB : nullptr);
             if (rc) return rc;
         }
     }

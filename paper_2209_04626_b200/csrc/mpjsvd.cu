@@ -42,7 +42,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -108,6 +108,8 @@ struct mpjsvd_handle_s {
     void* pinned_tab = nullptr;    // staging of the per-sweep pair-descriptor table
     size_t pinned_cap = 0;
     cudaEvent_t ev[10] = {};
+    cudaStream_t aux = nullptr;    // second stream: independent assembly chains (fork/join by events)
+    cudaEvent_t fork = nullptr, join = nullptr;
     Comm comm;                     // NCCL (multi-process sharding), inactive by default
 };
 
@@ -567,9 +569,10 @@ int switch_u_inplace(mpjsvd_handle h, const double* X, const double* Ulow, doubl
                      int n, bool lower_x, QrWork& qw, cudaStream_t st) {
     double* tau = P<double>(h, S_TAU_U);
     MPJ_TRY(gemm_f64_ex(1, 0, n, n, n, 1.0, X, ld, Ulow, ld, 0.0, Z, ld, lower_x ? 4 : 0, st));
-    MPJ_TRY(qr_blocked(Z, ld, n, n, tau, qw, P<double>(h, S_WY), st));
+    MPJ_TRY(ensure(h, S_TC_Z, sizeof(double) * wy_tcache_elems(n)));
+    MPJ_TRY(qr_blocked(Z, ld, n, n, tau, qw, P<double>(h, S_WY), st, P<double>(h, S_TC_Z)));
     MPJ_TRY(set_identity<double>(Q, ld, ld, n, st));
-    MPJ_TRY(form_q_wy(Z, n, n, ld, tau, Q, ld, P<double>(h, S_WY), st));
+    MPJ_TRY(form_q_wy(Z, n, n, ld, tau, Q, ld, P<double>(h, S_WY), st, P<double>(h, S_TC_Z), wy_cached_panels(n)));
     return 0;
 }
 
@@ -684,7 +687,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (m > n) {
         MPJ_TRY(ensure_qr_work(h, (int)m, (int)n, qw));
         PROF_B("qr_coop_tall");
-        MPJ_TRY(qr_blocked(dA, m_pad, (int)m, (int)n, P<double>(h, S_TAU_T0), qw, P<double>(h, S_WY), st));
+        MPJ_TRY(ensure(h, S_TC_TALL, sizeof(double) * wy_tcache_elems((int)n)));
+        MPJ_TRY(qr_blocked(dA, m_pad, (int)m, (int)n, P<double>(h, S_TAU_T0), qw, P<double>(h, S_WY), st,
+                           P<double>(h, S_TC_TALL)));
         PROF_E("qr_coop_tall");
         MPJ_TRY(upper_of(dA, m_pad, dA1, n_pad, (int)n, n_pad, st));
     } else {
@@ -707,7 +712,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         PROF_E("qrp_coop");
         MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
         PROF_B("qr_ap");
-        MPJ_TRY(qr_blocked(dA1L, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), qw, P<double>(h, S_WY), st));
+        MPJ_TRY(ensure(h, S_TC_P, sizeof(double) * wy_tcache_elems((int)n)));
+        MPJ_TRY(qr_blocked(dA1L, n_pad, (int)n, (int)n, P<double>(h, S_TAU_P), qw, P<double>(h, S_WY), st,
+                           P<double>(h, S_TC_P)));
         PROF_E("qr_ap");
     } else {
     PROF_B("qrp_coop");
@@ -726,7 +733,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (o.x_from_lq) {
         MPJ_TRY(transpose_upper(dA1L, n_pad, dRt, n_pad, (int)n, n_pad, st));
         PROF_B("lq_coop");
-        MPJ_TRY(qr_blocked(dRt, n_pad, (int)n, (int)n, P<double>(h, S_TAU_T), qw, P<double>(h, S_WY), st));
+        MPJ_TRY(ensure(h, S_TC_T, sizeof(double) * wy_tcache_elems((int)n)));
+        MPJ_TRY(qr_blocked(dRt, n_pad, (int)n, (int)n, P<double>(h, S_TAU_T), qw, P<double>(h, S_WY), st,
+                           P<double>(h, S_TC_T)));
         PROF_E("lq_coop");
         MPJ_TRY(lower_from_rt(dRt, n_pad, dX, n_pad, (int)n, n_pad, st));
     } else {
@@ -857,20 +866,36 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_TRY(finalize(dY, n_pad, dQ, n_pad, P<double>(h, S_SOUT), P<int>(h, S_RANK), dUX, n_pad, dVX, n_pad,
                      P<double>(h, S_KEYS) /* sorted sigma */, n_pad, (int)n, st));
     PROF_B("assemble_wy");
-    MPJ_TRY(apply_q_wy(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), dUX, n_pad, n, P<double>(h, S_WY), st));
+    // V = P Q_t V_X on the auxiliary stream (own WY and split-K workspaces; each launch captures the
+    // workspace pointer set when it is issued), U = Q_tall Q_p U_X on the main stream, joined below
+    const bool v_chain = o.x_from_lq != 0;
+    if (v_chain) {
+        MPJ_TRY(ensure(h, S_WY2, sizeof(double) * apply_q_work_elems(m_pad, n)));
+        MPJ_TRY(ensure(h, S_GEMMWS2, sizeof(double) * (size_t)8 * 64 * n_pad + sizeof(double) * 64 * 64 * 64));
+        MPJ_CUDA_TRY(cudaEventRecord(h->fork, st));
+        MPJ_CUDA_TRY(cudaStreamWaitEvent(h->aux, h->fork, 0));
+        gemm_set_workspace(P<double>(h, S_GEMMWS2), h->cap[S_GEMMWS2] / sizeof(double));
+        MPJ_TRY(apply_q_wy(dRt, n, (int)n, n_pad, P<double>(h, S_TAU_T), dVX, n_pad, n, P<double>(h, S_WY2), h->aux,
+                           P<double>(h, S_TC_T), wy_cached_panels((int)n)));
+        MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, h->aux));
+        MPJ_CUDA_TRY(cudaEventRecord(h->join, h->aux));
+        gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
+    }
+    MPJ_TRY(apply_q_wy(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), dUX, n_pad, n, P<double>(h, S_WY), st,
+                       o.mp_rrqr ? P<double>(h, S_TC_P) : nullptr, o.mp_rrqr ? wy_cached_panels((int)n) : 0));
     double* Ufin = dUX;
     long long ldUf = n_pad;
     if (m > n) {
         double* dUB = P<double>(h, S_UBIG);
         MPJ_CUDA_TRY(cudaMemsetAsync(dUB, 0, sizeof(double) * (size_t)m_pad * n, st));
         MPJ_TRY(copy_matrix(dUX, n_pad, dUB, m_pad, n, n, st));
-        MPJ_TRY(apply_q_wy(dA, m, (int)n, m_pad, P<double>(h, S_TAU_T0), dUB, m_pad, n, P<double>(h, S_WY), st));
+        MPJ_TRY(apply_q_wy(dA, m, (int)n, m_pad, P<double>(h, S_TAU_T0), dUB, m_pad, n, P<double>(h, S_WY), st,
+                           P<double>(h, S_TC_TALL), wy_cached_panels((int)n)));
         Ufin = dUB;
         ldUf = m_pad;
     }
-    if (o.x_from_lq)
-        MPJ_TRY(apply_q_wy(dRt, n, (int)n, n_pad, P<double>(h, S_TAU_T), dVX, n_pad, n, P<double>(h, S_WY), st));
-    MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, st));
+    if (v_chain) MPJ_CUDA_TRY(cudaStreamWaitEvent(st, h->join, 0));
+    else MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, st));
     PROF_E("assemble_wy");
     MPJ_CUDA_TRY(cudaEventRecord(ev[8], st));
     // ---- outputs (device -> device, or device -> host on the e2e path)
@@ -1037,6 +1062,13 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         h->own_stream = true;
     }
     for (auto& e : h->ev) cudaEventCreate(&e);
+    if (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        mpjsvd_destroy(h);
+        return MPJSVD_ERR_CUDA;
+    }
     if (cudaMallocHost(&h->host_pinned, 64) != cudaSuccess) {
         cudaGetLastError();
         mpjsvd_destroy(h);
@@ -1058,6 +1090,9 @@ int mpjsvd_destroy(mpjsvd_handle h) {
     if (h->host_pinned) cudaFreeHost(h->host_pinned);
     if (h->pinned_tab) cudaFreeHost(h->pinned_tab);
     h->comm.destroy();
+    if (h->aux) { cudaStreamSynchronize(h->aux); cudaStreamDestroy(h->aux); }
+    if (h->fork) cudaEventDestroy(h->fork);
+    if (h->join) cudaEventDestroy(h->join);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     cudaGetLastError();
