@@ -42,7 +42,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -676,6 +676,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     MPJ_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * 8, st));
     QrWork qw;
     std::vector<double> xnorms;
+    bool gates_read = false;   // X column norms to read back with the stats
     if (root) {
     // ---- input -> padded device copy (host memory is staged here: e2e path)
     MPJ_CUDA_TRY(cudaMemsetAsync(dA, 0, sizeof(double) * (size_t)m_pad * n, st));
@@ -745,11 +746,11 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- stage 3: gate measures, report only
     if (o.compute_gates) {
         PROF_B("gates_orth");
+        MPJ_TRY(ensure(h, S_XNORM, sizeof(double) * n));
         MPJ_TRY(gates_orth(dX, n_pad, n_pad, (int)n, dX32, n_pad, scal + 3, st));
         PROF_E("gates_orth");
-        MPJ_TRY(col_norms<double>(dX, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 1, st));
-        xnorms.resize(n);
-        MPJ_CUDA_TRY(cudaMemcpyAsync(xnorms.data(), P<double>(h, S_KEYS), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        MPJ_TRY(col_norms<double>(dX, n_pad, n_pad, (int)n, P<double>(h, S_XNORM), 1, st));
+        gates_read = true;
     }
     }  // root
     MPJ_CUDA_TRY(cudaEventRecord(ev[4], st));
@@ -909,6 +910,10 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- small read-backs for stats and error flags
     int hflags[8];
     double hscal[8];
+    if (gates_read) {
+        xnorms.resize(n);
+        MPJ_CUDA_TRY(cudaMemcpyAsync(xnorms.data(), P<double>(h, S_XNORM), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    }
     MPJ_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaMemcpyAsync(hscal, scal, sizeof(hscal), cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaStreamSynchronize(st));
