@@ -10,6 +10,10 @@ timeout 600 $CMD > $OUT/plain.log 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches_C5.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_qrp_lazy|k_pair_solve|k_pair_update_tc|k_pair_update_dmma|k_pair_gram_tc|k_pair_gram_dmma" -s 60 -c 6 \
+  -k regex:"k_qrp_lazy|k_pair_solve|k_pair_update_tc|k_pair_update_dmma|k_pair_gram_tma|k_pair_gram_dmma" -s 60 -c 7 \
   -o $OUT/prof_C5 $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu full rc=$?"
+# the QRP (one launch per step; the dominant single kernel): full set, first launch
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_qrp_lazy" -c 1 \
+  -o $OUT/prof_qrp_C5 $CMD > $OUT/ncu_qrp.log 2>&1
+echo "ncu qrp rc=$?"
