@@ -103,6 +103,8 @@ template <typename T>
 int gram_ctas_per_sm(int W, int use_tc);
 // tcgen05 fp32 kernels (k_tc.cu)
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
+// MPJSVD_SOLVE_TIMING=1: print k_pair_solve phase clocks (CTA 0) accumulated over a sweep (tools only)
+void solve_timing_report(const char* tag, int sweep);
 // 4-D TMA view of the column-major fp32 matrix (rows_pad x cols, ld) whose boxes land in the canonical
 // K-major SWIZZLE_NONE operand layout of k_pair_gram_tma; out = 128-byte CUtensorMap.  0 on success.
 int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);

@@ -143,8 +143,11 @@ template <int W>
 constexpr int inner_g_threads() { return (inner_nb_max<W>() + 31) / 32 * 32; }
 template <int W>
 constexpr int inner_e_items() { return (W / 2) * (W / 8); }
+// two leading "critical" warps: per round they update the diagonal blocks and the blocks that hold the
+// off-diagonal element of a next-round pair, then release the rotation warp (named barrier 1)
+constexpr int INNER_CRIT = 64;
 template <int W>
-constexpr int inner_nt() { return inner_g_threads<W>() + (inner_e_items<W>() + 31) / 32 * 32 + 32; }
+constexpr int inner_nt() { return INNER_CRIT + inner_g_threads<W>() + (inner_e_items<W>() + 31) / 32 * 32 + 32; }
 
 // rotation of one pair: (c, s), c - 1 and an active flag, read with one vector load
 template <typename T>
@@ -167,6 +170,9 @@ struct InnerSmem {
     Rot4<T> rot[2][W / 2];                             // current / next round
     T rt[2][W / 2], rg[2][W / 2], rpp[2][W / 2], rqq[2][W / 2];   // exact 2x2 diagonal update
     unsigned short spq[R][W / 2];                      // pair k of round r: p | q << 8 (p < q; q may be the bye)
+    unsigned char knx[R][W];                           // pair of index i in round r
+    short crit[R][W / 2];                              // round r: block (kA | kB << 8) holding next-round pair k' (-1: none / duplicate)
+    unsigned cmask[R][(W / 2 * (W / 2 + 1) / 2 + 31) / 32];   // round r: bitmask of those blocks
     int nrot[2];
     T red[32];
     long long dbg_t[2][32];                            // per-warp phase end clocks (debug timing only)
@@ -283,10 +289,32 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
     const int P = w2 / 2, NR = w2 - 1;
     const int NB = P * (P + 1) / 2;
     const int pwarp0 = nt - 32;                         // first thread of the rotation warp
+    constexpr int NCW = (W / 2 * (W / 2 + 1) / 2 + 31) / 32;
     for (int e = tid; e < NR * P; e += nt) {
         const int r = e / P, k = e - (e / P) * P;
         const int x = rr_slot(r, k, w2), y = rr_slot(r, w2 - 1 - k, w2);
         sm.spq[r][k] = (unsigned short)(min(x, y) | (max(x, y) << 8));
+        sm.knx[r][x] = (unsigned char)k;
+        sm.knx[r][y] = (unsigned char)k;
+    }
+    for (int e = tid; e < NR * NCW; e += nt) sm.cmask[e / NCW][e % NCW] = 0u;
+    __syncthreads();
+    // critical blocks of round r: the block (min(kx, ky), max(kx, ky)) of round r that holds the element
+    // (x, y) of next-round pair k' (kx, ky: the round-r pairs of x and y); first claimer keeps it
+    for (int e = tid; e < NR * P; e += nt) {
+        const int r = e / P, k = e - (e / P) * P;
+        const int rn = r + 1 < NR ? r + 1 : 0;
+        const unsigned pq = sm.spq[rn][k];
+        const int x = pq & 255, y = pq >> 8;
+        short blk = -1;
+        if (y < w && NR > 1) {
+            const int kx = sm.knx[r][x], ky = sm.knx[r][y];
+            const int a0 = min(kx, ky), b0 = max(kx, ky);
+            const int id = a0 * P - a0 * (a0 - 1) / 2 + (b0 - a0);
+            const unsigned bit = 1u << (id & 31);
+            if (a0 != b0 && !(atomicOr(&sm.cmask[r][id >> 5], bit) & bit)) blk = (short)(a0 | (b0 << 8));
+        }
+        sm.crit[r][k] = blk;
     }
     constexpr int EV = InnerSmem<T, W>::EV, ES = InnerSmem<T, W>::ES;
     for (int i = tid; i < W * ES; i += nt) sm.E[i] = T(0);
@@ -294,15 +322,17 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
     // fixed roles: pair-pair block (kA, kB) of G, or (pair kE, row chunk cE) of E: chunk c holds the
     // rows (j NCH + c) EV .. + EV - 1, j < 8 / EV, so that the NCH lanes of a pair read a contiguous
     // run of every column with 16-byte accesses
-    int kA = -1, kB = -1, kE = -1, r0E = 0;
-    if (tid < NB) {
-        int rem = tid, row = 0;
+    int kA = -1, kB = -1, kE = -1, r0E = 0, myblk = -1;
+    const int gt = tid - INNER_CRIT;                    // non-critical G thread index
+    if (tid >= INNER_CRIT && gt < NB) {
+        int rem = gt, row = 0;
         while (rem >= P - row) { rem -= P - row; ++row; }
         kA = row;
         kB = row + rem;
-    } else if (tid >= NG && tid < NG + P * NCH) {
-        kE = (tid - NG) / NCH;
-        r0E = (tid - NG) % NCH;                        // chunk index c
+        myblk = gt;
+    } else if (gt >= NG && gt < NG + P * NCH) {
+        kE = (gt - NG) / NCH;
+        r0E = (gt - NG) % NCH;                         // chunk index c
         // row-major E: rows c, c + NCH, ..., c + 7 NCH (interleaved, so that the NCH lanes of a pair hit
         // distinct banks; 8-row blocks put them only 0 or 8 double-words apart)
     }
@@ -329,8 +359,11 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
         const bool last = (r == NR - 1);
         const int rn = last ? 0 : r + 1;
         if (dbg && tid == 0) t_start = clock64();
-        // ---------------- phase A: G blocks (upper triangle G[min][max])
-        if (kA >= 0) {
+        // One phase per round.  The critical warps update the diagonal blocks and the blocks holding the
+        // next round's off-diagonal elements, then release the rotation warp (named barrier 1), which
+        // computes the next round's rotations while the other G warps finish the remaining blocks and the
+        // E warps apply this round's rotations to E; one CTA barrier ends the round.
+        auto g_block = [&](const int kA, const int kB) {
             const Rot4<T> RA = sm.rot[buf][kA];
             const unsigned pqa = sm.spq[r][kA];
             const int pa = pqa & 255, qa = pqa >> 8;
@@ -365,13 +398,19 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                     if (qav && qbv) sm.G[i11] = x11;
                 }
             }
-        }
-        if (dbg) { __syncwarp(); if (lane == 0) sm.dbg_t[0][warp] = clock64(); }
-        __syncthreads();
-        long long t_b1 = 0;
-        if (dbg && tid == 0) t_b1 = clock64();
-        // ---------------- phase B: next-round rotations | E <- (I + E) J - I
-        if (tid >= pwarp0) {
+        };
+        if (tid < INNER_CRIT) {
+            int ka = -1, kb = -1;
+            if (tid < 32) {
+                if (tid < P) ka = kb = tid;
+            } else if (tid - 32 < P) {
+                const int cb = sm.crit[r][tid - 32];
+                if (cb >= 0) { ka = cb & 255; kb = cb >> 8; }
+            }
+            if (ka >= 0) g_block(ka, kb);
+            asm volatile("bar.sync 1, %0;\n" ::"r"(INNER_CRIT + 32) : "memory");
+        } else if (tid >= pwarp0) {
+            asm volatile("bar.sync 1, %0;\n" ::"r"(INNER_CRIT + 32) : "memory");
             if (lane < P) {
                 const unsigned pq = sm.spq[rn][lane];
                 const int x = pq & 255, y = pq >> 8;
@@ -381,6 +420,8 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 const int act = set_rotation<T, W>(sm, buf ^ 1, lane, y, w, gxx, gyy, gxy, tol_in);
                 if (last) f_next |= act; else f_cur |= act;
             }
+        } else if (kA >= 0) {
+            if (kA != kB && !((sm.cmask[r][myblk >> 5] >> (myblk & 31)) & 1u)) g_block(kA, kB);
         } else if (kE >= 0) {
             const Rot4<T> R4 = sm.rot[buf][kE];
             if (R4.act != T(0)) {
@@ -430,20 +471,7 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 }
             }
         }
-        if (dbg) { __syncwarp(); if (lane == 0) sm.dbg_t[1][warp] = clock64(); }
-        if (dbg) __syncthreads();
-        if (dbg && tid == 0) {
-            // dbg[0] phase A (slowest G warp), [1] barrier 1, [2] rotation warp, [3] slowest E warp, [4] rounds
-            long long mA = 0, mE = 0;
-            for (int q = 0; q < (NG >> 5); ++q) mA = max(mA, sm.dbg_t[0][q]);
-            for (int q = NG >> 5; q < (nt >> 5) - 1; ++q) mE = max(mE, sm.dbg_t[1][q]);
-            const long long mR = sm.dbg_t[1][(nt >> 5) - 1];
-            dbg[0] += mA - t_start;
-            dbg[1] += t_b1 - mA;
-            dbg[2] += mR - t_b1;
-            dbg[3] += mE - t_b1;
-            dbg[4] += 1;
-        }
+        if (dbg && tid == 0) dbg[4] += 1;
         if (last) {
             const int any = __syncthreads_or(f_cur);
             f_cur = f_next;
@@ -478,8 +506,12 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
 // ------------------------------------------------------------------------
 // k_pair_solve: one CTA per pair.
 // ------------------------------------------------------------------------
+__device__ long long* g_solve_dbg = nullptr;   // phase clocks of k_pair_solve, CTA 0 (MPJSVD_SOLVE_TIMING=1)
+
 template <typename T, int W>
 __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) {
+    long long* sdbg = (blockIdx.x == 0 && threadIdx.x == 0) ? g_solve_dbg : nullptr;
+    const long long c0 = sdbg ? clock64() : 0;
     constexpr int GS = InnerSmem<T, W>::GS;
     extern __shared__ __align__(16) unsigned char smraw[];
     InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
@@ -528,6 +560,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
         }
     }
     off = block_max(off, sm.red);
+    const long long c1 = sdbg ? clock64() : 0;
     const bool rotate = off > a.tol;
     if (tid == 0) {
         atomic_max_nonneg(a.sweep_off, (double)off);
@@ -544,6 +577,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
     if (rotate) {
         int used = 0;
         inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
+        if (sdbg) { sdbg[1] += clock64() - c1; sdbg[3] += 1; }
         if (tid == 0) {
             atomicMax(a.sweep_inner, used);
             atomicAdd(a.sweep_inner + 1, used);
@@ -554,6 +588,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
             E[e] = (k < w && j < w) ? sm.E[InnerSmem<T, W>::eidx(k, j)] : T(0);   // E[k][j] row-major
         }
     }
+    if (sdbg) { sdbg[0] += c1 - c0; sdbg[2] += clock64() - c0; sdbg[4] += 1; }
     if (a.dlist) {                 // publish: E and flag of this pair are complete
         __syncthreads();
         if (tid == 0) {
@@ -1392,6 +1427,28 @@ int gram_ctas_per_sm(int W, int use_tc) {
 }
 template int gram_ctas_per_sm<float>(int, int);
 template int gram_ctas_per_sm<double>(int, int);
+
+void solve_timing_report(const char* tag, int sweep) {
+    static long long* dbg = nullptr;
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MPJSVD_SOLVE_TIMING");
+        on = (e && e[0] == '1') ? 1 : 0;
+        if (on) {
+            cudaMalloc(&dbg, 8 * sizeof(long long));
+            cudaMemset(dbg, 0, 8 * sizeof(long long));
+            cudaMemcpyToSymbol(g_solve_dbg, &dbg, sizeof(dbg));
+            return;
+        }
+    }
+    if (!on) return;
+    long long hv[8];
+    cudaMemcpy(hv, dbg, sizeof(hv), cudaMemcpyDeviceToHost);
+    const double nl = hv[4] > 0 ? (double)hv[4] : 1.0, ns = hv[3] > 0 ? (double)hv[3] : 1.0;
+    fprintf(stderr, "[solve timing %s sweep %d] launches=%lld solves=%lld per launch (cycles): prologue=%.0f total=%.0f; per solve: inner=%.0f\n",
+            tag, sweep, hv[4], hv[3], hv[0] / nl, hv[2] / nl, hv[1] / ns);
+    cudaMemset(dbg, 0, 8 * sizeof(long long));
+}
 
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook) {

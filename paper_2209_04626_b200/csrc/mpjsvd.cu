@@ -386,6 +386,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             }
         }
         if (h->prof.on) h->prof.resolve();
+        solve_timing_report(sizeof(T) == 4 ? "f32" : "f64", sw);
         const double off = hp[0];
         int upd = 0;
         memcpy(&upd, hp + 1, sizeof(int));
