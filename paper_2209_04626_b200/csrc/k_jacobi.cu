@@ -192,6 +192,23 @@ __device__ __forceinline__ void rot2(T c, T s, T& x, T& y) {
     y = ny;
 }
 
+// reciprocal and reciprocal square root: MUFU approximation + two Newton steps (fp64)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
+}
+
 // rotation parameters of pair k (indices p < q) into buffer `buf`; returns active
 template <typename T, int W>
 __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k, int q, int w, T gpp, T gqq, T gpq,
@@ -217,17 +234,21 @@ __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k,
             sn = t * c;
             cm1 = -__fdividef(t * t * c, 1.0f + r2 * c);
         } else {
-            T zeta = (gqq - gpp) / (T(2) * gpq);
-            if (fabs(zeta) > RealTraits<T>::rsqrt_u) {
-                t = T(1) / (T(2) * zeta);
+            // fp64: the same formulas with MUFU reciprocal / rsqrt refined by two Newton steps (<= 2 ulp
+            // from the IEEE quotients and roots; the refinement's accuracy is set by the outer fp64
+            // Gram and update, the rotation only has to be orthogonal to u64: c^2 + s^2 = 1 + O(u64))
+            const double zeta = (gqq - gpp) * rcp_nr(2.0 * gpq);
+            if (fabs(zeta) > RealTraits<double>::rsqrt_u) {
+                t = 0.5 * rcp_nr(zeta);
             } else {
-                T sg = zeta >= T(0) ? T(1) : T(-1);
-                t = sg / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
+                const double r1 = fma(zeta, zeta, 1.0);
+                const double sq = r1 * rsqrt_nr(r1);
+                t = (zeta >= 0.0 ? 1.0 : -1.0) * rcp_nr(fabs(zeta) + sq);
             }
-            T rt = sqrt(T(1) + t * t);
-            c = T(1) / rt;
+            const double r2 = fma(t, t, 1.0);
+            c = rsqrt_nr(r2);
             sn = t * c;
-            cm1 = -(t * t * c) / (T(1) + rt);
+            cm1 = -(t * t * c) * rcp_nr(1.0 + r2 * c);
         }
         active = 1;
     }
