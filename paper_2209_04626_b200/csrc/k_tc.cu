@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
 // ------------------------------------------------------------------------
 constexpr int UT_TPC = 16;
 
-__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<float> a, int ngroups) {
+__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<float> a, int ngroups, int tpc) {
     extern __shared__ __align__(1024) unsigned char ut_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ut_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char* Bh = sm;
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
                 if (pr < 0) { pair = -1; break; }
                 if (!a.flag[pr] || (which && !a.has_v)) continue;
                 const long long rows_pad = which ? a.nv_pad : a.m_pad;
-                if ((long long)grp * UT_TPC * UT_TM >= rows_pad) continue;
+                if ((long long)grp * tpc * UT_TM >= rows_pad) continue;
                 pair = pr;
                 break;
             }
@@ -679,8 +679,8 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
         if (pair < 0) break;
         const long long ld = which ? a.ldv : a.ldx;
         const long long rows_pad = which ? a.nv_pad : a.m_pad;
-        const long long row_lo = (long long)grp * UT_TPC * UT_TM;
-        const long long row_hi = min(rows_pad, row_lo + (long long)UT_TPC * UT_TM);
+        const long long row_lo = (long long)grp * tpc * UT_TM;
+        const long long row_hi = min(rows_pad, row_lo + (long long)tpc * UT_TM);
         const int ntile = (int)((row_hi - row_lo + UT_TM - 1) / UT_TM);
         const PairDesc<float> pd = a.pd[pair];
         const int w = pd.w0 + pd.w1;
@@ -894,7 +894,17 @@ int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
-    const int ngroups = (int)((rows_pad + (long long)UT_TPC * UT_TM - 1) / ((long long)UT_TPC * UT_TM));
+    // tiles per work item: the largest power of two <= UT_TPC that still gives every SM about three items
+    // (the dynamic claim then balances the CTAs; smaller items cost a pipeline ramp each).  Measured on
+    // B200: C3 (64 pairs x 4096 rows) 16 -> 4 tiles: 0.453 -> 0.437 s; C5 keeps 16
+    int tpc = UT_TPC;
+    while (tpc > 2 && (long long)a.npairs * (a.has_v ? 2 : 1) * ((rows_pad + (long long)tpc * UT_TM - 1) / ((long long)tpc * UT_TM)) < 3LL * nsm)
+        tpc >>= 1;
+    {
+        const char* e = getenv("MPJSVD_UPDATE_TPC");    // experiment hook: tiles per work item
+        if (e && atoi(e) > 0) tpc = atoi(e);
+    }
+    const int ngroups = (int)((rows_pad + (long long)tpc * UT_TM - 1) / ((long long)tpc * UT_TM));
     const long long items = (long long)a.npairs * 2 * ngroups;
     const unsigned grid = (unsigned)(items < nsm ? items : nsm);
     cudaLaunchConfig_t cfg = {};
@@ -907,7 +917,7 @@ int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     attr1[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr1;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl, a, ngroups);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl, a, ngroups, tpc);
     MPJ_LAUNCHED();
     if (e != cudaSuccess) {
         mpj_record_cuda_error(e, "cudaLaunchKernelEx(update pdl)", __FILE__, __LINE__);
