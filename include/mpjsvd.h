@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define MPJSVD_VERSION 120
+#define MPJSVD_VERSION 130
 #define MPJSVD_COMM_ID_BYTES 128
 
 /* return codes */
@@ -63,8 +63,22 @@ extern "C" {
 
 /* path (Alg. 3 gates; reading c-15) */
 #define MPJSVD_PATH_FORCE_MIXED 0     /* always run the fp32 Jacobi stage (default) */
-#define MPJSVD_PATH_AUTO 1            /* reserved: gate-driven choice (next) */
+#define MPJSVD_PATH_AUTO 1            /* Alg. 3 gates decide (DESIGN.md c-15):
+                                         cond gate -> tail gate -> orth gate -> fp32 Jacobi if orth <= tol_alg,
+                                         else the fp32 QR-SVD branch */
 #define MPJSVD_PATH_FORCE_FP64 2      /* skip the fp32 stage: Q = I, Y = X */
+
+/* stats.path_taken: 0 fp32 Jacobi (forced or AUTO), 2 fp64 only (forced), and under AUTO:
+   3 fp64 only (cond gate: scaled cond(R) <= tol_cond and cond(D) > cond_d_min),
+   4 fp64 only (tail gate: >= tail_frac n columns of X below 2^tail_cut_log2 max),
+   5 fp64 only (orth gate: ||X_t^T X_t - I||_max <= tol_orth),
+   6 fp32 QR-SVD (orth > tol_alg) */
+#define MPJSVD_TAKEN_JACOBI 0
+#define MPJSVD_TAKEN_FP64 2
+#define MPJSVD_TAKEN_SKIP_COND 3
+#define MPJSVD_TAKEN_SKIP_TAIL 4
+#define MPJSVD_TAKEN_SKIP_ORTH 5
+#define MPJSVD_TAKEN_QRSVD 6
 
 typedef struct mpjsvd_handle_s* mpjsvd_handle;
 
@@ -104,6 +118,13 @@ typedef struct {
                                   542-545, 563-573): the fp32 stage does not accumulate V; Q = qr(X^T working(U_low))
                                   by fp64 Householder QR (diag(R2) >= 0).  0: V-route, the fp32 stage accumulates V32
                                   and Q = qr(fl64(V32)) by CholeskyQR (reading c-11) */
+    /* AUTO gates (path = MPJSVD_PATH_AUTO; reading c-15) */
+    double tol_orth;           /* orth gate, default 1e-5 (PAPER.md:643-644 footnote) */
+    double tol_alg;            /* Jacobi if orth <= tol_alg, else the fp32 QR-SVD branch; default +inf */
+    double tol_cond_mult;      /* tol_cond = tol_cond_mult * n^(1/4) ("O(n^{1/4})"), default 1 */
+    double cond_d_min;         /* "condition number of D extremely large": max/min column norm > this, default 1e15 */
+    double tail_frac;          /* tail gate: at least ceil(tail_frac n) small columns, default 1/3 */
+    int32_t tail_cut_log2;     /* "small": ||x_j|| < 2^tail_cut_log2 max_j ||x_j||, default -60 */
 } mpjsvd_options;
 
 typedef struct {
@@ -123,6 +144,9 @@ typedef struct {
     int32_t skip_trace32[32], skip_trace64[32];  /* per sweep: pairs whose Gram and solve were skipped because
                                                     neither block rotated since their previous evaluation
                                                     (exact: same Gram, same metric, no rotation) */
+    double cond_scaled;        /* max_k r_k / min_k r_k, r_k = |R_kk| / ||R(:,k)||: estimate of the column-scaled
+                                  cond(R) used by the AUTO cond gate */
+    double cond_d;             /* max_j ||A1(:,j)|| / min_j ||A1(:,j)|| (cond(D) of A = B D) */
 } mpjsvd_stats;
 
 /* Fill *opts with the defaults above. */

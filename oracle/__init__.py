@@ -48,7 +48,9 @@ class Opts(C.Structure):
                 ("inner_tol_div", C.c_int32), ("max_sweeps32", C.c_int32),
                 ("max_sweeps64", C.c_int32), ("max_inner", C.c_int32), ("path", C.c_int32),
                 ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32),
-                ("max_inner32", C.c_int32), ("switch_u", C.c_int32)]
+                ("max_inner32", C.c_int32), ("switch_u", C.c_int32),
+                ("tol_orth", C.c_double), ("tol_alg", C.c_double), ("tol_cond_mult", C.c_double),
+                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -58,7 +60,7 @@ class Stats(C.Structure):
                 ("final_off32", C.c_double), ("final_off64", C.c_double),
                 ("off_trace32", C.c_double * 64), ("off_trace64", C.c_double * 64),
                 ("upd_trace32", C.c_int32 * 64), ("upd_trace64", C.c_int32 * 64),
-                ("perm", C.c_int32 * 1)]
+                ("perm", C.c_int32 * 1), ("cond_scaled", C.c_double), ("cond_d", C.c_double)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -66,12 +68,32 @@ class Stats(C.Structure):
             "sweeps32": s32, "sweeps64": s64, "converged": bool(self.converged),
             "orth_measure": self.orth_measure, "tail_fraction": self.tail_fraction,
             "cond_estimate": self.cond_estimate, "final_off32": self.final_off32,
+            "path_taken": self.path_taken, "cond_scaled": self.cond_scaled, "cond_d": self.cond_d,
             "final_off64": self.final_off64,
             "off_trace32": list(self.off_trace32[:min(s32, 64)]),
             "off_trace64": list(self.off_trace64[:min(s64, 64)]),
             "upd_trace32": list(self.upd_trace32[:min(s32, 64)]),
             "upd_trace64": list(self.upd_trace64[:min(s64, 64)]),
         }
+
+
+def _lowsvd(x32p, n, u32p, s32p):
+    """The fp32 QR SVD of the AUTO branch: LAPACK sgesvd (Golub-Kahan
+    bidiagonalisation + implicit-shift QR) as a library primitive; U in descending sigma order."""
+    try:
+        import scipy.linalg as sl
+        n = int(n)
+        x = np.ctypeslib.as_array(x32p, shape=(n * n,)).reshape((n, n), order="F").copy()
+        u, sv, _ = sl.svd(x, full_matrices=True, lapack_driver="gesvd", check_finite=False)
+        np.ctypeslib.as_array(u32p, shape=(n * n,))[:] = np.asfortranarray(u.astype(np.float32)).ravel(order="F")
+        np.ctypeslib.as_array(s32p, shape=(n,))[:] = sv.astype(np.float32)
+        return 0
+    except Exception:
+        return -1
+
+
+_LOWSVD_T = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_float), C.POINTER(C.c_float))
+_lowsvd_cb = _LOWSVD_T(_lowsvd)
 
 
 def lib():
@@ -109,6 +131,8 @@ def lib():
             L.oc_cyclic_jacobi.argtypes = [dp, i64, i64, i64, dp, i64, C.c_double, C.c_int32,
                                            C.POINTER(C.c_int64)]
             L.oc_cyclic_jacobi.restype = C.c_int32
+            L.om_set_lowsvd.argtypes = [_LOWSVD_T]
+            L.om_set_lowsvd(_lowsvd_cb)
             _lib = L
     return _lib
 

@@ -68,7 +68,16 @@ void om_default_opts(om_opts* o) {
     o->mp_rrqr = 0;
     o->max_inner32 = 1;
     o->switch_u = 1;
+    o->tol_orth = 1e-5;
+    o->tol_alg = INFINITY;
+    o->tol_cond_mult = 1.0;
+    o->cond_d_min = 1e15;
+    o->tail_frac = 1.0 / 3.0;
+    o->tail_cut_log2 = -60;
 }
+
+static om_lowsvd_fn g_lowsvd = NULL;
+void om_set_lowsvd(om_lowsvd_fn fn) { g_lowsvd = fn; }
 
 /* ---- Householder ------------------------------------------------------ */
 /* GVL Alg. 5.1.1 with beta = +||x|| (diag(R) >= 0, reading c-13). */
@@ -434,6 +443,7 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
     int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
     double* key = (double*)malloc(sizeof(double) * (size_t)n);
     double* tmpm = (double*)malloc(sizeof(double) * (size_t)nn);
+    double* a1n = NULL;
 
     for (int64_t j = 0; j < n; ++j) memcpy(Aw + j * m, A + j * lda, sizeof(double) * (size_t)m);
 
@@ -445,6 +455,10 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
     } else {
         for (int64_t j = 0; j < n; ++j) memcpy(A1 + j * n, Aw + j * m, sizeof(double) * (size_t)n);
     }
+
+    /* column norms of A1 = D of A = B D (the cond gate's cond(D)) */
+    a1n = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) a1n[j] = safe_norm(A1 + j * n, n);
 
     /* step 3: RRQR A1 P = Q_p R, by the mixed-precision RRQR of
        PAPER.md:494-495 ("We use this mixed precision algorithm ... in the preconditioning stage") */
@@ -499,9 +513,66 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         st->orth_measure = orth;
     }
 
-    if (o.path == OM_PATH_FORCE_FP64) {
+    /* gate quantities of AUTO (reading c-15): cond_scaled = max/min of r_k = |R_kk| / ||R(:,k)||
+       (||R(:,k)|| = ||A1(:, perm_k)||), cond_d = max/min column norm of A1 */
+    {
+        double rmx = 0.0, rmn = INFINITY, dmx = 0.0, dmn = INFINITY;
+        for (int64_t k = 0; k < n; ++k) {
+            const double cn = a1n[perm[k]];
+            const double rk = cn > 0.0 ? fabs(A1[k + k * n]) / cn : 0.0;
+            if (rk > rmx) rmx = rk;
+            if (rk < rmn) rmn = rk;
+            if (cn > dmx) dmx = cn;
+            if (cn < dmn) dmn = cn;
+        }
+        st->cond_scaled = rmn > 0.0 ? rmx / rmn : INFINITY;
+        st->cond_d = dmn > 0.0 ? dmx / dmn : INFINITY;
+    }
+    int32_t taken = o.path == OM_PATH_FORCE_FP64 ? OM_PATH_FORCE_FP64 : OM_PATH_FORCE_MIXED;
+    if (o.path == OM_PATH_AUTO) {
+        /* Alg. 3 order: cond gate, tail gate (654-663), orth gate (428-433),
+           then Jacobi if orth <= tol_alg else the QR SVD (435-445) */
+        const double tol_cond = o.tol_cond_mult * pow((double)n, 0.25);
+        double mxn = 0.0;
+        int64_t small = 0;
+        for (int64_t j = 0; j < n; ++j) { key[j] = safe_norm(X + j * n, n); if (key[j] > mxn) mxn = key[j]; }
+        for (int64_t j = 0; j < n; ++j) if (key[j] < ldexp(mxn, o.tail_cut_log2)) ++small;
+        if (st->cond_scaled <= tol_cond && st->cond_d > o.cond_d_min) taken = OM_TAKEN_SKIP_COND;
+        else if ((double)small >= ceil(o.tail_frac * (double)n)) taken = OM_TAKEN_SKIP_TAIL;
+        else if (st->orth_measure <= o.tol_orth) taken = OM_TAKEN_SKIP_ORTH;
+        else if (st->orth_measure <= o.tol_alg) taken = OM_PATH_FORCE_MIXED;
+        else taken = OM_TAKEN_QRSVD;
+    }
+    if (taken == OM_TAKEN_QRSVD) {
+        /* lower(X) = U_low S_low V_low^* by the QR SVD in fp32, U only; then the
+           U-route switch Q R2 = X^T working(U_low) (446-447) and Y = X Q */
+        st->path_taken = OM_TAKEN_QRSVD;
+        if (!g_lowsvd) { rc = -1; goto done; }
+        double mx = 0.0;
+        for (int64_t i = 0; i < nn; ++i) if (fabs(X[i]) > mx) mx = fabs(X[i]);
+        int e = 0;
+        frexp(mx, &e);
+        for (int64_t i = 0; i < nn; ++i) X32[i] = (float)ldexp(X[i], -e);
+        float* S32 = (float*)malloc(sizeof(float) * (size_t)n);
+        const int lrc = g_lowsvd(X32, n, V32, S32);   /* V32 buffer receives U32 */
+        free(S32);
+        if (lrc != 0) { rc = -3; goto done; }
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) tmpm[i + j * n] = (double)V32[i + j * n];
+        if (om_switch_u(X, n, n, tmpm, n, Q, n) != 0) { rc = -3; goto done; }
+#pragma omp parallel for schedule(static)
+        for (int64_t j = 0; j < n; ++j) {
+            double* yj = Y + j * n;
+            for (int64_t i = 0; i < n; ++i) yj[i] = 0.0;
+            for (int64_t k = 0; k < n; ++k) {
+                double q = Q[k + j * n];
+                const double* xk = X + k * n;
+                for (int64_t i = 0; i < n; ++i) yj[i] += xk[i] * q;
+            }
+        }
+    } else if (taken != OM_PATH_FORCE_MIXED) {
         /* Q = I, Y = X */
-        st->path_taken = OM_PATH_FORCE_FP64;
+        st->path_taken = taken;
         for (int64_t j = 0; j < n; ++j) Q[j + j * n] = 1.0;
         memcpy(Y, X, sizeof(double) * (size_t)nn);
     } else {
@@ -599,6 +670,6 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
 
 done:
     free(Aw); free(tau_tall); free(A1); free(tau_p); free(perm); free(Rt); free(tau_t);
-    free(X); free(X32); free(V32); free(Q); free(Y); free(idx); free(key); free(tmpm);
+    free(X); free(X32); free(V32); free(Q); free(Y); free(idx); free(key); free(tmpm); free(a1n);
     return rc;
 }

@@ -26,7 +26,13 @@
 #include <stdint.h>
 
 #define OM_PATH_FORCE_MIXED 0
+#define OM_PATH_AUTO 1
 #define OM_PATH_FORCE_FP64 2
+/* path_taken under AUTO (Alg. 3 gates; DESIGN.md c-15) */
+#define OM_TAKEN_SKIP_COND 3
+#define OM_TAKEN_SKIP_TAIL 4
+#define OM_TAKEN_SKIP_ORTH 5
+#define OM_TAKEN_QRSVD 6
 
 typedef struct {
     int32_t b;              /* block width (columns per block) */
@@ -43,6 +49,8 @@ typedef struct {
     int32_t max_inner32;    /* inner sweeps cap of the fp32 stage (c-5; default 1) */
     int32_t switch_u;       /* 1: U-route switch (Alg. 3 l.446-447): the fp32 stage
                                does not accumulate V; Q = qr(X^T U_low) (default); 0: V-route (c-11) */
+    double tol_orth, tol_alg, tol_cond_mult, cond_d_min, tail_frac;   /* AUTO gates (c-15) */
+    int32_t tail_cut_log2;
 } om_opts;
 
 typedef struct {
@@ -52,7 +60,15 @@ typedef struct {
     double off_trace32[64], off_trace64[64];
     int32_t upd_trace32[64], upd_trace64[64];
     int32_t perm[1];        /* unused placeholder (keeps layout simple) */
+    double cond_scaled;     /* max/min of |R_kk| / ||R(:,k)|| (column-scaled cond(R) estimate) */
+    double cond_d;          /* max/min column norm of A1 (cond(D) of A = B D) */
 } om_stats;
+
+/* The low-precision QR SVD of the AUTO branch: a library primitive
+   (LAPACK sgesvd, registered by the Python binding) computing U32 (n x n, ld n, columns in descending
+   singular value order) and S32 of the n x n fp32 matrix X32 (destroyed).  Returns 0 on success. */
+typedef int (*om_lowsvd_fn)(float* X32, int64_t n, float* U32, float* S32);
+void om_set_lowsvd(om_lowsvd_fn fn);
 
 void om_default_opts(om_opts* o);
 

@@ -39,7 +39,9 @@ class Options(C.Structure):
                 ("path", C.c_int32), ("x_from_lq", C.c_int32), ("compute_gates", C.c_int32),
                 ("stream", C.c_void_p), ("virtual_shards", C.c_int32), ("split_rows", C.c_int32),
                 ("fp32_tensor_cores", C.c_int32), ("pdl_overlap", C.c_int32),
-                ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32), ("switch_u", C.c_int32)]
+                ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32), ("switch_u", C.c_int32),
+                ("tol_orth", C.c_double), ("tol_alg", C.c_double), ("tol_cond_mult", C.c_double),
+                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -52,7 +54,8 @@ class Stats(C.Structure):
                 ("kernel_launches", C.c_int64),
                 ("inner_max_trace32", C.c_int32 * 32), ("inner_max_trace64", C.c_int32 * 32),
                 ("inner_sum_trace32", C.c_int32 * 32), ("inner_sum_trace64", C.c_int32 * 32),
-                ("skip_trace32", C.c_int32 * 32), ("skip_trace64", C.c_int32 * 32)]
+                ("skip_trace32", C.c_int32 * 32), ("skip_trace64", C.c_int32 * 32),
+                ("cond_scaled", C.c_double), ("cond_d", C.c_double)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -62,6 +65,7 @@ class Stats(C.Structure):
             "stage_ms": dict(zip(STAGES, list(self.stage_ms))), "total_ms": self.total_ms,
             "orth_measure": self.orth_measure, "tail_fraction": self.tail_fraction,
             "cond_estimate": self.cond_estimate, "final_off32": self.final_off32,
+            "cond_scaled": self.cond_scaled, "cond_d": self.cond_d,
             "final_off64": self.final_off64,
             "off_trace32": list(self.off_trace32[:min(s32, 32)]),
             "off_trace64": list(self.off_trace64[:min(s64, 32)]),

@@ -181,6 +181,12 @@ inline size_t wy_tcache_elems(int k) { return (size_t)((k + 127) / 128) * 128 * 
 int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,
                double* tcache = nullptr);
 
+// ---- fp32 QR SVD of the AUTO branch (lowsvd.cpp, cuSOLVER sgesvd via dlopen) ----
+size_t lowsvd_work_bytes(int n);
+int lowsvd_sgesvd(float* X32, int n, long long ldx, float* S, float* U, long long ldu, void* work, size_t work_bytes,
+                  cudaStream_t st);
+const char* lowsvd_last_error();
+
 // ---- misc (k_misc.cu) ----------------------------------------------------
 int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st);
 int copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows, long long cols,

@@ -42,7 +42,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -678,6 +678,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     QrWork qw;
     std::vector<double> xnorms;
     bool gates_read = false;   // X column norms to read back with the stats
+    const bool autop = o.path == MPJSVD_PATH_AUTO;
+    int taken = o.path == MPJSVD_PATH_FORCE_FP64 ? MPJSVD_TAKEN_FP64 : MPJSVD_TAKEN_JACOBI;
+    double cond_scaled = NAN, cond_d = NAN;
     if (root) {
     // ---- input -> padded device copy (host memory is staged here: e2e path)
     MPJ_CUDA_TRY(cudaMemsetAsync(dA, 0, sizeof(double) * (size_t)m_pad * n, st));
@@ -698,6 +701,11 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(copy_matrix(dA, m_pad, dA1, n_pad, n_pad, n, st));
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (autop) {
+        // column norms of A1 = D of A = B D (cond gate; reading c-15)
+        MPJ_TRY(ensure(h, S_A1N, sizeof(double) * n));
+        MPJ_TRY(col_norms<double>(dA1, n_pad, n_pad, (int)n, P<double>(h, S_A1N), 1, st));
+    }
     // ---- stage 1: column-pivoted QR  A1 P = Q_p R
     MPJ_TRY(ensure_qr_work(h, (int)n, (int)n, qw));
     if (o.mp_rrqr) {
@@ -745,7 +753,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[3], st));
     // ---- stage 3: gate measures, report only
-    if (o.compute_gates) {
+    if (o.compute_gates || autop) {
         PROF_B("gates_orth");
         MPJ_TRY(ensure(h, S_XNORM, sizeof(double) * n));
         MPJ_TRY(gates_orth(dX, n_pad, n_pad, (int)n, dX32, n_pad, scal + 3, st));
@@ -753,7 +761,50 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(col_norms<double>(dX, n_pad, n_pad, (int)n, P<double>(h, S_XNORM), 1, st));
         gates_read = true;
     }
+    if (autop) {
+        // Alg. 3 gates in order (reading c-15): cond, tail (654-663), orth
+        // (428-433, 636-650), then Jacobi if orth <= tol_alg else the fp32 QR SVD (435-445)
+        std::vector<double> rdiag(n), a1n(n), xn(n);
+        std::vector<int> pv(n);
+        double horth = 0.0;
+        MPJ_CUDA_TRY(cudaMemcpy2DAsync(rdiag.data(), sizeof(double), dA1L, sizeof(double) * (n_pad + 1), sizeof(double), n,
+                                       cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(a1n.data(), P<double>(h, S_A1N), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(xn.data(), P<double>(h, S_XNORM), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(pv.data(), P<int>(h, S_PERM), sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(&horth, scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        double rmx = 0.0, rmn = INFINITY, dmx = 0.0, dmn = INFINITY, xmx = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+            const double cn = a1n[pv[k]];
+            const double rk = cn > 0.0 ? fabs(rdiag[k]) / cn : 0.0;
+            rmx = rk > rmx ? rk : rmx;
+            rmn = rk < rmn ? rk : rmn;
+            dmx = cn > dmx ? cn : dmx;
+            dmn = cn < dmn ? cn : dmn;
+            xmx = xn[k] > xmx ? xn[k] : xmx;
+        }
+        cond_scaled = rmn > 0.0 ? rmx / rmn : INFINITY;
+        cond_d = dmn > 0.0 ? dmx / dmn : INFINITY;
+        long long small = 0;
+        for (int64_t j = 0; j < n; ++j) small += xn[j] < ldexp(xmx, o.tail_cut_log2) ? 1 : 0;
+        const double tol_cond = o.tol_cond_mult * pow((double)n, 0.25);
+        if (cond_scaled <= tol_cond && cond_d > o.cond_d_min) taken = MPJSVD_TAKEN_SKIP_COND;
+        else if ((double)small >= ceil(o.tail_frac * (double)n)) taken = MPJSVD_TAKEN_SKIP_TAIL;
+        else if (horth <= o.tol_orth) taken = MPJSVD_TAKEN_SKIP_ORTH;
+        else if (horth <= o.tol_alg) taken = MPJSVD_TAKEN_JACOBI;
+        else taken = MPJSVD_TAKEN_QRSVD;
+    }
     }  // root
+    if (autop && dist) {
+        // every rank takes root's branch
+        h_hdr[0] = taken;
+        MPJ_CUDA_TRY(cudaMemcpyAsync(d_hdr, h_hdr, sizeof(long long), cudaMemcpyHostToDevice, st));
+        MPJ_TRY(h->comm.bcast(d_hdr, sizeof(long long), 0, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr, d_hdr, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+        taken = (int)h_hdr[0];
+    }
     MPJ_CUDA_TRY(cudaEventRecord(ev[4], st));
     {
         const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
@@ -761,7 +812,46 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     // ---- stage 4: fp32 block Jacobi
     JacobiResult r32, r64;
-    if (o.path != MPJSVD_PATH_FORCE_FP64) {
+    if (taken == MPJSVD_TAKEN_QRSVD) {
+        // fp32 QR SVD of lower(X), U only (lowsvd.cpp), then the U-route switch
+        // Q R2 = X^T working(U_low) (446-447) and Y = X Q; non-root ranks wait for Y and Q
+        if (root) {
+            MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
+            MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
+            const size_t wb = lowsvd_work_bytes((int)n);
+            if (wb == 0) {
+                snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "fp32 QR SVD branch: %s", lowsvd_last_error());
+                return MPJSVD_ERR_NOT_SUPPORTED;
+            }
+            MPJ_TRY(ensure(h, S_U32, sizeof(float) * nn));
+            MPJ_TRY(ensure(h, S_S32, sizeof(float) * (size_t)n_pad));
+            MPJ_TRY(ensure(h, S_SVDWS, wb));
+            MPJ_TRY(ensure(h, S_IOTA, sizeof(int) * (size_t)n));
+            float* dU32 = P<float>(h, S_U32);
+            MPJ_CUDA_TRY(cudaMemsetAsync(dU32, 0, sizeof(float) * nn, st));
+            PROF_B("qrsvd32");
+            const int lrc = lowsvd_sgesvd(dX32, (int)n, n_pad, P<float>(h, S_S32), dU32, n_pad, P<void>(h, S_SVDWS), wb, st);
+            PROF_E("qrsvd32");
+            if (lrc) {
+                snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "fp32 QR SVD branch: %s", lowsvd_last_error());
+                return lrc == -7 ? MPJSVD_ERR_NOT_SUPPORTED : MPJSVD_ERR_CUDA;
+            }
+            std::vector<int> iota(n);
+            for (int i = 0; i < (int)n; ++i) iota[i] = i;
+            MPJ_CUDA_TRY(cudaMemcpyAsync(P<int>(h, S_IOTA), iota.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+            MPJ_TRY(sort_upcast_v(dU32, n_pad, P<int>(h, S_IOTA), dUX, n_pad, n_pad, (int)n, st));   // U_low, fp64
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+            PROF_B("switch_u");
+            MPJ_TRY(switch_u_inplace(h, dX, dUX, dVX, dQ, n_pad, (int)n, o.x_from_lq != 0, qw, st));
+            PROF_E("switch_u");
+            PROF_B("rv_gemm");
+            MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
+            PROF_E("rv_gemm");
+        } else {
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+        }
+        s.path_taken = MPJSVD_TAKEN_QRSVD;
+    } else if (taken == MPJSVD_TAKEN_JACOBI) {
         if (root) {
             MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
             MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
@@ -808,14 +898,15 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         } else {
             MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
         }
-        s.path_taken = MPJSVD_PATH_FORCE_MIXED;
+        s.path_taken = MPJSVD_TAKEN_JACOBI;
     } else {
+        // fp64 only: forced, or an AUTO gate fired (Q = I, Y = X)
         MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
         if (root) {
             MPJ_TRY(set_identity<double>(dQ, n_pad, n_pad, n, st));
             MPJ_TRY(copy_matrix(dX, n_pad, dY, n_pad, n_pad, n, st));
         }
-        s.path_taken = MPJSVD_PATH_FORCE_FP64;
+        s.path_taken = taken;
     }
     {
         const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
@@ -924,14 +1015,16 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
 
     fill_sweep_stats();
     s.cond_estimate = hscal[2] > 0 ? hscal[1] / hscal[2] : INFINITY;
-    s.orth_measure = o.compute_gates ? hscal[3] : NAN;
+    s.orth_measure = (o.compute_gates || autop) ? hscal[3] : NAN;
+    s.cond_scaled = cond_scaled;
+    s.cond_d = cond_d;
     s.tail_fraction = NAN;
-    if (o.compute_gates) {
-        // fraction of "small" columns of X: ||x_j|| < 2^-60 max_j ||x_j|| (reading c-15)
+    if (o.compute_gates || autop) {
+        // fraction of "small" columns of X: ||x_j|| < 2^tail_cut_log2 max_j ||x_j|| (reading c-15)
         double mx = 0.0;
         for (double v : xnorms) mx = v > mx ? v : mx;
         long long small = 0;
-        for (double v : xnorms) small += v < ldexp(mx, -60) ? 1 : 0;
+        for (double v : xnorms) small += v < ldexp(mx, o.tail_cut_log2) ? 1 : 0;
         s.tail_fraction = (double)small / (double)n;
     }
     s.stage_ms[0] = elapsed(ev[0], ev[1]);
@@ -1031,6 +1124,12 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->mp_rrqr = 0;
     o->max_inner32 = 1;
     o->switch_u = 1;
+    o->tol_orth = 1e-5;
+    o->tol_alg = INFINITY;
+    o->tol_cond_mult = 1.0;
+    o->cond_d_min = 1e15;
+    o->tail_frac = 1.0 / 3.0;
+    o->tail_cut_log2 = -60;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1042,7 +1141,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (o.virtual_shards < 1 || o.virtual_shards > 64 || o.split_rows < 0) return MPJSVD_ERR_INVALID_ARG;
     if (o.block_cols != 8 && o.block_cols != 16 && o.block_cols != 32) return MPJSVD_ERR_NOT_SUPPORTED;
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
-        o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 2))
+        o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

@@ -406,3 +406,25 @@ def test_skip_unchanged_pairs_is_exact(mp, monkeypatch, name, n, extra):
     assert sum(s0["skip_trace32"]) == 0 and sum(s0["skip_trace64"]) == 0
     # the final check sweep follows a sweep with few rotations: some pairs are skipped
     assert sum(s1["skip_trace32"]) + sum(s1["skip_trace64"]) > 0
+
+
+@pytest.mark.parametrize("case", ["cond", "tail", "orth", "jacobi", "qrsvd"])
+def test_auto_path_vs_oracle(mp, case):
+    """AUTO (reading c-15): the GPU takes the oracle's branch on inputs built
+    to trigger each gate (tests/test_oracle_pins.py auto_cases) and matches its sigma; the fp32 QR-SVD
+    branch (cuSOLVER sgesvd on the GPU, LAPACK sgesvd in the oracle) only seeds the fp64 refinement."""
+    import test_oracle_pins as pins
+    a, kw, taken, sig = pins.auto_cases()[case]
+    U, S, V, st = mp.factor(dev(a), path=1, **kw)
+    U, S, V = host(U), host(S), host(V)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, path=1, **kw)
+    assert rc == 0 and st["rc"] == 0
+    assert st["path_taken"] == sto["path_taken"] == taken, (st["path_taken"], sto["path_taken"], taken)
+    check_svd(a, U, S, V)
+    kap = kappa_s(a)
+    assert np.all(np.abs(S - so) / so <= tiered(so, kap))
+    if sig is not None:
+        assert np.max(np.abs(S - sig) / sig) <= 1e-13
+    assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
+    np.testing.assert_allclose(st["cond_scaled"], sto["cond_scaled"], rtol=1e-6)
+    np.testing.assert_allclose(st["cond_d"], sto["cond_d"], rtol=1e-12)

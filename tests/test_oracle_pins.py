@@ -493,3 +493,58 @@ def test_planted_sigma_construction_bound(name):
     s = oracle.mixed_svd(a)[1]
     planted = testmat.planted_sigma(name, n)
     assert np.abs(s - planted).max() <= 8 * np.sqrt(n) * U * planted[0]
+
+
+# ---------------------------------------------------------------- AUTO gates
+def auto_cases(n=64):
+    """Inputs that trigger each branch of the AUTO path (reading c-15)."""
+    rng = np.random.default_rng(21)
+    q = testmat.haar(n, n, 2101)
+    cases = {}
+    # cond gate: orthogonal columns (scaled cond(R) = 1) with norms spanning 1e20 (cond(D) > 1e15)
+    d = 10.0 ** np.linspace(0, 20, n)
+    cases["cond"] = (np.asfortranarray(q * d), {}, 3, np.sort(d)[::-1])
+    # tail gate: half of the columns scaled by 2^-70 (below 2^-60 max after preconditioning)
+    b = rng.standard_normal((n, n))
+    cases["tail"] = (np.asfortranarray(b * np.where(np.arange(n) < n // 2, 1.0, 2.0 ** -70)), {}, 4, None)
+    # orth gate: orthogonal columns, mild grading (cond(D) = 1e3 < 1e15): X is diagonal after QRP + LQ
+    d2 = 10.0 ** np.linspace(0, 3, n)
+    cases["orth"] = (np.asfortranarray(q * d2), {}, 5, np.sort(d2)[::-1])
+    # Jacobi (orth > tol_orth, tol_alg = inf) and the QR SVD branch (orth > tol_alg = 1e-3)
+    c1 = testmat.config_matrix("C1", n)
+    cases["jacobi"] = (c1, {}, 0, None)
+    cases["qrsvd"] = (c1, {"tol_alg": 1e-3}, 6, None)
+    return cases
+
+
+@pytest.mark.parametrize("case", ["cond", "tail", "orth", "jacobi", "qrsvd"])
+def test_auto_gates_take_the_papers_branch(case):
+    """Alg. 3's gates in order (cond, tail, orth, then Jacobi vs QR SVD by tol_alg): each input takes its
+    branch, the result is a valid SVD, and where sigma is known exactly (columns orthogonal: sigma = column
+    norms) it is reached to high relative accuracy."""
+    a, kw, taken, sig = auto_cases()[case]
+    n = a.shape[1]
+    u, s, v, st, rc = oracle.mixed_svd(a, path=1, **kw)
+    assert rc == 0 and st["path_taken"] == taken, (st["path_taken"], taken)
+    assert orth(u) <= 1e-13 and orth(v) <= 1e-13
+    assert np.linalg.norm(a - (u * s) @ v.T) / np.linalg.norm(a) <= 1e-13
+    if sig is not None:
+        assert np.max(np.abs(s - sig) / sig) <= 1e-13
+    else:
+        # third opinion: LAPACK dgejsv (high relative accuracy on column-graded inputs, F6)
+        sj = _dgejsv_sigma(a)
+        kap = np.linalg.cond(a / np.linalg.norm(a, axis=0))
+        assert np.all(np.abs(s - sj) / sj <= tiered_tol(sj, kap))
+    if taken in (3, 4, 5):
+        assert st["sweeps32"] == 0
+    assert st["sweeps64"] <= GOLD["refinement_sweeps"]["max_with_slack"] or taken in (3, 4, 5)
+
+
+def test_auto_qrsvd_branch_matches_jacobi_branch_sigma():
+    """Both low-precision solvers only seed the fp64 refinement: the final sigma of
+    the QR-SVD branch equals the Jacobi branch's to the refinement's accuracy."""
+    a = testmat.config_matrix("C2", 128)
+    s_j = oracle.mixed_svd(a, path=1)[1]
+    _, s_q, _, st, rc = oracle.mixed_svd(a, path=1, tol_alg=1e-3)
+    assert rc == 0 and st["path_taken"] == 6
+    assert np.max(np.abs(s_q - s_j) / s_j) <= 1e-12
