@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     T* dsm2 = ykp + nown;                      // 2 nown: per-half partial dots
     int* pcol = reinterpret_cast<int*>(dsm2 + 2 * nown); // QP_NB
     int* rflag = pcol + QP_NB;                      // nown: recompute flags
-    int* lpos = rflag + nown;                       // nown: logical position of owned column s
-    int* phys = lpos + nown;                        // n: column at logical position (this CTA's copy)
+    int* own = rflag + nown;                        // nown: physical column of owned slot s (-1: none); the
+                                                    // live columns are re-dealt round-robin at every panel end
+    int* phys = own + nown;                         // n: column at logical position (this CTA's copy)
     int* pos = phys + n;                            // n: logical position of physical column
     __shared__ int s_anyrec, s_piv;
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -154,9 +155,11 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     for (int e = tid; e < nown * QP_NB; e += QP_NT) Fown[e] = 0.0;
     for (int sl = tid; sl < nown; sl += QP_NT) {
         const int p = cta + G * sl;
-        lpos[sl] = p < n ? p : -1;                   // -1: no column in this slot
+        own[sl] = p < n ? p : -1;                    // -1: no column in this slot
         rflag[sl] = 0;
     }
+    // logical position of the column in owned slot sl (-1: empty slot)
+    auto lp = [&](int sl) -> int { return own[sl] >= 0 ? pos[own[sl]] : -1; };
     T best = -1.0;
     int best_pos = 0x7fffffff, best_col = -1;
     for (int p = cta, s = 0; p < n; p += G, ++s) {
@@ -222,8 +225,6 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 phys[k] = pv; phys[pj] = pk;
                 pos[pv] = k; pos[pk] = pj;
                 pcol[jj] = pv;
-                if (pk % G == cta) lpos[pk / G] = pj;
-                if (pv % G == cta) lpos[pv / G] = k;
             }
         }
         __syncthreads();
@@ -359,8 +360,8 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             const bool rev = (k & 1) != 0;
             for (int it = wid; it < 2 * nown; it += QP_NT / 32) {
                 const int sl = rev ? nown - 1 - (it >> 1) : (it >> 1), h = it & 1;
-                if (lpos[sl] <= k) continue;
-                const T* col = a.A + (long long)(cta + G * sl) * lda;
+                if (lp(sl) <= k) continue;
+                const T* col = a.A + (long long)own[sl] * lda;
                 const long long rb = k + h * L, re = min((long long)m, rb + L);
                 T acc0 = 0.0, acc1 = 0.0;
                 long long i = rb + lane;
@@ -387,8 +388,8 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         T cbest = -1.0;
         int cpos = 0x7fffffff, ccol = -1;
         for (int sl = tid; sl < nown; sl += QP_NT) {
-            if (lpos[sl] <= k) continue;
-            const int p = cta + G * sl;
+            if (lp(sl) <= k) continue;
+            const int p = own[sl];
             T* Fs = Fown + (size_t)sl * QP_NB;
             T f = tau * dsm[sl];
             for (int t = 0; t < jj; ++t) f += Fs[t] * auxv[t];
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         const bool anyrec = s_anyrec != 0;
         for (int sl = 0; anyrec && sl < nown; ++sl) {
             if (!rflag[sl]) continue;                  // flags are only set for live columns
-            const int p = cta + G * sl;
+            const int p = own[sl];
             T* col = a.A + (long long)p * lda;
             const T* Fs = Fown + (size_t)sl * QP_NB;
             T sq[1] = {0.0};
@@ -465,8 +466,8 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                         bool lv[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            lv[u] = (s0 + u < nown) && lpos[s0 + u] > k;
-                            yv[u] = lv[u] ? __ldcg(a.A + (long long)(cta + G * (s0 + u)) * lda + i) : 0.0;
+                            lv[u] = (s0 + u < nown) && lp(s0 + u) > k;
+                            yv[u] = lv[u] ? __ldcg(a.A + (long long)own[s0 + u] * lda + i) : 0.0;
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
 #pragma unroll
                             for (int t = 0; t < QP_NB; ++t)
                                 if (t <= jj) yv[u] -= vt[t] * Fs[t];
-                            a.A[(long long)(cta + G * (s0 + u)) * lda + i] = yv[u];
+                            a.A[(long long)own[s0 + u] * lda + i] = yv[u];
                         }
                     }
                 }
@@ -484,17 +485,32 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             for (int e = tid; e < nown * QP_NB; e += QP_NT) {
                 const int sl = e / QP_NB;
                 Fown[e] = 0.0;
-                if (cta + G * sl < n) a.F[(long long)(cta + G * sl) * QP_NB + (e % QP_NB)] = 0.0;
+                if (own[sl] >= 0) a.F[(long long)own[sl] * QP_NB + (e % QP_NB)] = 0.0;
+            }
+            if (k + 1 < n) {
+                // re-deal the live columns round-robin in logical order (CTA imbalance grows as pivots
+                // leave unevenly); no panel state is pending, only the partial norms move (via global memory)
+                for (int sl = tid; sl < nown; sl += QP_NT)
+                    if (lp(sl) > k) { a.w.vn1[own[sl]] = (double)vn1s[sl]; a.w.vn2[own[sl]] = (double)vn2s[sl]; }
+                grid.sync();
+                for (int sl = tid; sl < nown; sl += QP_NT) {
+                    const long long j = (long long)k + 1 + cta + (long long)G * sl;
+                    const int p = j < n ? phys[j] : -1;
+                    own[sl] = p;
+                    if (p >= 0) { vn1s[sl] = (T)__ldcg(a.w.vn1 + p); vn2s[sl] = (T)__ldcg(a.w.vn2 + p); }
+                    rflag[sl] = 0;
+                }
+                __syncthreads();
             }
         }
         tmark(5);
         // ---------------- candidate for the next step (argmax over the owned columns): warp 0
         if (tid < 32) {
             for (int sl = tid; sl < nown; sl += 32) {
-                if (lpos[sl] <= k) continue;
+                const int ps = lp(sl);
+                if (ps <= k) continue;
                 const T v1 = vn1s[sl];
-                const int ps = lpos[sl];
-                if (v1 > cbest || (v1 == cbest && ps < cpos)) { cbest = v1; cpos = ps; ccol = cta + G * sl; }
+                if (v1 > cbest || (v1 == cbest && ps < cpos)) { cbest = v1; cpos = ps; ccol = own[sl]; }
             }
             warp_argmax(cbest, cpos, ccol);
             if (tid == 0) {
