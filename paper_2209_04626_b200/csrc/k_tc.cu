@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 #include "common.cuh"
 #include "jacobi.h"
 
@@ -619,7 +620,21 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc(JacobiRound<float> 
 // ------------------------------------------------------------------------
 constexpr int UT_TPC = 16;
 
-__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<float> a, int ngroups, int tpc) {
+__device__ __forceinline__ void tma_load_2d(uint32_t sdst, const CUtensorMap* map, int c0, int c1, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(sdst), "l"(map), "r"(c0), "r"(c1), "r"(tc::smem_u32(mbar))
+        : "memory");
+}
+
+
+
+// TMA = true (U-route, X only): the raw tiles arrive by TMA (two 2-D boxes of 128 rows x 32 columns per tile,
+// mbarrier complete_tx, ring slots tracked by a per-CTA running tile count) instead of 2048 16-byte cp.async
+// per tile; columns / rows past the matrix are zero-filled (a bye block is addressed past the last column)
+template <bool TMA>
+__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<float> a, int ngroups, int tpc,
+                                                                  const __grid_constant__ CUtensorMap umap) {
     extern __shared__ __align__(1024) unsigned char ut_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ut_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char* Bh = sm;
@@ -628,6 +643,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
     unsigned char* Al = sm + 65536;
     float* ring = reinterpret_cast<float*>(sm + 98304);
     __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ __align__(8) uint64_t rfull[UT_NR];
     __shared__ uint32_t tmem_base;
     __shared__ float* colp[64];
     __shared__ int item[3];                     // pair, which, group (pair < 0: stop)
@@ -637,6 +653,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
     if (tid == 0) {
         tc::mbar_init(&mbar[0]);
         tc::mbar_init(&mbar[1]);
+        for (int q = 0; q < UT_NR; ++q) tc::mbar_init(&rfull[q]);
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     tc::fence_before();
@@ -649,6 +666,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
     const uint32_t rbase = tc::smem_u32(ring);
     const long long total = (long long)a.npairs * 2 * ngroups;
     uint32_t ph[2] = {0u, 0u};                  // completed waits per accumulator barrier
+    long long gt0 = 0;                          // TMA: raw tiles of the previous items (ring slot / parity)
     while (true) {
         if (tid == 0) {
             int pair = -1, which = 0, grp = 0;
@@ -688,7 +706,21 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
         float* const s1 = which ? pd.v1 : pd.x1;
         if (tid < 64) colp[tid] = tid < w ? (tid < pd.w0 ? s0 + (long long)tid * ld : s1 + (long long)(tid - pd.w0) * ld) : nullptr;
         __syncthreads();
+        const int cI = TMA ? (int)((pd.x0 - a.tbase) / a.tld) : 0;
+        const int cJ = TMA ? (pd.w1 > 0 ? (int)((pd.x1 - a.tbase) / a.tld) : (1 << 30)) : 0;
         auto issue = [&](int t) {
+            if constexpr (TMA) {
+                if (tid == 0) {
+                    const int slot = (int)((gt0 + t) % UT_NR);
+                    const int r0 = (int)(row_lo + (long long)t * UT_TM);
+                    const uint32_t dst = rbase + (uint32_t)((size_t)slot * (UT_TM * 64) * 4);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic reads of the slot done
+                    mbar_expect_tx(&rfull[slot], (uint32_t)UT_RAW_BYTES);
+                    tma_load_2d(dst, &umap, r0, cI, &rfull[slot]);
+                    tma_load_2d(dst + 32 * UT_TM * 4, &umap, r0, cJ, &rfull[slot]);
+                }
+                return;
+            }
             const int slot = t % UT_NR;
             const long long r0 = row_lo + (long long)t * UT_TM;
 #pragma unroll
@@ -704,7 +736,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
 #pragma unroll
         for (int t = 0; t < UT_NR - 1; ++t) {
             if (t < ntile) issue(t);
-            cp_commit();
+            if constexpr (!TMA) cp_commit();
         }
         const float* Eg = a.E + (long long)pair * (64 * 64);
         for (int it = tid; it < 64 * 16; it += UT_NT) {
@@ -736,12 +768,16 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
         };
         for (int t = 0; t < ntile; ++t) {
             const int b = t & 1;
-            cp_wait<UT_NR - 2>();
-            tc::fence_before();
-            __syncthreads();
+            if constexpr (TMA) {
+                tc::mbar_wait(&rfull[(gt0 + t) % UT_NR], (uint32_t)(((gt0 + t) / UT_NR) & 1));
+            } else {
+                cp_wait<UT_NR - 2>();
+                tc::fence_before();
+                __syncthreads();
+            }
             if (t >= 1) { tc::mbar_wait(&mbar[b ^ 1], ph[b ^ 1] & 1u); ++ph[b ^ 1]; }
             tc::fence_after();
-            const float* raw = ring + (size_t)(t % UT_NR) * (UT_TM * 64);
+            const float* raw = ring + (size_t)(TMA ? (gt0 + t) % UT_NR : t % UT_NR) * (UT_TM * 64);
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
                 float wv[16];
@@ -762,7 +798,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
             tc::fence_before();
             __syncthreads();
             if (t + UT_NR - 1 < ntile) issue(t + UT_NR - 1);
-            cp_commit();
+            if constexpr (!TMA) cp_commit();
             if (tid == 0) {
                 tc::fence_after();
                 const uint32_t ah = tc::smem_u32(Ah), al = tc::smem_u32(Al), bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
@@ -790,6 +826,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
         }
         tc::fence_before();
         __syncthreads();                        // item done: smem, TMEM free for the next item
+        gt0 += ntile;
     }
     if (warp == 0) tc::tmem_free<128>(tmem);
 }
@@ -819,6 +856,31 @@ static const GramVariant& gram_variant() {
         if (v < 0 || v >= (int)(sizeof(g_gram_variants) / sizeof(g_gram_variants[0]))) v = 0;
     }
     return g_gram_variants[v];
+}
+
+int make_update_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    }
+    if (!fn || ld % 4 != 0) return -1;
+    const cuuint64_t gdim[2] = {(cuuint64_t)rows_pad, (cuuint64_t)cols};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {UT_TM, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
+                          gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
@@ -887,7 +949,8 @@ namespace mpj {
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_pair_update_tc_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
+        cudaFuncSetAttribute(k_pair_update_tc_pdl<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
+        cudaFuncSetAttribute(k_pair_update_tc_pdl<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
         attr = true;
     }
     int dev = 0, nsm = 148;
@@ -917,7 +980,13 @@ int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     attr1[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr1;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl, a, ngroups, tpc);
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof(dummy));
+    cudaError_t e;
+    if (a.umap && !a.has_v)
+        e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl<true>, a, ngroups, tpc, *reinterpret_cast<const CUtensorMap*>(a.umap));
+    else
+        e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl<false>, a, ngroups, tpc, dummy);
     MPJ_LAUNCHED();
     if (e != cudaSuccess) {
         mpj_record_cuda_error(e, "cudaLaunchKernelEx(update pdl)", __FILE__, __LINE__);

@@ -304,7 +304,9 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     // TMA-fed fp32 Gram: one tensor map over the matrix holding every local slab (the matrix itself on
     // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
     alignas(64) static thread_local unsigned char tmap_buf[128];
+    alignas(64) static thread_local unsigned char umap_buf[128];
     a.tmap = nullptr;
+    a.umap = nullptr;
     a.tbase = nullptr;
     a.tld = 0;
     if constexpr (sizeof(T) == 4) {
@@ -318,10 +320,13 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             for (int g = 0; g < S.plan.G; ++g) nlocal_ += S.local(g) ? 1 : 0;
             // contiguous store: the n columns of X; shard store: nlocal * nbuf slabs of b columns
             cols = S.plan.G == 1 && S.me < 0 && S.slab_x == (long long)b * ldx ? n : (long long)nlocal_ * S.plan.nbuf * b;
-            if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols) == 0) {
-                a.tmap = tmap_buf;
+            if (base) {
                 a.tbase = base;
                 a.tld = ldx;
+            }
+            if (base && !has_v && make_update_tmap(umap_buf, base, ldx, m_pad, cols) == 0) a.umap = umap_buf;
+            if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols) == 0) {
+                a.tmap = tmap_buf;
                 // a TMA box covers 64 rows and only zero-fills past the matrix: row slabs must be whole boxes
                 a.rows_per_split = round_up(a.rows_per_split, 64LL);
                 a.nsplit = (int)ceil_div(m_pad, a.rows_per_split);
