@@ -429,6 +429,9 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 if (cb >= 0) { ka = cb & 255; kb = cb >> 8; }
             }
             if (ka >= 0) g_block(ka, kb);
+            // release the other G and E warps (barrier 2), then the rotation warp (barrier 1): the critical
+            // blocks get the shared-memory pipe to themselves
+            asm volatile("bar.arrive 2, %0;\n" ::"r"(pwarp0) : "memory");
             asm volatile("bar.sync 1, %0;\n" ::"r"(INNER_CRIT + 32) : "memory");
         } else if (tid >= pwarp0) {
             asm volatile("bar.sync 1, %0;\n" ::"r"(INNER_CRIT + 32) : "memory");
@@ -441,9 +444,11 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 const int act = set_rotation<T, W>(sm, buf ^ 1, lane, y, w, gxx, gyy, gxy, tol_in);
                 if (last) f_next |= act; else f_cur |= act;
             }
-        } else if (kA >= 0) {
+        } else {
+          asm volatile("bar.sync 2, %0;\n" ::"r"(pwarp0) : "memory");
+          if (kA >= 0) {
             if (kA != kB && !((sm.cmask[r][myblk >> 5] >> (myblk & 31)) & 1u)) g_block(kA, kB);
-        } else if (kE >= 0) {
+          } else if (kE >= 0) {
             const Rot4<T> R4 = sm.rot[buf][kE];
             if (R4.act != T(0)) {
                 const unsigned pq = sm.spq[r][kE];
@@ -492,7 +497,26 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 }
             }
         }
-        if (dbg && tid == 0) dbg[4] += 1;
+        }
+        if (dbg) {
+            // per-warp end clocks of this round's work: [0] critical warps 0-1, [1] rotation warp,
+            // [2] slowest other G warp, [3] slowest E warp (all from the round start)
+            __syncwarp();
+            if (lane == 0) sm.dbg_t[0][tid >> 5] = clock64();
+            __syncthreads();
+            if (tid == 0) {
+                long long mc = 0, mr = 0, mg = 0, me = 0;
+                const int nw = nt >> 5, gw0 = INNER_CRIT >> 5, gw1 = (INNER_CRIT + NG) >> 5;
+                for (int q = 0; q < nw; ++q) {
+                    const long long v = sm.dbg_t[0][q] - t_start;
+                    if (q < gw0) mc = max(mc, v);
+                    else if (q == nw - 1) mr = v;
+                    else if (q < gw1) mg = max(mg, v);
+                    else me = max(me, v);
+                }
+                dbg[0] += mc; dbg[1] += mr; dbg[2] += mg; dbg[3] += me; dbg[4] += 1;
+            }
+        }
         if (last) {
             const int any = __syncthreads_or(f_cur);
             f_cur = f_next;
@@ -1506,7 +1530,7 @@ static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, 
         else cudaMemcpyToSymbolAsync(g_inner_dbg_d, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
         cudaStreamSynchronize(st);
         const double rounds = hv[4] > 0 ? (double)hv[4] : 1.0;
-        fprintf(stderr, "[inner timing %s w=%d] rounds=%lld per round (cycles): phaseA=%.0f barrier1=%.0f rotation=%.0f E=%.0f\n",
+        fprintf(stderr, "[inner timing %s w=%d] rounds=%lld per round (cycles from round start): critical=%.0f rotation=%.0f G=%.0f E=%.0f\n",
                 sizeof(T) == 4 ? "f32" : "f64", w, hv[4], hv[0] / rounds, hv[1] / rounds, hv[2] / rounds, hv[3] / rounds);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -4;
