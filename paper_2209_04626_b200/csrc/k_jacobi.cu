@@ -445,7 +445,9 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
                 if (last) f_next |= act; else f_cur |= act;
             }
         } else {
-          asm volatile("bar.sync 2, %0;\n" ::"r"(pwarp0) : "memory");
+          // G warps wait for the critical blocks; the E warps (which do not touch G) also arrive, and start at once
+          if (tid < INNER_CRIT + NG) asm volatile("bar.sync 2, %0;\n" ::"r"(pwarp0) : "memory");
+          else asm volatile("bar.arrive 2, %0;\n" ::"r"(pwarp0) : "memory");
           if (kA >= 0) {
             if (kA != kB && !((sm.cmask[r][myblk >> 5] >> (myblk & 31)) & 1u)) g_block(kA, kB);
           } else if (kE >= 0) {
