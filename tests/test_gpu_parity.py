@@ -428,3 +428,27 @@ def test_auto_path_vs_oracle(mp, case):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
     np.testing.assert_allclose(st["cond_scaled"], sto["cond_scaled"], rtol=1e-6)
     np.testing.assert_allclose(st["cond_d"], sto["cond_d"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("opts,oopts", [
+    ({"fp32_tensor_cores": 0}, {}),
+    ({"pdl_overlap": 0}, {}),
+    ({"pdl_overlap": 0, "switch_u": 0}, {"switch_u": 0}),
+    ({"block_cols": 16}, {"b": 16}),
+    ({"x_from_lq": 0}, {"x_from_lq": 0}),
+    ({"max_inner32": 2}, {"max_inner32": 2}),
+])
+def test_option_paths_vs_oracle(mp, opts, oopts):
+    """Non-default implementation paths (FFMA fp32 stage, serial solve/update, V-route without overlap,
+    b = 16 (SIMT kernels), X = R, two fp32 inner sweeps) against the oracle run with the same
+    algorithmic options: valid SVD, tiered sigma bound, sweeps +-1."""
+    a = testmat.config_matrix("C3", 384)
+    U, S, V, st = mp.factor(dev(a), **opts)
+    U, S, V = host(U), host(S), host(V)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, **oopts)
+    assert rc == 0 and st["rc"] == 0
+    check_svd(a, U, S, V)
+    assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+    assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
+    if not opts.get("x_from_lq", 1) == 0:
+        assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
