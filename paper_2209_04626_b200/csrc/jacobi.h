@@ -175,6 +175,9 @@ size_t apply_q_work_elems(long long m, long long ncols);
 // Q = H_0 ... H_{k-1} formed in place on C (m x m, the identity on entry), trailing blocks only.
 int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,
               double* work, cudaStream_t st, const double* tcache = nullptr, int ncached = 0);
+// T factors of all WY panels of a k-reflector factorisation into tcache (wy_tcache_elems(k))
+int wy_tfactors(const double* Vr, long long m, int k, long long ldv, const double* tau, double* tcache, double* work,
+                cudaStream_t st);
 // number of WY panels of a k-reflector factorisation whose T qr_blocked leaves in its cache (all but the last)
 inline int wy_cached_panels(int k) { return (k + 127) / 128 - 1; }
 inline size_t wy_tcache_elems(int k) { return (size_t)((k + 127) / 128) * 128 * 128; }

@@ -468,6 +468,7 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
         }
     }
     if (t_out) MPJ_CUDA_TRY(cudaMemcpyAsync(t_out, T, sizeof(double) * WY_NB * WY_NB, cudaMemcpyDeviceToDevice, st));
+    if (!C) return 0;                                   // T only (wy_tfactors)
 apply:
     // transposed products keep the long dimension (ncols) in the GEMM's M: W1^T = C^T Vp,
     // W2^T = W1^T T^(T) (T^T for trans), C -= Vp W2 = Vp (W2^T)^T
@@ -477,6 +478,21 @@ apply:
     if (rc) return rc;
     rc = gemm_f64(0, 1, rows, ncols, WY_NB, -1.0, Vp, ldw, W2, ncols, 1.0, C, ldc, st);
     return rc;
+}
+
+// T factors of every WY panel of Q = H_0 ... H_{k-1} (reflectors as left by qr_blocked / the QRP), for a later
+// apply_q_wy with tcache (all panels cached); work as for apply_q_wy with ncols = 0
+int wy_tfactors(const double* Vr, long long m, int k, long long ldv, const double* tau, double* tcache, double* work,
+                cudaStream_t st) {
+    const int npan = (k + WY_NB - 1) / WY_NB;
+    for (int pnl = 0; pnl < npan; ++pnl) {
+        const int j0 = pnl * WY_NB;
+        const int kb = k - j0 < WY_NB ? k - j0 : WY_NB;
+        int rc = apply_panel(Vr + j0 + (long long)j0 * ldv, ldv, m - j0, kb, tau + j0, nullptr, 1, 0, 0, work, st,
+                             nullptr, tcache + (size_t)pnl * WY_NB * WY_NB);
+        if (rc) return rc;
+    }
+    return 0;
 }
 
 int apply_q_wy(const double* Vr, long long m, int k, long long ldv, const double* tau, double* C, long long ldc,

@@ -109,7 +109,7 @@ struct mpjsvd_handle_s {
     size_t pinned_cap = 0;
     cudaEvent_t ev[10] = {};
     cudaStream_t aux = nullptr;    // second stream: independent assembly chains (fork/join by events)
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, tpdone = nullptr;
     Comm comm;                     // NCCL (multi-process sharding), inactive by default
 };
 
@@ -683,6 +683,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     QrWork qw;
     std::vector<double> xnorms;
     bool gates_read = false;   // X column norms to read back with the stats
+    bool tcp_all = false;      // T factors of every Q_p panel precomputed on the auxiliary stream
     const bool autop = o.path == MPJSVD_PATH_AUTO;
     int taken = o.path == MPJSVD_PATH_FORCE_FP64 ? MPJSVD_TAKEN_FP64 : MPJSVD_TAKEN_JACOBI;
     double cond_scaled = NAN, cond_d = NAN;
@@ -741,6 +742,18 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     PROF_E("qrp_coop");
     MPJ_TRY(gather_cols(dA1, n_pad, P<int>(h, S_PERM), dA1L, n_pad, n_pad, (int)n, st));
+    // T factors of Q_p for the assembly, on the auxiliary stream while the later stages run (own WY and
+    // split-K workspaces; each launch captures the workspace pointer set when it is issued)
+    MPJ_TRY(ensure(h, S_TC_P, sizeof(double) * wy_tcache_elems((int)n)));
+    MPJ_TRY(ensure(h, S_WY2, sizeof(double) * apply_q_work_elems(m_pad, n)));
+    MPJ_TRY(ensure(h, S_GEMMWS2, sizeof(double) * (size_t)8 * 64 * n_pad + sizeof(double) * 64 * 64 * 64));
+    MPJ_CUDA_TRY(cudaEventRecord(h->fork, st));
+    MPJ_CUDA_TRY(cudaStreamWaitEvent(h->aux, h->fork, 0));
+    gemm_set_workspace(P<double>(h, S_GEMMWS2), h->cap[S_GEMMWS2] / sizeof(double));
+    MPJ_TRY(wy_tfactors(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), P<double>(h, S_TC_P), P<double>(h, S_WY2), h->aux));
+    MPJ_CUDA_TRY(cudaEventRecord(h->tpdone, h->aux));
+    gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
+    tcp_all = true;
     }
     MPJ_TRY(diag_stats(dA1L, n_pad, (int)n, scal + 1, flags + 1, st));
     MPJ_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -979,8 +992,10 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_CUDA_TRY(cudaEventRecord(h->join, h->aux));
         gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
     }
+    if (tcp_all) MPJ_CUDA_TRY(cudaStreamWaitEvent(st, h->tpdone, 0));   // Q_p's T factors (aux stream)
     MPJ_TRY(apply_q_wy(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), dUX, n_pad, n, P<double>(h, S_WY), st,
-                       o.mp_rrqr ? P<double>(h, S_TC_P) : nullptr, o.mp_rrqr ? wy_cached_panels((int)n) : 0));
+                       (o.mp_rrqr || tcp_all) ? P<double>(h, S_TC_P) : nullptr,
+                       tcp_all ? (int)ceil_div(n, 128) : (o.mp_rrqr ? wy_cached_panels((int)n) : 0)));
     double* Ufin = dUX;
     long long ldUf = n_pad;
     if (m > n) {
@@ -1174,7 +1189,8 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     for (auto& e : h->ev) cudaEventCreate(&e);
     if (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->tpdone, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         mpjsvd_destroy(h);
         return MPJSVD_ERR_CUDA;
@@ -1203,6 +1219,7 @@ int mpjsvd_destroy(mpjsvd_handle h) {
     if (h->aux) { cudaStreamSynchronize(h->aux); cudaStreamDestroy(h->aux); }
     if (h->fork) cudaEventDestroy(h->fork);
     if (h->join) cudaEventDestroy(h->join);
+    if (h->tpdone) cudaEventDestroy(h->tpdone);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     cudaGetLastError();
