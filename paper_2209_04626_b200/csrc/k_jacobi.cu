@@ -581,13 +581,29 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
     }
     // fixed-order reduction over row slabs (deterministic)
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
-    for (int e = tid; e < W * W; e += nt) {
-        const int p = e / W, q = e - (e / W) * W;
-        if (p < w && q < w && p >= q) {      // partials hold (at least) the lower triangle
-            T s = T(0);
-            for (int sp = 0; sp < a.nsplit; ++sp) s += part[(long long)sp * (W * W) + p * W + q];
-            sm.G[p * GS + q] = s;
-            sm.G[q * GS + p] = s;
+    {
+        // each thread owns up to RE elements; the split loop is outermost so that the RE loads of one split
+        // are in flight together (same summation order per element: split 0, 1, ...)
+        constexpr int RE = (W * W + inner_nt<W>() - 1) / inner_nt<W>();
+        T acc[RE];
+#pragma unroll
+        for (int u = 0; u < RE; ++u) acc[u] = T(0);
+        for (int sp = 0; sp < a.nsplit; ++sp) {
+            const T* ps = part + (long long)sp * (W * W);
+#pragma unroll
+            for (int u = 0; u < RE; ++u) {
+                const int e = tid + u * nt;
+                if (e < W * W) acc[u] += __ldcg(ps + e);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RE; ++u) {
+            const int e = tid + u * nt;
+            const int p = e / W, q = e - (e / W) * W;
+            if (e < W * W && p < w && q < w && p >= q) {      // partials hold (at least) the lower triangle
+                sm.G[p * GS + q] = acc[u];
+                sm.G[q * GS + p] = acc[u];
+            }
         }
     }
     __syncthreads();
