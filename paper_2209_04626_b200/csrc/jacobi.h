@@ -101,7 +101,7 @@ struct ProfHook {
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook = nullptr);
 template <typename T>
-int gram_ctas_per_sm(int W, int use_tc);
+int gram_ctas_per_sm(int W, int use_tc, long long rows_pad);
 // tcgen05 fp32 kernels (k_tc.cu)
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
 // MPJSVD_SOLVE_TIMING=1: print k_pair_solve phase clocks (CTA 0) accumulated over a sweep (tools only)
@@ -109,11 +109,12 @@ void solve_timing_report(const char* tag, int sweep);
 // 4-D TMA view of the column-major fp32 matrix (rows_pad x cols, ld) whose boxes land in the canonical
 // K-major SWIZZLE_NONE operand layout of k_pair_gram_tma; out = 128-byte CUtensorMap.  0 on success.
 int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
+int gram_tma_kt(long long rows_pad);
 int make_update_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);
 // persistent overlapped variant: drains pairs in the order the solve publishes them (a.pdl)
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st);
-int gram_tc_ctas_per_sm();
+int gram_tc_ctas_per_sm(long long rows_pad);
 template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
 

@@ -1458,7 +1458,7 @@ solve:
 
 // resident CTAs per SM of the Gram kernel used for (T, W) (for the split choice)
 template <typename T>
-int gram_ctas_per_sm(int W, int use_tc) {
+int gram_ctas_per_sm(int W, int use_tc, long long rows_pad) {
     int per = 1;
     if constexpr (sizeof(T) == 8) {
         const size_t smem = gram_dmma_smem(W);
@@ -1474,7 +1474,7 @@ int gram_ctas_per_sm(int W, int use_tc) {
         }
     } else {
         if (W == 64 && use_tc) {
-            per = gram_tc_ctas_per_sm();
+            per = gram_tc_ctas_per_sm(rows_pad);
         } else if (W == 64) {
             const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
             cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
@@ -1488,8 +1488,8 @@ int gram_ctas_per_sm(int W, int use_tc) {
     cudaGetLastError();
     return per < 1 ? 1 : per;
 }
-template int gram_ctas_per_sm<float>(int, int);
-template int gram_ctas_per_sm<double>(int, int);
+template int gram_ctas_per_sm<float>(int, int, long long);
+template int gram_ctas_per_sm<double>(int, int, long long);
 
 void solve_timing_report(const char* tag, int sweep) {
     static long long* dbg = nullptr;

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tc(JacobiRound<float>
 // after its MMAs complete.  Rows past the matrix and columns past its last
 // column are zero-filled by the TMA unit.
 // ------------------------------------------------------------------------
-constexpr int GM_KT = 64, GM_ST = 3;
+template <int GM_KT, int GM_ST>
 constexpr size_t gram_tma_smem() { return (size_t)GM_ST * (128 * GM_KT * 4) + 1024; }
 
 __device__ __forceinline__ void tma_load_4d(uint32_t sdst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -302,8 +302,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
                  : "memory");
 }
 
-__global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tma(JacobiRound<float> a, const __grid_constant__ CUtensorMap tmap) {
-    constexpr int STAGE = 128 * GM_KT * 4;              // 32 KB: raw (16 KB) + lo (16 KB)
+template <int GM_KT, int GM_ST, int MINB>
+__global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tma(JacobiRound<float> a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int STAGE = 128 * GM_KT * 4;              // raw (64 x KT) + lo (64 x KT)
     constexpr uint32_t SBO = (GM_KT / 4) * 128;         // 2048 B between 8-row (M) groups
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
     reset_publication(a);
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tma(JacobiRound<float> a
         tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
         // lo parts of the landed raw chunks: 1024 16-byte chunks, 8 per thread, linear (conflict-free)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < GM_KT / 8; ++u) {
             const int f = tid + GT_NT * u;
             const float4 x = reinterpret_cast<const float4*>(st)[f];
             reinterpret_cast<float4*>(st + 8 * SBO)[f] = tc::lo4(x, tc::hi4(x));
@@ -403,7 +404,17 @@ __global__ void __launch_bounds__(GT_NT, 2) k_pair_gram_tma(JacobiRound<float> a
     if (warp == 0) tc::tmem_free<64>(tmem);
 }
 
+// rows per stage of the TMA Gram (MPJSVD_GRAM_KT = 32 or 64): KT = 64 -> 3 x 32 KB stages, 2 CTAs per SM;
+// KT = 32 -> 3 x 16 KB stages, 4 CTAs per SM
+// Default by row count (measured on B200): 32 for >= 6144 rows (C5: Gram 237 -> 217 ms), 64 below (C3: 33 vs 35 ms)
+int gram_tma_kt(long long rows_pad) {
+    const char* e = getenv("MPJSVD_GRAM_KT");
+    if (e && (atoi(e) == 32 || atoi(e) == 64)) return atoi(e);
+    return rows_pad >= 6144 ? 32 : 64;
+}
+
 int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols) {
+    const int kt = gram_tma_kt(rows_pad);
     typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -420,7 +431,7 @@ int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pa
     if (!fn || cols % 8 != 0 || rows_pad % 4 != 0 || ld % 4 != 0) return -1;
     const cuuint64_t gdim[4] = {4, 8, (cuuint64_t)(rows_pad / 4), (cuuint64_t)(cols / 8)};
     const cuuint64_t gstride[3] = {(cuuint64_t)ld * 4, 16, (cuuint64_t)ld * 4 * 8};
-    const cuuint32_t box[4] = {4, 8, GM_KT / 4, 4};
+    const cuuint32_t box[4] = {4, 8, (cuuint32_t)(kt / 4), 4};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           const_cast<float*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -887,11 +898,16 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
     if (a.tmap) {
         static bool attr_m = false;
         if (!attr_m) {
-            cudaFuncSetAttribute(k_pair_gram_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem());
+            cudaFuncSetAttribute(k_pair_gram_tma<64, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem<64, 3>());
+            cudaFuncSetAttribute(k_pair_gram_tma<32, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem<32, 3>());
             attr_m = true;
         }
-        k_pair_gram_tma<<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem(), st>>>(
-            a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
+        if (gram_tma_kt(a.m_pad) == 32)
+            k_pair_gram_tma<32, 3, 4><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 3>(), st>>>(
+                a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
+        else
+            k_pair_gram_tma<64, 3, 2><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<64, 3>(), st>>>(
+                a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
         MPJ_LAUNCHED();
         return 0;
     }
@@ -936,7 +952,11 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
     return 0;
 }
 
-int gram_tc_ctas_per_sm() {
+int gram_tc_ctas_per_sm(long long rows_pad) {
+    {
+        const char* env = getenv("MPJSVD_GRAM_TMA");
+        if (!(env && env[0] == '0')) return gram_tma_kt(rows_pad) == 32 ? 4 : 2;
+    }
     // shared memory bound: (stages + alignment + static) per CTA of 228 KB per SM
     const GramVariant& gv = gram_variant();
     const int per = (int)((228 * 1024) / (gv.smem + 2048));

@@ -263,7 +263,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     } else {
         // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
         // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
-        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc);
+        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc, m_pad);
         const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
         double best = 1e30;
         for (long long ns = 1; ns <= maxsplit; ++ns) {
