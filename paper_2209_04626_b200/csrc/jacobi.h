@@ -128,6 +128,9 @@ struct QrWork {
     int* cand_pos;      // 2 * grid
     int* cand_col;      // 2 * grid
     int grid;           // cooperative grid size used
+    int* ready = nullptr;  // 1024 per-column release flags (zeroed once) of qr_panel_chain; null: k_qr_coop panels
+    cudaStream_t la_stream = nullptr;   // qr_blocked look-ahead: panel p+1 factored here beside p's trailing update
+    cudaEvent_t la_ev0 = nullptr, la_ev1 = nullptr;
 };
 // In-place Householder QR (pivot = 1: Businger-Golub column pivoting) of the
 // m x n matrix A (lda).  Columns stay at their physical place; phys[k] (copy
@@ -135,6 +138,9 @@ struct QrWork {
 int qr_coop(double* A, long long lda, int m, int n, double* tau, int pivot, QrWork& w,
             int* phys_out, cudaStream_t st);
 int qr_coop_grid(int m, int* grid);  // cooperative grid size for this m
+// Unpivoted QR of the m x n panel A (n <= 1024) by k_qr_panel (one CTA per column, per-column release flags
+// `ready`, no grid barrier); same outputs as qr_coop with pivot = 0 up to rounding order.
+int qr_panel_chain(double* A, long long lda, int m, int n, double* tau, int* ready, cudaStream_t st);
 // Column-pivoted QR with xLAQPS-style lazy panel updates (k_qrp.cu); same
 // outputs as qr_coop(pivot = 1).  work >= qrp_lazy_work_doubles(n, grid).
 int qrp_lazy(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, int* phys_out,

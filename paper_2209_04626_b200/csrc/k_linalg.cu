@@ -425,7 +425,7 @@ size_t apply_q_work_elems(long long m, long long ncols) {
 // `rows`, ld ldp; reflector i has its unit at row i).
 static int apply_panel(const double* P, long long ldp, long long rows, int kb, const double* tau, double* C,
                        long long ldc, long long ncols, int trans, double* work, cudaStream_t st,
-                       const double* t_in = nullptr, double* t_out = nullptr) {
+                       const double* t_in = nullptr, double* t_out = nullptr, bool reuse = false) {
     const long long ldw = round_up(rows, 32);
     double* Vp = work;                                  // rows x WY_NB (ld ldw)
     double* S = Vp + (size_t)ldw * WY_NB;               // WY_NB x WY_NB
@@ -435,9 +435,10 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     double* W2 = W1 + (size_t)WY_NB * ncols;
     int gx = (int)ceil_div(rows, 256);
     if (gx > 128) gx = 128;
+    int rc = 0;
+    if (reuse) goto apply;                              // Vp and T of this panel are still in work
     k_make_panel<<<dim3(gx, WY_NB), 256, 0, st>>>(P, ldp, rows, 0, kb, Vp, ldw);
     MPJ_LAUNCHED();
-    int rc = 0;
     if (t_in) {
         // T of this panel was formed by the factorisation that produced the reflectors
         MPJ_CUDA_TRY(cudaMemcpyAsync(T, t_in, sizeof(double) * WY_NB * WY_NB, cudaMemcpyDeviceToDevice, st));
@@ -534,17 +535,52 @@ int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double*
 // DMMA GEMM.  Used for the tall QR and the LQ of R
 // (QR of R^T).  Same reflectors / R as the unblocked algorithm
 // up to rounding.
+static int factor_panel(double* Pn, long long lda, int rows, int kb, double* tau, QrWork& w, cudaStream_t st) {
+    if (w.ready) return qr_panel_chain(Pn, lda, rows, kb, tau, w.ready, st);
+    QrWork wp = w;
+    int grid = 0;
+    int rc = qr_coop_grid(rows, &grid);
+    if (rc) return rc;
+    wp.grid = grid < kb ? grid : kb;
+    return qr_coop(Pn, lda, rows, kb, tau, 0, wp, nullptr, st);
+}
+
 int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,
                double* tcache) {
+    if (w.ready && w.la_stream && n > WY_NB) {
+        // look-ahead (LAPACK-style): panel p's reflectors update panel p+1's columns first; panel p+1 is then
+        // factored on la_stream while the rest of p's trailing update runs here
+        int rc = factor_panel(A, lda, m, n < WY_NB ? n : WY_NB, tau, w, st);
+        if (rc) return rc;
+        for (int j0 = 0; j0 < n; j0 += WY_NB) {
+            const int kb = n - j0 < WY_NB ? n - j0 : WY_NB;
+            double* Pn = A + j0 + (long long)j0 * lda;
+            if (j0 > 0) MPJ_CUDA_TRY(cudaStreamWaitEvent(st, w.la_ev1, 0));
+            const int j1 = j0 + kb;
+            if (j1 >= n) break;
+            const int kb1 = n - j1 < WY_NB ? n - j1 : WY_NB;
+            double* tslot = tcache ? tcache + (size_t)(j0 / WY_NB) * WY_NB * WY_NB : nullptr;
+            rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)kb * lda, lda, kb1, 1, work, st, nullptr,
+                             tslot);
+            if (rc) return rc;
+            MPJ_CUDA_TRY(cudaEventRecord(w.la_ev0, st));
+            MPJ_CUDA_TRY(cudaStreamWaitEvent(w.la_stream, w.la_ev0, 0));
+            rc = factor_panel(A + j1 + (long long)j1 * lda, lda, m - j1, kb1, tau + j1, w, w.la_stream);
+            if (rc) return rc;
+            MPJ_CUDA_TRY(cudaEventRecord(w.la_ev1, w.la_stream));
+            if (j1 + kb1 < n) {
+                rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)(kb + kb1) * lda, lda, n - j1 - kb1, 1,
+                                 work, st, nullptr, nullptr, true);
+                if (rc) return rc;
+            }
+        }
+        MPJ_CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
     for (int j0 = 0; j0 < n; j0 += WY_NB) {
         const int kb = n - j0 < WY_NB ? n - j0 : WY_NB;
         double* Pn = A + j0 + (long long)j0 * lda;
-        QrWork wp = w;
-        int grid = 0;
-        int rc = qr_coop_grid(m - j0, &grid);
-        if (rc) return rc;
-        wp.grid = grid < kb ? grid : kb;
-        rc = qr_coop(Pn, lda, m - j0, kb, tau + j0, 0, wp, nullptr, st);
+        int rc = factor_panel(Pn, lda, m - j0, kb, tau + j0, w, st);
         if (rc) return rc;
         if (j0 + kb < n) {
             rc = apply_panel(Pn, lda, m - j0, kb, tau + j0, Pn + (long long)kb * lda, lda, n - j0 - kb, 1, work, st,

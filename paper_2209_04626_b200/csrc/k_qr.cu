@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <float.h>
+#include <atomic>
 #include "common.cuh"
 #include "jacobi.h"
 
@@ -310,6 +311,123 @@ int qr_coop(double* A, long long lda, int m, int n, double* tau, int pivot, QrWo
     MPJ_LAUNCHED();
     if (phys_out)
         MPJ_CUDA_TRY(cudaMemcpyAsync(phys_out, w.phys_all, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    return 0;
+}
+
+// ------------------------------------------------------------------------
+// Unpivoted panel QR (the panels of qr_blocked) without grid barriers.
+// CTA c owns panel column c for the whole kernel, register resident (rows
+// tid + QR_NT j).  It applies H_0 .. H_{c-1} in order, each as soon as its
+// reflector is published, then forms its own reflector H_c (same formulas as
+// k_qr_coop), writes v / R_cc / R(0:c, c) into A and tau[c], and releases
+// ready[c] = epoch.  The chain of step k therefore runs through one CTA (the
+// owner of column k+1) instead of a grid-wide barrier per step, and the
+// kernel is safe to run beside other kernels (no co-residency requirement:
+// a CTA only waits for lower-numbered CTAs).
+// ------------------------------------------------------------------------
+template <int RPT>
+__global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, long long lda, int m,
+                                                       double* __restrict__ tau, int* ready, int epoch) {
+    extern __shared__ double vsh[];           // v of the current step at this thread's rows
+    __shared__ double red[32];
+    __shared__ double s_alpha;
+    const int c = blockIdx.x, tid = threadIdx.x;
+    double* col = A + (long long)c * lda;
+    double y[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int i = tid + QR_NT * j;
+        y[j] = i < m ? col[i] : 0.0;
+    }
+    for (int k = 0; k < c; ++k) {
+        if (tid == 0) {
+            while (ld_acquire_gpu(ready + k) != epoch) { }
+            __threadfence();
+        }
+        __syncthreads();
+        const double* vk = A + (long long)k * lda;
+        const double tk = __ldcg(tau + k);
+        double d = 0.0;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + QR_NT * j;
+            double v = 0.0;
+            if (i > k && i < m) v = __ldcg(vk + i);
+            else if (i == k) v = 1.0;
+            vsh[tid + QR_NT * j] = v;
+            d += v * y[j];
+        }
+        d = block_sum(d, red);
+        const double wv = tk * d;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) y[j] -= wv * vsh[tid + QR_NT * j];
+    }
+    // own reflector H_c of y(c:m)
+    double sig = 0.0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int i = tid + QR_NT * j;
+        if (i == c) s_alpha = y[j];
+        if (i > c && i < m) sig += y[j] * y[j];
+    }
+    sig = block_sum(sig, red);                // also orders s_alpha
+    const double alpha = s_alpha;
+    double tk, v0, mu;
+    bool scale_v = true;
+    if (sig == 0.0) {
+        scale_v = false;
+        if (alpha >= 0.0) { tk = 0.0; mu = alpha; v0 = 1.0; }
+        else { tk = 2.0; mu = -alpha; v0 = 1.0; }
+    } else {
+        mu = sqrt(alpha * alpha + sig);
+        v0 = alpha <= 0.0 ? alpha - mu : -sig / (alpha + mu);
+        tk = 2.0 * v0 * v0 / (sig + v0 * v0);
+    }
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int i = tid + QR_NT * j;
+        if (i < m) col[i] = i < c ? y[j] : (i == c ? mu : (scale_v ? y[j] / v0 : y[j]));
+    }
+    if (tid == 0) tau[c] = tk;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_gpu(ready + c, epoch);
+}
+
+template <int RPT>
+static void* panel_kernel_ptr() { return (void*)k_qr_panel<RPT>; }
+
+static void* panel_kernel_for(int rpt) {
+    switch (rpt) {
+        case 1: return panel_kernel_ptr<1>();
+        case 2: return panel_kernel_ptr<2>();
+        case 4: return panel_kernel_ptr<4>();
+        case 8: return panel_kernel_ptr<8>();
+        case 16: return panel_kernel_ptr<16>();
+        case 32: return panel_kernel_ptr<32>();
+        default: return nullptr;
+    }
+}
+
+int qr_panel_chain(double* A, long long lda, int m, int n, double* tau, int* ready, cudaStream_t st) {
+    static std::atomic<int> epoch{0};
+    if (n <= 0) return 0;
+    const int rpt = rpt_for(m);
+    void* fn = panel_kernel_for(rpt);
+    if (!fn || n > 1024) return -7;
+    const size_t smem = sizeof(double) * (size_t)QR_NT * rpt;
+    static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
+    int slot = 0;
+    while ((1 << slot) < rpt) ++slot;
+    if (attr_set[slot] < smem) {
+        MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[slot] = smem;
+    }
+    int ep = ++epoch;
+    if (ep <= 0) { epoch = 1; ep = 1; }
+    void* params[] = {&A, &lda, &m, &tau, &ready, &ep};
+    MPJ_CUDA_TRY(cudaLaunchKernel(fn, dim3(n), dim3(QR_NT), params, smem, st));
+    MPJ_LAUNCHED();
     return 0;
 }
 

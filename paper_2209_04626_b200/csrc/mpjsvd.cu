@@ -41,7 +41,7 @@ namespace {
 enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
-    S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC,
+    S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC, S_QR_RDY,
     S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
 };
 
@@ -110,6 +110,8 @@ struct mpjsvd_handle_s {
     cudaEvent_t ev[10] = {};
     cudaStream_t aux = nullptr;    // second stream: independent assembly chains (fork/join by events)
     cudaEvent_t fork = nullptr, join = nullptr, tpdone = nullptr;
+    cudaStream_t qaux = nullptr;   // look-ahead panel factorisations of qr_blocked
+    cudaEvent_t qev0 = nullptr, qev1 = nullptr;
     Comm comm;                     // NCCL (multi-process sharding), inactive by default
 };
 
@@ -551,6 +553,16 @@ int ensure_qr_work(mpjsvd_handle h, int m, int n, QrWork& w) {
     w.cand_val = P<double>(h, S_QR_CV);
     w.cand_pos = P<int>(h, S_QR_CP);
     w.cand_col = P<int>(h, S_QR_CC);
+    if (h->cap[S_QR_RDY] < sizeof(int) * 1024) {
+        MPJ_TRY(ensure(h, S_QR_RDY, sizeof(int) * 1024));
+        MPJ_CUDA_TRY(cudaMemsetAsync(h->buf[S_QR_RDY], 0, sizeof(int) * 1024, h->stream));
+    }
+    w.ready = getenv("MPJSVD_QR_PANEL_COOP") ? nullptr : P<int>(h, S_QR_RDY);
+    const char* la = getenv("MPJSVD_QR_LOOKAHEAD");
+    const bool lookahead = w.ready && !(la && la[0] == '0');
+    w.la_stream = lookahead ? h->qaux : nullptr;
+    w.la_ev0 = h->qev0;
+    w.la_ev1 = h->qev1;
     w.grid = grid;
     return 0;
 }
@@ -1190,7 +1202,10 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->tpdone, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&h->tpdone, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->qaux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->qev0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->qev1, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         mpjsvd_destroy(h);
         return MPJSVD_ERR_CUDA;
@@ -1220,6 +1235,9 @@ int mpjsvd_destroy(mpjsvd_handle h) {
     if (h->fork) cudaEventDestroy(h->fork);
     if (h->join) cudaEventDestroy(h->join);
     if (h->tpdone) cudaEventDestroy(h->tpdone);
+    if (h->qaux) { cudaStreamSynchronize(h->qaux); cudaStreamDestroy(h->qaux); }
+    if (h->qev0) cudaEventDestroy(h->qev0);
+    if (h->qev1) cudaEventDestroy(h->qev1);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
     cudaGetLastError();

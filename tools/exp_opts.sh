@@ -12,6 +12,6 @@ for spec in "$@"; do
 import json,sys
 d=json.load(open(sys.argv[1]))
 k={kk:round(v['ms_per_step'],1) for kk,v in d['kernels'].items() if 'pair' in kk}
-print(sys.argv[2], round(d['value'],4), d['sweeps32'], d['sweeps64'], {kk:round(v,1) for kk,v in d['stage_ms'].items() if kk in ('fp32','fp64')}, k)
+print(sys.argv[2], round(d['value'],4), d['sweeps32'], d['sweeps64'], {kk:round(v,1) for kk,v in d['stage_ms'].items() if kk in ('fp32','fp64','lq','lift','assemble','qr_tall')}, k)
 PY
 done
