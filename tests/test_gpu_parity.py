@@ -151,6 +151,34 @@ def test_qr_vs_oracle(mp, m, n, pivot):
     assert np.abs(q @ r - a[:, perm]).max() <= 1e-13 * np.abs(a).max()
 
 
+@pytest.mark.parametrize("mode", [{"MPJSVD_QR_PANEL_COOP": "1"}, {"MPJSVD_QR_LOOKAHEAD": "0"}, {}])
+def test_blocked_qr_panel_modes(mp, monkeypatch, mode):
+    """Blocked Householder QR with its three panel schedules: the cooperative (grid-barrier) panel kernel,
+    the flag-chained panel kernel, and the chained kernel with look-ahead (panel p+1 factored on a side stream
+    beside panel p's trailing update).  Several 128-column panels, a ragged last panel, tall and square; the
+    whole mixed-precision SVD (LQ and U-route switch both run the blocked QR) against the oracle."""
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    for m, n in ((1000, 300), (700, 700), (2100, 520)):
+        rng = np.random.default_rng(m * n)
+        a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
+        packed, tau, _ = mp.qr(dev(a), pivot=0)
+        packed, tau = host(packed), host(tau)
+        p_o, tau_o, _ = oracle.qr(a)
+        r, r_o = np.triu(packed[:n]), np.triu(p_o[:n])
+        assert np.abs(r - r_o).max() <= 1e-12 * np.abs(r_o).max()
+        assert np.abs(tau - tau_o).max() <= 1e-12
+        q = oracle.form_q(packed, tau, n)
+        assert orth(q) < 1e-13
+        assert np.abs(q @ r - a).max() <= 1e-13 * np.abs(a).max()
+    a = testmat.config_matrix("C3", 512)
+    U, S, V, st = mp.factor(dev(a))
+    check_svd(a, host(U), host(S), host(V))
+    uo, so, vo, sto, rc = oracle.mixed_svd(a)
+    assert np.all(np.abs(host(S) - so) / so <= tiered(so, kappa_s(a)))
+    assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1 and abs(st["sweeps64"] - sto["sweeps64"]) <= 1
+
+
 def test_qrp_recompute_path(mp):
     """Strongly decaying partial norms (sigma 1 -> 1e-14) force the partial-norm
     recomputation (xLAQP2 rule) on many columns: pivots and R must still match."""
