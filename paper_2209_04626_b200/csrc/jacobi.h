@@ -186,8 +186,12 @@ int form_q_wy(const double* Vr, long long m, int k, long long ldv, const double*
 int wy_tfactors(const double* Vr, long long m, int k, long long ldv, const double* tau, double* tcache, double* work,
                 cudaStream_t st);
 // number of WY panels of a k-reflector factorisation whose T qr_blocked leaves in its cache (all but the last)
-inline int wy_cached_panels(int k) { return (k + 127) / 128 - 1; }
-inline size_t wy_tcache_elems(int k) { return (size_t)((k + 127) / 128) * 128 * 128; }
+#ifndef MPJ_WY_PANEL
+#define MPJ_WY_PANEL 256
+#endif
+constexpr int WY_PANEL = MPJ_WY_PANEL;   // reflectors per compact-WY panel (blocked QR, WY application)
+inline int wy_cached_panels(int k) { return (k + WY_PANEL - 1) / WY_PANEL - 1; }
+inline size_t wy_tcache_elems(int k) { return (size_t)((k + WY_PANEL - 1) / WY_PANEL) * WY_PANEL * WY_PANEL; }
 // Blocked Householder QR (no pivoting) in place; work >= apply_q_work_elems(m, n).
 // tcache (optional, wy_tcache_elems(n)): receives the T factor of every panel with a trailing update
 int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,

@@ -364,7 +364,7 @@ int trsm_right_upper(const double* R, long long ldr, double* Q, long long ldq, l
 //   Vp explicit (unit diagonal), S = Vp^T Vp, T (LAPACK xLARFT 'F','C'),
 //   W1 = Vp^T C, W2 = T W1, C -= Vp W2.
 // ------------------------------------------------------------------------
-constexpr int WY_NB = 128;   // panel of the WY application / blocked QR
+constexpr int WY_NB = WY_PANEL;   // panel of the WY application / blocked QR
 constexpr int LT_NB = 64;    // block of the T formation (k_larft)
 
 __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j0, int kb, double* Vp,

@@ -1007,7 +1007,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (tcp_all) MPJ_CUDA_TRY(cudaStreamWaitEvent(st, h->tpdone, 0));   // Q_p's T factors (aux stream)
     MPJ_TRY(apply_q_wy(dA1L, n, (int)n, n_pad, P<double>(h, S_TAU_P), dUX, n_pad, n, P<double>(h, S_WY), st,
                        (o.mp_rrqr || tcp_all) ? P<double>(h, S_TC_P) : nullptr,
-                       tcp_all ? (int)ceil_div(n, 128) : (o.mp_rrqr ? wy_cached_panels((int)n) : 0)));
+                       tcp_all ? (int)ceil_div(n, WY_PANEL) : (o.mp_rrqr ? wy_cached_panels((int)n) : 0)));
     double* Ufin = dUX;
     long long ldUf = n_pad;
     if (m > n) {
