@@ -340,10 +340,8 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
         y[j] = i < m ? col[i] : 0.0;
     }
     for (int k = 0; k < c; ++k) {
-        if (tid == 0) {
+        if (tid == 0)
             while (ld_acquire_gpu(ready + k) != epoch) { }
-            __threadfence();
-        }
         __syncthreads();
         const double* vk = A + (long long)k * lda;
         const double tk = __ldcg(tau + k);
@@ -383,15 +381,24 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
         v0 = alpha <= 0.0 ? alpha - mu : -sig / (alpha + mu);
         tk = 2.0 * v0 * v0 / (sig + v0 * v0);
     }
+    // publish v (rows > c) and tau first: one fence by the releasing thread after the barrier (cumulative)
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int i = tid + QR_NT * j;
-        if (i < m) col[i] = i < c ? y[j] : (i == c ? mu : (scale_v ? y[j] / v0 : y[j]));
+        if (i > c && i < m) col[i] = scale_v ? y[j] / v0 : y[j];
     }
     if (tid == 0) tau[c] = tk;
-    __threadfence();
     __syncthreads();
-    if (tid == 0) st_release_gpu(ready + c, epoch);
+    if (tid == 0) {
+        __threadfence();
+        st_release_gpu(ready + c, epoch);
+    }
+    // R(0:c, c) is read only by later kernels
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int i = tid + QR_NT * j;
+        if (i <= c) col[i] = i < c ? y[j] : mu;
+    }
 }
 
 template <int RPT>
