@@ -386,33 +386,36 @@ __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j
 // Vp^T Vp) and tau are staged in shared memory first, so the kb dependent
 // steps run on shared memory only.
 __global__ void k_larft(const double* S, int kb, const double* tau, int j0, double* T) {
-    // S, T: LT_NB x LT_NB blocks of ld WY_NB matrices (column-major); T upper triangular
+    // S, T: LT_NB x LT_NB blocks of ld WY_NB matrices (column-major); T upper triangular.
+    // LT_NB x 8 threads: row r = tid / 8, the 8 lanes of a row split the dot product T[r, r:i] S[r:i, i].
+    // Step i reads columns < i of t and writes column i, so one barrier per step suffices.
     extern __shared__ double lsm[];
     double* t = lsm;                                  // [LT_NB][LT_NB + 1]: t[r * (LT_NB + 1) + c]
     double* sv = t + LT_NB * (LT_NB + 1);             // [LT_NB][LT_NB + 1]: S
     double* ts = sv + LT_NB * (LT_NB + 1);            // tau
     constexpr int LS = LT_NB + 1;
-    const int r = threadIdx.x;
-    for (int e = r; e < LT_NB * LT_NB; e += blockDim.x) {
+    const int tid = threadIdx.x, r = tid >> 3, q = tid & 7;
+    for (int e = tid; e < LT_NB * LT_NB; e += blockDim.x) {
         const int a = e % LT_NB, c = e / LT_NB;
         t[a * LS + c] = 0.0;
         sv[a * LS + c] = S[a + (long long)c * WY_NB];
     }
-    if (r < kb) ts[r] = tau[j0 + r];
+    if (tid < kb) ts[tid] = tau[j0 + tid];
     __syncthreads();
     for (int i = 0; i < kb; ++i) {
-        double val = 0.0;
-        if (r < i) {
-            double s = 0.0;
-            for (int c = r; c < i; ++c) s += t[r * LS + c] * sv[c * LS + i];
-            val = -ts[i] * s;
+        double s = 0.0;
+        if (r < i)
+            for (int c = r + q; c < i; c += 8) s += t[r * LS + c] * sv[c * LS + i];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (q == 0) {
+            if (r < i) t[r * LS + i] = -ts[i] * s;
+            else if (r == i) t[i * LS + i] = ts[i];
         }
         __syncthreads();
-        if (r < i) t[r * LS + i] = val;
-        if (r == i) t[i * LS + i] = ts[i];
-        __syncthreads();
     }
-    for (int e = r; e < LT_NB * LT_NB; e += blockDim.x) T[(e % LT_NB) + (long long)(e / LT_NB) * WY_NB] = t[(e % LT_NB) * LS + e / LT_NB];
+    for (int e = tid; e < LT_NB * LT_NB; e += blockDim.x) T[(e % LT_NB) + (long long)(e / LT_NB) * WY_NB] = t[(e % LT_NB) * LS + e / LT_NB];
 }
 static size_t larft_smem() { return sizeof(double) * (2 * (size_t)LT_NB * (LT_NB + 1) + LT_NB); }
 
@@ -456,7 +459,7 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     MPJ_CUDA_TRY(cudaMemsetAsync(T, 0, sizeof(double) * WY_NB * WY_NB, st));
     for (int b0 = 0; b0 < kb; b0 += LT_NB) {
         const int bk = kb - b0 < LT_NB ? kb - b0 : LT_NB;
-        k_larft<<<1, LT_NB, larft_smem(), st>>>(S + b0 + (long long)b0 * WY_NB, bk, tau, b0,
+        k_larft<<<1, LT_NB * 8, larft_smem(), st>>>(S + b0 + (long long)b0 * WY_NB, bk, tau, b0,
                                                   T + b0 + (long long)b0 * WY_NB);
         MPJ_LAUNCHED();
         if (b0 > 0) {
