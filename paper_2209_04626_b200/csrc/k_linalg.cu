@@ -385,7 +385,12 @@ __global__ void k_make_panel(const double* Vr, long long ldv, long long m, int j
 // -tau_i T[0:i, 0:i] S[0:i, i], T[i][i] = tau_i.  S (the strict upper part of
 // Vp^T Vp) and tau are staged in shared memory first, so the kb dependent
 // steps run on shared memory only.
-__global__ void k_larft(const double* S, int kb, const double* tau, int j0, double* T) {
+__global__ void k_larft(const double* S, int kb_all, const double* tau, double* T) {
+    // CTA z forms the diagonal block z (reflectors z LT_NB .. z LT_NB + kb - 1) of the panel's T
+    const int j0 = blockIdx.x * LT_NB;
+    const int kb = kb_all - j0 < LT_NB ? kb_all - j0 : LT_NB;
+    S += j0 + (long long)j0 * WY_NB;
+    T += j0 + (long long)j0 * WY_NB;
     // S, T: LT_NB x LT_NB blocks of ld WY_NB matrices (column-major); T upper triangular.
     // LT_NB x 8 threads: row r = tid / 8, the 8 lanes of a row split the dot product T[r, r:i] S[r:i, i].
     // Step i reads columns < i of t and writes column i, so one barrier per step suffices.
@@ -457,12 +462,11 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     // T in LT_NB blocks: diagonal blocks by k_larft, then the recursive coupling
     // T[0:a, a:b] = -T[0:a, 0:a] S[0:a, a:b] T[a:b, a:b] (LAPACK xLARFT, recursive form)
     MPJ_CUDA_TRY(cudaMemsetAsync(T, 0, sizeof(double) * WY_NB * WY_NB, st));
-    for (int b0 = 0; b0 < kb; b0 += LT_NB) {
+    k_larft<<<(unsigned)ceil_div(kb, LT_NB), LT_NB * 8, larft_smem(), st>>>(S, kb, tau, T);   // diagonal blocks
+    MPJ_LAUNCHED();
+    for (int b0 = LT_NB; b0 < kb; b0 += LT_NB) {
         const int bk = kb - b0 < LT_NB ? kb - b0 : LT_NB;
-        k_larft<<<1, LT_NB * 8, larft_smem(), st>>>(S + b0 + (long long)b0 * WY_NB, bk, tau, b0,
-                                                  T + b0 + (long long)b0 * WY_NB);
-        MPJ_LAUNCHED();
-        if (b0 > 0) {
+        {
             // W = S[0:b0, b0:b0+bk] T22 ; T12 = -T11 W
             rc = gemm_f64(0, 0, b0, bk, bk, 1.0, S + (long long)b0 * WY_NB, WY_NB, T + b0 + (long long)b0 * WY_NB,
                           WY_NB, 0.0, T12w, WY_NB, st);
