@@ -316,36 +316,55 @@ int qr_coop(double* A, long long lda, int m, int n, double* tau, int pivot, QrWo
 
 // ------------------------------------------------------------------------
 // Unpivoted panel QR (the panels of qr_blocked) without grid barriers.
-// CTA c owns panel column c for the whole kernel, register resident (rows
-// tid + QR_NT j).  It applies H_0 .. H_{c-1} in order, each as soon as its
-// reflector is published, then forms its own reflector H_c (same formulas as
-// k_qr_coop), writes v / R_cc / R(0:c, c) into A and tau[c], and releases
-// ready[c] = epoch.  The chain of step k therefore runs through one CTA (the
-// owner of column k+1) instead of a grid-wide barrier per step, and the
-// kernel is safe to run beside other kernels (no co-residency requirement:
-// a CTA only waits for lower-numbered CTAs).
+// CTA z owns the CPC panel columns c0 = z CPC .. c0 + CPC - 1 for the whole
+// kernel, register resident (rows tid + QR_NT j).  It applies H_0 .. H_{c0-1}
+// in order, each as soon as its reflector is published, then forms its own
+// reflectors one after the other (same formulas as k_qr_coop), applying each
+// to its later columns locally, writes v and tau, and releases the flags
+// ready[c0 ..] = epoch.  The chain therefore crosses CTAs (flag + L2 round
+// trip) once per CPC columns instead of a grid-wide barrier per column, and
+// the kernel is safe to run beside other kernels (no co-residency
+// requirement: a CTA only waits for lower-numbered CTAs).
 // ------------------------------------------------------------------------
-template <int RPT>
-__global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, long long lda, int m,
+template <int CPC>
+__device__ __forceinline__ void block_sum_vec(double (&v)[CPC], double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < CPC; ++q) {
+        v[q] = warp_sum(v[q]);
+        if (lane == 0) red[q * 32 + wid] = v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < CPC; ++q) v[q] = warp_sum(lane < nw ? red[q * 32 + lane] : 0.0);
+    __syncthreads();
+}
+
+template <int RPT, int CPC>
+__global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, long long lda, int m, int n,
                                                        double* __restrict__ tau, int* ready, int epoch) {
     extern __shared__ double vsh[];           // v of the current step at this thread's rows
-    __shared__ double red[32];
+    __shared__ double red[32 * CPC];
     __shared__ double s_alpha;
-    const int c = blockIdx.x, tid = threadIdx.x;
-    double* col = A + (long long)c * lda;
-    double y[RPT];
+    const int c0 = blockIdx.x * CPC, tid = threadIdx.x;
+    const int nc = n - c0 < CPC ? n - c0 : CPC;
+    double y[CPC][RPT];
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-        const int i = tid + QR_NT * j;
-        y[j] = i < m ? col[i] : 0.0;
-    }
-    for (int k = 0; k < c; ++k) {
+    for (int q = 0; q < CPC; ++q)
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + QR_NT * j;
+            y[q][j] = (q < nc && i < m) ? A[(long long)(c0 + q) * lda + i] : 0.0;
+        }
+    for (int k = 0; k < c0; ++k) {
         if (tid == 0)
             while (ld_acquire_gpu(ready + k) != epoch) { }
         __syncthreads();
         const double* vk = A + (long long)k * lda;
         const double tk = __ldcg(tau + k);
-        double d = 0.0;
+        double d[CPC];
+#pragma unroll
+        for (int q = 0; q < CPC; ++q) d[q] = 0.0;
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int i = tid + QR_NT * j;
@@ -353,65 +372,109 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
             if (i > k && i < m) v = __ldcg(vk + i);
             else if (i == k) v = 1.0;
             vsh[tid + QR_NT * j] = v;
-            d += v * y[j];
+#pragma unroll
+            for (int q = 0; q < CPC; ++q) d[q] += v * y[q][j];
         }
-        d = block_sum(d, red);
-        const double wv = tk * d;
+        block_sum_vec<CPC>(d, red);
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) y[j] -= wv * vsh[tid + QR_NT * j];
-    }
-    // own reflector H_c of y(c:m)
-    double sig = 0.0;
+        for (int q = 0; q < CPC; ++q) {
+            const double wv = tk * d[q];
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-        const int i = tid + QR_NT * j;
-        if (i == c) s_alpha = y[j];
-        if (i > c && i < m) sig += y[j] * y[j];
+            for (int j = 0; j < RPT; ++j) y[q][j] -= wv * vsh[tid + QR_NT * j];
+        }
     }
-    sig = block_sum(sig, red);                // also orders s_alpha
-    const double alpha = s_alpha;
-    double tk, v0, mu;
-    bool scale_v = true;
-    if (sig == 0.0) {
-        scale_v = false;
-        if (alpha >= 0.0) { tk = 0.0; mu = alpha; v0 = 1.0; }
-        else { tk = 2.0; mu = -alpha; v0 = 1.0; }
-    } else {
-        mu = sqrt(alpha * alpha + sig);
-        v0 = alpha <= 0.0 ? alpha - mu : -sig / (alpha + mu);
-        tk = 2.0 * v0 * v0 / (sig + v0 * v0);
-    }
-    // publish v (rows > c) and tau first: one fence by the releasing thread after the barrier (cumulative)
+    double mus[CPC];
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-        const int i = tid + QR_NT * j;
-        if (i > c && i < m) col[i] = scale_v ? y[j] / v0 : y[j];
+    for (int q = 0; q < CPC; ++q) {
+        mus[q] = 0.0;
+        if (q >= nc) break;
+        const int c = c0 + q;
+        // own reflector H_c of y_q(c:m)
+        double sig = 0.0;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + QR_NT * j;
+            if (i == c) s_alpha = y[q][j];
+            if (i > c && i < m) sig += y[q][j] * y[q][j];
+        }
+        sig = block_sum(sig, red);            // also orders s_alpha
+        const double alpha = s_alpha;
+        double tk, v0, mu;
+        bool scale_v = true;
+        if (sig == 0.0) {
+            scale_v = false;
+            if (alpha >= 0.0) { tk = 0.0; mu = alpha; v0 = 1.0; }
+            else { tk = 2.0; mu = -alpha; v0 = 1.0; }
+        } else {
+            mu = sqrt(alpha * alpha + sig);
+            v0 = alpha <= 0.0 ? alpha - mu : -sig / (alpha + mu);
+            tk = 2.0 * v0 * v0 / (sig + v0 * v0);
+        }
+        mus[q] = mu;
+        double* col = A + (long long)c * lda;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + QR_NT * j;
+            if (i > c && i < m) {
+                if (scale_v) y[q][j] = y[q][j] / v0;
+                col[i] = y[q][j];
+            }
+        }
+        if (tid == 0) tau[c] = tk;
+        // H_c applied to this CTA's later columns (v_c = 1, v = y_q below row c)
+#pragma unroll
+        for (int q2 = q + 1; q2 < CPC; ++q2) {
+            if (q2 >= nc) break;
+            double d = 0.0;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const int i = tid + QR_NT * j;
+                const double v = (i > c && i < m) ? y[q][j] : (i == c ? 1.0 : 0.0);
+                d += v * y[q2][j];
+            }
+            d = block_sum(d, red);
+            const double wv = tk * d;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const int i = tid + QR_NT * j;
+                const double v = (i > c && i < m) ? y[q][j] : (i == c ? 1.0 : 0.0);
+                y[q2][j] -= wv * v;
+            }
+        }
     }
-    if (tid == 0) tau[c] = tk;
+    // publish: one fence by the releasing thread after the barrier (cumulative)
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        st_release_gpu(ready + c, epoch);
+        for (int q = 0; q < nc; ++q) st_release_gpu(ready + c0 + q, epoch);
     }
     // R(0:c, c) is read only by later kernels
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-        const int i = tid + QR_NT * j;
-        if (i <= c) col[i] = i < c ? y[j] : mu;
+    for (int q = 0; q < CPC; ++q) {
+        if (q >= nc) break;
+        const int c = c0 + q;
+        double* col = A + (long long)c * lda;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + QR_NT * j;
+            if (i <= c) col[i] = i < c ? y[q][j] : mus[q];
+        }
     }
 }
 
-template <int RPT>
-static void* panel_kernel_ptr() { return (void*)k_qr_panel<RPT>; }
+template <int RPT, int CPC>
+static void* panel_kernel_ptr() { return (void*)k_qr_panel<RPT, CPC>; }
 
-static void* panel_kernel_for(int rpt) {
+// columns per CTA: 2 while two register-resident columns fit (RPT <= 16), else 1
+static void* panel_kernel_for(int rpt, int* cpc) {
+    *cpc = rpt <= 16 ? 2 : 1;
     switch (rpt) {
-        case 1: return panel_kernel_ptr<1>();
-        case 2: return panel_kernel_ptr<2>();
-        case 4: return panel_kernel_ptr<4>();
-        case 8: return panel_kernel_ptr<8>();
-        case 16: return panel_kernel_ptr<16>();
-        case 32: return panel_kernel_ptr<32>();
+        case 1: return panel_kernel_ptr<1, 2>();
+        case 2: return panel_kernel_ptr<2, 2>();
+        case 4: return panel_kernel_ptr<4, 2>();
+        case 8: return panel_kernel_ptr<8, 2>();
+        case 16: return panel_kernel_ptr<16, 2>();
+        case 32: return panel_kernel_ptr<32, 1>();
         default: return nullptr;
     }
 }
@@ -420,7 +483,8 @@ int qr_panel_chain(double* A, long long lda, int m, int n, double* tau, int* rea
     static std::atomic<int> epoch{0};
     if (n <= 0) return 0;
     const int rpt = rpt_for(m);
-    void* fn = panel_kernel_for(rpt);
+    int cpc = 1;
+    void* fn = panel_kernel_for(rpt, &cpc);
     if (!fn || n > 1024) return -7;
     const size_t smem = sizeof(double) * (size_t)QR_NT * rpt;
     static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
@@ -432,8 +496,8 @@ int qr_panel_chain(double* A, long long lda, int m, int n, double* tau, int* rea
     }
     int ep = ++epoch;
     if (ep <= 0) { epoch = 1; ep = 1; }
-    void* params[] = {&A, &lda, &m, &tau, &ready, &ep};
-    MPJ_CUDA_TRY(cudaLaunchKernel(fn, dim3(n), dim3(QR_NT), params, smem, st));
+    void* params[] = {&A, &lda, &m, &n, &tau, &ready, &ep};
+    MPJ_CUDA_TRY(cudaLaunchKernel(fn, dim3((n + cpc - 1) / cpc), dim3(QR_NT), params, smem, st));
     MPJ_LAUNCHED();
     return 0;
 }
