@@ -412,11 +412,15 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
         }
         mus[q] = mu;
         double* col = A + (long long)c * lda;
+        // v = x / v0 as x * (1 / v0) (RPT divisions per thread were a visible share of the column step);
+        // the exact quotient where 1 / v0 would leave the normal range
+        const bool recip = fabs(v0) > 1e-290 && fabs(v0) < 1e290;
+        const double rv0 = 1.0 / v0;
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
             const int i = tid + QR_NT * j;
             if (i > c && i < m) {
-                if (scale_v) y[q][j] = y[q][j] / v0;
+                if (scale_v) y[q][j] = recip ? y[q][j] * rv0 : y[q][j] / v0;
                 col[i] = y[q][j];
             }
         }
