@@ -333,40 +333,74 @@ __global__ void k_gate_scale(const double* X, long long ldx, long long rows_pad,
         Xt[i + j * ldt] = d > 0.0f ? (float)X[i + j * ldx] / d : 0.0f;
 }
 
-// 64 x 64 tiles of X_t^T X_t (lower tiles only), max |g - delta| -> out
-__global__ void __launch_bounds__(256) k_gate_orth(const float* Xt, long long ldt, long long rows_pad, int n, double* out) {
+// 128 x 128 tiles of X_t^T X_t (lower tiles only), max |g - delta| -> out.  256 threads, 8 x 8 outputs per
+// thread (rows ty*4 + {0..3} and 64 + ty*4 + {0..3}, likewise columns: float4 shared-memory reads), 16-row
+// K chunks double-buffered in shared memory with the next chunk prefetched into registers.
+constexpr int GO_T = 128, GO_K = 16, GO_LD = GO_T + 4;
+__global__ void __launch_bounds__(256) k_gate_orth(const float* __restrict__ Xt, long long ldt, long long rows_pad,
+                                                   int n, double* out) {
     const int bi = blockIdx.x, bj = blockIdx.y;
     if (bj > bi) return;
-    __shared__ float As[32][65], Bs[32][65];
+    __shared__ __align__(16) float As[2][GO_K][GO_LD];
+    __shared__ __align__(16) float Bs[2][GO_K][GO_LD];
     __shared__ double red[32];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    float acc[4][4] = {};
-    for (long long k0 = 0; k0 < rows_pad; k0 += 32) {
-        for (int e = tid; e < 32 * 64; e += 256) {
-            int kk = e & 31, c = e >> 5;
-            long long ci = (long long)bi * 64 + c, cj = (long long)bj * 64 + c;
-            As[kk][c] = ci < n ? Xt[k0 + kk + ci * ldt] : 0.f;
-            Bs[kk][c] = cj < n ? Xt[k0 + kk + cj * ldt] : 0.f;
+    // loader: column lc = tid / 2 of the tile, rows lr .. lr + 7 of the chunk
+    const int lc = tid >> 1, lr = (tid & 1) * 8;
+    const long long ci = (long long)bi * GO_T + lc, cj = (long long)bj * GO_T + lc;
+    const float* pa = Xt + ci * ldt + lr;
+    const float* pb = Xt + cj * ldt + lr;
+    const bool va = ci < n, vb = cj < n;
+    float4 ra0, ra1, rb0, rb1;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto load = [&](long long k0) {
+        ra0 = va ? __ldg(reinterpret_cast<const float4*>(pa + k0)) : z4;
+        ra1 = va ? __ldg(reinterpret_cast<const float4*>(pa + k0 + 4)) : z4;
+        rb0 = vb ? __ldg(reinterpret_cast<const float4*>(pb + k0)) : z4;
+        rb1 = vb ? __ldg(reinterpret_cast<const float4*>(pb + k0 + 4)) : z4;
+    };
+    auto store = [&](int buf) {
+        const float a[8] = {ra0.x, ra0.y, ra0.z, ra0.w, ra1.x, ra1.y, ra1.z, ra1.w};
+        const float b[8] = {rb0.x, rb0.y, rb0.z, rb0.w, rb1.x, rb1.y, rb1.z, rb1.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r) { As[buf][lr + r][lc] = a[r]; Bs[buf][lr + r][lc] = b[r]; }
+    };
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    load(0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
+    for (long long k0 = 0; k0 < rows_pad; k0 += GO_K) {
+        const bool more = k0 + GO_K < rows_pad;
+        if (more) load(k0 + GO_K);
+#pragma unroll
+        for (int kk = 0; kk < GO_K; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
+        if (more) store(buf ^ 1);
         __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < 32; ++kk) {
-            float a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty + 16 * i]; b[i] = Bs[kk][tx + 16 * i]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
+        buf ^= 1;
     }
     double mx = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            long long gi = (long long)bi * 64 + ty + 16 * i, gj = (long long)bj * 64 + tx + 16 * j;
+        for (int j = 0; j < 8; ++j) {
+            const long long gi = (long long)bi * GO_T + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+            const long long gj = (long long)bj * GO_T + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
             if (gi < n && gj < n) mx = fmax(mx, fabs((double)acc[i][j] - (gi == gj ? 1.0 : 0.0)));
         }
     mx = block_max(mx, red);
@@ -378,7 +412,8 @@ int gates_orth(const double* X, long long ldx, long long rows_pad, int n, float*
     k_gate_scale<<<n, 256, 0, st>>>(X, ldx, rows_pad, n, Xt, ldt);
     MPJ_LAUNCHED();
     MPJ_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
-    dim3 g((unsigned)ceil_div(n, 64), (unsigned)ceil_div(n, 64));
+    if (ldt % 4 || rows_pad % GO_K || ((uintptr_t)Xt & 15)) return -1;   // MPJSVD_ERR_INVALID_ARG
+    dim3 g((unsigned)ceil_div(n, GO_T), (unsigned)ceil_div(n, GO_T));
     k_gate_orth<<<g, 256, 0, st>>>(Xt, ldt, rows_pad, n, out);
     MPJ_LAUNCHED();
     MPJ_CUDA_TRY(cudaGetLastError());

@@ -179,6 +179,19 @@ def test_blocked_qr_panel_modes(mp, monkeypatch, mode):
     assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1 and abs(st["sweeps64"] - sto["sweeps64"]) <= 1
 
 
+@pytest.mark.parametrize("name,n", [("C1", 200), ("C3", 512), ("C2", 352), ("orthcols", 300)])
+def test_gate_orth_measure_vs_oracle(mp, name, n):
+    """The orth gate measure ||X_t^T X_t - I||_max (fp32; k_gate_orth, 128 x 128 tiles, ragged
+    n) against the oracle's plain fp32 triple loop: equal up to fp32 summation order."""
+    if name == "orthcols":
+        a = np.asfortranarray(testmat.haar(n, n, 5) * 10.0 ** np.linspace(0, -12, n))
+    else:
+        a = testmat.config_matrix(name, n)
+    st = mp.factor(dev(a))[3]
+    sto = oracle.mixed_svd(a)[3]
+    assert abs(st["orth_measure"] - sto["orth_measure"]) <= 1e-5 + 1e-3 * sto["orth_measure"]
+
+
 def test_qrp_recompute_path(mp):
     """Strongly decaying partial norms (sigma 1 -> 1e-14) force the partial-norm
     recomputation (xLAQP2 rule) on many columns: pivots and R must still match."""
