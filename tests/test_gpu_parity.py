@@ -159,7 +159,8 @@ def test_blocked_qr_panel_modes(mp, monkeypatch, mode):
     whole mixed-precision SVD (LQ and U-route switch both run the blocked QR) against the oracle."""
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
-    for m, n in ((1000, 300), (700, 700), (2100, 520)):
+    # odd panel widths (a CTA with one column), a 1-column panel, and > 8192 rows (one column per CTA)
+    for m, n in ((1000, 300), (700, 700), (2100, 520), (1000, 301), (600, 257), (9000, 131)):
         rng = np.random.default_rng(m * n)
         a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
         packed, tau, _ = mp.qr(dev(a), pivot=0)
