@@ -365,22 +365,43 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
         double d[CPC];
 #pragma unroll
         for (int q = 0; q < CPC; ++q) d[q] = 0.0;
+        if constexpr (RPT * (CPC + 1) <= 48) {
+            // v at this thread's rows stays in registers (no shared-memory round trip on the chain)
+            double vr[RPT];
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            const int i = tid + QR_NT * j;
-            double v = 0.0;
-            if (i > k && i < m) v = __ldcg(vk + i);
-            else if (i == k) v = 1.0;
-            vsh[tid + QR_NT * j] = v;
+            for (int j = 0; j < RPT; ++j) {
+                const int i = tid + QR_NT * j;
+                vr[j] = (i > k && i < m) ? __ldcg(vk + i) : (i == k ? 1.0 : 0.0);
+            }
 #pragma unroll
-            for (int q = 0; q < CPC; ++q) d[q] += v * y[q][j];
-        }
-        block_sum_vec<CPC>(d, red);
+            for (int j = 0; j < RPT; ++j)
 #pragma unroll
-        for (int q = 0; q < CPC; ++q) {
-            const double wv = tk * d[q];
+                for (int q = 0; q < CPC; ++q) d[q] += vr[j] * y[q][j];
+            block_sum_vec<CPC>(d, red);
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) y[q][j] -= wv * vsh[tid + QR_NT * j];
+            for (int q = 0; q < CPC; ++q) {
+                const double wv = tk * d[q];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) y[q][j] -= wv * vr[j];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const int i = tid + QR_NT * j;
+                double v = 0.0;
+                if (i > k && i < m) v = __ldcg(vk + i);
+                else if (i == k) v = 1.0;
+                vsh[tid + QR_NT * j] = v;
+#pragma unroll
+                for (int q = 0; q < CPC; ++q) d[q] += v * y[q][j];
+            }
+            block_sum_vec<CPC>(d, red);
+#pragma unroll
+            for (int q = 0; q < CPC; ++q) {
+                const double wv = tk * d[q];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) y[q][j] -= wv * vsh[tid + QR_NT * j];
+            }
         }
     }
     double mus[CPC];
