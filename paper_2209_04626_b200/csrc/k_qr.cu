@@ -446,6 +446,13 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
             }
         }
         if (tid == 0) tau[c] = tk;
+        // release column c at once (the next CTA applies H_c while this one forms its next reflector);
+        // one fence by the releasing thread after the barrier (cumulative)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release_gpu(ready + c, epoch);
+        }
         // H_c applied to this CTA's later columns (v_c = 1, v = y_q below row c)
 #pragma unroll
         for (int q2 = q + 1; q2 < CPC; ++q2) {
@@ -466,12 +473,6 @@ __global__ void __launch_bounds__(QR_NT, 1) k_qr_panel(double* __restrict__ A, l
                 y[q2][j] -= wv * v;
             }
         }
-    }
-    // publish: one fence by the releasing thread after the barrier (cumulative)
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        for (int q = 0; q < nc; ++q) st_release_gpu(ready + c0 + q, epoch);
     }
     // R(0:c, c) is read only by later kernels
 #pragma unroll
