@@ -125,6 +125,18 @@ typedef struct {
     double cond_d_min;         /* "condition number of D extremely large": max/min column norm > this, default 1e15 */
     double tail_frac;          /* tail gate: at least ceil(tail_frac n) small columns, default 1/3 */
     int32_t tail_cut_log2;     /* "small": ||x_j|| < 2^tail_cut_log2 max_j ||x_j||, default -60 */
+    /* kernel-variant switches (defaults = the measured best; the alternatives are kept for the
+       bitwise-equality tests and for experiments) */
+    int32_t gram_tma;          /* 1 (default): the fp32 tcgen05 Gram loads its operands by TMA; 0: cp.async */
+    int32_t gram_kt;           /* rows per TMA Gram stage: 0 (default) auto (32 for >= 6144 rows, else 64), 32, 64 */
+    int32_t gram_variant;      /* cp.async tcgen05 Gram stage variant 0..5 (default 0; used only with gram_tma = 0) */
+    int32_t update_tpc;        /* tiles per work item of the overlapped fp32 update; 0 (default): ~3 items per SM */
+    int32_t skip_unchanged;    /* 1 (default): skip the Gram and solve of a pair whose blocks did not rotate since
+                                  its previous evaluation (exact); 0: evaluate every pair */
+    int32_t qr_panel_mode;     /* blocked Householder QR panels: 0 (default) flag-chained with look-ahead,
+                                  1 cooperative grid-barrier kernel, 2 flag-chained without look-ahead */
+    int32_t diag_timing;       /* diagnostics to stderr, bit mask: 1 QRP phases, 2 fp32/fp64 solve phases,
+                                  4 cp.async Gram phases, 8 batched inner-solve phases (default 0) */
 } mpjsvd_options;
 
 typedef struct {
@@ -144,8 +156,8 @@ typedef struct {
     int32_t skip_trace32[32], skip_trace64[32];  /* per sweep: pairs whose Gram and solve were skipped because
                                                     neither block rotated since their previous evaluation
                                                     (exact: same Gram, same metric, no rotation) */
-    double cond_scaled;        /* max_k r_k / min_k r_k, r_k = |R_kk| / ||R(:,k)||: estimate of the column-scaled
-                                  cond(R) used by the AUTO cond gate */
+    double cond_scaled;        /* kappa_1(R diag(1/c)), c_k = ||A1(:, perm_k)|| = ||R(:,k)||: the column-scaled
+                                  cond_R of the AUTO cond gate (Alg. 3 l.423; DESIGN.md c-15); NaN unless AUTO */
     double cond_d;             /* max_j ||A1(:,j)|| / min_j ||A1(:,j)|| (cond(D) of A = B D) */
 } mpjsvd_stats;
 

@@ -128,6 +128,14 @@ def lib():
             L.om_switch_u.argtypes = [dp, i64, i64, dp, i64, dp, i64]
             L.om_mixed_svd.argtypes = [dp, i64, i64, i64, C.POINTER(Opts), dp, i64, dp, dp, i64,
                                        C.POINTER(Stats)]
+            L.om_gate_orth.argtypes = [dp, i64, i64, fp]
+            L.om_gate_orth.restype = C.c_double
+            L.om_gate_tail.argtypes = [dp, i64, i64, C.c_int32]
+            L.om_gate_tail.restype = C.c_double
+            L.om_gate_cond_scaled.argtypes = [dp, i64, i64, dp]
+            L.om_gate_cond_scaled.restype = C.c_double
+            L.om_gate_cond_d.argtypes = [dp, i64]
+            L.om_gate_cond_d.restype = C.c_double
             L.oc_cyclic_jacobi.argtypes = [dp, i64, i64, i64, dp, i64, C.c_double, C.c_int32,
                                            C.POINTER(C.c_int64)]
             L.oc_cyclic_jacobi.restype = C.c_int32
@@ -275,6 +283,31 @@ def switch_u(x: np.ndarray, ulow: np.ndarray) -> tuple[np.ndarray, int]:
     q = np.zeros((n, n), order="F")
     rc = lib().om_switch_u(_dp(x), n, n, _dp(ulow), n, _dp(q), n)
     return q, rc
+
+
+def gate_orth(x: np.ndarray) -> float:
+    """orth = ||X_t^T X_t - I||_max in fp32 (om_gate_orth)."""
+    x = np.asfortranarray(x, dtype=np.float64)
+    n = x.shape[0]
+    work = np.zeros(n * n, dtype=np.float32)
+    return float(lib().om_gate_orth(_dp(x), n, n, _fp(work)))
+
+
+def gate_tail(x: np.ndarray, cut_log2: int = -60) -> float:
+    x = np.asfortranarray(x, dtype=np.float64)
+    return float(lib().om_gate_tail(_dp(x), x.shape[0], x.shape[0], cut_log2))
+
+
+def gate_cond_scaled(r: np.ndarray, c: np.ndarray) -> float:
+    """kappa_1(R diag(1/c)) of the upper triangle of r (om_gate_cond_scaled)."""
+    r = np.asfortranarray(r, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    return float(lib().om_gate_cond_scaled(_dp(r), r.shape[0], r.shape[0], _dp(c)))
+
+
+def gate_cond_d(cn: np.ndarray) -> float:
+    cn = np.ascontiguousarray(cn, dtype=np.float64)
+    return float(lib().om_gate_cond_d(_dp(cn), cn.size))
 
 
 def mixed_svd(a: np.ndarray, **opts):

@@ -409,6 +409,83 @@ static void argsort_desc(const double* key, int64_t n, int64_t* idx) {
     free(rank);
 }
 
+/* ---- gate measures of Alg. 3 (reading c-15) -------------------------
+   Each is a plain loop over its definition; pinned in tests/test_oracle_pins.py (exact constructions,
+   closed forms, invariances, LAPACK). */
+
+/* orth = || X_t^T X_t - I ||_max with X_t = lower(X) D^-1, D_jj the 2-norm of column j of lower(X)
+   (PAPER.md:429-431): lower(X) = fl32(X); ||fl32(x_j)|| is summed in fp64 and rounded to fp32; the Gram
+   X_t^T X_t is "one matrix-matrix multiplication in the lower precision": fp32 products
+   accumulated in fp32 in ascending row order (reading c-17).  work: n*n floats. */
+double om_gate_orth(const double* X, int64_t n, int64_t ldx, float* Xt) {
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) { float f = (float)X[i + j * ldx]; s += (double)f * (double)f; }
+        float d = (float)sqrt(s);
+        for (int64_t i = 0; i < n; ++i) Xt[i + j * n] = d > 0 ? (float)X[i + j * ldx] / d : 0.0f;
+    }
+    double orth = 0.0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(max : orth)
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i <= j; ++i) {
+            float acc = 0.0f;
+            for (int64_t r = 0; r < n; ++r) acc += Xt[r + i * n] * Xt[r + j * n];
+            double dev = fabs((double)acc - (i == j ? 1.0 : 0.0));
+            if (dev > orth) orth = dev;
+        }
+    return orth;
+}
+
+/* fraction of "small" columns of X: ||x_j|| < 2^cut_log2 max_k ||x_k|| (reading c-15) */
+double om_gate_tail(const double* X, int64_t n, int64_t ldx, int32_t cut_log2) {
+    double mxn = 0.0;
+    double* cn = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) { cn[j] = safe_norm(X + j * ldx, n); if (cn[j] > mxn) mxn = cn[j]; }
+    int64_t small = 0;
+    for (int64_t j = 0; j < n; ++j) if (cn[j] < ldexp(mxn, cut_log2)) ++small;
+    free(cn);
+    return (double)small / (double)n;
+}
+
+/* cond_R of Alg. 3 l.423 / kappa(R) of PAPER.md:629-634 for the column-scaled R: kappa_1(R_s) =
+   ||R_s||_1 ||R_s^-1||_1, R_s = R diag(1/c) (R = upper triangle of R, ldr; c_k > 0 the column scales).
+   R_s^-1 = diag(c) R^-1; column j of R^-1 by back substitution R z = e_j. */
+double om_gate_cond_scaled(const double* R, int64_t n, int64_t ldr, const double* c) {
+    double nrm = 0.0, inv = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (!(c[k] > 0.0) || R[k + k * ldr] == 0.0) return INFINITY;
+        double s = 0.0;
+        for (int64_t i = 0; i <= k; ++i) s += fabs(R[i + k * ldr]);
+        s /= c[k];
+        if (s > nrm) nrm = s;
+    }
+#pragma omp parallel for schedule(dynamic, 8) reduction(max : inv)
+    for (int64_t j = 0; j < n; ++j) {
+        double* z = (double*)malloc(sizeof(double) * (size_t)(j + 1));
+        z[j] = 1.0 / R[j + j * ldr];
+        for (int64_t i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t l = i + 1; l <= j; ++l) s += R[i + l * ldr] * z[l];
+            z[i] = -s / R[i + i * ldr];
+        }
+        double cs = 0.0;
+        for (int64_t i = 0; i <= j; ++i) cs += c[i] * fabs(z[i]);
+        if (cs > inv) inv = cs;
+        free(z);
+    }
+    return nrm * inv;
+}
+
+/* condition number of D in A = B D (Alg. 3 l.423-424): max/min column norm */
+double om_gate_cond_d(const double* cn, int64_t n) {
+    double dmx = 0.0, dmn = INFINITY;
+    for (int64_t k = 0; k < n; ++k) {
+        if (cn[k] > dmx) dmx = cn[k];
+        if (cn[k] < dmn) dmn = cn[k];
+    }
+    return dmn > 0.0 ? dmx / dmn : INFINITY;
+}
+
 /* ---- Algorithm 3 ------------------------------------------------------- */
 int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_opts* opts,
                  double* U, int64_t ldu, double* S, double* Vout, int64_t ldv, om_stats* st) {
@@ -481,52 +558,25 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
 
     /* step 5: gate measures, report only (c-15) */
     {
-        double mxn = 0.0, mnr = INFINITY, mxr = 0.0;
+        double mnr = INFINITY, mxr = 0.0;
         for (int64_t j = 0; j < n; ++j) {
             double rjj = fabs(A1[j + j * n]);
             if (rjj > mxr) mxr = rjj;
             if (rjj < mnr) mnr = rjj;
         }
         st->cond_estimate = mnr > 0 ? mxr / mnr : INFINITY;
-        double* cn = key;
-        for (int64_t j = 0; j < n; ++j) { cn[j] = safe_norm(X + j * n, n); if (cn[j] > mxn) mxn = cn[j]; }
-        int64_t small = 0;
-        for (int64_t j = 0; j < n; ++j) if (cn[j] < ldexp(mxn, -60)) ++small;
-        st->tail_fraction = (double)small / (double)n;
-        /* orth = || X_t^T X_t - I ||_max, X_t = fl32(X) D^-1 in fp32 */
-        float* Xt = X32;
-        for (int64_t j = 0; j < n; ++j) {
-            double s = 0.0;
-            for (int64_t i = 0; i < n; ++i) { float f = (float)X[i + j * n]; s += (double)f * (double)f; }
-            float d = (float)sqrt(s);
-            for (int64_t i = 0; i < n; ++i) Xt[i + j * n] = d > 0 ? (float)X[i + j * n] / d : 0.0f;
-        }
-        double orth = 0.0;
-#pragma omp parallel for schedule(dynamic, 4) reduction(max : orth)
-        for (int64_t j = 0; j < n; ++j)
-            for (int64_t i = 0; i <= j; ++i) {
-                float acc = 0.0f;
-                for (int64_t r = 0; r < n; ++r) acc += Xt[r + i * n] * Xt[r + j * n];
-                double dev = fabs((double)acc - (i == j ? 1.0 : 0.0));
-                if (dev > orth) orth = dev;
-            }
-        st->orth_measure = orth;
+        st->tail_fraction = om_gate_tail(X, n, n, -60);
+        st->orth_measure = om_gate_orth(X, n, n, X32);
     }
 
-    /* gate quantities of AUTO (reading c-15): cond_scaled = max/min of r_k = |R_kk| / ||R(:,k)||
-       (||R(:,k)|| = ||A1(:, perm_k)||), cond_d = max/min column norm of A1 */
-    {
-        double rmx = 0.0, rmn = INFINITY, dmx = 0.0, dmn = INFINITY;
-        for (int64_t k = 0; k < n; ++k) {
-            const double cn = a1n[perm[k]];
-            const double rk = cn > 0.0 ? fabs(A1[k + k * n]) / cn : 0.0;
-            if (rk > rmx) rmx = rk;
-            if (rk < rmn) rmn = rk;
-            if (cn > dmx) dmx = cn;
-            if (cn < dmn) dmn = cn;
-        }
-        st->cond_scaled = rmn > 0.0 ? rmx / rmn : INFINITY;
-        st->cond_d = dmn > 0.0 ? dmx / dmn : INFINITY;
+    /* gate quantities of AUTO (reading c-15): cond_scaled = kappa_1 of R diag(1/c), c_k = ||R(:,k)|| =
+       ||A1(:, perm_k)||; cond_d = max/min column norm of A1.  Computed under AUTO only (O(n^3)). */
+    st->cond_scaled = NAN;
+    st->cond_d = NAN;
+    if (o.path == OM_PATH_AUTO) {
+        for (int64_t k = 0; k < n; ++k) key[k] = a1n[perm[k]];
+        st->cond_scaled = om_gate_cond_scaled(A1, n, n, key);
+        st->cond_d = om_gate_cond_d(a1n, n);
     }
     int32_t taken = o.path == OM_PATH_FORCE_FP64 ? OM_PATH_FORCE_FP64 : OM_PATH_FORCE_MIXED;
     if (o.path == OM_PATH_AUTO) {

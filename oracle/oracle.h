@@ -60,8 +60,8 @@ typedef struct {
     double off_trace32[64], off_trace64[64];
     int32_t upd_trace32[64], upd_trace64[64];
     int32_t perm[1];        /* unused placeholder (keeps layout simple) */
-    double cond_scaled;     /* max/min of |R_kk| / ||R(:,k)|| (column-scaled cond(R) estimate) */
-    double cond_d;          /* max/min column norm of A1 (cond(D) of A = B D) */
+    double cond_scaled;     /* kappa_1(R diag(1/||R(:,k)||)) (AUTO only, else NaN) */
+    double cond_d;          /* max/min column norm of A1 (cond(D) of A = B D; AUTO only, else NaN) */
 } om_stats;
 
 /* The low-precision QR SVD of the AUTO branch: a library primitive
@@ -119,6 +119,13 @@ int om_switch_u(const double* X, int64_t n, int64_t ldx, const double* Ulow, int
                 double* Q, int64_t ldq);
 
 /* --- the whole method ------------------------------------------------- */
+/* Gate measures of Alg. 3 (DESIGN.md c-15), on X n x n (ldx) / upper R:
+   orth = ||X_t^T X_t - I||_max (fp32; work: n*n floats), tail = fraction of columns with norm below
+   2^cut_log2 max, cond_scaled = kappa_1(R diag(1/c)), cond_d = max/min of cn[0..n). */
+double om_gate_orth(const double* X, int64_t n, int64_t ldx, float* work);
+double om_gate_tail(const double* X, int64_t n, int64_t ldx, int32_t cut_log2);
+double om_gate_cond_scaled(const double* R, int64_t n, int64_t ldr, const double* c);
+double om_gate_cond_d(const double* cn, int64_t n);
 int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_opts* opts,
                  double* U, int64_t ldu, double* S, double* V, int64_t ldv, om_stats* st);
 

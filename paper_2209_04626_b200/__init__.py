@@ -41,7 +41,10 @@ class Options(C.Structure):
                 ("fp32_tensor_cores", C.c_int32), ("pdl_overlap", C.c_int32),
                 ("mp_rrqr", C.c_int32), ("max_inner32", C.c_int32), ("switch_u", C.c_int32),
                 ("tol_orth", C.c_double), ("tol_alg", C.c_double), ("tol_cond_mult", C.c_double),
-                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32)]
+                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32),
+                ("gram_tma", C.c_int32), ("gram_kt", C.c_int32), ("gram_variant", C.c_int32),
+                ("update_tpc", C.c_int32), ("skip_unchanged", C.c_int32), ("qr_panel_mode", C.c_int32),
+                ("diag_timing", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -313,7 +316,12 @@ def factor(A, handle: Handle | None = None, **opts):
     import torch
     own = handle is None
     if own:
-        stream = torch.cuda.current_stream().cuda_stream if A.is_cuda else None
+        if A.is_cuda:
+            # bind the handle to A's device and that device's current stream (not the current device's)
+            opts.setdefault("device_id", A.device.index)
+            stream = torch.cuda.current_stream(A.device).cuda_stream
+        else:
+            stream = None
         handle = Handle(stream=stream, **opts)
     try:
         Ac, lda = _col_major(A)
@@ -384,14 +392,14 @@ def inner_solve(G, tol_in: float, max_inner: int = 30, handle: Handle | None = N
             handle.close()
 
 
-def qr(A, pivot: int = 1, handle: Handle | None = None):
+def qr(A, pivot: int = 1, handle: Handle | None = None, **opts):
     """Step-level: Householder QR on a copy of a device fp64 tensor.
     pivot = 1: column-pivoted (lazy cooperative kernel of the path), 2: the
     unblocked pivoted kernel, 0: blocked unpivoted QR.  Returns (packed, tau, perm)."""
     import torch
     own = handle is None
     if own:
-        handle = Handle(stream=torch.cuda.current_stream().cuda_stream)
+        handle = Handle(stream=torch.cuda.current_stream().cuda_stream, **opts)
     try:
         Ac, lda = _col_major(A.clone())
         m, n = Ac.shape

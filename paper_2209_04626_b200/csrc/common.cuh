@@ -14,9 +14,18 @@
 
 void mpj_record_cuda_error(cudaError_t e, const char* what, const char* file, int line);
 
+// mpjsvd_options.diag_timing of the call in progress on this host thread (set at every entry point)
+extern thread_local int g_mpj_diag;
+
 // count of kernel launches issued by the engine (reported in stats)
 extern thread_local int64_t g_mpj_launches;
 #define MPJ_LAUNCHED() (++g_mpj_launches)
+
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device (the attribute is per
+// device; cached per (kernel, device) under a lock, so handles on several GPUs or threads are safe).
+cudaError_t mpj_set_smem(const void* fn, size_t bytes);
+template <typename F>
+static inline cudaError_t set_smem(F* fn, size_t bytes) { return mpj_set_smem(reinterpret_cast<const void*>(fn), bytes); }
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -61,6 +70,16 @@ __device__ __forceinline__ T block_max(T v, T* red) {
     __syncthreads();
     return r;
 }
+
+// wall-clock nanoseconds (for spin-wait time-outs that must not depend on the clock rate,
+// time-slicing or a sanitizer's slowdown)
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// a consumer gives up waiting for a producer after this long (a hung producer, not a slow one)
+constexpr unsigned long long MPJ_SPIN_TIMEOUT_NS = 120ull * 1000000000ull;
 
 // atomic max of a non-negative double via its bit pattern (exact, order-free)
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {

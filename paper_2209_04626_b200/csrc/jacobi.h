@@ -65,6 +65,11 @@ struct JacobiRound {
     int* last_mod;
     double* pair_off;
     int gidx, R, skip;
+    // kernel-variant switches from the handle's options (no environment reads on the launch path)
+    int gram_kt;        // rows per TMA Gram stage (32 / 64), resolved on the host
+    int gram_variant;   // cp.async tcgen05 Gram variant
+    int update_tpc;     // 0: auto
+    int diag;           // mpjsvd_options.diag_timing
 };
 
 // the pair's blocks are unchanged since its previous evaluation (exactly one sweep ago)
@@ -101,20 +106,20 @@ struct ProfHook {
 template <typename T>
 int launch_jacobi_round(const JacobiRound<T>& a, int W, cudaStream_t st, const ProfHook* hook = nullptr);
 template <typename T>
-int gram_ctas_per_sm(int W, int use_tc, long long rows_pad);
+int gram_ctas_per_sm(int W, int use_tc, long long rows_pad, int tma, int kt, int variant);
 // tcgen05 fp32 kernels (k_tc.cu)
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st);
 // MPJSVD_SOLVE_TIMING=1: print k_pair_solve phase clocks (CTA 0) accumulated over a sweep (tools only)
 void solve_timing_report(const char* tag, int sweep);
 // 4-D TMA view of the column-major fp32 matrix (rows_pad x cols, ld) whose boxes land in the canonical
 // K-major SWIZZLE_NONE operand layout of k_pair_gram_tma; out = 128-byte CUtensorMap.  0 on success.
-int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
-int gram_tma_kt(long long rows_pad);
+int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols, int kt);
+int gram_tma_kt(long long rows_pad, int forced);
 int make_update_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);
 // persistent overlapped variant: drains pairs in the order the solve publishes them (a.pdl)
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st);
-int gram_tc_ctas_per_sm(long long rows_pad);
+int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant);
 template <typename T>
 int launch_inner_batch(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st);
 
@@ -209,6 +214,10 @@ int copy_matrix(const double* src, long long lds, double* dst, long long ldd, lo
                 cudaStream_t st);
 template <typename T>
 int set_identity(T* A, long long lda, long long rows_pad, long long n, cudaStream_t st);
+// AUTO cond gate (DESIGN.md c-15): out2[0] = ||R_s||_1, out2[1] = ||R_s^-1||_1 for R_s = R diag(1/c),
+// c_k = a1n[perm[k]] (written to c); Z (rows_pad x n, ldz) is workspace.
+int gate_cond_scaled(const double* R, long long ldr, const double* a1n, const int* perm, int n, double* c,
+                     double* Z, long long ldz, long long rows_pad, double* out2, cudaStream_t st);
 int transpose_upper(const double* R, long long ldr, double* Rt, long long ldt, int n, long long rows_pad,
                     cudaStream_t st);
 int lower_from_rt(const double* Rt, long long ldt, double* X, long long ldx, int n, long long rows_pad,

@@ -1119,11 +1119,14 @@ __global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma_pdl(JacobiRound<d
                 which = rem / ngroups;
                 grp = rem % ngroups;
                 int pr = ld_acquire_gpu(a.dlist + p);
-                long long spins = 0;
+                unsigned long long t0 = 0;
                 while (pr < 0) {
                     __nanosleep(256);
                     pr = ld_acquire_gpu(a.dlist + p);
-                    if (++spins > (1LL << 24)) { atomicExch(a.dctr + 2, 1); break; }
+                    if (pr >= 0) break;
+                    const unsigned long long t = global_ns();
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > MPJ_SPIN_TIMEOUT_NS) { atomicExch(a.dctr + 2, 1); break; }
                 }
                 if (pr < 0) { pair = -1; break; }
                 if (!a.flag[pr] || (which && !a.has_v)) continue;
@@ -1213,11 +1216,7 @@ __global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma_pdl(JacobiRound<d
 template <int W>
 static int launch_update_dmma_pdl(const JacobiRound<double>& a, cudaStream_t st) {
     const size_t dsm = update_dmma_smem<W>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pair_update_dmma_pdl<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-        attr = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_pair_update_dmma_pdl<W>, (size_t)(dsm)));
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1363,12 +1362,7 @@ template <typename T, int W>
 static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHook* hook) {
     if (hook) hook->begin(hook->ctx, KName<T>::gram);
     if constexpr (sizeof(T) == 8) {
-        static bool attr_g = false;
-        if (!attr_g) {
-            cudaFuncSetAttribute(k_pair_gram_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)gram_dmma_smem(W));
-            attr_g = true;
-        }
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_dmma<W>, (size_t)(gram_dmma_smem(W))));
         k_pair_gram_dmma<W><<<dim3(a.nsplit, a.npairs), 128, gram_dmma_smem(W), st>>>(a);
     } else if constexpr (W == 64) {
         if (a.use_tc) {
@@ -1377,11 +1371,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
             goto solve;
         }
         const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
-        static bool attr_t = false;
-        if (!attr_t) {
-            cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
-            attr_t = true;
-        }
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_f32t, (size_t)(g32)));
         k_pair_gram_f32t<<<dim3(a.nsplit, a.npairs), G32_NT, g32, st>>>(a);
     } else {
         k_pair_gram<T, W><<<dim3(a.nsplit, a.npairs), 64, 0, st>>>(a);
@@ -1390,11 +1380,7 @@ static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHo
     if (hook) hook->end(hook->ctx, KName<T>::gram);
 solve:
     const size_t sms = sizeof(InnerSmem<T, W>);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_pair_solve<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-        attr_set = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_pair_solve<T, W>, sms));
     // overlapped update (fp32 tcgen05 with programmatic dependent launch): no event may sit
     // between the solve and the update, so one bracket covers both
     const bool overlap = a.pdl && (sizeof(T) == 8 || (W == 64 && a.use_tc));
@@ -1419,30 +1405,18 @@ solve:
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
     constexpr int VEC = 16 / sizeof(T);
     const size_t usm = sizeof(T) * (size_t)W * ((64 + VEC) + (W + VEC)) + sizeof(long long) * W;
-    static bool attr_u = false;
-    if (!attr_u) {
-        cudaFuncSetAttribute(k_pair_update<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
-        attr_u = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_pair_update<T, W>, usm));
     if (hook) hook->begin(hook->ctx, KName<T>::update);
     if constexpr (sizeof(T) == 8) {
         const size_t dsm = update_dmma_smem<W>();
-        static bool attr_d = false;
-        if (!attr_d) {
-            cudaFuncSetAttribute(k_pair_update_dmma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-            attr_d = true;
-        }
+        MPJ_CUDA_TRY(set_smem(k_pair_update_dmma<W>, (size_t)(dsm)));
         k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, (long long)UD_RC * UD_TPC), a.npairs, a.has_v ? 2 : 1),
                                 UD_NT, dsm, st>>>(a);
     } else if (W == 64 && a.use_tc) {
         if constexpr (sizeof(T) == 4) launch_update_tc(a, st);
     } else {
         const size_t fsm = sizeof(float) * (size_t)W * ((128 + 4) + (W + 4)) + sizeof(long long) * W;
-        static bool attr_f = false;
-        if (!attr_f) {
-            cudaFuncSetAttribute(k_pair_update_f32<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-            attr_f = true;
-        }
+        MPJ_CUDA_TRY(set_smem(k_pair_update_f32<W>, (size_t)(fsm)));
         (void)usm;
         k_pair_update_f32<W><<<dim3((unsigned)ceil_div(rows_pad, 128), a.npairs, a.has_v ? 2 : 1), 256, fsm, st>>>(a);
     }
@@ -1458,7 +1432,7 @@ solve:
 
 // resident CTAs per SM of the Gram kernel used for (T, W) (for the split choice)
 template <typename T>
-int gram_ctas_per_sm(int W, int use_tc, long long rows_pad) {
+int gram_ctas_per_sm(int W, int use_tc, long long rows_pad, int tma, int kt, int variant) {
     int per = 1;
     if constexpr (sizeof(T) == 8) {
         const size_t smem = gram_dmma_smem(W);
@@ -1474,7 +1448,7 @@ int gram_ctas_per_sm(int W, int use_tc, long long rows_pad) {
         }
     } else {
         if (W == 64 && use_tc) {
-            per = gram_tc_ctas_per_sm(rows_pad);
+            per = gram_tc_ctas_per_sm(rows_pad, tma, kt, variant);
         } else if (W == 64) {
             const size_t g32 = sizeof(float4) * G32_ST * 64 * 8;
             cudaFuncSetAttribute(k_pair_gram_f32t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g32);
@@ -1488,23 +1462,18 @@ int gram_ctas_per_sm(int W, int use_tc, long long rows_pad) {
     cudaGetLastError();
     return per < 1 ? 1 : per;
 }
-template int gram_ctas_per_sm<float>(int, int, long long);
-template int gram_ctas_per_sm<double>(int, int, long long);
+template int gram_ctas_per_sm<float>(int, int, long long, int, int, int);
+template int gram_ctas_per_sm<double>(int, int, long long, int, int, int);
 
 void solve_timing_report(const char* tag, int sweep) {
     static long long* dbg = nullptr;
-    static int on = -1;
-    if (on < 0) {
-        const char* e = getenv("MPJSVD_SOLVE_TIMING");
-        on = (e && e[0] == '1') ? 1 : 0;
-        if (on) {
-            cudaMalloc(&dbg, 8 * sizeof(long long));
-            cudaMemset(dbg, 0, 8 * sizeof(long long));
-            cudaMemcpyToSymbol(g_solve_dbg, &dbg, sizeof(dbg));
-            return;
-        }
+    if (!(g_mpj_diag & 2)) return;
+    if (!dbg) {
+        cudaMalloc(&dbg, 8 * sizeof(long long));
+        cudaMemset(dbg, 0, 8 * sizeof(long long));
+        cudaMemcpyToSymbol(g_solve_dbg, &dbg, sizeof(dbg));
+        return;
     }
-    if (!on) return;
     long long hv[8];
     cudaMemcpy(hv, dbg, sizeof(hv), cudaMemcpyDeviceToHost);
     const double nl = hv[4] > 0 ? (double)hv[4] : 1.0, ns = hv[3] > 0 ? (double)hv[3] : 1.0;
@@ -1528,10 +1497,9 @@ template int launch_jacobi_round<double>(const JacobiRound<double>&, int, cudaSt
 template <typename T, int W>
 static int inner_batch_w(T* G, T* E, int w, T tol_in, int max_inner, int count, int* rot, cudaStream_t st) {
     const size_t sms = sizeof(InnerSmem<T, W>);
-    cudaFuncSetAttribute(k_inner_solve_batch<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
+    MPJ_CUDA_TRY(set_smem(k_inner_solve_batch<T, W>, sms));
     static long long* dbg = nullptr;
-    const char* env = getenv("MPJSVD_INNER_TIMING");
-    const bool timing = env && env[0] == '1';
+    const bool timing = (g_mpj_diag & 8) != 0;
     if (timing) {
         if (!dbg) cudaMalloc(&dbg, 8 * sizeof(long long));
         cudaMemsetAsync(dbg, 0, 8 * sizeof(long long), st);

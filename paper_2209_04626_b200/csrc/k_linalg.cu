@@ -183,12 +183,8 @@ void gemm_set_workspace(double* ws, size_t elems) {
 int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
                 const double* B, long long ldb, double beta, double* C, long long ldc, int shape, cudaStream_t st) {
     if (M <= 0 || N <= 0) return 0;
-    static bool attr = false;
     const size_t smem = sizeof(double) * (size_t)GM_ST * GM_BK * (GM_SA + GM_SB);
-    if (!attr) {
-        cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_gemm_f64, smem));
     const int vec_a = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
     const int vec_b = (ldb % 2 == 0) && (((uintptr_t)B & 15) == 0);
     dim3 grid((unsigned)ceil_div(M, GM_BM), (unsigned)ceil_div(N, GM_BN));
@@ -454,11 +450,7 @@ static int apply_panel(const double* P, long long ldp, long long rows, int kb, c
     }
     rc = gemm_f64(1, 0, WY_NB, WY_NB, rows, 1.0, Vp, ldw, Vp, ldw, 0.0, S, WY_NB, st);
     if (rc) return rc;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)larft_smem());
-        attr = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_larft, (size_t)(larft_smem())));
     // T in LT_NB blocks: diagonal blocks by k_larft, then the recursive coupling
     // T[0:a, a:b] = -T[0:a, 0:a] S[0:a, a:b] T[a:b, a:b] (LAPACK xLARFT, recursive form)
     MPJ_CUDA_TRY(cudaMemsetAsync(T, 0, sizeof(double) * WY_NB * WY_NB, st));

@@ -420,4 +420,43 @@ int gates_orth(const double* X, long long ldx, long long rows_pad, int n, float*
     return 0;
 }
 
+// ---- cond gate of AUTO (Alg. 3 l.423; DESIGN.md c-15): kappa_1(R diag(1/c)) with
+// c_k = ||A1(:, perm_k)|| = ||R(:,k)||.  Z = diag(c) R^-1 = R_s^-1 comes from the triangular solve; these
+// kernels give the column scales and the two 1-norms (max over columns of the absolute column sums).
+__global__ void k_gate_scales(const double* a1n, const int* perm, int n, double* c, double* Z, long long ldz,
+                              long long rows_pad) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y) {
+        const double cj = a1n[perm[j]];
+        if (blockIdx.x == 0 && threadIdx.x == 0) c[j] = cj;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            Z[i + j * ldz] = i == j ? cj : 0.0;
+    }
+}
+// out = max_j (sum_{i < rows_j} |Z_ij|) / (c ? c_j : 1), rows_j = j + 1 (upper) or rows
+__global__ void k_col_abs_sum_max(const double* Z, long long ldz, long long rows, int n, const double* c, int upper,
+                                  double* out) {
+    __shared__ double red[32];
+    for (int j = blockIdx.x; j < n; j += gridDim.x) {
+        const long long r = upper ? (long long)j + 1 : rows;
+        double s = 0.0;
+        for (long long i = threadIdx.x; i < r; i += blockDim.x) s += fabs(Z[i + (long long)j * ldz]);
+        s = block_sum(s, red);
+        if (threadIdx.x == 0) atomic_max_nonneg(out, c ? s / c[j] : s);
+    }
+}
+int gate_cond_scaled(const double* R, long long ldr, const double* a1n, const int* perm, int n, double* c,
+                     double* Z, long long ldz, long long rows_pad, double* out2, cudaStream_t st) {
+    MPJ_CUDA_TRY(cudaMemsetAsync(out2, 0, 2 * sizeof(double), st));
+    k_gate_scales<<<grid2d(rows_pad, n), 256, 0, st>>>(a1n, perm, n, c, Z, ldz, rows_pad);
+    MPJ_LAUNCHED();
+    k_col_abs_sum_max<<<n < 1184 ? n : 1184, 256, 0, st>>>(R, ldr, n, n, c, 1, out2);   // ||R_s||_1
+    MPJ_LAUNCHED();
+    int rc = trsm_right_upper(R, ldr, Z, ldz, rows_pad, n, st);                        // Z = diag(c) R^-1
+    if (rc) return rc;
+    k_col_abs_sum_max<<<n < 1184 ? n : 1184, 256, 0, st>>>(Z, ldz, n, n, nullptr, 0, out2 + 1);   // ||R_s^-1||_1
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 }  // namespace mpj

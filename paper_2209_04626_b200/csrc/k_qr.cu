@@ -513,13 +513,7 @@ int qr_panel_chain(double* A, long long lda, int m, int n, double* tau, int* rea
     void* fn = panel_kernel_for(rpt, &cpc);
     if (!fn || n > 1024) return -7;
     const size_t smem = sizeof(double) * (size_t)QR_NT * rpt;
-    static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
-    int slot = 0;
-    while ((1 << slot) < rpt) ++slot;
-    if (attr_set[slot] < smem) {
-        MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set[slot] = smem;
-    }
+    MPJ_CUDA_TRY(mpj_set_smem(reinterpret_cast<const void*>(fn), smem));
     int ep = ++epoch;
     if (ep <= 0) { epoch = 1; ep = 1; }
     void* params[] = {&A, &lda, &m, &n, &tau, &ready, &ep};

@@ -217,7 +217,10 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 if (v > bv || (v == bv && psv[j] < bp)) { bv = v; bp = psv[j]; bc = pcv[j]; }
             }
             warp_argmax(bv, bp, bc);
-            const int pv = __shfl_sync(0xffffffffu, bc, 0);
+            int pv = __shfl_sync(0xffffffffu, bc, 0);
+            // no finite candidate (NaN partial norms): keep the column in place instead of indexing
+            // with -1 (the host returns MPJSVD_ERR_NONFINITE before the QRP; this guards direct calls)
+            if (pv < 0) pv = phys[k];
             if (tid < jj) fpiv[tid] = __ldcg(a.F + (long long)pv * QP_NB + tid);
             if (tid == 0) {
                 s_piv = pv;
@@ -613,8 +616,7 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
     args.nown = nown;
     args.dbg = nullptr;
     static long long* dbg = nullptr;
-    const char* env = getenv("MPJSVD_QRP_TIMING");
-    if (env && env[0] == '1') {
+    if (g_mpj_diag & 1) {
         if (!dbg) cudaMalloc(&dbg, (16 + 10 * 1024) * sizeof(long long));
         args.dbg = dbg;
     }

@@ -407,14 +407,12 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tma(JacobiRound<float
 // rows per stage of the TMA Gram (MPJSVD_GRAM_KT = 32 or 64): KT = 64 -> 3 x 32 KB stages, 2 CTAs per SM;
 // KT = 32 -> 3 x 16 KB stages, 4 CTAs per SM
 // Default by row count (measured on B200): 32 for >= 6144 rows (C5: Gram 237 -> 217 ms), 64 below (C3: 33 vs 35 ms)
-int gram_tma_kt(long long rows_pad) {
-    const char* e = getenv("MPJSVD_GRAM_KT");
-    if (e && (atoi(e) == 32 || atoi(e) == 64)) return atoi(e);
+int gram_tma_kt(long long rows_pad, int forced) {
+    if (forced == 32 || forced == 64) return forced;
     return rows_pad >= 6144 ? 32 : 64;
 }
 
-int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols) {
-    const int kt = gram_tma_kt(rows_pad);
+int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols, int kt) {
     typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -688,11 +686,14 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
                 which = rem / ngroups;
                 grp = rem % ngroups;
                 int pr = ld_acquire_gpu(a.dlist + p);
-                long long spins = 0;
+                unsigned long long t0 = 0;
                 while (pr < 0) {
                     __nanosleep(256);
                     pr = ld_acquire_gpu(a.dlist + p);
-                    if (++spins > (1LL << 24)) { atomicExch(a.dctr + 2, 1); break; }
+                    if (pr >= 0) break;
+                    const unsigned long long t = global_ns();
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > MPJ_SPIN_TIMEOUT_NS) { atomicExch(a.dctr + 2, 1); break; }
                 }
                 if (pr < 0) { pair = -1; break; }
                 if (!a.flag[pr] || (which && !a.has_v)) continue;
@@ -859,13 +860,8 @@ static const GramVariant g_gram_variants[] = {
     {k_pair_gram_tc<32, 4, 3>, gram_tc_smem<32, 4>(), 3},
     {k_pair_gram_tc<64, 4, 1>, gram_tc_smem<64, 4>(), 1},
 };
-static const GramVariant& gram_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("MPJSVD_GRAM_VARIANT");
-        v = e ? atoi(e) : 0;
-        if (v < 0 || v >= (int)(sizeof(g_gram_variants) / sizeof(g_gram_variants[0]))) v = 0;
-    }
+static const GramVariant& gram_variant(int v) {
+    if (v < 0 || v >= (int)(sizeof(g_gram_variants) / sizeof(g_gram_variants[0]))) v = 0;
     return g_gram_variants[v];
 }
 
@@ -896,13 +892,9 @@ int make_update_tmap(void* out, const float* base, long long ld, long long rows_
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
     if (a.tmap) {
-        static bool attr_m = false;
-        if (!attr_m) {
-            cudaFuncSetAttribute(k_pair_gram_tma<64, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem<64, 3>());
-            cudaFuncSetAttribute(k_pair_gram_tma<32, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tma_smem<32, 3>());
-            attr_m = true;
-        }
-        if (gram_tma_kt(a.m_pad) == 32)
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<64, 3, 2>, gram_tma_smem<64, 3>()));
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<32, 3, 4>, gram_tma_smem<32, 3>()));
+        if (a.gram_kt == 32)
             k_pair_gram_tma<32, 3, 4><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 3>(), st>>>(
                 a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
         else
@@ -911,15 +903,11 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
         MPJ_LAUNCHED();
         return 0;
     }
-    const GramVariant& gv = gram_variant();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gv.smem);
-        attr = true;
-    }
+    const GramVariant& gv = gram_variant(a.gram_variant);
+    MPJ_CUDA_TRY(set_smem(gv.fn, (size_t)(gv.smem)));
     static long long* dbg = nullptr;
     static long long calls = 0;
-    static const bool timing = getenv("MPJSVD_GRAM_TIMING") != nullptr;
+    const bool timing = (a.diag & 4) != 0;
     if (timing && !dbg) {
         cudaMalloc(&dbg, 8 * sizeof(long long));
         cudaMemset(dbg, 0, 8 * sizeof(long long));
@@ -938,11 +926,7 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
 }
 
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pair_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
-        attr = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_pair_update_tc, (size_t)(update_tc_smem())));
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
     const long long tiles = (rows_pad + UT_TM - 1) / UT_TM;
     const int tpc = tiles >= 16 ? 16 : (int)tiles;
@@ -952,13 +936,10 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
     return 0;
 }
 
-int gram_tc_ctas_per_sm(long long rows_pad) {
-    {
-        const char* env = getenv("MPJSVD_GRAM_TMA");
-        if (!(env && env[0] == '0')) return gram_tma_kt(rows_pad) == 32 ? 4 : 2;
-    }
+int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
+    if (tma) return gram_tma_kt(rows_pad, kt) == 32 ? 4 : 2;
     // shared memory bound: (stages + alignment + static) per CTA of 228 KB per SM
-    const GramVariant& gv = gram_variant();
+    const GramVariant& gv = gram_variant(variant);
     const int per = (int)((228 * 1024) / (gv.smem + 2048));
     return per < gv.per_sm ? per : gv.per_sm;
 }
@@ -967,12 +948,8 @@ int gram_tc_ctas_per_sm(long long rows_pad) {
 
 namespace mpj {
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pair_update_tc_pdl<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
-        cudaFuncSetAttribute(k_pair_update_tc_pdl<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_tc_smem());
-        attr = true;
-    }
+    MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<true>, (size_t)(update_tc_smem())));
+    MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<false>, (size_t)(update_tc_smem())));
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -983,10 +960,7 @@ int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     int tpc = UT_TPC;
     while (tpc > 2 && (long long)a.npairs * (a.has_v ? 2 : 1) * ((rows_pad + (long long)tpc * UT_TM - 1) / ((long long)tpc * UT_TM)) < 3LL * nsm)
         tpc >>= 1;
-    {
-        const char* e = getenv("MPJSVD_UPDATE_TPC");    // experiment hook: tiles per work item
-        if (e && atoi(e) > 0) tpc = atoi(e);
-    }
+    if (a.update_tpc > 0) tpc = a.update_tpc;    // options.update_tpc (experiments)
     const int ngroups = (int)((rows_pad + (long long)tpc * UT_TM - 1) / ((long long)tpc * UT_TM));
     const long long items = (long long)a.npairs * 2 * ngroups;
     const unsigned grid = (unsigned)(items < nsm ? items : nsm);

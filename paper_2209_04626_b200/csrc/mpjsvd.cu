@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -21,7 +22,22 @@
 #include "shard.h"
 
 thread_local int64_t g_mpj_launches = 0;
+thread_local int g_mpj_diag = 0;
 static thread_local char g_last_cuda_err[512] = "no error";
+
+cudaError_t mpj_set_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{fn, dev}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
 
 void mpj_record_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
     snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "%s (%d) in %s at %s:%d", cudaGetErrorString(e), (int)e,
@@ -42,7 +58,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC, S_QR_RDY,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_GATEC, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -265,7 +281,8 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     } else {
         // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
         // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
-        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc, m_pad);
+        const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc, m_pad, h->opts.gram_tma,
+                                                                           h->opts.gram_kt, h->opts.gram_variant);
         const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
         double best = 1e30;
         for (long long ns = 1; ns <= maxsplit; ++ns) {
@@ -300,6 +317,10 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.partial = P<T>(h, S_PART); a.E = P<T>(h, S_E); a.flag = P<int>(h, S_JFLAG);
     a.tol = tol; a.tol_in = tol_in; a.max_inner = max_inner;
     a.use_tc = use_tc;
+    a.gram_kt = gram_tma_kt(m_pad, h->opts.gram_kt);
+    a.gram_variant = h->opts.gram_variant;
+    a.update_tpc = h->opts.update_tpc;
+    a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
@@ -312,8 +333,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.tbase = nullptr;
     a.tld = 0;
     if constexpr (sizeof(T) == 4) {
-        const char* env = getenv("MPJSVD_GRAM_TMA");
-        if (use_tc && !(env && env[0] == '0')) {
+        if (use_tc && h->opts.gram_tma) {
             T* base = nullptr;
             long long cols = 0;
             for (int g = 0; g < S.plan.G; ++g)
@@ -327,7 +347,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
                 a.tld = ldx;
             }
             if (base && !has_v && make_update_tmap(umap_buf, base, ldx, m_pad, cols) == 0) a.umap = umap_buf;
-            if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols) == 0) {
+            if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols, a.gram_kt) == 0) {
                 a.tmap = tmap_buf;
                 // a TMA box covers 64 rows and only zero-fills past the matrix: row slabs must be whole boxes
                 a.rows_per_split = round_up(a.rows_per_split, 64LL);
@@ -341,10 +361,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     MPJ_TRY(ensure(h, S_POFF, sizeof(double) * (size_t)R * npairs));
     a.last_mod = P<int>(h, S_LMOD);
     a.R = R;
-    {
-        const char* env = getenv("MPJSVD_SKIP_UNCHANGED");
-        a.skip = (S.me < 0 && !(env && env[0] == '0')) ? 1 : 0;
-    }
+    a.skip = (S.me < 0 && h->opts.skip_unchanged) ? 1 : 0;
     MPJ_CUDA_TRY(cudaMemsetAsync(a.last_mod, 0xff, sizeof(int) * (size_t)(S.plan.M + 8), st));   // -1
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
@@ -557,9 +574,8 @@ int ensure_qr_work(mpjsvd_handle h, int m, int n, QrWork& w) {
         MPJ_TRY(ensure(h, S_QR_RDY, sizeof(int) * 1024));
         MPJ_CUDA_TRY(cudaMemsetAsync(h->buf[S_QR_RDY], 0, sizeof(int) * 1024, h->stream));
     }
-    w.ready = getenv("MPJSVD_QR_PANEL_COOP") ? nullptr : P<int>(h, S_QR_RDY);
-    const char* la = getenv("MPJSVD_QR_LOOKAHEAD");
-    const bool lookahead = w.ready && !(la && la[0] == '0');
+    w.ready = h->opts.qr_panel_mode == 1 ? nullptr : P<int>(h, S_QR_RDY);
+    const bool lookahead = w.ready && h->opts.qr_panel_mode == 0;
     w.la_stream = lookahead ? h->qaux : nullptr;
     w.la_ev0 = h->qev0;
     w.la_ev1 = h->qev1;
@@ -699,12 +715,24 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     const bool autop = o.path == MPJSVD_PATH_AUTO;
     int taken = o.path == MPJSVD_PATH_FORCE_FP64 ? MPJSVD_TAKEN_FP64 : MPJSVD_TAKEN_JACOBI;
     double cond_scaled = NAN, cond_d = NAN;
+    bool input_ok = true;
     if (root) {
     // ---- input -> padded device copy (host memory is staged here: e2e path)
     MPJ_CUDA_TRY(cudaMemsetAsync(dA, 0, sizeof(double) * (size_t)m_pad * n, st));
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(dA, sizeof(double) * m_pad, A, sizeof(double) * lda, sizeof(double) * m, n,
                                    a_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     MPJ_TRY(check_finite(dA, m_pad, m, n, flags + 0, st));
+    // a non-finite input must not reach the QRP (its argmax has no finite candidate): read the flag now
+    MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr + 7, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        int bad = 0;
+        memcpy(&bad, h_hdr + 7, sizeof(int));
+        input_ok = bad == 0;
+    }
+    if (!input_ok && !dist) return MPJSVD_ERR_NONFINITE;
+    }  // root
+    if (root && input_ok) {
 
     // ---- stage 0: tall QR  A = Q_tall R1
     if (m > n) {
@@ -794,27 +822,27 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (autop) {
         // Alg. 3 gates in order (reading c-15): cond, tail (654-663), orth
         // (428-433, 636-650), then Jacobi if orth <= tol_alg else the fp32 QR SVD (435-445)
-        std::vector<double> rdiag(n), a1n(n), xn(n);
-        std::vector<int> pv(n);
-        double horth = 0.0;
-        MPJ_CUDA_TRY(cudaMemcpy2DAsync(rdiag.data(), sizeof(double), dA1L, sizeof(double) * (n_pad + 1), sizeof(double), n,
-                                       cudaMemcpyDeviceToHost, st));
+        // cond_R = kappa_1(R diag(1/c)), c_k = ||A1(:, perm_k)||: Z = diag(c) R^-1 by the triangular solve
+        // (dY is free until Y = X Q), the two 1-norms by column reductions
+        MPJ_TRY(ensure(h, S_GATEC, sizeof(double) * (size_t)n + 2 * sizeof(double)));
+        double* d_gc = P<double>(h, S_GATEC);
+        MPJ_TRY(gate_cond_scaled(dA1L, n_pad, P<double>(h, S_A1N), P<int>(h, S_PERM), (int)n, d_gc, dY, n_pad, n_pad,
+                                 d_gc + n, st));
+        std::vector<double> a1n(n), xn(n);
+        double horth = 0.0, norms2[2] = {0.0, 0.0};
         MPJ_CUDA_TRY(cudaMemcpyAsync(a1n.data(), P<double>(h, S_A1N), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(xn.data(), P<double>(h, S_XNORM), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-        MPJ_CUDA_TRY(cudaMemcpyAsync(pv.data(), P<int>(h, S_PERM), sizeof(int) * n, cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(&horth, scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPJ_CUDA_TRY(cudaMemcpyAsync(norms2, d_gc + n, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
-        double rmx = 0.0, rmn = INFINITY, dmx = 0.0, dmn = INFINITY, xmx = 0.0;
+        double dmx = 0.0, dmn = INFINITY, xmx = 0.0;
         for (int64_t k = 0; k < n; ++k) {
-            const double cn = a1n[pv[k]];
-            const double rk = cn > 0.0 ? fabs(rdiag[k]) / cn : 0.0;
-            rmx = rk > rmx ? rk : rmx;
-            rmn = rk < rmn ? rk : rmn;
-            dmx = cn > dmx ? cn : dmx;
-            dmn = cn < dmn ? cn : dmn;
+            dmx = a1n[k] > dmx ? a1n[k] : dmx;
+            dmn = a1n[k] < dmn ? a1n[k] : dmn;
             xmx = xn[k] > xmx ? xn[k] : xmx;
         }
-        cond_scaled = rmn > 0.0 ? rmx / rmn : INFINITY;
+        cond_scaled = norms2[0] * norms2[1];
+        if (!(cond_scaled == cond_scaled)) cond_scaled = INFINITY;
         cond_d = dmn > 0.0 ? dmx / dmn : INFINITY;
         long long small = 0;
         for (int64_t j = 0; j < n; ++j) small += xn[j] < ldexp(xmx, o.tail_cut_log2) ? 1 : 0;
@@ -1090,6 +1118,7 @@ static int jacobi_entry(mpjsvd_handle h, T* X, int64_t m, int64_t n, int64_t ldx
                         T tol, T tol_in, int32_t max_sweeps, bool stagnation, int32_t* sweeps, mpjsvd_stats* stats,
                         bool is64) {
     if (!h || !X || m < 1 || n < 1 || ldx < m || (V && ldv < nv) || max_sweeps < 1) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32), nv_pad = round_up(nv > 0 ? nv : 1, 32);
     MPJ_TRY(ensure(h, S_TMP1, sizeof(T) * (size_t)m_pad * n));
@@ -1162,6 +1191,13 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->cond_d_min = 1e15;
     o->tail_frac = 1.0 / 3.0;
     o->tail_cut_log2 = -60;
+    o->gram_tma = 1;
+    o->gram_kt = 0;
+    o->gram_variant = 0;
+    o->update_tpc = 0;
+    o->skip_unchanged = 1;
+    o->qr_panel_mode = 0;
+    o->diag_timing = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1174,6 +1210,9 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (o.block_cols != 8 && o.block_cols != 16 && o.block_cols != 32) return MPJSVD_ERR_NOT_SUPPORTED;
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
+        return MPJSVD_ERR_INVALID_ARG;
+    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_variant < 0 || o.gram_variant > 5 ||
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;
@@ -1375,6 +1414,7 @@ int mpjsvd_get_profile(mpjsvd_handle h, int32_t idx, char* name, int32_t name_le
 int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda, double* U, int64_t ldu,
                   double* S, double* V, int64_t ldv, mpjsvd_stats* stats) {
     if (!h) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     const bool root = !h->comm.active() || h->comm.rank == 0;
     if (root && (!A || !U || !S || !V)) return MPJSVD_ERR_INVALID_ARG;
     if (n < 2 || m < n || (root && (lda < m || ldu < m || ldv < n))) return MPJSVD_ERR_INVALID_ARG;
@@ -1388,6 +1428,7 @@ int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_
 int mpjsvd_gemm_f64(mpjsvd_handle h, int32_t transa, int32_t transb, int64_t M, int64_t N, int64_t K, double alpha,
                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (!h || !A || !B || !C) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     MPJ_TRY(ensure(h, S_GEMMWS, sizeof(double) * (size_t)(M > 0 ? M : 1) * (N > 0 ? N : 1) * 16));
     gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
     int rc = gemm_f64(transa, transb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h->stream);
@@ -1398,6 +1439,7 @@ int mpjsvd_gemm_f64(mpjsvd_handle h, int32_t transa, int32_t transb, int64_t M, 
 int mpjsvd_inner_solve(mpjsvd_handle h, int32_t is_f64, void* G, void* E, int32_t w, int32_t count, double tol_in,
                        int32_t max_inner, int32_t* rotations) {
     if (!h || !G || !E || w < 1 || w > 64 || count < 1) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     MPJ_TRY(ensure(h, S_TMP1, sizeof(int) * (size_t)count));
     int rc = is_f64 ? launch_inner_batch<double>((double*)G, (double*)E, w, tol_in, max_inner, count,
                                                   P<int>(h, S_TMP1), h->stream)
@@ -1427,6 +1469,7 @@ int mpjsvd_block_jacobi_f32(mpjsvd_handle h, float* X, int64_t m, int64_t n, int
 int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, double* tau, int32_t* perm,
               int32_t pivot) {
     if (!h || !A || !tau || m < n || n < 1 || lda < m) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32);
@@ -1488,6 +1531,7 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
 
 int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq) {
     if (!h || !V32 || !Q || n < 1 || ldv32 < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long n_pad = round_up(n, 32);
@@ -1517,6 +1561,7 @@ int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, dou
 int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
                     double* Q, int64_t ldq, int32_t x_lower) {
     if (!h || !X || !Ulow || !Q || n < 1 || ldx < n || ldu < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long n_pad = round_up(n, 32);
@@ -1546,6 +1591,7 @@ int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, co
 int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv, const double* tau, double* C,
                    int64_t ldc, int64_t ncols) {
     if (!h || !Vr || !tau || !C || k > m || ldv < m || ldc < m) return MPJSVD_ERR_INVALID_ARG;
+    g_mpj_diag = h->opts.diag_timing;
     gemm_set_workspace(nullptr, 0);
     MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m, ncols)));
     MPJ_TRY(apply_q_wy(Vr, m, (int)k, ldv, tau, C, ldc, ncols, P<double>(h, S_WY), h->stream));

@@ -17,12 +17,37 @@ import os
 
 import numpy as np
 
+try:
+    from threadpoolctl import threadpool_limits
+except ImportError:  # pragma: no cover
+    threadpool_limits = None
+
+# OpenBLAS partitions the QR / GEMM work of the Haar constructions by thread count, and the
+# partition changes the rounding: the same seeds give different bits with 8 and 16 BLAS
+# threads (measured: this container vs the GPU box).  Every construction therefore runs with
+# exactly BLAS_THREADS threads, so that the inputs -- and the digests stored in the oracle
+# goldens -- are bit-identical on every host.
+BLAS_THREADS = 8
+GEN_VERSION = "g2"      # cache key: bump when the bits of a construction change
+
+
+def _pinned(fn):
+    def wrapped(*a, **k):
+        if threadpool_limits is None:
+            return fn(*a, **k)
+        with threadpool_limits(limits=BLAS_THREADS, user_api="blas"):
+            return fn(*a, **k)
+    wrapped.__name__ = fn.__name__
+    wrapped.__doc__ = fn.__doc__
+    return wrapped
+
 __all__ = [
     "haar", "geom", "config_matrix", "CONFIGS", "planted_sigma",
     "exact_sigma_matrix", "graded_matrix", "sylvester_hadamard", "digest",
 ]
 
 
+@_pinned
 def haar(rows: int, cols: int, seed: int) -> np.ndarray:
     """Haar-distributed orthonormal columns: economy QR of a seeded N(0,1)
     matrix with the R diagonal sign folded into Q."""
@@ -67,6 +92,7 @@ def planted_sigma(name: str, n: int | None = None) -> np.ndarray | None:
     raise KeyError(name)
 
 
+@_pinned
 def config_matrix(name: str, n: int | None = None, m: int | None = None) -> np.ndarray:
     """Build config `name` (C1..C5, SURVEY.md sec. 8(d) pseudo-code).
 
@@ -107,6 +133,7 @@ def sylvester_hadamard(n: int) -> np.ndarray:
     return h
 
 
+@_pinned
 def exact_sigma_matrix(n: int, seed: int | None = None, emax: int = 13):
     """Pin P2: A = (1/n) (S1 P1 H) diag(sigma) (S2 P2 H)^T.
 
@@ -156,7 +183,7 @@ def cached_config(name: str, n: int | None = None, cache_dir: str | None = None)
     matrix is regenerated whenever the cache file is missing)."""
     cache_dir = cache_dir or os.environ.get("MPJSVD_CACHE", "/tmp/mpjsvd_cache")
     m0, n0, _ = CONFIGS[name]
-    key = f"{name}_{n0 if n is None else n}.npy"
+    key = f"{name}_{n0 if n is None else n}_{GEN_VERSION}.npy"
     path = os.path.join(cache_dir, key)
     try:
         return np.load(path, mmap_mode=None)

@@ -151,19 +151,64 @@ def test_qr_vs_oracle(mp, m, n, pivot):
     assert np.abs(q @ r - a[:, perm]).max() <= 1e-13 * np.abs(a).max()
 
 
-@pytest.mark.parametrize("mode", [{"MPJSVD_QR_PANEL_COOP": "1"}, {"MPJSVD_QR_LOOKAHEAD": "0"}, {}])
-def test_blocked_qr_panel_modes(mp, monkeypatch, mode):
+@pytest.mark.parametrize("m,n", [(8192, 600), (4200, 1200), (2100, 1500)])
+def test_qrp_row_instantiations_vs_oracle(mp, m, n):
+    """The lazy QRP kernel is instantiated by row count (rows per thread RPT = 16 for 4097..8192 rows: C5's
+    8192 x 8192 A1; RPT = 8 for 2049..4096: C3) and deals ~n/148 columns to each CTA.  At those row counts,
+    with several columns per CTA, the pivot sequence is identical to the oracle's Businger-Golub QRP and R,
+    tau agree to 1e-12."""
+    rng = np.random.default_rng(m * 3 + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
+    packed, tau, perm = mp.qr(dev(a), pivot=1)
+    packed, tau, perm = host(packed), host(tau), host(perm)
+    p_o, perm_o, tau_o, _ = oracle.qrp(a)
+    assert np.array_equal(perm, perm_o)
+    r, r_o = np.triu(packed[:n]), np.triu(p_o[:n])
+    assert np.abs(r - r_o).max() <= 1e-12 * np.abs(r_o).max()
+    assert np.abs(tau - tau_o).max() <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,kt,with_v", [(6144, 256, 0, False), (6144, 256, 0, True), (8192, 128, 0, False),
+                                           (512, 256, 32, False), (1000, 192, 32, True), (7000, 128, 64, False)])
+def test_block_jacobi_f32_gram_variants_vs_oracle(mp, m, n, kt, with_v):
+    """fp32 block Jacobi through the TMA Gram variant the C5 path runs (32-row stages at 4 CTAs/SM, chosen
+    for >= 6144 rows; forced with gram_kt = 32 at small sizes, 64 forced at large) and the TMA-fed update
+    (U-route: no V), with the path's one inner sweep per pair (max_inner32 = 1, reading c-5), against the
+    oracle's plain fp32 block Jacobi: sweeps +-1, sigma (column norms) within the TF32x3 stage's accuracy,
+    orthogonality of the normalised columns at the fp32 tolerance."""
+    rng = np.random.default_rng(m + 17 * n)
+    a = (testmat.haar(m, n, 11 + n) * np.geomspace(1.0, 1e-3, n)) @ testmat.haar(n, n, 12 + n).T
+    x0 = np.asfortranarray(a).astype(np.float32)
+    t = np.float32(4 * np.sqrt(m) * 2.0 ** -24)
+    v0 = np.eye(n, dtype=np.float32) if with_v else None
+    xo, vo, sw_o, _, _ = oracle.block_jacobi(x0, v0, 32, t, t / 8, max_sweeps=20, max_inner=1,
+                                             stagnation=True, dtype=np.float32)
+    X = dev(x0, torch.float32)
+    V = dev(np.eye(n), torch.float32) if with_v else None
+    sw, st = mp.block_jacobi(X, V, float(t), float(t / 8), 20, stagnation=True, max_inner=1, gram_kt=kt)
+    X = host(X).astype(np.float64)
+    assert abs(abs(sw) - abs(sw_o)) <= 1, (sw, sw_o)
+    s_gpu = np.sort(np.linalg.norm(X, axis=0))[::-1]
+    s_or = np.sort(np.linalg.norm(xo.astype(np.float64), axis=0))[::-1]
+    assert np.max(np.abs(s_gpu - s_or) / s_or) < 1e-4
+    xn = X / np.linalg.norm(X, axis=0)
+    assert np.abs(xn.T @ xn - np.eye(n)).max() < 1e-4
+    if with_v:
+        assert orth(host(V).astype(np.float64)) < 1e-4
+    del rng
+
+
+@pytest.mark.parametrize("mode", [1, 2, 0])
+def test_blocked_qr_panel_modes(mp, mode):
     """Blocked Householder QR with its three panel schedules: the cooperative (grid-barrier) panel kernel,
     the flag-chained panel kernel, and the chained kernel with look-ahead (panel p+1 factored on a side stream
     beside panel p's trailing update).  Several 128-column panels, a ragged last panel, tall and square; the
     whole mixed-precision SVD (LQ and U-route switch both run the blocked QR) against the oracle."""
-    for k, v in mode.items():
-        monkeypatch.setenv(k, v)
     # odd panel widths (a CTA with one column), a 1-column panel, and > 8192 rows (one column per CTA)
     for m, n in ((1000, 300), (700, 700), (2100, 520), (1000, 301), (600, 257), (9000, 131)):
         rng = np.random.default_rng(m * n)
         a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
-        packed, tau, _ = mp.qr(dev(a), pivot=0)
+        packed, tau, _ = mp.qr(dev(a), pivot=0, qr_panel_mode=mode)
         packed, tau = host(packed), host(tau)
         p_o, tau_o, _ = oracle.qr(a)
         r, r_o = np.triu(packed[:n]), np.triu(p_o[:n])
@@ -173,7 +218,7 @@ def test_blocked_qr_panel_modes(mp, monkeypatch, mode):
         assert orth(q) < 1e-13
         assert np.abs(q @ r - a).max() <= 1e-13 * np.abs(a).max()
     a = testmat.config_matrix("C3", 512)
-    U, S, V, st = mp.factor(dev(a))
+    U, S, V, st = mp.factor(dev(a), qr_panel_mode=mode)
     check_svd(a, host(U), host(S), host(V))
     uo, so, vo, sto, rc = oracle.mixed_svd(a)
     assert np.all(np.abs(host(S) - so) / so <= tiered(so, kappa_s(a)))
@@ -407,20 +452,18 @@ def test_factor_mixed_precision_rrqr_vs_oracle(mp, name, n):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
 
 
-def test_gram_tma_equals_cp_async_gram(mp, monkeypatch):
+def test_gram_tma_equals_cp_async_gram(mp):
     """The TMA-fed fp32 Gram (k_pair_gram_tma) lands the same operand layout and issues the same MMA
     sequence as the cp.async Gram: with the same row slabs (split_rows = 128) the whole SVD is bitwise
     equal; the default (automatic) slabs stay within the parity bar."""
     a = testmat.config_matrix("C3", 512)
     res = {}
-    for tma in ("1", "0"):
-        monkeypatch.setenv("MPJSVD_GRAM_TMA", tma)
-        U, S, V, st = mp.factor(dev(a), split_rows=128)
+    for tma in (1, 0):
+        U, S, V, st = mp.factor(dev(a), split_rows=128, gram_tma=tma)
         res[tma] = (host(U), host(S), host(V), st["sweeps32"], st["sweeps64"])
-    for x, y in zip(res["1"], res["0"]):
+    for x, y in zip(res[1], res[0]):
         assert np.array_equal(np.asarray(x), np.asarray(y))
     # ragged n (last block narrower) and an odd block count (bye pairs) through the TMA Gram
-    monkeypatch.setenv("MPJSVD_GRAM_TMA", "1")
     for n in (200, 352):
         b = testmat.config_matrix("C1", n)
         U, S, V, st = mp.factor(dev(b))
@@ -431,18 +474,17 @@ def test_gram_tma_equals_cp_async_gram(mp, monkeypatch):
 
 @pytest.mark.parametrize("name,n,extra", [("C1", 256, {}), ("C3", 512, {"virtual_shards": 2}),
                                           ("C2", 384, {"max_sweeps64": 30})])
-def test_skip_unchanged_pairs_is_exact(mp, monkeypatch, name, n, extra):
+def test_skip_unchanged_pairs_is_exact(mp, name, n, extra):
     """Skipping the Gram and solve of a pair whose blocks did not rotate since its previous evaluation
     (one sweep earlier) is exact: outputs and sweep counts are bitwise those of evaluating every pair."""
     a = testmat.config_matrix(name, n)
     res = {}
-    for sk in ("1", "0"):
-        monkeypatch.setenv("MPJSVD_SKIP_UNCHANGED", sk)
-        U, S, V, st = mp.factor(dev(a), **extra)
+    for sk in (1, 0):
+        U, S, V, st = mp.factor(dev(a), skip_unchanged=sk, **extra)
         res[sk] = (host(U), host(S), host(V), st)
-    for x, y in zip(res["1"][:3], res["0"][:3]):
+    for x, y in zip(res[1][:3], res[0][:3]):
         assert np.array_equal(x, y)
-    s1, s0 = res["1"][3], res["0"][3]
+    s1, s0 = res[1][3], res[0][3]
     for k in ("sweeps32", "sweeps64", "upd_trace32", "upd_trace64", "off_trace32", "off_trace64"):
         assert s1[k] == s0[k], k
     assert sum(s0["skip_trace32"]) == 0 and sum(s0["skip_trace64"]) == 0
@@ -470,6 +512,21 @@ def test_auto_path_vs_oracle(mp, case):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
     np.testing.assert_allclose(st["cond_scaled"], sto["cond_scaled"], rtol=1e-6)
     np.testing.assert_allclose(st["cond_d"], sto["cond_d"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("name,n", [("C2", 384), ("C3", 512), ("C4", 256), ("C5", 320)])
+def test_gate_measures_vs_oracle(mp, name, n):
+    """All AUTO gate quantities (reading c-15) on the config recipes: the column-
+    scaled kappa_1(R_s) (GPU: triangular solve on DMMA GEMMs + column reductions; oracle: back substitution),
+    cond(D), the orth measure and the tail fraction equal the oracle's up to rounding order; same branch."""
+    a = testmat.config_matrix(name, n)
+    st = mp.factor(dev(a), path=1)[3]
+    sto = oracle.mixed_svd(a, path=1)[3]
+    assert st["path_taken"] == sto["path_taken"]
+    assert abs(st["cond_scaled"] - sto["cond_scaled"]) <= 1e-9 * sto["cond_scaled"] * max(1.0, 1e-4 * sto["cond_scaled"])
+    assert abs(st["cond_d"] - sto["cond_d"]) <= 1e-12 * sto["cond_d"]
+    assert abs(st["orth_measure"] - sto["orth_measure"]) <= 1e-5 + 1e-3 * sto["orth_measure"]
+    assert st["tail_fraction"] == sto["tail_fraction"]
 
 
 @pytest.mark.parametrize("opts,oopts", [

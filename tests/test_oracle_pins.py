@@ -548,3 +548,109 @@ def test_auto_qrsvd_branch_matches_jacobi_branch_sigma():
     _, s_q, _, st, rc = oracle.mixed_svd(a, path=1, tol_alg=1e-3)
     assert rc == 0 and st["path_taken"] == 6
     assert np.max(np.abs(s_q - s_j) / s_j) <= 1e-12
+
+
+# ---------------------------------------------------------------- gate measures
+def _hadamard_cols(n, seed):
+    """P H D: Sylvester-Hadamard (n = 4^k, so H/sqrt(n) is exact), random row permutation and power-of-two
+    column scales.  Columns exactly orthogonal in any arithmetic; X X^T != I (transposition shows)."""
+    rng = np.random.default_rng(seed)
+    h = testmat.sylvester_hadamard(n)[rng.permutation(n)]
+    return np.asfortranarray(h * 2.0 ** rng.integers(-20, 20, n)), rng
+
+
+@pytest.mark.parametrize("n", [4, 16, 64])
+def test_gate_orth_exactly_orthogonal_columns_is_zero(n):
+    """Exactly orthogonal dyadic columns: X_t = P H / sqrt(n) is exact in fp32, so ||X_t^T X_t - I||_max = 0
+    exactly (a missing normalisation, a transposed product X X^T, or a wrong norm fails)."""
+    x, _ = _hadamard_cols(n, n)
+    assert oracle.gate_orth(x) == 0.0
+    # rows scaled unevenly: columns no longer orthogonal, the measure sees it (X X^T is still diagonal-free)
+    y = x * np.linspace(1.0, 2.0, n)[:, None]
+    assert oracle.gate_orth(y) > 1e-3
+
+
+def test_gate_orth_closed_forms():
+    """Closed forms in the paper's lower precision ("one matrix-matrix multiplication in
+    the lower precision"):
+      X = [[3, 0], [4, 5]] (columns (3,4), (0,5)): X_t = ((3/5, 4/5), (0, 1)) in fp32, off-diagonal
+        fl32(4/5) * 1 = fl32(0.8); the diagonal of column 1 is fl32(0.6)^2 + fl32(0.8)^2 rounded -> orth =
+        fl32(0.8) exactly;
+      X = [[1, -2^-12], [2^-12, 1]]: both norms round to 1 in fp32, the columns are exactly orthogonal,
+        and 1 + 2^-24 rounds to 1 in an fp32 accumulation: orth = 0 (an fp64-accumulated Gram gives 2^-24)."""
+    x = np.array([[3.0, 0.0], [4.0, 5.0]], order="F")
+    assert oracle.gate_orth(x) == float(np.float32(0.8))
+    e = 2.0 ** -12
+    y = np.array([[1.0, -e], [e, 1.0]], order="F")
+    assert oracle.gate_orth(y) == 0.0
+
+
+def test_gate_orth_scaling_invariance_and_error_bound():
+    """Power-of-two column scaling is exact through fl32 and the normalisation: bitwise invariance.  For a
+    random X the fp32 measure is within the fp32 GEMM bound of the exact value of the same definition."""
+    rng = np.random.default_rng(5)
+    n = 48
+    x = np.asfortranarray(rng.standard_normal((n, n)))
+    s = 2.0 ** rng.integers(-30, 30, n)
+    assert oracle.gate_orth(x) == oracle.gate_orth(np.asfortranarray(x * s))
+    x32 = x.astype(np.float32).astype(np.float64)
+    xt = x32 / np.linalg.norm(x32, axis=0)
+    exact = np.abs(xt.T @ xt - np.eye(n)).max()
+    assert abs(oracle.gate_orth(x) - exact) <= 2 * n * 2.0 ** -24
+
+
+def test_gate_tail_counts_small_columns():
+    """Tail fraction: columns strictly below 2^cut max are counted; a column exactly at
+    the cut is not."""
+    n = 12
+    x, _ = _hadamard_cols(16, 3)
+    x = np.asfortranarray(x[:n, :n] * 0 + np.eye(n))
+    scales = np.array([1.0, 0.5, 2.0 ** -60, 2.0 ** -61, 2.0 ** -70, 1.0, 1.0, 2.0 ** -80, 1.0, 1.0, 1.0, 1.0])
+    x = np.asfortranarray(x * scales)
+    assert oracle.gate_tail(x, -60) == 3.0 / n
+    assert oracle.gate_tail(x, -10) == 4.0 / n
+    assert oracle.gate_tail(x, -100) == 0.0
+
+
+def test_gate_cond_scaled_closed_forms_and_lapack():
+    """cond_R of the column-scaled R (Alg. 3 l.423; reading c-15) = kappa_1(R diag(1/c)):
+      R = diag(d), c = |d|: R_s = I -> 1 exactly (any grading of D is removed);
+      R = [[1, t], [0, 1]], c = (1, sqrt(1+t^2)): ||R_s||_1 = (|t|+1)/sqrt(1+t^2) or 1, R_s^-1 =
+        [[1, -t], [0, sqrt(1+t^2)]] -> closed form below;
+      a random upper-triangular R with its true column norms: numpy.linalg.cond(R_s, 1) (LAPACK)."""
+    d = 2.0 ** np.arange(-20, 20, 4)
+    assert oracle.gate_cond_scaled(np.diag(d), np.abs(d)) == 1.0
+    t = 3.0
+    r = np.array([[1.0, t], [0.0, 1.0]], order="F")
+    c = np.array([1.0, np.sqrt(1 + t * t)])
+    nrm = max(1.0, (abs(t) + 1) / np.sqrt(1 + t * t))
+    inv = max(1.0, abs(t) + np.sqrt(1 + t * t))
+    assert abs(oracle.gate_cond_scaled(r, c) - nrm * inv) <= 4 * U * nrm * inv
+    rng = np.random.default_rng(9)
+    n = 40
+    r = np.triu(rng.standard_normal((n, n))) + 4 * np.eye(n)
+    r = np.asfortranarray(r * 10.0 ** rng.uniform(-6, 6, n))
+    c = np.linalg.norm(r, axis=0)
+    ref = np.linalg.cond(r / c, 1)
+    assert abs(oracle.gate_cond_scaled(r, c) - ref) <= 1e-12 * ref
+    # only the upper triangle is read (reflectors may sit below the diagonal)
+    junk = np.asfortranarray(r + np.tril(rng.standard_normal((n, n)), -1))
+    assert oracle.gate_cond_scaled(junk, c) == oracle.gate_cond_scaled(r, c)
+
+
+def test_gate_cond_d_closed_form():
+    """cond(D) of A = B D (Alg. 3 l.423-424): max/min column norm."""
+    assert oracle.gate_cond_d(np.array([2.0, 8.0, 0.5, 1.0])) == 16.0
+    assert oracle.gate_cond_d(np.array([3.0, 3.0])) == 1.0
+
+
+def test_gate_measures_in_mixed_svd_are_the_gate_functions():
+    """mixed_svd's reported measures are those of its own X = L / R (AUTO): orthogonal columns with a
+    known grading give cond_d = the grading's span, cond_scaled = 1 to rounding, orth ~ 0."""
+    n = 64
+    q = testmat.haar(n, n, 77)
+    d = 10.0 ** np.linspace(0, 8, n)
+    u, s, v, st, rc = oracle.mixed_svd(np.asfortranarray(q * d), path=1)
+    assert abs(st["cond_d"] / 1e8 - 1) <= 1e-12
+    assert abs(st["cond_scaled"] - 1.0) <= 1e-10
+    assert st["orth_measure"] <= 1e-6
