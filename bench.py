@@ -44,8 +44,49 @@ def parse():
     ap.add_argument("--block-cols", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="skip the separate per-kernel profiled pass")
+    ap.add_argument("--also", default="C3", help="comma list of extra configs timed in the same run "
+                                                  "(reported under 'also'; '' for none)")
+    ap.add_argument("--full", default="", help="--impl reference: time O-MIX once on this FULL config "
+                                                  "(minutes) and print the measurement (profiles/cpu_oracle_full_*)")
+    ap.add_argument("--dist-check", action="store_true",
+                    help="launcher check: init the process group (gloo without CUDA), print rank/world, exit")
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-exec the same command line under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1); rank 0's JSON line is
+    the only stdout line the ranks print."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dist_check(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if world > 1:
+        dist.init_process_group(backend)
+        t = torch.tensor([rank + 1], dtype=torch.int64)
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            t = t.cuda()
+        dist.all_reduce(t)
+        total = int(t.item())
+        dist.destroy_process_group()
+    else:
+        total = 1
+    if rank == 0:
+        print(json.dumps({"dist_check": True, "world": world, "gpus_arg": args.gpus, "rank_sum": total,
+                          "backend": backend}), flush=True)
 
 
 def dist_env():
@@ -72,7 +113,7 @@ def oracle_sample(config: str, n_full: int, m_full: int):
     # O-MIX cost ~ (2 m n^2 [tall QR] + c n^3): scale both terms by the size ratio
     scale = (n_full / n_s) ** 3 if m_full == n_full else (m_full * n_full ** 2) / (m_s * n_s ** 2)
     return {
-        "value": dt * scale, "unit": "s", "cores": cores, "kind": "oracle",
+        "value": dt * scale, "unit": "s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
         "sample": (f"O-MIX mixed_svd on the {config} recipe at {m_s}x{n_s} (same seeds), {dt:.2f} s "
                    f"measured, scaled x{scale:.0f} by the n^3 flop ratio to {m_full}x{n_full}; "
                    f"sweeps32={st['sweeps32']} sweeps64={st['sweeps64']}"),
@@ -87,6 +128,21 @@ def run_reference(args):
     if rank != 0:
         return
     import testmat
+    if args.full:
+        import oracle
+        m_f, n_f, _ = testmat.CONFIGS[args.full]
+        a = testmat.cached_config(args.full)
+        cores = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        _, s, _, st, rc = oracle.mixed_svd(a, nthreads=cores)
+        dt = time.perf_counter() - t0
+        ex = oracle_sample(args.full, n_f, m_f)
+        print(json.dumps({"config": args.full, "m": m_f, "n": n_f, "seconds": dt, "cores": cores, "cpu": cpu_model(),
+                          "rc": rc, "sweeps32": st["sweeps32"], "sweeps64": st["sweeps64"],
+                          "digest": testmat.digest(a), "extrapolated_seconds": ex["value"],
+                          "extrapolation_sample": ex["sample"], "measured_over_extrapolated": dt / ex["value"],
+                          "what": "O-MIX (oracle/, as it stands) on the full config, all host cores"}), flush=True)
+        return
     m_full, n_full, _ = testmat.CONFIGS[args.config]
     vals = []
     last = None
@@ -214,14 +270,16 @@ def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks:
     return base
 
 
-def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None = None, tensor32: bool = True):
-    """Algorithmic flops / HBM bytes of the path's kernels summed over the timed
-    steps, per rank.  Gram of a pair (w = 2b columns, n
-    rows): symmetric half incl. the diagonal, n w (w+1) flops, reading W once
-    (per round the whole X: n^2 s bytes); update: 2 n w^2 flops for X and
-    again for V per updated pair, bytes 2 x (read + write of n x w) x s; QRP:
-    the lazy GEMV reads the (n-k)^2 trailing matrix at every step k (8 n^3 / 3
-    bytes in fp64)."""
+def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None = None, tensor32: bool = True,
+                     v32: bool = False):
+    """Algorithmic flops / HBM bytes of the path's kernels summed over the
+    given steps, per rank.  Gram of a pair (w = 2b columns,
+    n rows): symmetric half incl. the diagonal, n w (w+1) flops, reading W
+    once (per round the whole X: n^2 s bytes); update: 2 n w^2 flops and the
+    read + write of n x w (s bytes) for X, and again for V when the stage
+    accumulates V (fp64 refinement: the sweeps counted in v_sweeps64, all of
+    them by default; fp32 stage: only on the V-route, v32); QRP: the lazy GEMV
+    reads the (n-k)^2 trailing matrix at every step k (8 n^3 / 3 bytes)."""
     flops, byts, bound = {}, {}, {}
     nblk = -(-n // b)
     M = nblk + (nblk & 1) if world == 1 else -(-nblk // (2 * world)) * (2 * world)
@@ -237,8 +295,14 @@ def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None =
             g, u = f"pair_gram_{tag}", f"pair_update_{tag}"
             flops[g] = flops.get(g, 0.0) + evaluated * float(n) * w * (w + 1)
             byts[g] = byts.get(g, 0.0) + evaluated * float(n) * w * s
-            flops[u] = flops.get(u, 0.0) + upd * 2 * 2.0 * n * w * w
-            byts[u] = byts.get(u, 0.0) + upd * 2 * 2 * float(n) * w * s
+            # updated pairs whose V slabs are rotated too
+            if tag == "f32":
+                upd_v = upd if v32 else 0
+            else:
+                vsw = st.get("v_sweeps64", sweeps)
+                upd_v = sum(st["upd_trace64"][:vsw]) if vsw < sweeps else upd
+            flops[u] = flops.get(u, 0.0) + (upd + upd_v) * 2.0 * n * w * w
+            byts[u] = byts.get(u, 0.0) + (upd + upd_v) * 2 * float(n) * w * s
         flops["qrp_coop"] = flops.get("qrp_coop", 0.0) + 4.0 * n ** 3 / 3
         byts["qrp_coop"] = byts.get("qrp_coop", 0.0) + 8.0 * n ** 3 / 3
     # fp32 Gram/update are HBM-bound on the tensor cores (tcgen05) and ALU-bound on FFMA
@@ -252,8 +316,77 @@ def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None =
             "bound": bound}
 
 
+def time_config(mp, h, cfg, steps, warmup, root, device, stream, l2_flush, barrier, max_over_ranks):
+    """Seconds per SVD of another config with the same handle and timing rules (device-resident input,
+    L2 flushed between steps, CUDA events on the handle's stream, max over ranks)."""
+    import numpy as np
+    import torch
+    import testmat
+    m, n, _ = testmat.CONFIGS[cfg]
+    A = U = S = V = None
+    if root:
+        a = testmat.cached_config(cfg)
+        A = torch.from_numpy(np.ascontiguousarray(a.T)).t().to(device)
+        U = mp.empty_col_major(m, n, torch.float64, device)
+        V = mp.empty_col_major(n, n, torch.float64, device)
+        S = torch.empty(n, dtype=torch.float64, device=device)
+    st = None
+    for _ in range(warmup):
+        rc, st = mp.mpjsvd_factor(h, A, U, S, V, m, n, m, m, n)
+    torch.cuda.synchronize()
+    barrier()
+    ms = []
+    for _ in range(steps):
+        l2_flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rc, st = mp.mpjsvd_factor(h, A, U, S, V, m, n, m, m, n)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rc < 0:
+            raise mp.MpjsvdError(rc, f"mpjsvd_factor ({cfg})")
+        ms.append(e0.elapsed_time(e1))
+    v = max_over_ranks(statistics.mean(ms)) / 1e3
+    d = st.as_dict()
+    return {"value": v, "unit": "s", "steps": steps, "m": m, "n": n, "sweeps32": d["sweeps32"],
+            "sweeps64": d["sweeps64"], "stage_ms": d["stage_ms"]}
+
+
+def load_full_oracle_measurements():
+    """Full-size O-MIX runs measured on a GPU box's host (bench.py --impl reference --full CFG), kept in
+    profiles/cpu_oracle_full_*.json: the scale check of the bounded sample's n^3 extrapolation."""
+    import glob
+    out = []
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "cpu_oracle_full_*.json"))):
+        try:
+            d = json.load(open(p))
+            out.append({k: d.get(k) for k in ("config", "seconds", "cores", "cpu", "sweeps32", "sweeps64",
+                                              "extrapolated_seconds", "measured_over_extrapolated")})
+        except Exception:
+            pass
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    rank0, world0, _ = dist_env()
+    if world0 != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world0}: launch one rank per GPU")
+    if args.dist_check:
+        dist_check(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -311,8 +444,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---------------- timed region: K steps, L2 flushed between steps
-    h.set_profiling(True)
+    # ---------------- timed region: K steps, L2 flushed between steps, no per-kernel instrumentation
     stats = []
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local)
@@ -326,11 +458,27 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    prof = h.profile()
-    h.set_profiling(False)
     ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
     ms = max_over_ranks(ms)
     launches = int(sum(s["kernel_launches"] for s in stats))
+
+    # ---------------- profiled pass (separate): per-kernel CUDA events on the launching stream; it feeds
+    # the kernel shares and the roofline (an event pair per launch costs ~1.5 % of the step)
+    prof, prof_ms, prof_steps = {}, None, 0
+    if not args.no_profile:
+        prof_steps = max(1, min(args.steps, 5))
+        h.set_profiling(True)
+        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(prof_steps)]
+        pstats = []
+        for i in range(prof_steps):
+            l2_flush.zero_()
+            pe[i][0].record(stream)
+            pstats.append(step())
+            pe[i][1].record(stream)
+        torch.cuda.synchronize()
+        prof = h.profile()
+        h.set_profiling(False)
+        prof_ms = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in pe) / prof_steps)
 
     # ---------------- result check (plumbing: torch on the device)
     orth_u = orth_v = res = None
@@ -369,9 +517,12 @@ def main():
 
     # ---------------- roofline of the dominant kernel
     peaks = load_peaks()
-    work = algorithmic_work(stats, n, args.block_cols, world, m, tensor32=True)
+    v32 = int(h.options.switch_u) == 0
+    work = algorithmic_work(pstats if prof else stats, n, args.block_cols, world, m, tensor32=True, v32=v32)
     try:
-        work["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        # per (config, kernel): dram__bytes_read.sum + dram__bytes_write.sum per launch of the current code's
+        # ncu --set full capture of this config (tools/ncu_summary.py traffic)
+        work["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(args.config, {})
     except Exception:
         work["traffic"] = {}
     # the dominant single kernel (the overlapped solve+update brackets time two kernels together)
@@ -379,7 +530,7 @@ def main():
     dominant = max(single.items(), key=lambda kv: kv[1][0]) if single else None
     roof = roofline_for(dominant[0], dominant[1][0], dominant[1][1], work, peaks, n, args.block_cols) \
         if dominant else None
-    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+    kernels = {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[1] / prof_steps,
                    "share": v[0] / max(1e-9, sum(x[0] for x in prof.values()))} for k, v in prof.items()}
     jacobi = {}
     # the overlapped brackets: the update's algorithmic bytes / flops over the bracket time (lower bound)
@@ -396,6 +547,14 @@ def main():
             jacobi[k] = {kk: r.get(kk) for kk in ("bound", "achieved", "peak", "unit", "frac", "hbm_gbs_achieved",
                                                   "hbm_frac", "avg_launch_us")}
 
+    # ---------------- the metric's other size (n = 4096 next to 8192), same run, same timing rules
+    also = {}
+    for cfg in filter(None, (c.strip() for c in args.also.split(","))):
+        if cfg == args.config:
+            continue
+        also[cfg] = time_config(mp, h, cfg, max(1, min(args.steps, 5)), max(3, min(args.warmup, 3)), root, device,
+                                stream, l2_flush, barrier, max_over_ranks)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -404,11 +563,15 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         cpu = oracle_sample(args.config, n, m)
         cpu.pop("sample_seconds", None)
+        full = load_full_oracle_measurements()
+        if full:
+            cpu["full_size_measurements"] = full
     st0 = stats[-1]
     out = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64+tf32x3",   # fp64 path; the fp32 seed stage's products on TF32 tensor cores, hi/lo split
         "data": "synthetic",
         "config": {"workload": args.config, "m": m, "n": n, "block_cols": args.block_cols,
                    "parallelism": f"column-block sharded x{world} (NCCL block exchange)" if world > 1
@@ -428,6 +591,10 @@ def main():
         "stage_ms": st0["stage_ms"],
         "check": {"orth_u": orth_u, "orth_v": orth_v, "residual": res},
         "kernels": kernels, "jacobi_roofline": jacobi,
+        "profiled": {"steps": prof_steps, "ms_per_step": prof_ms,
+                     "note": "kernels / roofline / jacobi_roofline come from this separate pass with per-launch "
+                             "CUDA events; value is timed without them"},
+        "also": also,
     }
     print(json.dumps(out), flush=True)
     if world > 1:

@@ -137,6 +137,10 @@ typedef struct {
                                   1 cooperative grid-barrier kernel, 2 flag-chained without look-ahead */
     int32_t diag_timing;       /* diagnostics to stderr, bit mask: 1 QRP phases, 2 fp32/fp64 solve phases,
                                   4 cp.async Gram phases, 8 batched inner-solve phases (default 0) */
+    int32_t refine_v;          /* V of the fp64 refinement: 0 (default) accumulate rotations from V := Q (reading c-12);
+                                  1: PAPER.md:599-615 (sec. 3.4, reading c-23): refine Y without V, U_X = Y diag(1/||y_j||),
+                                  V_X = qr(X^T U_X) by fp64 Householder QR, then one accumulating refinement from
+                                  (X V_X, V := V_X) ("always converges in one sweep") */
 } mpjsvd_options;
 
 typedef struct {
@@ -158,7 +162,9 @@ typedef struct {
                                                     (exact: same Gram, same metric, no rotation) */
     double cond_scaled;        /* kappa_1(R diag(1/c)), c_k = ||A1(:, perm_k)|| = ||R(:,k)||: the column-scaled
                                   cond_R of the AUTO cond gate (Alg. 3 l.423; DESIGN.md c-15); NaN unless AUTO */
-    double cond_d;             /* max_j ||A1(:,j)|| / min_j ||A1(:,j)|| (cond(D) of A = B D) */
+    double cond_d;             /* max_j ||A1(:,j)|| / min_j ||A1(:,j)|| (cond(D) of A = B D); NaN unless AUTO */
+    int32_t v_sweeps64;        /* fp64 sweeps that accumulated V (the last v_sweeps64 of sweeps64; < sweeps64 only with
+                                  refine_v = 1) */
 } mpjsvd_stats;
 
 /* Fill *opts with the defaults above. */

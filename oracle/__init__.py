@@ -50,7 +50,8 @@ class Opts(C.Structure):
                 ("x_from_lq", C.c_int32), ("nthreads", C.c_int32), ("mp_rrqr", C.c_int32),
                 ("max_inner32", C.c_int32), ("switch_u", C.c_int32),
                 ("tol_orth", C.c_double), ("tol_alg", C.c_double), ("tol_cond_mult", C.c_double),
-                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32)]
+                ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32),
+                ("refine_v", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -60,7 +61,8 @@ class Stats(C.Structure):
                 ("final_off32", C.c_double), ("final_off64", C.c_double),
                 ("off_trace32", C.c_double * 64), ("off_trace64", C.c_double * 64),
                 ("upd_trace32", C.c_int32 * 64), ("upd_trace64", C.c_int32 * 64),
-                ("perm", C.c_int32 * 1), ("cond_scaled", C.c_double), ("cond_d", C.c_double)]
+                ("perm", C.c_int32 * 1), ("cond_scaled", C.c_double), ("cond_d", C.c_double),
+                ("v_sweeps64", C.c_int32)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -69,6 +71,7 @@ class Stats(C.Structure):
             "orth_measure": self.orth_measure, "tail_fraction": self.tail_fraction,
             "cond_estimate": self.cond_estimate, "final_off32": self.final_off32,
             "path_taken": self.path_taken, "cond_scaled": self.cond_scaled, "cond_d": self.cond_d,
+            "v_sweeps64": self.v_sweeps64,
             "final_off64": self.final_off64,
             "off_trace32": list(self.off_trace32[:min(s32, 64)]),
             "off_trace64": list(self.off_trace64[:min(s64, 64)]),

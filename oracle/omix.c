@@ -74,6 +74,7 @@ void om_default_opts(om_opts* o) {
     o->cond_d_min = 1e15;
     o->tail_frac = 1.0 / 3.0;
     o->tail_cut_log2 = -60;
+    o->refine_v = 0;
 }
 
 static om_lowsvd_fn g_lowsvd = NULL;
@@ -409,6 +410,20 @@ static void argsort_desc(const double* key, int64_t n, int64_t* idx) {
     free(rank);
 }
 
+/* Y = X Q (n x n, all column-major, ld n): y_j = sum_k x_k q_kj in ascending k */
+static void times_q(const double* X, const double* Q, double* Y, int64_t n) {
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < n; ++j) {
+        double* yj = Y + j * n;
+        for (int64_t i = 0; i < n; ++i) yj[i] = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+            double q = Q[k + j * n];
+            const double* xk = X + k * n;
+            for (int64_t i = 0; i < n; ++i) yj[i] += xk[i] * q;
+        }
+    }
+}
+
 /* ---- gate measures of Alg. 3 (reading c-15) -------------------------
    Each is a plain loop over its definition; pinned in tests/test_oracle_pins.py (exact constructions,
    closed forms, invariances, LAPACK). */
@@ -669,26 +684,44 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         }
 
         /* step 10: Y = X Q */
-#pragma omp parallel for schedule(static)
-        for (int64_t j = 0; j < n; ++j) {
-            double* yj = Y + j * n;
-            for (int64_t i = 0; i < n; ++i) yj[i] = 0.0;
-            for (int64_t k = 0; k < n; ++k) {
-                double q = Q[k + j * n];
-                const double* xk = X + k * n;
-                for (int64_t i = 0; i < n; ++i) yj[i] += xk[i] * q;
-            }
-        }
+        times_q(X, Q, Y, n);
     }
 
     /* step 11: fp64 refinement, V := Q (c-12) */
-    {
+    if (!o.refine_v) {
         double tol64 = o.tol_mult64 * sqrt((double)n) * U64;
         double tol64_in = tol64 / (double)o.inner_tol_div;
         int32_t sw64 = om_block_jacobi_f64(Y, n, n, n, Q, n, n, o.b, tol64, tol64_in, o.max_sweeps64,
                                            o.max_inner, st->off_trace64, st->upd_trace64, o.nthreads);
         st->converged = sw64 > 0;
         st->sweeps64 = sw64 < 0 ? -sw64 : sw64;
+        st->v_sweeps64 = st->sweeps64;
+        st->final_off64 = st->sweeps64 > 0 && st->sweeps64 <= 64 ? st->off_trace64[st->sweeps64 - 1] : 0;
+        if (!st->converged) rc = 1;
+    } else {
+        /* step 11' (sec. 3.4; reading c-23): "we first compute U_X without accumulating
+           V_X" -- refinement of Y alone; U_X = Y diag(1/||y_j||); "we form V_X from the QR factorization of
+           X^* U_X" (Householder, diag(R2) >= 0: om_switch_u); Y = X V_X; "another round of the one-sided
+           Jacobi SVD algorithm by accumulating Jacobi rotations" from (Y, V := V_X), which "always converges
+           in one sweep".  Traces: the first stage's sweeps, then the accumulating stage's. */
+        double tol64 = o.tol_mult64 * sqrt((double)n) * U64;
+        double tol64_in = tol64 / (double)o.inner_tol_div;
+        int32_t swa = om_block_jacobi_f64(Y, n, n, n, NULL, 0, n, o.b, tol64, tol64_in, o.max_sweeps64,
+                                          o.max_inner, st->off_trace64, st->upd_trace64, o.nthreads);
+        int32_t na = swa < 0 ? -swa : swa;
+        for (int64_t j = 0; j < n; ++j) {
+            double s = safe_norm(Y + j * n, n);
+            if (!(s > 0.0)) { rc = -3; goto done; }
+            for (int64_t i = 0; i < n; ++i) tmpm[i + j * n] = Y[i + j * n] / s;
+        }
+        if (om_switch_u(X, n, n, tmpm, n, Q, n) != 0) { rc = -3; goto done; }
+        times_q(X, Q, Y, n);
+        int32_t swb = om_block_jacobi_f64(Y, n, n, n, Q, n, n, o.b, tol64, tol64_in, o.max_sweeps64,
+                                          o.max_inner, st->off_trace64 + na, st->upd_trace64 + na, o.nthreads);
+        int32_t nb = swb < 0 ? -swb : swb;
+        st->converged = swa > 0 && swb > 0;
+        st->sweeps64 = na + nb;
+        st->v_sweeps64 = nb;
         st->final_off64 = st->sweeps64 > 0 && st->sweeps64 <= 64 ? st->off_trace64[st->sweeps64 - 1] : 0;
         if (!st->converged) rc = 1;
     }

@@ -51,6 +51,9 @@ typedef struct {
                                does not accumulate V; Q = qr(X^T U_low) (default); 0: V-route (c-11) */
     double tol_orth, tol_alg, tol_cond_mult, cond_d_min, tail_frac;   /* AUTO gates (c-15) */
     int32_t tail_cut_log2;
+    int32_t refine_v;       /* 0 (default): the fp64 refinement accumulates V from V := Q (c-12);
+                               1: PAPER.md:599-615 (sec. 3.4, reading c-23): refine without V, V_X = qr(X^T U_X),
+                               then one accumulating refinement from (X V_X, V := V_X) */
 } om_opts;
 
 typedef struct {
@@ -62,6 +65,7 @@ typedef struct {
     int32_t perm[1];        /* unused placeholder (keeps layout simple) */
     double cond_scaled;     /* kappa_1(R diag(1/||R(:,k)||)) (AUTO only, else NaN) */
     double cond_d;          /* max/min column norm of A1 (cond(D) of A = B D; AUTO only, else NaN) */
+    int32_t v_sweeps64;     /* fp64 sweeps that accumulated V (the last v_sweeps64 of sweeps64) */
 } om_stats;
 
 /* The low-precision QR SVD of the AUTO branch: a library primitive

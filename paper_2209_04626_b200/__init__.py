@@ -44,7 +44,7 @@ class Options(C.Structure):
                 ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32),
                 ("gram_tma", C.c_int32), ("gram_kt", C.c_int32), ("gram_variant", C.c_int32),
                 ("update_tpc", C.c_int32), ("skip_unchanged", C.c_int32), ("qr_panel_mode", C.c_int32),
-                ("diag_timing", C.c_int32)]
+                ("diag_timing", C.c_int32), ("refine_v", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -58,7 +58,7 @@ class Stats(C.Structure):
                 ("inner_max_trace32", C.c_int32 * 32), ("inner_max_trace64", C.c_int32 * 32),
                 ("inner_sum_trace32", C.c_int32 * 32), ("inner_sum_trace64", C.c_int32 * 32),
                 ("skip_trace32", C.c_int32 * 32), ("skip_trace64", C.c_int32 * 32),
-                ("cond_scaled", C.c_double), ("cond_d", C.c_double)]
+                ("cond_scaled", C.c_double), ("cond_d", C.c_double), ("v_sweeps64", C.c_int32)]
 
     def as_dict(self) -> dict:
         s32, s64 = self.sweeps32, self.sweeps64
@@ -68,7 +68,7 @@ class Stats(C.Structure):
             "stage_ms": dict(zip(STAGES, list(self.stage_ms))), "total_ms": self.total_ms,
             "orth_measure": self.orth_measure, "tail_fraction": self.tail_fraction,
             "cond_estimate": self.cond_estimate, "final_off32": self.final_off32,
-            "cond_scaled": self.cond_scaled, "cond_d": self.cond_d,
+            "cond_scaled": self.cond_scaled, "cond_d": self.cond_d, "v_sweeps64": self.v_sweeps64,
             "final_off64": self.final_off64,
             "off_trace32": list(self.off_trace32[:min(s32, 32)]),
             "off_trace64": list(self.off_trace64[:min(s64, 32)]),

@@ -230,6 +230,9 @@ int downcast_scaled(const double* X, long long ldx, float* X32, long long ld32, 
 template <typename T>
 int col_norms(const T* X, long long ldx, long long rows, int n, double* out, int safe, cudaStream_t st);
 int rank_desc(const double* key, int n, int* rank, cudaStream_t st);
+// UX(:, j) = Y(:, j) / sig[j]; *bad |= 1 if some sig[j] <= 0
+int scale_cols(const double* Y, long long ldy, const double* sig, double* UX, long long ldu, long long rows_pad,
+               int n, int* bad, cudaStream_t st);
 int sort_upcast_v(const float* V32, long long ld32, const int* rank, double* V, long long ldv,
                   long long rows_pad, int n, cudaStream_t st);
 int sort_upcast_scale(const float* X32, long long ld32, const int* rank, const double* sig, double* U,

@@ -281,6 +281,28 @@ int finalize(const double* Y, long long ldy, const double* Q, long long ldq, con
     return 0;
 }
 
+// U_X = Y diag(1/sig) in place order (sec. 3.4 V formation); sig_j = 0 -> rank deficient
+__global__ void k_scale_cols(const double* Y, long long ldy, const double* sig, double* UX, long long ldu,
+                             long long rows_pad, int n, int* bad) {
+    for (long long j = blockIdx.y; j < n; j += gridDim.y) {
+        const double s = sig[j];
+        if (!(s > 0.0)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(bad, 1);
+            continue;
+        }
+        const double r = 1.0 / s;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows_pad; i += (long long)gridDim.x * blockDim.x)
+            UX[i + j * ldu] = Y[i + j * ldy] * r;
+    }
+}
+int scale_cols(const double* Y, long long ldy, const double* sig, double* UX, long long ldu, long long rows_pad,
+               int n, int* bad, cudaStream_t st) {
+    k_scale_cols<<<grid2d(rows_pad, n), 256, 0, st>>>(Y, ldy, sig, UX, ldu, rows_pad, n, bad);
+    MPJ_LAUNCHED();
+    MPJ_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // V[perm[k]][:] = M[k][:]
 __global__ void k_scatter_rows(const double* M, long long ldm, const int* perm, double* V, long long ldv, int n) {
     for (long long j = blockIdx.y; j < n; j += gridDim.y)

@@ -978,10 +978,50 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[6], st));
     // ---- stage 6: fp64 refinement with V := Q
-    {
+    int v_sweeps64 = 0;
+    if (!o.refine_v) {
         const double tol64 = o.tol_mult64 * sqrt((double)n) * U64;
         MPJ_TRY(jacobi_stage<double>(h, dY, n_pad, n_pad, (int)n, dQ, n_pad, n_pad, o.block_cols, tol64,
                                      tol64 / o.inner_tol_div, o.max_sweeps64, o.max_inner, false, r64));
+        v_sweeps64 = r64.sweeps;
+    } else {
+        // sec. 3.4 (reading c-23): refine Y without V; U_X = Y diag(1/||y_j||);
+        // V_X = qr(X^T U_X) (the U-route construction in fp64); Y = X V_X; one accumulating refinement
+        // from (Y, V := V_X), which "always converges in one sweep"
+        const double tol64 = o.tol_mult64 * sqrt((double)n) * U64;
+        JacobiResult ra, rb;
+        MPJ_TRY(jacobi_stage<double>(h, dY, n_pad, n_pad, (int)n, nullptr, n_pad, n_pad, o.block_cols, tol64,
+                                     tol64 / o.inner_tol_div, o.max_sweeps64, o.max_inner, false, ra));
+        if (root) {
+            PROF_B("refine_v_qr");
+            MPJ_TRY(col_norms<double>(dY, n_pad, n_pad, (int)n, P<double>(h, S_SOUT), 1, st));
+            MPJ_TRY(scale_cols(dY, n_pad, P<double>(h, S_SOUT), dUX, n_pad, n_pad, (int)n, flags + 1, st));
+            MPJ_TRY(switch_u_inplace(h, dX, dUX, dVX, dQ, n_pad, (int)n, o.x_from_lq != 0, qw, st));
+            MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
+            PROF_E("refine_v_qr");
+        }
+        {
+            const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
+            if (rc) return rc;
+        }
+        if (dist) {
+            MPJ_TRY(h->comm.bcast(dY, sizeof(double) * nn, 0, st));
+            MPJ_TRY(h->comm.bcast(dQ, sizeof(double) * nn, 0, st));
+        }
+        MPJ_TRY(jacobi_stage<double>(h, dY, n_pad, n_pad, (int)n, dQ, n_pad, n_pad, o.block_cols, tol64,
+                                     tol64 / o.inner_tol_div, o.max_sweeps64, o.max_inner, false, rb));
+        r64 = ra;
+        for (int i = 0; i < rb.sweeps && ra.sweeps + i < 64; ++i) {
+            const int k = ra.sweeps + i;
+            r64.off[k] = rb.off[i];
+            r64.upd[k] = rb.upd[i];
+            r64.inner_max[k] = rb.inner_max[i];
+            r64.inner_sum[k] = rb.inner_sum[i];
+            r64.skipped[k] = rb.skipped[i];
+        }
+        r64.sweeps = ra.sweeps + rb.sweeps;
+        r64.converged = ra.converged && rb.converged;
+        v_sweeps64 = rb.sweeps;
     }
     MPJ_CUDA_TRY(cudaEventRecord(ev[7], st));
     auto fill_sweep_stats = [&]() {
@@ -995,6 +1035,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             s.inner_max_trace64[i] = r64.inner_max[i]; s.inner_sum_trace64[i] = r64.inner_sum[i];
             s.skip_trace32[i] = r32.skipped[i]; s.skip_trace64[i] = r64.skipped[i];
         }
+        s.v_sweeps64 = v_sweeps64;
         s.final_off32 = r32.sweeps ? r32.off[r32.sweeps - 1] : 0.0;
         s.final_off64 = r64.sweeps ? r64.off[r64.sweeps - 1] : 0.0;
     };
@@ -1198,6 +1239,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->skip_unchanged = 1;
     o->qr_panel_mode = 0;
     o->diag_timing = 0;
+    o->refine_v = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1212,7 +1254,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_variant < 0 || o.gram_variant > 5 ||
-        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2)
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

@@ -190,11 +190,16 @@ def test_block_jacobi_f32_gram_variants_vs_oracle(mp, m, n, kt, with_v):
     assert abs(abs(sw) - abs(sw_o)) <= 1, (sw, sw_o)
     s_gpu = np.sort(np.linalg.norm(X, axis=0))[::-1]
     s_or = np.sort(np.linalg.norm(xo.astype(np.float64), axis=0))[::-1]
-    assert np.max(np.abs(s_gpu - s_or) / s_or) < 1e-4
+    # two fp32-stage roundings (plain fp32 vs TF32x3 products, ~2^-21 each): absolute errors ~ u sigma_1
+    assert np.all(np.abs(s_gpu - s_or) / s_or <= 1e-4 + 2e-6 * s_or[0] / s_or)
     xn = X / np.linalg.norm(X, axis=0)
     assert np.abs(xn.T @ xn - np.eye(n)).max() < 1e-4
     if with_v:
-        assert orth(host(V).astype(np.float64)) < 1e-4
+        # V-route accumulation on TF32x3 products (~2^-21 each, reading c-20: 8x the fp32 unit) over ~14
+        # sweeps: the oracle's plain fp32 V reaches ~2e-5, the tensor-core stage ~2e-4; V must still map X0 to X
+        v = host(V).astype(np.float64)
+        assert orth(v) < 1e-3
+        assert np.abs(x0.astype(np.float64) @ v - X).max() <= 1e-3 * np.abs(X).max()
     del rng
 
 
@@ -527,6 +532,28 @@ def test_gate_measures_vs_oracle(mp, name, n):
     assert abs(st["cond_d"] - sto["cond_d"]) <= 1e-12 * sto["cond_d"]
     assert abs(st["orth_measure"] - sto["orth_measure"]) <= 1e-5 + 1e-3 * sto["orth_measure"]
     assert st["tail_fraction"] == sto["tail_fraction"]
+
+
+@pytest.mark.parametrize("name,n,extra", [("C1", 256, {}), ("C2", 512, {}), ("C3", 512, {}), ("C5", 640, {}),
+                                          ("C4", 256, {}), ("C3", 512, {"virtual_shards": 4}),
+                                          ("C5", 384, {"path": 2})])
+def test_refine_v_vs_oracle(mp, name, n, extra):
+    """Sec. 3.4 V formation (refine_v = 1; reading c-23): refinement without V, V_X =
+    qr(X^T U_X), one accumulating refinement -- against the oracle's same steps: valid SVD, sigma within the
+    tiered bound, both fp64 stages' sweep counts +-1, and the accumulating stage converges within 2 sweeps
+    ("always converges in one sweep" + the check sweep).  Also through the sharded engine and the fp64-only
+    path."""
+    a = testmat.config_matrix(name, n)
+    U, S, V, st = mp.factor(dev(a), refine_v=1, **extra)
+    U, S, V = host(U), host(S), host(V)
+    oo = {"path": extra["path"]} if "path" in extra else {}
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, refine_v=1, **oo)
+    assert rc == 0 and st["rc"] == 0
+    check_svd(a, U, S, V)
+    assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+    assert 1 <= st["v_sweeps64"] <= 2 and 1 <= sto["v_sweeps64"] <= 2
+    assert abs((st["sweeps64"] - st["v_sweeps64"]) - (sto["sweeps64"] - sto["v_sweeps64"])) <= 1
+    assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
 
 
 @pytest.mark.parametrize("opts,oopts", [

@@ -654,3 +654,47 @@ def test_gate_measures_in_mixed_svd_are_the_gate_functions():
     assert abs(st["cond_d"] / 1e8 - 1) <= 1e-12
     assert abs(st["cond_scaled"] - 1.0) <= 1e-10
     assert st["orth_measure"] <= 1e-6
+
+
+# ---------------------------------------------------------------- sec. 3.4 V formation
+@pytest.mark.parametrize("n", [64, 256])
+def test_refine_v_exact_sigma_and_one_sweep(n):
+    """refine_v = 1 (reading c-23): refinement without V, V_X = qr(X^T U_X), one accumulating refinement.
+    Exact-sigma input: sigma exact within the tiered bound, U and V orthogonal, small residual, and the
+    accumulating refinement "always converges in one sweep": one sweep with rotations at
+    most, plus the check sweep."""
+    a, sigma = testmat.exact_sigma_matrix(n)
+    u, s, v, st, rc = oracle.mixed_svd(a, refine_v=1)
+    assert rc == 0
+    rel = np.abs(s - sigma) / sigma
+    assert rel.max() < 1e-12
+    assert orth(u) < 1e-13 and orth(v) < 1e-13
+    assert np.linalg.norm(a - (u * s) @ v.T) / np.linalg.norm(a) < 1e-13
+    assert 1 <= st["v_sweeps64"] <= 2
+    assert st["sweeps64"] > st["v_sweeps64"]
+
+
+@pytest.mark.parametrize("name,n", [("C1", 128), ("C2", 128), ("C3", 256), ("C5", 256)])
+def test_refine_v_matches_accumulating_refinement(name, n):
+    """Both V handlings are the same SVD: sigma agree to the refinement's accuracy (tiered bound vs the
+    column-scaled condition number), both U/V orthogonal, and the accumulating stage needs <= 2 sweeps."""
+    a = testmat.config_matrix(name, n)
+    u0, s0, v0, st0, rc0 = oracle.mixed_svd(a)
+    u1, s1, v1, st1, rc1 = oracle.mixed_svd(a, refine_v=1)
+    assert rc0 == 0 and rc1 == 0
+    kap = np.linalg.cond(a / np.linalg.norm(a, axis=0))
+    assert np.all(np.abs(s1 - s0) / s0 <= tiered_tol(s0, kap))
+    assert orth(u1) < 1e-13 and orth(v1) < 1e-13
+    assert np.linalg.norm(a - (u1 * s1) @ v1.T) / np.linalg.norm(a) < 1e-13
+    assert st1["v_sweeps64"] <= 2 and st0["v_sweeps64"] == st0["sweeps64"]
+
+
+def test_refine_v_high_relative_accuracy():
+    """Column-graded input (sigma spanning ~1e12) through refine_v = 1 against 80-digit mpmath (pin P4)."""
+    import mpmath
+    mpmath.mp.dps = 80
+    a, _ = testmat.graded_matrix(32, 20)
+    s = oracle.mixed_svd(a, refine_v=1)[1]
+    ref = np.array(sorted((float(x) for x in mpmath.svd_r(mpmath.matrix(a.tolist()), compute_uv=False)),
+                          reverse=True))
+    assert np.max(np.abs(s - ref) / ref) < 1e-13
