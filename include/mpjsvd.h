@@ -298,6 +298,15 @@ int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, dou
 int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, const double* Ulow, int64_t ldu,
                     double* Q, int64_t ldq, int32_t x_lower);
 
+/* Step-level: the fp32 QR SVD of the AUTO branch ("QR SVD algorithm in the
+   lower precision ... without generating V_low"; reading c-24): fp32 Householder bidiagonalisation,
+   fp32 implicit-shift QR on the bidiagonal, left rotations and reflectors accumulated in fp64.  X32: n x n
+   fp32 (ldx >= n, device or host; not modified).  U: n x n fp64 (ldu >= n) receives U_low, columns in
+   descending singular value order; S (n floats, may be NULL) the singular values.  Errors: INVALID_ARG,
+   RANK_DEFICIENT (an exact zero singular value), CUDA (incl. no convergence in 6 n^2 QR steps),
+   OUT_OF_MEMORY, NOT_SUPPORTED (n > 16384). */
+int mpjsvd_qrsvd32(mpjsvd_handle h, const float* X32, int64_t n, int64_t ldx, double* U, int64_t ldu, float* S);
+
 /* C <- Q C with Q = H_0 ... H_{k-1} packed as returned by mpjsvd_qr (rows m). */
 int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int64_t ldv,
                    const double* tau, double* C, int64_t ldc, int64_t ncols);

@@ -21,7 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["omix.c", "ocyc.c"]
+_SRCS = ["omix.c", "ocyc.c", "qrsvd.c"]
 _DEPS = _SRCS + ["bj_impl.inc", "oracle.h"]
 _lock = threading.Lock()
 _lib = None
@@ -80,25 +80,6 @@ class Stats(C.Structure):
         }
 
 
-def _lowsvd(x32p, n, u32p, s32p):
-    """The fp32 QR SVD of the AUTO branch: LAPACK sgesvd (Golub-Kahan
-    bidiagonalisation + implicit-shift QR) as a library primitive; U in descending sigma order."""
-    try:
-        import scipy.linalg as sl
-        n = int(n)
-        x = np.ctypeslib.as_array(x32p, shape=(n * n,)).reshape((n, n), order="F").copy()
-        u, sv, _ = sl.svd(x, full_matrices=True, lapack_driver="gesvd", check_finite=False)
-        np.ctypeslib.as_array(u32p, shape=(n * n,))[:] = np.asfortranarray(u.astype(np.float32)).ravel(order="F")
-        np.ctypeslib.as_array(s32p, shape=(n,))[:] = sv.astype(np.float32)
-        return 0
-    except Exception:
-        return -1
-
-
-_LOWSVD_T = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_float), C.POINTER(C.c_float))
-_lowsvd_cb = _LOWSVD_T(_lowsvd)
-
-
 def lib():
     global _lib
     with _lock:
@@ -142,8 +123,7 @@ def lib():
             L.oc_cyclic_jacobi.argtypes = [dp, i64, i64, i64, dp, i64, C.c_double, C.c_int32,
                                            C.POINTER(C.c_int64)]
             L.oc_cyclic_jacobi.restype = C.c_int32
-            L.om_set_lowsvd.argtypes = [_LOWSVD_T]
-            L.om_set_lowsvd(_lowsvd_cb)
+            L.om_qrsvd32.argtypes = [fp, i64, i64, dp, i64, fp]
             _lib = L
     return _lib
 
@@ -311,6 +291,16 @@ def gate_cond_scaled(r: np.ndarray, c: np.ndarray) -> float:
 def gate_cond_d(cn: np.ndarray) -> float:
     cn = np.ascontiguousarray(cn, dtype=np.float64)
     return float(lib().om_gate_cond_d(_dp(cn), cn.size))
+
+
+def qrsvd32(x32: np.ndarray):
+    """The fp32 QR SVD of the AUTO branch (qrsvd.c, reading c-24): (U fp64 n x n, sigma fp32, rc)."""
+    x32 = np.asfortranarray(x32, dtype=np.float32)
+    n = x32.shape[0]
+    u = np.zeros((n, n), order="F")
+    s = np.zeros(n, dtype=np.float32)
+    rc = lib().om_qrsvd32(_fp(x32), n, n, _dp(u), n, _fp(s))
+    return u, s, rc
 
 
 def mixed_svd(a: np.ndarray, **opts):

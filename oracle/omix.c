@@ -77,8 +77,6 @@ void om_default_opts(om_opts* o) {
     o->refine_v = 0;
 }
 
-static om_lowsvd_fn g_lowsvd = NULL;
-void om_set_lowsvd(om_lowsvd_fn fn) { g_lowsvd = fn; }
 
 /* ---- Householder ------------------------------------------------------ */
 /* GVL Alg. 5.1.1 with beta = +||x|| (diag(R) >= 0, reading c-13). */
@@ -612,29 +610,17 @@ int om_mixed_svd(const double* A, int64_t m, int64_t n, int64_t lda, const om_op
         /* lower(X) = U_low S_low V_low^* by the QR SVD in fp32, U only; then the
            U-route switch Q R2 = X^T working(U_low) (446-447) and Y = X Q */
         st->path_taken = OM_TAKEN_QRSVD;
-        if (!g_lowsvd) { rc = -1; goto done; }
         double mx = 0.0;
         for (int64_t i = 0; i < nn; ++i) if (fabs(X[i]) > mx) mx = fabs(X[i]);
         int e = 0;
         frexp(mx, &e);
         for (int64_t i = 0; i < nn; ++i) X32[i] = (float)ldexp(X[i], -e);
         float* S32 = (float*)malloc(sizeof(float) * (size_t)n);
-        const int lrc = g_lowsvd(X32, n, V32, S32);   /* V32 buffer receives U32 */
+        const int lrc = om_qrsvd32(X32, n, n, tmpm, n, S32);   /* qrsvd.c: U_low (fp64, sorted) */
         free(S32);
-        if (lrc != 0) { rc = -3; goto done; }
-        for (int64_t j = 0; j < n; ++j)
-            for (int64_t i = 0; i < n; ++i) tmpm[i + j * n] = (double)V32[i + j * n];
+        if (lrc != 0) { rc = lrc < 0 ? -3 : 1; goto done; }
         if (om_switch_u(X, n, n, tmpm, n, Q, n) != 0) { rc = -3; goto done; }
-#pragma omp parallel for schedule(static)
-        for (int64_t j = 0; j < n; ++j) {
-            double* yj = Y + j * n;
-            for (int64_t i = 0; i < n; ++i) yj[i] = 0.0;
-            for (int64_t k = 0; k < n; ++k) {
-                double q = Q[k + j * n];
-                const double* xk = X + k * n;
-                for (int64_t i = 0; i < n; ++i) yj[i] += xk[i] * q;
-            }
-        }
+        times_q(X, Q, Y, n);
     } else if (taken != OM_PATH_FORCE_MIXED) {
         /* Q = I, Y = X */
         st->path_taken = taken;

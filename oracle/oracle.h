@@ -68,11 +68,12 @@ typedef struct {
     int32_t v_sweeps64;     /* fp64 sweeps that accumulated V (the last v_sweeps64 of sweeps64) */
 } om_stats;
 
-/* The low-precision QR SVD of the AUTO branch: a library primitive
-   (LAPACK sgesvd, registered by the Python binding) computing U32 (n x n, ld n, columns in descending
-   singular value order) and S32 of the n x n fp32 matrix X32 (destroyed).  Returns 0 on success. */
-typedef int (*om_lowsvd_fn)(float* X32, int64_t n, float* U32, float* S32);
-void om_set_lowsvd(om_lowsvd_fn fn);
+/* The low-precision QR SVD of the AUTO branch (qrsvd.c, reading c-24):
+   fp32 Householder bidiagonalisation + fp32 implicit-shift QR on the bidiagonal, left rotations and
+   reflectors accumulated into U (n x n fp64, ldu; columns in descending singular value order); S the
+   singular values (fp32, descending).  X32 (ldx) is not modified.  0 ok, 1 no convergence, -3 a zero
+   diagonal of B (rank deficient). */
+int om_qrsvd32(const float* X32, int64_t n, int64_t ldx, double* U, int64_t ldu, float* S);
 
 void om_default_opts(om_opts* o);
 

@@ -90,7 +90,7 @@ _lib = None
 EXPORTS = [
     "mpjsvd_default_options", "mpjsvd_create", "mpjsvd_factor", "mpjsvd_destroy", "mpjsvd_strerror",
     "mpjsvd_last_cuda_error", "mpjsvd_version", "mpjsvd_block_jacobi_f64", "mpjsvd_block_jacobi_f32",
-    "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_switch_u", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
+    "mpjsvd_inner_solve", "mpjsvd_qr", "mpjsvd_lift", "mpjsvd_switch_u", "mpjsvd_qrsvd32", "mpjsvd_apply_q", "mpjsvd_gemm_f64",
     "mpjsvd_set_profiling", "mpjsvd_get_profile", "mpjsvd_comm_unique_id", "mpjsvd_comm_init",
     "mpjsvd_comm_info", "mpjsvd_plan_create", "mpjsvd_plan_info", "mpjsvd_plan_pairs", "mpjsvd_plan_advance",
     "mpjsvd_plan_locate", "mpjsvd_plan_destroy",
@@ -125,6 +125,7 @@ def lib():
         L.mpjsvd_lift.argtypes = [vp, vp, i64, i64, vp, i64]
         L.mpjsvd_switch_u.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, i32]
         L.mpjsvd_apply_q.argtypes = [vp, vp, i64, i64, i64, vp, vp, i64, i64]
+        L.mpjsvd_qrsvd32.argtypes = [vp, vp, i64, i64, vp, i64, vp]
         L.mpjsvd_gemm_f64.argtypes = [vp, i32, i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]
         L.mpjsvd_set_profiling.argtypes = [vp, i32]
         L.mpjsvd_get_profile.argtypes = [vp, i32, C.c_char_p, i32, C.POINTER(dbl), C.POINTER(i64)]
@@ -449,6 +450,27 @@ def switch_u(X, Ulow, x_lower: bool = True, handle: Handle | None = None):
                                    int(x_lower))
         _check(rc, "mpjsvd_switch_u")
         return Q
+    finally:
+        if own:
+            handle.close()
+
+
+def qrsvd32(X32, handle: Handle | None = None):
+    """Step-level: the fp32 QR SVD of the AUTO branch (U only; reading c-24) of a device fp32 n x n tensor.
+    Returns (U fp64 n x n column-major, S fp32 descending)."""
+    import torch
+    own = handle is None
+    if own:
+        handle = Handle(stream=torch.cuda.current_stream().cuda_stream)
+    try:
+        n = X32.shape[0]
+        Xc = X32.t().contiguous().t()
+        U = empty_col_major(n, n, torch.float64, X32.device)
+        S = torch.empty(n, dtype=torch.float32, device=X32.device)
+        rc = lib().mpjsvd_qrsvd32(handle.ptr, C.c_void_p(Xc.data_ptr()), n, Xc.stride(1), C.c_void_p(U.data_ptr()),
+                                  U.stride(1), C.c_void_p(S.data_ptr()))
+        _check(rc, "mpjsvd_qrsvd32")
+        return U, S
     finally:
         if own:
             handle.close()

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libmpjsvd.so")
-SOURCES = ["mpjsvd.cu", "k_jacobi.cu", "k_qr.cu", "k_qrp.cu", "k_linalg.cu", "k_misc.cu", "k_tc.cu", "comm.cpp", "lowsvd.cpp"]
+SOURCES = ["mpjsvd.cu", "k_jacobi.cu", "k_qr.cu", "k_qrp.cu", "k_linalg.cu", "k_misc.cu", "k_tc.cu", "comm.cpp", "k_qrsvd.cu"]
 HEADERS = ["common.cuh", "jacobi.h", "shard.h", "comm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

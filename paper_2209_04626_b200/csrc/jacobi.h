@@ -202,12 +202,13 @@ inline size_t wy_tcache_elems(int k) { return (size_t)((k + WY_PANEL - 1) / WY_P
 int qr_blocked(double* A, long long lda, int m, int n, double* tau, QrWork& w, double* work, cudaStream_t st,
                double* tcache = nullptr);
 
-// ---- fp32 QR SVD of the AUTO branch (lowsvd.cpp, cuSOLVER sgesvd via dlopen) ----
-size_t lowsvd_work_bytes(int n);
-int lowsvd_sgesvd(float* X32, int n, long long ldx, float* S, float* U, long long ldu, void* work, size_t work_bytes,
-                  cudaStream_t st);
-const char* lowsvd_last_error();
-
+// ---- fp32 QR SVD of the AUTO branch (k_qrsvd.cu, reading c-24) ----
+// X32 (n x n, ldx; destroyed: holds the bidiagonalisation) -> U (n x n fp64, ldu; columns in descending
+// singular value order).  UB: n x n fp64 scratch (ldu); P: packed fp64 reflectors (ldp >= n); work:
+// qrsvd32_work_bytes(n); wy_work: apply_q_work_elems(ldp, n) doubles.  *bad set on an exact zero singular value.
+size_t qrsvd32_work_bytes(int n);
+int qrsvd32(float* X32, long long ldx, int n, double* U, long long ldu, double* UB, double* P, long long ldp,
+            void* work, double* wy_work, int* bad, cudaStream_t st, float* S_out = nullptr);
 // ---- misc (k_misc.cu) ----------------------------------------------------
 int check_finite(const double* A, long long lda, long long m, long long n, int* bad, cudaStream_t st);
 int copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows, long long cols,

@@ -871,33 +871,17 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- stage 4: fp32 block Jacobi
     JacobiResult r32, r64;
     if (taken == MPJSVD_TAKEN_QRSVD) {
-        // fp32 QR SVD of lower(X), U only (lowsvd.cpp), then the U-route switch
-        // Q R2 = X^T working(U_low) (446-447) and Y = X Q; non-root ranks wait for Y and Q
+        // fp32 QR SVD of lower(X), U only (k_qrsvd.cu, reading c-24), then the
+        // U-route switch Q R2 = X^T working(U_low) (446-447) and Y = X Q; non-root ranks wait for Y and Q
         if (root) {
             MPJ_TRY(maxabs(dX, n_pad, n_pad, n, scal + 0, st));
             MPJ_TRY(downcast_scaled(dX, n_pad, dX32, n_pad, n_pad, (int)n, scal + 0, st));
-            const size_t wb = lowsvd_work_bytes((int)n);
-            if (wb == 0) {
-                snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "fp32 QR SVD branch: %s", lowsvd_last_error());
-                return MPJSVD_ERR_NOT_SUPPORTED;
-            }
-            MPJ_TRY(ensure(h, S_U32, sizeof(float) * nn));
-            MPJ_TRY(ensure(h, S_S32, sizeof(float) * (size_t)n_pad));
-            MPJ_TRY(ensure(h, S_SVDWS, wb));
-            MPJ_TRY(ensure(h, S_IOTA, sizeof(int) * (size_t)n));
-            float* dU32 = P<float>(h, S_U32);
-            MPJ_CUDA_TRY(cudaMemsetAsync(dU32, 0, sizeof(float) * nn, st));
+            MPJ_TRY(ensure(h, S_SVDWS, qrsvd32_work_bytes((int)n)));
             PROF_B("qrsvd32");
-            const int lrc = lowsvd_sgesvd(dX32, (int)n, n_pad, P<float>(h, S_S32), dU32, n_pad, P<void>(h, S_SVDWS), wb, st);
+            // U_B in dY, packed fp64 reflectors in dVX (both free until the switch), U_low -> dUX
+            MPJ_TRY(qrsvd32(dX32, n_pad, (int)n, dUX, n_pad, dY, dVX, n_pad, P<void>(h, S_SVDWS), P<double>(h, S_WY),
+                            flags + 1, st));
             PROF_E("qrsvd32");
-            if (lrc) {
-                snprintf(g_last_cuda_err, sizeof(g_last_cuda_err), "fp32 QR SVD branch: %s", lowsvd_last_error());
-                return lrc == -7 ? MPJSVD_ERR_NOT_SUPPORTED : MPJSVD_ERR_CUDA;
-            }
-            std::vector<int> iota(n);
-            for (int i = 0; i < (int)n; ++i) iota[i] = i;
-            MPJ_CUDA_TRY(cudaMemcpyAsync(P<int>(h, S_IOTA), iota.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
-            MPJ_TRY(sort_upcast_v(dU32, n_pad, P<int>(h, S_IOTA), dUX, n_pad, n_pad, (int)n, st));   // U_low, fp64
             MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
             PROF_B("switch_u");
             MPJ_TRY(switch_u_inplace(h, dX, dUX, dVX, dQ, n_pad, (int)n, o.x_from_lq != 0, qw, st));
@@ -1627,6 +1611,47 @@ int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, co
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(Q, sizeof(double) * ldq, Qw, sizeof(double) * n_pad, sizeof(double) * n, n,
                                    cudaMemcpyDefault, st));
     MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int mpjsvd_qrsvd32(mpjsvd_handle h, const float* X32, int64_t n, int64_t ldx, double* U, int64_t ldu, float* S) {
+    if (!h || !X32 || !U || n < 1 || ldx < n || ldu < n) return MPJSVD_ERR_INVALID_ARG;
+    if (n > 16384) return MPJSVD_ERR_NOT_SUPPORTED;
+    g_mpj_diag = h->opts.diag_timing;
+    if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); return MPJSVD_ERR_CUDA; }
+    gemm_set_workspace(nullptr, 0);
+    cudaStream_t st = h->stream;
+    const long long n_pad = round_up(n, 32);
+    const size_t nn = (size_t)n_pad * n;
+    MPJ_TRY(ensure(h, S_TMP1, sizeof(double) * 3 * nn));
+    MPJ_TRY(ensure(h, S_TMP2, sizeof(float) * nn));
+    MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(n_pad, n)));
+    MPJ_TRY(ensure(h, S_SVDWS, qrsvd32_work_bytes((int)n)));
+    MPJ_TRY(ensure(h, S_FLAGS, sizeof(int) * 8));
+    MPJ_TRY(ensure(h, S_SCAL, sizeof(double) * 8 + sizeof(float) * (size_t)n));
+    double* Uw = P<double>(h, S_TMP1);
+    double* UBw = Uw + nn;
+    double* Pw = UBw + nn;
+    float* Xw = P<float>(h, S_TMP2);
+    int* flags = P<int>(h, S_FLAGS);
+    MPJ_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * 8, st));
+    MPJ_CUDA_TRY(cudaMemsetAsync(Xw, 0, sizeof(float) * nn, st));
+    MPJ_CUDA_TRY(cudaMemsetAsync(Uw, 0, sizeof(double) * nn, st));
+    MPJ_CUDA_TRY(cudaMemcpy2DAsync(Xw, sizeof(float) * n_pad, X32, sizeof(float) * ldx, sizeof(float) * n, n,
+                                   cudaMemcpyDefault, st));
+    MPJ_TRY(qrsvd32(Xw, n_pad, (int)n, Uw, n_pad, UBw, Pw, n_pad, P<void>(h, S_SVDWS), P<double>(h, S_WY),
+                    flags + 1, st, reinterpret_cast<float*>(P<double>(h, S_SCAL) + 8)));
+    MPJ_CUDA_TRY(cudaMemcpy2DAsync(U, sizeof(double) * ldu, Uw, sizeof(double) * n_pad, sizeof(double) * n, n,
+                                   cudaMemcpyDefault, st));
+    int hf = 0;
+    MPJ_CUDA_TRY(cudaMemcpyAsync(&hf, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hf) return MPJSVD_ERR_RANK_DEFICIENT;
+    if (S) {
+        MPJ_CUDA_TRY(cudaMemcpyAsync(S, reinterpret_cast<float*>(P<double>(h, S_SCAL) + 8), sizeof(float) * n,
+                                     cudaMemcpyDefault, st));
+        MPJ_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     return 0;
 }
 

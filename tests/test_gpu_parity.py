@@ -578,3 +578,48 @@ def test_option_paths_vs_oracle(mp, opts, oopts):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
     if not opts.get("x_from_lq", 1) == 0:
         assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
+
+
+@pytest.mark.parametrize("name,n", [("exact", 64), ("C1", 256), ("C3", 500), ("C2", 384), ("C5", 1000)])
+def test_qrsvd32_vs_oracle(mp, name, n):
+    """The hand-written fp32 QR SVD of the AUTO branch (k_bidiag32 cooperative bidiagonalisation, k_bdqr32
+    implicit-shift QR, k_rot_apply fp64 accumulation, WY application; reading c-24) against the oracle's
+    plain-C steps (oracle/qrsvd.c): sigma within twice the fp32 bound n u32 sigma_1, U orthogonal to the
+    fp32 level, U^T X with orthogonal rows, and left singular vectors equal up to sign where sigma is well
+    separated."""
+    U32 = 2.0 ** -24
+    if name == "exact":
+        a, _ = testmat.exact_sigma_matrix(n)
+    else:
+        a = testmat.config_matrix(name, n)
+        a = np.asfortranarray(np.linalg.qr(a.T)[1].T)     # X = L like the path (lower triangular)
+    x = np.asfortranarray((a / np.abs(a).max()).astype(np.float32))
+    U, S = mp.qrsvd32(dev(x, torch.float32))
+    U, S = host(U), host(S).astype(np.float64)
+    uo, so, rc = oracle.qrsvd32(x)
+    so = so.astype(np.float64)
+    assert rc == 0
+    assert np.all(np.diff(S) <= 0)
+    assert np.abs(S - so).max() <= 2 * n * U32 * so[0]
+    assert orth(U) <= 4 * n * U32
+    g = U.T @ x.astype(np.float64)
+    gg = g @ g.T
+    assert np.abs(gg - np.diag(np.diag(gg))).max() <= 8 * n * U32 * so[0] ** 2
+    gap = np.minimum(np.r_[np.inf, -np.diff(so)], np.r_[-np.diff(so), np.inf]) / so[0]
+    ok = gap > 1e-3
+    dots = np.abs(np.sum(U * uo, axis=0))
+    assert np.all(dots[ok] >= 1 - 1e-3)
+
+
+def test_auto_qrsvd_branch_larger_vs_oracle(mp):
+    """AUTO with tol_alg = 1e-3 (every C-config input then takes the QR SVD branch, F2): end to end against
+    the oracle's same branch at n = 512 -- valid SVD, tiered sigma, fp64 sweeps +-1."""
+    a = testmat.config_matrix("C3", 512)
+    U, S, V, st = mp.factor(dev(a), path=1, tol_alg=1e-3)
+    U, S, V = host(U), host(S), host(V)
+    uo, so, vo, sto, rc = oracle.mixed_svd(a, path=1, tol_alg=1e-3)
+    assert rc == 0 and st["rc"] == 0
+    assert st["path_taken"] == sto["path_taken"] == 6
+    check_svd(a, U, S, V)
+    assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+    assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1

@@ -698,3 +698,65 @@ def test_refine_v_high_relative_accuracy():
     ref = np.array(sorted((float(x) for x in mpmath.svd_r(mpmath.matrix(a.tolist()), compute_uv=False)),
                           reverse=True))
     assert np.max(np.abs(s - ref) / ref) < 1e-13
+
+
+# ---------------------------------------------------------------- fp32 QR SVD
+U32 = 2.0 ** -24
+
+
+@pytest.mark.parametrize("n", [16, 64, 256])
+def test_qrsvd32_exact_sigma_within_fp32_bound(n):
+    """The lower-precision QR SVD (qrsvd.c, reading c-24) of fl32(A) for the exact-sigma construction:
+    |sigma_i - sigma_i(A)| <= n u32 sigma_1 (input rounding + backward error of bidiagonalisation and QR
+    iteration, Weyl), U orthogonal to the fp32 level, and U^T X has orthogonal rows of norms sigma."""
+    a, sigma = testmat.exact_sigma_matrix(n)
+    x = a.astype(np.float32)
+    u, s, rc = oracle.qrsvd32(x)
+    assert rc == 0
+    assert np.all(np.diff(s.astype(np.float64)) <= 0)
+    assert np.abs(s - sigma).max() <= n * U32 * sigma[0]
+    assert orth(u) <= 4 * n * U32
+    g = u.T @ x.astype(np.float64)
+    gg = g @ g.T
+    assert np.abs(gg - np.diag(np.diag(gg))).max() <= 8 * n * U32 * sigma[0] ** 2
+    assert np.abs(np.sqrt(np.diag(gg)) - s).max() <= n * U32 * sigma[0]
+
+
+def test_qrsvd32_closed_forms():
+    """Diagonal input (signs, distinct magnitudes): no rotation survives, sigma = sorted |d| exactly and |U| is
+    the sorting permutation; [[1, 1], [0, 1]]: sigma = (phi, 1/phi) to fp32 accuracy; an exact zero on the
+    bidiagonal's diagonal is rank deficient (rc = -3, reading c-18)."""
+    d = np.array([0.5, -2.0, 0.25, 1.0, -0.125], dtype=np.float32)
+    u, s, rc = oracle.qrsvd32(np.diag(d))
+    assert rc == 0
+    order = np.argsort(-np.abs(d), kind="stable")
+    assert np.array_equal(s, np.abs(d)[order])
+    assert np.array_equal(np.abs(u), np.eye(5)[:, order])
+    u, s, rc = oracle.qrsvd32(np.array([[1.0, 1.0], [0.0, 1.0]], dtype=np.float32))
+    phi = (1 + np.sqrt(5)) / 2
+    assert rc == 0 and abs(s[0] - phi) <= 4 * U32 * phi and abs(s[1] - 1 / phi) <= 4 * U32 * phi
+    z = np.asfortranarray(np.random.default_rng(3).standard_normal((6, 6)).astype(np.float32))
+    z[:, 2] = 0.0
+    u, s, rc = oracle.qrsvd32(z)
+    # singular input: either an exact zero on B's diagonal (rc -3) or a computed sigma_min at rounding level
+    assert rc == -3 or (rc == 0 and s[-1] <= 6 * U32 * s[0])
+    z[:, 0] = 0.0
+    z[0, :] = 0.0     # first column zero: the first reflector is the identity and d_0 = 0 exactly
+    assert oracle.qrsvd32(z)[2] == -3
+
+
+def test_qrsvd32_vs_lapack_sgesvd():
+    """Third opinion: LAPACK sgesvd (the routine the paper's x86 code calls for this branch)
+    on the C1 recipe: sigma within the fp32 bound, left singular vectors equal up to sign where the sigma are
+    well separated."""
+    import scipy.linalg as sl
+    n = 128
+    x = testmat.config_matrix("C1", n).astype(np.float32)
+    u, s, rc = oracle.qrsvd32(x)
+    ul, sl_, _ = sl.svd(x, lapack_driver="gesvd")
+    assert rc == 0
+    assert np.abs(s - sl_).max() <= n * U32 * sl_[0]
+    gap = np.minimum(np.r_[np.inf, -np.diff(sl_)], np.r_[-np.diff(sl_), np.inf]) / sl_[0]
+    ok = gap > 1e-3
+    dots = np.abs(np.sum(u * ul.astype(np.float64), axis=0))
+    assert np.all(dots[ok] >= 1 - 1e-3)
