@@ -7,14 +7,17 @@
  * paper's four stages:
  *   (1) preconditioning: [m > n] Householder QR A = Q_tall R1,
  *       column-pivoted QR A1 P = Q_p R, LQ R = L Q_2 and
- *       X = L (reading R1);
- *   (2) fp32 one-sided block Jacobi on fl32(X 2^-e) accumulating V32
- *       (Alg. 1);
- *   (3) precision switch: Q = qr(fl64(V32)) by CholeskyQR, Y = X Q
- *       (PAPER.md:553-561, 450);
- *   (4) fp64 one-sided block Jacobi on (Y, V := Q) to eps_tol, then
- *       sigma_j = ||y_j||, U_X = Y diag(1/sigma), descending sort
- *       (PAPER.md:452-455, 575-597, 305-310);
+ *       X = L (reading c-7);
+ *   (2) fp32 one-sided block Jacobi on fl32(X 2^-e) computing U_low only
+ *       (Alg. 1) -- or, under
+ *       path = AUTO, the gates of Alg. 3 and possibly the fp32 QR SVD
+ *       (DESIGN.md c-15, c-24);
+ *   (3) precision switch (U-route, the paper's Alg. 3 l.446-447): Q from the
+ *       Householder QR of X^T working(U_low), Y = X Q (
+ *       DESIGN.md c-11; switch_u = 0 selects the V-route CholeskyQR of V32);
+ *   (4) fp64 one-sided block Jacobi on (Y, V := Q) to eps_tol (or the sec. 3.4
+ *       V formation, refine_v = 1, DESIGN.md c-23), then sigma_j = ||y_j||,
+ *       U_X = Y diag(1/sigma), descending sort;
  * and assembles U = Q_tall Q_p U_X, V = P Q_t V_X.
  *
  * Conventions (all entry points):
@@ -60,6 +63,7 @@ extern "C" {
 #define MPJSVD_ERR_NCCL (-5)          /* NCCL missing or failed (see mpjsvd_last_cuda_error) */
 #define MPJSVD_ERR_OUT_OF_MEMORY (-6)
 #define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1, block_cols unsupported, n > 16384 */
+#define MPJSVD_ERR_BREAKDOWN (-8)     /* finite input, non-finite intermediate (fp32 stage overflow, switch) */
 
 /* path (Alg. 3 gates; reading c-15) */
 #define MPJSVD_PATH_FORCE_MIXED 0     /* always run the fp32 Jacobi stage (default) */
@@ -144,7 +148,8 @@ typedef struct {
 } mpjsvd_options;
 
 typedef struct {
-    int32_t path_taken;        /* MPJSVD_PATH_FORCE_MIXED or _FORCE_FP64 */
+    int32_t path_taken;        /* MPJSVD_TAKEN_*: 0 fp32 Jacobi, 2 fp64 only (forced), 3/4/5 fp64 only by the AUTO
+                                  cond / tail / orth gate, 6 fp32 QR SVD (AUTO, orth > tol_alg) */
     int32_t sweeps32, sweeps64, converged;
     double stage_ms[8];        /* qr_tall, qrp, lq, gates, fp32, lift, fp64, assemble (CUDA events) */
     double total_ms;           /* device time from entry to outputs written */

@@ -699,7 +699,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             MPJ_CUDA_TRY(cudaStreamSynchronize(st));
             memcpy(hf, h_hdr + 4, sizeof(hf));
         }
-        h_hdr[0] = hf[0] ? code_if_flag0 : ((hf[1] || hf[2]) ? code_if_flag12 : 0);
+        h_hdr[0] = hf[0] ? code_if_flag0 : ((hf[1] || hf[2]) ? code_if_flag12 : (hf[3] ? MPJSVD_ERR_BREAKDOWN : 0));
         MPJ_CUDA_TRY(cudaMemcpyAsync(d_hdr, h_hdr, sizeof(long long), cudaMemcpyHostToDevice, st));
         MPJ_TRY(h->comm.bcast(d_hdr, sizeof(long long), 0, st));
         MPJ_CUDA_TRY(cudaMemcpyAsync(h_hdr, d_hdr, sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -912,6 +912,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         if (root) {
         // sort by sigma32 (descending, stable) and upcast V32 -> Q
         MPJ_TRY(col_norms<float>(dX32, n_pad, n_pad, (int)n, P<double>(h, S_KEYS), 0, st));
+        MPJ_TRY(check_finite(P<double>(h, S_KEYS), n, n, 1, flags + 3, st));     // fp32 stage breakdown
         MPJ_TRY(rank_desc(P<double>(h, S_KEYS), (int)n, P<int>(h, S_RANK), st));
         if (uroute) {
             // U_low = working(X32 Sigma32^-1), sigma32-descending
@@ -937,6 +938,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         // X lower triangular (X = L, reading c-7): K range of a row tile ends at its last row
         MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
         PROF_E("rv_gemm");
+        MPJ_TRY(check_finite(dY, n_pad, n, n, flags + 3, st));                   // switch / lift breakdown
         } else {
             MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
         }
@@ -1097,6 +1099,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (h->prof.on) h->prof.resolve();
     if (hflags[0]) return MPJSVD_ERR_NONFINITE;
     if (hflags[1] || hflags[2]) return MPJSVD_ERR_RANK_DEFICIENT;
+    if (hflags[3]) return MPJSVD_ERR_BREAKDOWN;
 
     fill_sweep_stats();
     s.cond_estimate = hscal[2] > 0 ? hscal[1] / hscal[2] : INFINITY;
@@ -1320,6 +1323,7 @@ const char* mpjsvd_strerror(int code) {
         case MPJSVD_ERR_NCCL: return "NCCL error (see mpjsvd_last_cuda_error)";
         case MPJSVD_ERR_OUT_OF_MEMORY: return "out of device memory";
         case MPJSVD_ERR_NOT_SUPPORTED: return "not supported in this build";
+        case MPJSVD_ERR_BREAKDOWN: return "non-finite intermediate from a finite input (fp32 stage or precision switch)";
         default: return "unknown error code";
     }
 }

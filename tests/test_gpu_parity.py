@@ -442,6 +442,32 @@ def test_errors(mp):
     assert st["rc"] == 1 and not st["converged"]
 
 
+@pytest.mark.parametrize("kind", ["nan_row", "nan_cols", "inf_col", "all_nan"])
+def test_nonfinite_inputs_fail_cleanly(mp, kind):
+    """a NaN/Inf input must return MPJSVD_ERR_NONFINITE before the QRP (whose argmax has no
+    finite candidate) -- a whole NaN row, several NaN columns, an Inf column, all NaN -- on the square and the
+    tall path and with mp_rrqr; the same handle then factors a valid matrix correctly (no context damage)."""
+    a = testmat.config_matrix("C1", 256)
+    bad = a.copy()
+    if kind == "nan_row":
+        bad[17, :] = np.nan
+    elif kind == "nan_cols":
+        bad[:, [3, 100, 255]] = np.nan
+    elif kind == "inf_col":
+        bad[:, 9] = np.inf
+    else:
+        bad[:] = np.nan
+    h = mp.Handle(stream=torch.cuda.current_stream().cuda_stream)
+    for arr, kw in ((bad, {}), (np.vstack([bad, bad]), {}), (bad, {"mp_rrqr": 1})):
+        hh = mp.Handle(stream=torch.cuda.current_stream().cuda_stream, **kw) if kw else h
+        with pytest.raises(mp.MpjsvdError) as e:
+            mp.factor(dev(np.asfortranarray(arr)), handle=hh)
+        assert e.value.code == -2
+    U, S, V, st = mp.factor(dev(a), handle=h)
+    check_svd(a, host(U), host(S), host(V))
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("name,n", [("C3", 512), ("C2", 384), ("C4", 256)])
 def test_factor_mixed_precision_rrqr_vs_oracle(mp, name, n):
     """The mixed-precision RRQR preconditioning (PAPER.md:496-512, Alg. 4;
