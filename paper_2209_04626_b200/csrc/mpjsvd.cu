@@ -229,9 +229,11 @@ void build_sweep(JStore<T>& S, int b, int n, std::vector<PairDesc<T>>& table,
 }
 
 // Transfers of one round's inter-rank moves (bye blocks carry no data).
+// lmod (NCCL ranks with the exact skip on): each moved block's last-rotation round travels with it
+// (4 bytes in the same group), so the receiving rank can skip the block's pairs exactly like one process.
 template <typename T>
 int exchange(mpjsvd_handle h, JStore<T>& S, const std::vector<ShardPlan::Move>& mv, size_t bytes_x,
-             size_t bytes_v, cudaStream_t st) {
+             size_t bytes_v, cudaStream_t st, int* lmod = nullptr) {
     if (mv.empty()) return 0;
     const bool nccl = h->comm.active();
     if (nccl) MPJ_TRY(h->comm.group_start());
@@ -248,9 +250,11 @@ int exchange(mpjsvd_handle h, JStore<T>& S, const std::vector<ShardPlan::Move>& 
         } else if (sl) {
             if (!rc) rc = h->comm.send(S.bx(m.src_rank, m.src_buf), bytes_x, m.dst_rank, st);
             if (!rc && bytes_v) rc = h->comm.send(S.bv(m.src_rank, m.src_buf), bytes_v, m.dst_rank, st);
+            if (!rc && lmod) rc = h->comm.send(lmod + m.blk, sizeof(int), m.dst_rank, st);
         } else if (dl) {
             if (!rc) rc = h->comm.recv(S.bx(m.dst_rank, m.dst_buf), bytes_x, m.src_rank, st);
             if (!rc && bytes_v) rc = h->comm.recv(S.bv(m.dst_rank, m.dst_buf), bytes_v, m.src_rank, st);
+            if (!rc && lmod) rc = h->comm.recv(lmod + m.blk, sizeof(int), m.src_rank, st);
         }
     }
     if (nccl) {
@@ -356,12 +360,14 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         }
     }
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
-    // exact skip of unchanged pairs (one process holds every block's history; NCCL ranks evaluate all)
+    // exact skip of unchanged pairs (every block's last-rotation round: one array per process; across NCCL
+    // ranks the entry travels with the block in the per-round exchange)
     MPJ_TRY(ensure(h, S_LMOD, sizeof(int) * (size_t)(S.plan.M + 8)));
     MPJ_TRY(ensure(h, S_POFF, sizeof(double) * (size_t)R * npairs));
     a.last_mod = P<int>(h, S_LMOD);
     a.R = R;
-    a.skip = (S.me < 0 && h->opts.skip_unchanged) ? 1 : 0;
+    a.skip = h->opts.skip_unchanged ? 1 : 0;
+    int* lmod_ship = (S.me >= 0 && a.skip) ? a.last_mod : nullptr;
     MPJ_CUDA_TRY(cudaMemsetAsync(a.last_mod, 0xff, sizeof(int) * (size_t)(S.plan.M + 8), st));   // -1
 
     double* hp = reinterpret_cast<double*>(h->host_pinned);
@@ -386,13 +392,14 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             MPJ_TRY(launch_jacobi_round<T>(a, W, st, h->prof.on ? &hook : nullptr));
             if (!moves[r].empty()) {
                 if (h->prof.on) h->prof.begin("exchange");
-                MPJ_TRY(exchange<T>(h, S, moves[r], bytes_x, bytes_v, st));
+                MPJ_TRY(exchange<T>(h, S, moves[r], bytes_x, bytes_v, st, lmod_ship));
                 if (h->prof.on) h->prof.end("exchange");
             }
         }
         if (h->comm.active()) {
             MPJ_TRY(h->comm.allreduce_max_f64(d_off + (sw - 1), 1, st));
             MPJ_TRY(h->comm.allreduce_sum_i32(d_upd + (sw - 1), 1, st));
+            MPJ_TRY(h->comm.allreduce_sum_i32(d_skip + (sw - 1), 1, st));
         }
         MPJ_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(hp + 2), d_inner + 2 * (sw - 1), 2 * sizeof(int),
                                      cudaMemcpyDeviceToHost, st));
