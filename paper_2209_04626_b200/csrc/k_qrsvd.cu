@@ -326,6 +326,78 @@ __global__ void k_rot_apply(double* U, long long ldu, int n, const float2* __res
     }
 }
 
+// The same rotations, RB consecutive steps per pass over a row (wavefront): at outer position p step s applies
+// its rotation at i = p - s, so a row keeps a window of RB + 1 elements in registers and every element is read
+// and written once per RB steps instead of once per step.  Positions outside a step's [lo, hi) are identity.
+// Identical arithmetic per rotation as k_rot_apply (same order of the two FMAs per element).
+template <int RB>
+__global__ void k_rot_apply_wave(double* U, long long ldu, int n, const float2* __restrict__ rot,
+                                 const int2* __restrict__ steps, const long long* __restrict__ offs, int nsteps) {
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double* ur = U + r;
+    for (int s0 = 0; s0 < nsteps; s0 += RB) {
+        int lo[RB], hi[RB];
+        long long of[RB];
+        int lmin = 1 << 30, hmax = -1;
+#pragma unroll
+        for (int s = 0; s < RB; ++s) {
+            if (s0 + s < nsteps) {
+                const int2 sp = steps[s0 + s];
+                lo[s] = sp.x;
+                hi[s] = sp.y;
+                of[s] = offs[s0 + s] - sp.x;
+            } else {
+                lo[s] = 1 << 30;
+                hi[s] = -1;
+                of[s] = 0;
+            }
+            lmin = min(lmin, lo[s]);
+            hmax = max(hmax, hi[s]);
+        }
+        // window w[j] = u[p - RB + 1 + j], j = 0..RB, at outer position p
+        double w[RB + 1];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) w[j] = 0.0;
+        w[RB - 1] = ur[(long long)lmin * ldu];
+        const int pend = hmax - 1 + RB - 1;
+        for (int p = lmin; p <= pend; ++p) {
+            w[RB] = (p + 1 <= hmax) ? ur[(long long)(p + 1) * ldu] : 0.0;
+#pragma unroll
+            for (int s = 0; s < RB; ++s) {
+                const int i = p - s;
+                if (i >= lo[s] && i < hi[s]) {
+                    const float2 cs = rot[of[s] + i];
+                    const double c = cs.x, sn = cs.y;
+                    const double a = w[RB - 1 - s], b = w[RB - s];
+                    w[RB - 1 - s] = c * a + sn * b;
+                    w[RB - s] = c * b - sn * a;
+                }
+            }
+            const int q = p - RB + 1;                 // element leaving the window: final for this batch
+            if (q >= lmin) ur[(long long)q * ldu] = w[0];
+#pragma unroll
+            for (int j = 0; j < RB; ++j) w[j] = w[j + 1];
+        }
+        // the window still holds u[pend - RB + 2 .. pend + 1] in w[0 .. RB - 1]
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const int q = pend - RB + 2 + j;
+            if (q >= lmin && q <= hmax) ur[(long long)q * ldu] = w[j];
+        }
+    }
+}
+
+__global__ void k_step_offsets(const int2* steps, int nsteps, long long* offs) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        long long o = 0;
+        for (int s = 0; s < nsteps; ++s) {
+            offs[s] = o;
+            o += steps[s].y - steps[s].x;
+        }
+    }
+}
+
 // packed fp64 copy of the fp32 reflectors (for the WY application) and |d| as fp64 sort keys
 __global__ void k_qrsvd_prep(const float* A, long long lda, const float* tau, const float* d, int n, double* P,
                              long long ldp, double* tau64, double* keys) {
@@ -359,7 +431,7 @@ size_t qrsvd32_work_bytes(int n) {
     b += sizeof(float) * (size_t)n * 4;                 // d, e, tau, rowbuf
     b += sizeof(float) * (size_t)n;                     // p
     b += sizeof(float) * (size_t)nsm * n;               // ppart
-    b += sizeof(float2) * (size_t)cap_rot + sizeof(int2) * (size_t)cap_steps + 256;
+    b += sizeof(float2) * (size_t)cap_rot + (sizeof(int2) + sizeof(long long)) * (size_t)cap_steps + 512;
     b += sizeof(double) * (size_t)n * 2 + sizeof(int) * (size_t)n + 1024;
     return b;
 }
@@ -382,6 +454,7 @@ int qrsvd32(float* X32, long long ldx, int n, double* U, long long ldu, double* 
     float* ppart = (float*)take(sizeof(float) * (size_t)nsm * n);
     float2* rot = (float2*)take(sizeof(float2) * (size_t)cap_rot);
     int2* steps = (int2*)take(sizeof(int2) * (size_t)cap_steps);
+    long long* offs = (long long*)take(sizeof(long long) * (size_t)cap_steps);
     BdqrState* bst = (BdqrState*)take(sizeof(BdqrState));
     double* tau64 = (double*)take(sizeof(double) * n);
     double* keys = (double*)take(sizeof(double) * n);
@@ -413,7 +486,9 @@ int qrsvd32(float* X32, long long ldx, int n, double* U, long long ldu, double* 
         MPJ_CUDA_TRY(cudaMemcpyAsync(&hs, bst, sizeof(hs), cudaMemcpyDeviceToHost, st));
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
         if (hs.nsteps > 0) {
-            k_rot_apply<<<(unsigned)ceil_div(n, 64), 64, 0, st>>>(UB, ldu, n, rot, steps, hs.nsteps);
+            k_step_offsets<<<1, 32, 0, st>>>(steps, hs.nsteps, offs);
+            MPJ_LAUNCHED();
+            k_rot_apply_wave<8><<<(unsigned)ceil_div(n, 32), 32, 0, st>>>(UB, ldu, n, rot, steps, offs, hs.nsteps);
             MPJ_LAUNCHED();
         }
         if (hs.done) break;

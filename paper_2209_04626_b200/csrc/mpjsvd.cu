@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mpjsvd.h"
 #include "common.cuh"
 #include "comm.h"
@@ -617,6 +619,24 @@ int switch_u_inplace(mpjsvd_handle h, const double* X, const double* Ulow, doubl
     return 0;
 }
 
+// NVTX range per stage of factor (nsys / ncu --nvtx), closed on every exit path
+struct NvtxStages {
+    bool open = false;
+    void mark(const char* name) {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    void close() {
+        if (open) nvtxRangePop();
+        open = false;
+    }
+    ~NvtxStages() { close(); }
+};
+static const char* const kStageNames[10] = {"mpjsvd:qr_tall", "mpjsvd:qrp", "mpjsvd:lq", "mpjsvd:gates",
+                                            "mpjsvd:fp32_stage", "mpjsvd:switch", "mpjsvd:fp64_stage",
+                                            "mpjsvd:assemble", "mpjsvd:outputs", nullptr};
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
@@ -631,6 +651,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     const mpjsvd_options& o = h->opts;
     h->prof.st = h->stream;
     cudaStream_t st = h->stream;
+    NvtxStages nvtx;
     const long long m_pad = round_up(m, 32), n_pad = round_up(n, 32);
     const bool a_dev = A && is_device_ptr(A), u_dev = U && is_device_ptr(U), s_dev = S && is_device_ptr(S),
                v_dev = V && is_device_ptr(V);
@@ -713,7 +734,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
         return (int)h_hdr[0];
     };
-    MPJ_CUDA_TRY(cudaEventRecord(ev[0], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[0], st)); nvtx.mark(kStageNames[0]);
     MPJ_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * 8, st));
     QrWork qw;
     std::vector<double> xnorms;
@@ -753,7 +774,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     } else {
         MPJ_TRY(copy_matrix(dA, m_pad, dA1, n_pad, n_pad, n, st));
     }
-    MPJ_CUDA_TRY(cudaEventRecord(ev[1], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[1], st)); nvtx.mark(kStageNames[1]);
     if (autop) {
         // column norms of A1 = D of A = B D (cond gate; reading c-15)
         MPJ_TRY(ensure(h, S_A1N, sizeof(double) * n));
@@ -803,7 +824,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     tcp_all = true;
     }
     MPJ_TRY(diag_stats(dA1L, n_pad, (int)n, scal + 1, flags + 1, st));
-    MPJ_CUDA_TRY(cudaEventRecord(ev[2], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[2], st)); nvtx.mark(kStageNames[2]);
     // ---- stage 2: R = L Q_2 via QR of R^T; X = L
     if (o.x_from_lq) {
         MPJ_TRY(transpose_upper(dA1L, n_pad, dRt, n_pad, (int)n, n_pad, st));
@@ -816,7 +837,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     } else {
         MPJ_TRY(upper_of(dA1L, n_pad, dX, n_pad, (int)n, n_pad, st));
     }
-    MPJ_CUDA_TRY(cudaEventRecord(ev[3], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[3], st)); nvtx.mark(kStageNames[3]);
     // ---- stage 3: gate measures, report only
     if (o.compute_gates || autop) {
         PROF_B("gates_orth");
@@ -870,7 +891,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
         taken = (int)h_hdr[0];
     }
-    MPJ_CUDA_TRY(cudaEventRecord(ev[4], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[4], st)); nvtx.mark(kStageNames[4]);
     {
         const int rc = agree_status(MPJSVD_ERR_NONFINITE, MPJSVD_ERR_RANK_DEFICIENT);
         if (rc) return rc;
@@ -889,7 +910,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             MPJ_TRY(qrsvd32(dX32, n_pad, (int)n, dUX, n_pad, dY, dVX, n_pad, P<void>(h, S_SVDWS), P<double>(h, S_WY),
                             flags + 1, st));
             PROF_E("qrsvd32");
-            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st)); nvtx.mark(kStageNames[5]);
             PROF_B("switch_u");
             MPJ_TRY(switch_u_inplace(h, dX, dUX, dVX, dQ, n_pad, (int)n, o.x_from_lq != 0, qw, st));
             PROF_E("switch_u");
@@ -897,7 +918,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
             MPJ_TRY(gemm_f64_ex(0, 0, n_pad, n, n, 1.0, dX, n_pad, dQ, n_pad, 0.0, dY, n_pad, o.x_from_lq ? 2 : 0, st));
             PROF_E("rv_gemm");
         } else {
-            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st)); nvtx.mark(kStageNames[5]);
         }
         s.path_taken = MPJSVD_TAKEN_QRSVD;
     } else if (taken == MPJSVD_TAKEN_JACOBI) {
@@ -928,7 +949,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         } else {
             MPJ_TRY(sort_upcast_v(dV32, n_pad, P<int>(h, S_RANK), dQ, n_pad, n_pad, (int)n, st));
         }
-        MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+        MPJ_CUDA_TRY(cudaEventRecord(ev[5], st)); nvtx.mark(kStageNames[5]);
         // ---- stage 5: switch precisions, Y = X Q
         if (uroute) {
             // Q = qr(X^T U_low) (U-route); dVX is free until the finalise step
@@ -947,12 +968,12 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         PROF_E("rv_gemm");
         MPJ_TRY(check_finite(dY, n_pad, n, n, flags + 3, st));                   // switch / lift breakdown
         } else {
-            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+            MPJ_CUDA_TRY(cudaEventRecord(ev[5], st)); nvtx.mark(kStageNames[5]);
         }
         s.path_taken = MPJSVD_TAKEN_JACOBI;
     } else {
         // fp64 only: forced, or an AUTO gate fired (Q = I, Y = X)
-        MPJ_CUDA_TRY(cudaEventRecord(ev[5], st));
+        MPJ_CUDA_TRY(cudaEventRecord(ev[5], st)); nvtx.mark(kStageNames[5]);
         if (root) {
             MPJ_TRY(set_identity<double>(dQ, n_pad, n_pad, n, st));
             MPJ_TRY(copy_matrix(dX, n_pad, dY, n_pad, n_pad, n, st));
@@ -969,7 +990,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(h->comm.bcast(dQ, sizeof(double) * nn, 0, st));
         PROF_E("bcast");
     }
-    MPJ_CUDA_TRY(cudaEventRecord(ev[6], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[6], st)); nvtx.mark(kStageNames[6]);
     // ---- stage 6: fp64 refinement with V := Q
     int v_sweeps64 = 0;
     if (!o.refine_v) {
@@ -1016,7 +1037,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         r64.converged = ra.converged && rb.converged;
         v_sweeps64 = rb.sweeps;
     }
-    MPJ_CUDA_TRY(cudaEventRecord(ev[7], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[7], st)); nvtx.mark(kStageNames[7]);
     auto fill_sweep_stats = [&]() {
         s.sweeps32 = r32.sweeps;
         s.sweeps64 = r64.sweeps;
@@ -1034,7 +1055,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     };
     if (!root) {
         // non-root ranks end after the sharded refinement (outputs live on rank 0)
-        MPJ_CUDA_TRY(cudaEventRecord(ev[9], st));
+        MPJ_CUDA_TRY(cudaEventRecord(ev[9], st)); nvtx.close();
         MPJ_CUDA_TRY(cudaStreamSynchronize(st));
         if (h->prof.on) h->prof.resolve();
         fill_sweep_stats();
@@ -1084,7 +1105,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     if (v_chain) MPJ_CUDA_TRY(cudaStreamWaitEvent(st, h->join, 0));
     else MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, st));
     PROF_E("assemble_wy");
-    MPJ_CUDA_TRY(cudaEventRecord(ev[8], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[8], st)); nvtx.mark(kStageNames[8]);
     // ---- outputs (device -> device, or device -> host on the e2e path)
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(U, sizeof(double) * ldu, Ufin, sizeof(double) * ldUf, sizeof(double) * m, n,
                                    u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
@@ -1092,7 +1113,7 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
                                    v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaMemcpyAsync(S, P<double>(h, S_KEYS), sizeof(double) * n,
                                  s_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    MPJ_CUDA_TRY(cudaEventRecord(ev[9], st));
+    MPJ_CUDA_TRY(cudaEventRecord(ev[9], st)); nvtx.close();
     // ---- small read-backs for stats and error flags
     int hflags[8];
     double hscal[8];

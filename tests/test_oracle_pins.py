@@ -760,3 +760,44 @@ def test_qrsvd32_vs_lapack_sgesvd():
     ok = gap > 1e-3
     dots = np.abs(np.sum(u * ul.astype(np.float64), axis=0))
     assert np.all(dots[ok] >= 1 - 1e-3)
+
+
+# ---------------------------------------------------------------- fp32-stage exits (reading c-10)
+def _one_pair_matrix(theta):
+    """64 x 64 identity with column 40 += theta column 3: two blocks of b = 32, one pair per sweep; the pair
+    metric is theta / sqrt(1 + theta^2) exactly as constructed (dyadic theta, exact in fp32)."""
+    x = np.eye(64, dtype=np.float32)
+    x[3, 40] = np.float32(theta)
+    return np.asfortranarray(x)
+
+
+def test_fp32_near_convergence_exit():
+    """m = 64: eps_tol32 = 4 sqrt(64) 2^-24 = 2^-19 exactly.  A pair metric of 1.5 eps_tol rotates (> eps_tol)
+    and then ends the stage (<= 2 eps_tol, the near-convergence exit): 1 sweep, converged.  At 3 eps_tol there is
+    no exit after sweep 1 and the check sweep finds nothing: 2 sweeps.  Without the exit (fp64 rule,
+    stagnation = False) 1.5 eps_tol also takes 2 sweeps."""
+    tol = np.float32(2.0 ** -19)
+    assert tol == np.float32(4 * np.sqrt(64) * 2.0 ** -24)
+    for theta, stag, expect in ((1.5 * 2.0 ** -19, True, 1), (3 * 2.0 ** -19, True, 2), (1.5 * 2.0 ** -19, False, 2)):
+        x = _one_pair_matrix(theta)
+        xo, _, sw, offs, upd = oracle.block_jacobi(x, None, 32, tol, tol / 8, max_sweeps=20, max_inner=1,
+                                                   stagnation=stag, dtype=np.float32)
+        assert sw == expect, (theta, stag, sw, offs, upd)
+        assert upd[0] == 1
+        assert abs(offs[0] - theta / np.sqrt(1 + theta * theta)) <= 1e-6 * theta
+
+
+def test_fp32_stagnation_exit_rule():
+    """An unreachable tolerance (1e-20) in fp32: the stage stops by the stagnation exit (reading c-10) at the
+    first sweep k >= 3 whose max metric is <= 1e-4 and > 1/4 of the previous sweep's, reports convergence,
+    and no earlier sweep met that condition."""
+    a = testmat.config_matrix("C1", 96)
+    x = np.asfortranarray(np.linalg.qr(a.T)[1].T).astype(np.float32)
+    xo, _, sw, offs, upd = oracle.block_jacobi(x, None, 32, np.float32(1e-20), np.float32(1e-21), max_sweeps=20,
+                                               max_inner=1, stagnation=True, dtype=np.float32)
+    assert sw > 0
+    k = sw
+    assert k >= 3 and offs[k - 1] <= 1e-4 and offs[k - 1] > 0.25 * offs[k - 2]
+    for j in range(3, k):
+        assert not (offs[j - 1] <= 1e-4 and offs[j - 1] > 0.25 * offs[j - 2])
+    assert np.all(upd[:k] > 0)

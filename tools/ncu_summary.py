@@ -3,6 +3,9 @@
 
   python tools/ncu_summary.py launches <launches.csv>         # per-kernel share of a launch list
   python tools/ncu_summary.py report <file.ncu-rep> [...]     # key --set full metrics per kernel
+  python tools/ncu_summary.py traffic <CONFIG> <file.ncu-rep> [...]
+        # dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged per kernel, merged into
+        # profiles/ncu_traffic.json under CONFIG (the 'traffic' field of bench.py's roofline)
 """
 import collections
 import csv
@@ -100,9 +103,56 @@ def report(path):
             print(f"  {k:38s} {v} {u}")
 
 
+# bench.py kernel keys <- ncu kernel-name prefixes
+TRAFFIC_KEYS = [("qrp_coop", "k_qrp_lazy"), ("pair_gram_f32", "k_pair_gram_tma"), ("pair_gram_f32", "k_pair_gram_tc"),
+                ("pair_update_f32", "k_pair_update_tc"), ("pair_solve_f32", "k_pair_solve<float"),
+                ("pair_gram_f64", "k_pair_gram_dmma"), ("pair_update_f64", "k_pair_update_dmma"),
+                ("pair_solve_f64", "k_pair_solve<double")]
+
+
+def traffic(config, paths):
+    import json
+    import os
+    acc = collections.defaultdict(list)
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(io.StringIO(raw)))
+        if len(rr) < 3:
+            continue
+        h, units = rr[0], rr[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        for row in rr[2:]:
+            d = dict(zip(h, row))
+            name = d.get("Kernel Name", "").replace("void ", "").replace("mpj::", "")
+            try:
+                rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale.get(units[h.index("dram__bytes_read.sum")], 1)
+                wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale.get(units[h.index("dram__bytes_write.sum")], 1)
+            except (KeyError, ValueError):
+                continue
+            for key, pref in TRAFFIC_KEYS:
+                if name.startswith(pref):
+                    acc[key].append(rd + wr)
+                    break
+    out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+    try:
+        allv = json.load(open(out_path))
+    except Exception:
+        allv = {}
+    if "_source" in allv and not isinstance(allv.get("_source"), dict):
+        allv = {k: v for k, v in allv.items() if isinstance(v, dict)}     # round-1 flat layout: drop
+    entry = {k: sum(v) / len(v) for k, v in acc.items()}
+    entry["_source"] = ", ".join(paths) + " (ncu --set full; dram read + write bytes per launch, mean over captured launches)"
+    entry["_launches"] = {k: len(v) for k, v in acc.items()}
+    allv[config] = entry
+    json.dump(allv, open(out_path, "w"), indent=1)
+    print(json.dumps(entry, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3:])
     else:
         for p in sys.argv[2:]:
             report(p)
