@@ -43,6 +43,23 @@ def tiered(sref, kappa):
     return np.maximum(1e-12, 1e3 * U64 * np.minimum(kappa, sref[0] / sref))
 
 
+def record_ratio(got, sref, kappa):
+    """Achieved max |dsigma_i| / (sigma_i u min(kappa_s, sigma_1/sigma_i)) of a tiered comparison, appended to
+    $MPJSVD_RECORD_DIR/tiered_ratios.jsonl (how much of the 1e3 constant a test uses)."""
+    import json
+    import os
+    d = os.environ.get("MPJSVD_RECORD_DIR")
+    if not d:
+        return
+    got, sref = np.asarray(got, dtype=np.float64), np.asarray(sref, dtype=np.float64)
+    r = np.abs(got - sref) / sref / (U64 * np.minimum(kappa, sref[0] / sref))
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "tiered_ratios.jsonl"), "a") as f:
+        f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "n": int(sref.size),
+                            "kappa": float(kappa), "max_ratio": float(r.max()),
+                            "max_rel": float((np.abs(got - sref) / sref).max())}) + "\n")
+
+
 def kappa_s(a):
     d = np.linalg.norm(a, axis=0)
     s = np.linalg.svd(a / d, compute_uv=False)
@@ -226,6 +243,7 @@ def test_blocked_qr_panel_modes(mp, mode):
     U, S, V, st = mp.factor(dev(a), qr_panel_mode=mode)
     check_svd(a, host(U), host(S), host(V))
     uo, so, vo, sto, rc = oracle.mixed_svd(a)
+    record_ratio(host(S), so, kappa_s(a))
     assert np.all(np.abs(host(S) - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1 and abs(st["sweeps64"] - sto["sweeps64"]) <= 1
 
@@ -348,6 +366,7 @@ def test_factor_vs_oracle(mp, name, n, kappa, route):
     check_svd(a, U, S, V)
     k = kappa if kappa is not None else kappa_s(a)
     rel = np.abs(S - so) / so
+    record_ratio(S, so, k)
     if k <= 1e4:
         assert rel.max() <= 1e-12, rel.max()
     assert np.all(rel <= tiered(so, k))
@@ -367,6 +386,7 @@ def test_factor_ragged_shapes(mp, m, n):
     U, S, V = host(U), host(S), host(V)
     check_svd(a, U, S, V)
     so = oracle.mixed_svd(a)[1]
+    record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
 
 
@@ -478,6 +498,7 @@ def test_factor_mixed_precision_rrqr_vs_oracle(mp, name, n):
     uo, so, vo, sto, rc = oracle.mixed_svd(a, mp_rrqr=1)
     assert rc == 0 and st["rc"] == 0
     check_svd(a, U, S, V)
+    record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
@@ -537,6 +558,7 @@ def test_auto_path_vs_oracle(mp, case):
     assert st["path_taken"] == sto["path_taken"] == taken, (st["path_taken"], sto["path_taken"], taken)
     check_svd(a, U, S, V)
     kap = kappa_s(a)
+    record_ratio(S, so, kap)
     assert np.all(np.abs(S - so) / so <= tiered(so, kap))
     if sig is not None:
         assert np.max(np.abs(S - sig) / sig) <= 1e-13
@@ -576,6 +598,7 @@ def test_refine_v_vs_oracle(mp, name, n, extra):
     uo, so, vo, sto, rc = oracle.mixed_svd(a, refine_v=1, **oo)
     assert rc == 0 and st["rc"] == 0
     check_svd(a, U, S, V)
+    record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert 1 <= st["v_sweeps64"] <= 2 and 1 <= sto["v_sweeps64"] <= 2
     assert abs((st["sweeps64"] - st["v_sweeps64"]) - (sto["sweeps64"] - sto["v_sweeps64"])) <= 1
@@ -600,6 +623,7 @@ def test_option_paths_vs_oracle(mp, opts, oopts):
     uo, so, vo, sto, rc = oracle.mixed_svd(a, **oopts)
     assert rc == 0 and st["rc"] == 0
     check_svd(a, U, S, V)
+    record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
     if not opts.get("x_from_lq", 1) == 0:
@@ -647,5 +671,6 @@ def test_auto_qrsvd_branch_larger_vs_oracle(mp):
     assert rc == 0 and st["rc"] == 0
     assert st["path_taken"] == sto["path_taken"] == 6
     check_svd(a, U, S, V)
+    record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
