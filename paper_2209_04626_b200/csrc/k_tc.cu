@@ -404,6 +404,130 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tma(JacobiRound<float
     if (warp == 0) tc::tmem_free<64>(tmem);
 }
 
+// k_pair_gram_tma_ws: the TMA Gram with warp specialisation.  Lane 0 of warp 0 is the producer and the MMA
+// issuer (TMA of tile t + ST - 1 into the stage of tile t - 1 once that tile's MMAs completed; the MMAs of tile
+// t once its lo parts are written); warps 1..3 write the lo parts of each landed stage and arrive on the
+// stage's lo_ready barrier (96 arrivals) -- no CTA-wide barrier per tile, so the lo work of the next tile
+// overlaps the producer's waits.  Same operand layout, MMA sequence and epilogue as k_pair_gram_tma (bitwise
+// equal results).
+__device__ __forceinline__ void mbar_init_n(uint64_t* mbar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tc::smem_u32(mbar)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(mbar)) : "memory");
+}
+
+template <int GM_KT, int GM_ST, int MINB>
+__global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tma_ws(JacobiRound<float> a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int STAGE = 128 * GM_KT * 4;
+    constexpr uint32_t SBO = (GM_KT / 4) * 128;
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    constexpr int RAW4 = 64 * GM_KT / 4;                // float4 chunks of the raw half of a stage
+    reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
+    extern __shared__ __align__(1024) unsigned char gw_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gw_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[GM_ST], lor[GM_ST], done[GM_ST], fin;
+    __shared__ uint32_t tmem_base;
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
+    const bool hasJ = pd.w1 > 0;
+    const uint32_t tx = hasJ ? 2u * 32u * GM_KT * 4u : 32u * GM_KT * 4u;
+    if (warp == 0) tc::tmem_alloc<64>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < GM_ST; ++s) {
+            tc::mbar_init(&full[s]);
+            mbar_init_n(&lor[s], GT_NT - 32);
+            tc::mbar_init(&done[s]);
+        }
+        tc::mbar_init(&fin);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (!hasJ) {
+        for (int s = 0; s < GM_ST; ++s)
+            for (int i = tid; i < 4 * (int)SBO / 16; i += GT_NT)
+                reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4 * SBO)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tc::fence_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg + GM_KT - 1) / GM_KT);
+    const uint32_t sbase = tc::smem_u32(sm);
+    if (warp == 0) {
+        if (tid == 0) {
+            auto issue = [&](int t) {
+                const int s = t % GM_ST;
+                const int kq = (int)((rbeg + (long long)t * GM_KT) >> 2);
+                mbar_expect_tx(&full[s], tx);
+                tma_load_4d(sbase + (uint32_t)(s * STAGE), &tmap, 0, 0, kq, cI >> 3, &full[s]);
+                if (hasJ) tma_load_4d(sbase + (uint32_t)(s * STAGE) + 4 * SBO, &tmap, 0, 0, kq, cJ >> 3, &full[s]);
+            };
+            for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
+            for (int t = 0; t < ntile; ++t) {
+                const int s = t % GM_ST;
+                tc::mbar_wait(&lor[s], (uint32_t)((t / GM_ST) & 1));
+                tc::fence_after();
+                const uint32_t base = sbase + (uint32_t)(s * STAGE);
+#pragma unroll
+                for (int ks = 0; ks < GM_KT / 8; ++ks) {
+                    const uint64_t ad = tc::sdesc(base + ks * 256, 128, SBO);
+                    tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);
+                }
+                tc::commit(&done[s]);
+                if (t >= 1 && t - 1 + GM_ST < ntile) {
+                    const int sp = (t - 1) % GM_ST;
+                    tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
+                    issue(t - 1 + GM_ST);
+                }
+            }
+            if (ntile > 0) tc::commit(&fin);
+        }
+        __syncwarp();
+    } else {
+        const int lt = tid - 32;
+        for (int t = 0; t < ntile; ++t) {
+            const int s = t % GM_ST;
+            unsigned char* st = sm + (size_t)s * STAGE;
+            tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
+            for (int f = lt; f < RAW4; f += GT_NT - 32) {
+                const float4 x = reinterpret_cast<const float4*>(st)[f];
+                reinterpret_cast<float4*>(st + 8 * SBO)[f] = tc::lo4(x, tc::hi4(x));
+            }
+            tc::fence_async_smem();
+            mbar_arrive(&lor[s]);
+        }
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);
+    if (ntile > 0) {
+        tc::mbar_wait(&fin, 0);
+        tc::fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += GT_NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
+        }
+    } else {
+        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
 // rows per stage of the TMA Gram (MPJSVD_GRAM_KT = 32 or 64): KT = 64 -> 3 x 32 KB stages, 2 CTAs per SM;
 // KT = 32 -> 3 x 16 KB stages, 4 CTAs per SM
 // Default by row count (measured on B200): 32 for >= 6144 rows (C5: Gram 237 -> 217 ms), 64 below (C3: 33 vs 35 ms)
@@ -894,6 +1018,22 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
     if (a.tmap) {
         MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<64, 3, 2>, gram_tma_smem<64, 3>()));
         MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<32, 3, 4>, gram_tma_smem<32, 3>()));
+        if (a.gram_variant == 8 || a.gram_variant == 9) {
+            // experiment: warp-specialised TMA Gram (8: 3 stages, 9: 4 stages at KT = 32 / 3 at KT = 64)
+            const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(a.tmap);
+            if (a.gram_kt == 32 && a.gram_variant == 9) {
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_tma_ws<32, 4, 3>, gram_tma_smem<32, 4>()));
+                k_pair_gram_tma_ws<32, 4, 3><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 4>(), st>>>(a, tm);
+            } else if (a.gram_kt == 32) {
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_tma_ws<32, 3, 4>, gram_tma_smem<32, 3>()));
+                k_pair_gram_tma_ws<32, 3, 4><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 3>(), st>>>(a, tm);
+            } else {
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_tma_ws<64, 3, 2>, gram_tma_smem<64, 3>()));
+                k_pair_gram_tma_ws<64, 3, 2><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<64, 3>(), st>>>(a, tm);
+            }
+            MPJ_LAUNCHED();
+            return 0;
+        }
         if (a.gram_kt == 32)
             k_pair_gram_tma<32, 3, 4><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 3>(), st>>>(
                 a, *reinterpret_cast<const CUtensorMap*>(a.tmap));
@@ -937,7 +1077,11 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 }
 
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
-    if (tma) return gram_tma_kt(rows_pad, kt) == 32 ? 4 : 2;
+    if (tma) {
+        const int k = gram_tma_kt(rows_pad, kt);
+        if (variant == 9 && k == 32) return 3;
+        return k == 32 ? 4 : 2;
+    }
     // shared memory bound: (stages + alignment + static) per CTA of 228 KB per SM
     const GramVariant& gv = gram_variant(variant);
     const int per = (int)((228 * 1024) / (gv.smem + 2048));

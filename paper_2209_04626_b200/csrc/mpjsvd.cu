@@ -1268,7 +1268,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
-    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_variant < 0 || o.gram_variant > 5 ||
+    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_variant < 0 || o.gram_variant > 9 ||
         o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();

@@ -674,3 +674,16 @@ def test_auto_qrsvd_branch_larger_vs_oracle(mp):
     record_ratio(S, so, kappa_s(a))
     assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
+
+
+@pytest.mark.parametrize("variant,kt", [(8, 0), (9, 0), (8, 32), (9, 32)])
+def test_gram_tma_warp_specialised_bitwise(mp, variant, kt):
+    """The warp-specialised TMA Gram (gram_variant 8 / 9: producer + MMA lane, lo-part warps, per-stage
+    mbarriers instead of a CTA barrier per tile) issues the same MMAs on the same operands as k_pair_gram_tma:
+    the whole SVD is bitwise equal when the row slabs are the same (split_rows fixed)."""
+    a = testmat.config_matrix("C3", 512)
+    r0 = mp.factor(dev(a), split_rows=128, gram_kt=kt)
+    r1 = mp.factor(dev(a), split_rows=128, gram_kt=kt, gram_variant=variant)
+    for x, y in zip(r0[:3], r1[:3]):
+        assert torch.equal(x, y)
+    assert r0[3]["sweeps32"] == r1[3]["sweeps32"] and r0[3]["sweeps64"] == r1[3]["sweeps64"]
