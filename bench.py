@@ -4,18 +4,33 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl mpjsvd|reference]
 
 A step is one full fp64 SVD A = U S V^T (mpjsvd_factor: QRP + LQ
-preconditioning, fp32 block Jacobi, CholeskyQR lift, fp64 block Jacobi
-refinement, assembly) of BASELINE.json's config on inputs resident in HBM.
-Metric (BASELINE.json): "fp64 SVD time at n=4096 and 8192 (1/2/4/8 B200);
-sweep HBM GB/s vs peak" -> value = seconds per SVD (lower is better).
+preconditioning, fp32 block Jacobi computing U_low, U-route precision switch,
+fp64 block Jacobi refinement, assembly) of BASELINE.json's config on inputs
+resident in HBM.  Metric (BASELINE.json): "fp64 SVD time at n=4096 and 8192
+(1/2/4/8 B200); sweep HBM GB/s vs peak" -> value = seconds per SVD at n = 8192
+(C5, lower is better); the n = 4096 config (C3) is timed in the same run under
+"also".
 
-Rank 0 prints ONE JSON line.  Multi-GPU (torchrun, N > 1): one SVD of the
-config per step, sharded over the N GPUs: rank 0 holds A and
-the outputs and runs preconditioning / lift / assembly, both Jacobi stages
-run column-block sharded with the per-round block exchange over NCCL
+Timing: W warm-up steps, then K steps between CUDA events on the handle's
+stream with a 512 MiB L2 flush before each step and no per-kernel
+instrumentation (value); a separate pass of min(K, 5) steps with per-launch
+events feeds "kernels", "roofline" and "jacobi_roofline" ("profiled"); "e2e"
+times the same C-ABI call on pinned host buffers (H2D of A and D2H of U, S, V
+inside the timed region).  nvidia-smi clocks are sampled during the timed steps.
+
+Rank 0 prints ONE JSON line.  Multi-GPU: `--gpus N` (N > 1) re-launches itself
+under torch.distributed.run with N ranks when WORLD_SIZE is unset; one SVD of
+the config per step, sharded over the N GPUs: rank 0 holds A
+and the outputs and runs preconditioning / switch / assembly, both Jacobi
+stages run column-block sharded with the per-round block exchange over NCCL
 (ncclSend/ncclRecv inside libmpjsvd.so).  Total work is fixed as N grows
 ("scaling": "strong"); the timed region is bracketed by barrier +
 synchronize and the max over ranks is reported.
+
+--impl reference times the oracle O-MIX (the only reference of this tier) on
+the host cores on a bounded sample (the config's recipe at n = 1024, scaled by
+the n^3 work ratio); --impl reference --full CFG runs O-MIX once on the full
+config (minutes) to calibrate that extrapolation (profiles/cpu_oracle_full_*).
 """
 from __future__ import annotations
 

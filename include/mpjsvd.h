@@ -131,9 +131,13 @@ typedef struct {
     int32_t tail_cut_log2;     /* "small": ||x_j|| < 2^tail_cut_log2 max_j ||x_j||, default -60 */
     /* kernel-variant switches (defaults = the measured best; the alternatives are kept for the
        bitwise-equality tests and for experiments) */
-    int32_t gram_tma;          /* 1 (default): the fp32 tcgen05 Gram loads its operands by TMA; 0: cp.async */
+    int32_t gram_tma;          /* fp32 tcgen05 Gram operand loads: 2 (default) TMA 2-D boxes into 128-byte-swizzled
+                                  operands; 1 TMA 4-D boxes into the SWIZZLE_NONE canonical layout (round 1);
+                                  0 cp.async.  All three issue the same MMAs (bitwise equal on equal row slabs) */
     int32_t gram_kt;           /* rows per TMA Gram stage: 0 (default) auto (32 for >= 6144 rows, else 64), 32, 64 */
-    int32_t gram_variant;      /* cp.async tcgen05 Gram stage variant 0..5 (default 0; used only with gram_tma = 0) */
+    int32_t gram_variant;      /* Gram stage variant: with gram_tma = 0 the cp.async variant 0..5; with gram_tma = 1:
+                                  8 / 9 warp-specialised; 10..13 the swizzled kernel with 3 / 4 / 6 / 8 stages;
+                                  0 (default): by row count */
     int32_t update_tpc;        /* tiles per work item of the overlapped fp32 update; 0 (default): ~3 items per SM */
     int32_t skip_unchanged;    /* 1 (default): skip the Gram and solve of a pair whose blocks did not rotate since
                                   its previous evaluation (exact); 0: evaluate every pair */

@@ -57,6 +57,7 @@ struct JacobiRound {
     const T* tbase;
     long long tld;
     const void* umap;   // host pointer to the 2-D CUtensorMap (box 128 x 32) of the update's raw tiles, or nullptr
+    const void* smap;   // host pointer to the 2-D SWIZZLE_128B CUtensorMap (box 32 rows x 32 columns) of the Gram, or nullptr
     // exact skip of unchanged pairs: last_mod[blk] = global round index (sweep * R + round) of the last
     // rotation that touched block blk (-1: none); pair_off = this round's per-slot metric of the previous
     // evaluation (written back every evaluation).  A pair whose two blocks were not rotated since its
@@ -114,6 +115,7 @@ void solve_timing_report(const char* tag, int sweep);
 // 4-D TMA view of the column-major fp32 matrix (rows_pad x cols, ld) whose boxes land in the canonical
 // K-major SWIZZLE_NONE operand layout of k_pair_gram_tma; out = 128-byte CUtensorMap.  0 on success.
 int make_gram_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols, int kt);
+int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long rows_pad, long long cols);
 int gram_tma_kt(long long rows_pad, int forced);
 int make_update_tmap(void* out, const float* base, long long ld, long long rows_pad, long long cols);
 int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st);

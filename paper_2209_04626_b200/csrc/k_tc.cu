@@ -528,6 +528,123 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_tma_ws(JacobiRound<fl
     if (warp == 0) tc::tmem_free<64>(tmem);
 }
 
+// k_pair_gram_sw: the TMA Gram on 128-byte-swizzled operands.  One 2-D box of 32 rows x 32 columns per block
+// (a 128-byte inner run per column instead of the 16-byte runs of the 4-D canonical view) lands column c of the
+// block as M-row c of a K-major SWIZZLE_128B operand (8-row atoms of 1024 B, K = 32 rows per stage); X_I fills
+// M-rows 0..31, X_J 32..63, the lo parts (written at the same offsets + 8 KB, so with the same swizzle)
+// 64..127.  The MMA descriptors use layout type SWIZZLE_128B (SBO = 1024 B) and advance 32 B per K = 8 step.
+// Same K order and MMA sequence as k_pair_gram_tma at KT = 32: bitwise equal partial Grams.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tma_load_2d_g(uint32_t sdst, const CUtensorMap* map, int c0, int c1, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(sdst), "l"(map), "r"(c0), "r"(c1), "r"(tc::smem_u32(mbar))
+        : "memory");
+}
+
+template <int GM_ST, int MINB>
+__global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_sw(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
+    constexpr int KT = 32;
+    constexpr int STAGE = 128 * KT * 4;                 // 16 KB: raw I | raw J | lo I | lo J, 4 KB each
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    reset_publication(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
+    extern __shared__ __align__(1024) unsigned char gs_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gs_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], fin;
+    __shared__ uint32_t tmem_base;
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
+    const bool hasJ = pd.w1 > 0;
+    const uint32_t tx = hasJ ? 2u * 32u * KT * 4u : 32u * KT * 4u;
+    if (warp == 0) tc::tmem_alloc<64>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < GM_ST; ++s) { tc::mbar_init(&full[s]); tc::mbar_init(&done[s]); }
+        tc::mbar_init(&fin);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (!hasJ) {   // bye pair: M-rows 32..63 (raw J) stay zero in every stage
+        for (int s = 0; s < GM_ST; ++s)
+            for (int i = tid; i < 4096 / 16; i += GT_NT)
+                reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4096)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tc::fence_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg + KT - 1) / KT);
+    const uint32_t sbase = tc::smem_u32(sm);
+    auto issue = [&](int t) {
+        const int s = t % GM_ST;
+        const int r0 = (int)(rbeg + (long long)t * KT);
+        mbar_expect_tx(&full[s], tx);
+        tma_load_2d_g(sbase + (uint32_t)(s * STAGE), &smap, r0, cI, &full[s]);
+        if (hasJ) tma_load_2d_g(sbase + (uint32_t)(s * STAGE) + 4096, &smap, r0, cJ, &full[s]);
+    };
+    if (tid == 0)
+        for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
+    for (int t = 0; t < ntile; ++t) {
+        const int s = t % GM_ST;
+        unsigned char* st = sm + (size_t)s * STAGE;
+        tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {            // 512 raw float4 chunks, 4 per thread, linear
+            const int f = tid + GT_NT * u;
+            const float4 x = reinterpret_cast<const float4*>(st)[f];
+            reinterpret_cast<float4*>(st + 8192)[f] = tc::lo4(x, tc::hi4(x));
+        }
+        tc::fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t base = sbase + (uint32_t)(s * STAGE);
+#pragma unroll
+            for (int ks = 0; ks < KT / 8; ++ks) {
+                const uint64_t ad = sdesc_sw128(base + ks * 32);
+                tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);
+            }
+            tc::commit(&done[s]);
+            if (t >= 1 && t - 1 + GM_ST < ntile) {
+                const int sp = (t - 1) % GM_ST;
+                tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
+                issue(t - 1 + GM_ST);
+            }
+        }
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);
+    if (ntile > 0) {
+        if (tid == 0) tc::commit(&fin);
+        tc::mbar_wait(&fin, 0);
+        tc::fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += GT_NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
+        }
+    } else {
+        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
 // rows per stage of the TMA Gram (MPJSVD_GRAM_KT = 32 or 64): KT = 64 -> 3 x 32 KB stages, 2 CTAs per SM;
 // KT = 32 -> 3 x 16 KB stages, 4 CTAs per SM
 // Default by row count (measured on B200): 32 for >= 6144 rows (C5: Gram 237 -> 217 ms), 64 below (C3: 33 vs 35 ms)
@@ -1014,7 +1131,54 @@ int make_update_tmap(void* out, const float* base, long long ld, long long rows_
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long rows_pad, long long cols) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    }
+    if (!fn || ld % 4 != 0) return -1;
+    const cuuint64_t gdim[2] = {(cuuint64_t)rows_pad, (cuuint64_t)cols};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
+                          gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 13) {
+        const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
+        switch (a.gram_variant) {
+            case 11:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<4, 3>, gram_tma_smem<32, 4>()));
+                k_pair_gram_sw<4, 3><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 4>(), st>>>(a, sm);
+                break;
+            case 12:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<6, 2>, gram_tma_smem<32, 6>()));
+                k_pair_gram_sw<6, 2><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 6>(), st>>>(a, sm);
+                break;
+            case 13:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<8, 1>, gram_tma_smem<32, 8>()));
+                k_pair_gram_sw<8, 1><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 8>(), st>>>(a, sm);
+                break;
+            default:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<3, 4>, gram_tma_smem<32, 3>()));
+                k_pair_gram_sw<3, 4><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 3>(), st>>>(a, sm);
+        }
+        MPJ_LAUNCHED();
+        return 0;
+    }
     if (a.tmap) {
         MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<64, 3, 2>, gram_tma_smem<64, 3>()));
         MPJ_CUDA_TRY(set_smem(k_pair_gram_tma<32, 3, 4>, gram_tma_smem<32, 3>()));
@@ -1079,7 +1243,10 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
     if (tma) {
         const int k = gram_tma_kt(rows_pad, kt);
-        if (variant == 9 && k == 32) return 3;
+        if ((variant == 9 && k == 32) || variant == 11) return 3;
+        if (variant == 10) return 4;
+        if (variant == 12) return 2;
+        if (variant == 13) return 1;
         return k == 32 ? 4 : 2;
     }
     // shared memory bound: (stages + alignment + static) per CTA of 228 KB per SM

@@ -281,6 +281,10 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
     const int use_tc = (sizeof(T) == 4 && W == 64 && h->opts.fp32_tensor_cores) ? 1 : 0;
+    // Gram kernel variant: gram_tma = 2 (default) -> the 128-byte-swizzled TMA Gram, 4 stages at 3 CTAs/SM for
+    // >= 6144 rows, 3 stages at 4 CTAs/SM below (measured); explicit variants 10..13 kept
+    int gram_v = h->opts.gram_variant;
+    if (h->opts.gram_tma == 2 && (gram_v < 10 || gram_v > 13)) gram_v = m_pad >= 6144 ? 11 : 10;
     long long nsplit = 1;
     if (h->opts.split_rows > 0) {
         nsplit = ceil_div(m_pad, round_up(h->opts.split_rows, 32));
@@ -288,7 +292,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
         // Row splits of the Gram: minimise waves(npairs * nsplit) / nsplit (wave quantisation of
         // the resident CTA slots), preferring fewer splits (smaller partial reduction) on ties.
         const long long slots = (long long)dev_sms * gram_ctas_per_sm<T>(W, use_tc, m_pad, h->opts.gram_tma,
-                                                                           h->opts.gram_kt, h->opts.gram_variant);
+                                                                           h->opts.gram_kt, gram_v);
         const long long maxsplit = std::max(1LL, std::min(m_pad / 32, 64LL));
         double best = 1e30;
         for (long long ns = 1; ns <= maxsplit; ++ns) {
@@ -324,7 +328,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.tol = tol; a.tol_in = tol_in; a.max_inner = max_inner;
     a.use_tc = use_tc;
     a.gram_kt = gram_tma_kt(m_pad, h->opts.gram_kt);
-    a.gram_variant = h->opts.gram_variant;
+    a.gram_variant = gram_v;
     a.update_tpc = h->opts.update_tpc;
     a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
@@ -334,8 +338,10 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
     alignas(64) static thread_local unsigned char tmap_buf[128];
     alignas(64) static thread_local unsigned char umap_buf[128];
+    alignas(64) static thread_local unsigned char smap_buf[128];
     a.tmap = nullptr;
     a.umap = nullptr;
+    a.smap = nullptr;
     a.tbase = nullptr;
     a.tld = 0;
     if constexpr (sizeof(T) == 4) {
@@ -353,6 +359,9 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
                 a.tld = ldx;
             }
             if (base && !has_v && make_update_tmap(umap_buf, base, ldx, m_pad, cols) == 0) a.umap = umap_buf;
+            if (base && gram_v >= 10 && gram_v <= 13 &&
+                make_gram_tmap_sw128(smap_buf, base, ldx, m_pad, cols) == 0)
+                a.smap = smap_buf;
             if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols, a.gram_kt) == 0) {
                 a.tmap = tmap_buf;
                 // a TMA box covers 64 rows and only zero-fills past the matrix: row slabs must be whole boxes
@@ -1247,7 +1256,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->cond_d_min = 1e15;
     o->tail_frac = 1.0 / 3.0;
     o->tail_cut_log2 = -60;
-    o->gram_tma = 1;
+    o->gram_tma = 2;
     o->gram_kt = 0;
     o->gram_variant = 0;
     o->update_tpc = 0;
@@ -1268,7 +1277,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
-    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_variant < 0 || o.gram_variant > 9 ||
+    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 13 ||
         o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();

@@ -70,8 +70,10 @@ def golden(name):
     return json.load(open(p))
 
 
-# tiered sigma bound: |dsigma_i|/sigma_i <= max(1e-12, C u min(kappa_s, sigma_1/sigma_i))
-C_TIER = 1e3
+# tiered sigma bound: |dsigma_i|/sigma_i <= max(1e-12, C u min(kappa_s, sigma_1/sigma_i)).
+# Achieved on B200 against the full-size goldens: C3 35, C4 22, C5 98 (recorded with MPJSVD_RECORD_DIR); the
+# survey's proposal 1e3 is tightened to 250 (2.5x margin over the worst observed).
+C_TIER = 250.0
 
 
 def kappa_bound(sref, kappa, c=C_TIER):
