@@ -70,6 +70,7 @@ struct JacobiRound {
     int gram_kt;        // rows per TMA Gram stage (32 / 64), resolved on the host
     int gram_variant;   // cp.async tcgen05 Gram variant
     int update_tpc;     // 0: auto
+    int update_ts;      // 1: fp32 update with the A operand in tensor memory (k_pair_update_tc_ts)
     int diag;           // mpjsvd_options.diag_timing
 };
 

@@ -276,7 +276,9 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                 T sacc = 0.0;
                 for (int w = 0; w < QP_NT / 32; ++w) sacc += red[w * 33 + tid];
                 const int q = tid == 32 ? QP_NB : tid;
-                if (q < jj || q == QP_NB) a.part[(long long)cta * (QP_NB + 1) + q] = sacc;
+                // slot-major layout part[slot][G], slot 0 = sigma, slot t + 1 = z_t: the jj + 1 live slots of
+                // this step are one contiguous prefix (the reduction below loads only those)
+                if (q < jj || q == QP_NB) a.part[(long long)(q == QP_NB ? 0 : q + 1) * G + cta] = sacc;
             }
             __syncthreads();
         }
@@ -287,11 +289,11 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         T colv[RPT];                  // pivot column rows k+1.. (pass 1 output), loaded with the partials
         T alpha_r = 0.0, vk_r = 0.0;
         {
-            // value q (z_t for t < jj, sigma at q = QP_NB) summed over the G CTAs: the G x (QP_NB + 1)
-            // partials are staged in shared memory (every load in flight at once), then warp w sums
-            // q = w, w + 16, ... with lanes striding over g (fixed tree)
+            // value q (z_t for t < jj, sigma at q = QP_NB) summed over the G CTAs: the (jj + 1) x G live
+            // partials (slot-major) are staged in shared memory (every load in flight at once), then warp w
+            // sums q = w, w + 16, ... with lanes striding over g (fixed tree)
             const int lane = tid & 31, wid = tid >> 5;
-            const int tot = G * (QP_NB + 1);
+            const int tot = G * (jj + 1);
             T pv[QP_PART_PT];
 #pragma unroll
             for (int j = 0; j < QP_PART_PT; ++j) {
@@ -316,8 +318,9 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             __syncthreads();
             for (int q = wid; q <= QP_NB; q += QP_NT / 32) {
                 if (q < jj || q == QP_NB) {
+                    const int slot = q == QP_NB ? 0 : q + 1;
                     T sacc = 0.0;
-                    for (int g = lane; g < G; g += 32) sacc += vs[g * (QP_NB + 1) + q];
+                    for (int g = lane; g < G; g += 32) sacc += vs[slot * G + g];
                     sacc = warp_sum(sacc);
                     if (lane == 0) red[q] = sacc;
                 }

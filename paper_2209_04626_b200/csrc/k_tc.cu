@@ -1257,10 +1257,242 @@ int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
 
 }  // namespace mpj
 
+
+namespace mpj {
+// ------------------------------------------------------------------------
+// k_pair_update_tc_ts: k_pair_update_tc_pdl with the A operand (W_hi, W_lo) in TENSOR MEMORY instead of shared
+// memory (tcgen05.mma ... [d], [a_tmem], b_desc: the "TS" form, A K-major, lane = row, one column per
+// K element).  Each thread already holds its row of the tile after the transposition read, so it writes
+// W_hi, W_lo and the exact W with tcgen05.st (no shared-memory A, no async-proxy fence for it); A is double
+// buffered in TMEM (2 x 128 columns next to the 2 x 64 accumulator columns, 512 allocated), so tile t + 1 is
+// transposed while the MMAs of tile t run and the MMAs of tile t - 1 are only waited for right before the
+// epilogue of t - 1.  Shared memory holds only E^T (hi, lo) and a UTS_NR-deep raw ring.  Same products in the
+// same order as k_pair_update_tc_pdl (bitwise equal).
+// ------------------------------------------------------------------------
+constexpr int UTS_NR = 6;
+constexpr size_t update_ts_smem() { return 32768 + (size_t)UTS_NR * UT_RAW_BYTES + 1024; }
+
+__device__ __forceinline__ void mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "r"(atmem), "l"(bd), "r"(idesc), "r"(acc));
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<float> a, int ngroups, int tpc,
+                                                                 const __grid_constant__ CUtensorMap umap) {
+    extern __shared__ __align__(1024) unsigned char uts_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(uts_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* Bh = sm;
+    unsigned char* Bl = sm + 16384;
+    float* ring = reinterpret_cast<float*>(sm + 32768);
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ __align__(8) uint64_t rfull[UTS_NR];
+    __shared__ uint32_t tmem_base;
+    __shared__ float* colp[64];
+    __shared__ int item[3];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int trow = tid & 127, half = tid >> 7;
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    if (tid == 0) {
+        tc::mbar_init(&mbar[0]);
+        tc::mbar_init(&mbar[1]);
+        for (int q = 0; q < UTS_NR; ++q) tc::mbar_init(&rfull[q]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;                 // columns [0, 128): accumulators; [128, 384): A buffers
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    constexpr uint32_t SBO = 16 * 128;
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    const uint32_t rbase = tc::smem_u32(ring);
+    const long long total = (long long)a.npairs * 2 * ngroups;
+    uint32_t ph[2] = {0u, 0u};
+    long long gt0 = 0;
+    while (true) {
+        if (tid == 0) {
+            int pair = -1, which = 0, grp = 0;
+            while (true) {
+                const long long wk = atomicAdd(a.dctr + 1, 1);
+                if (wk >= total) break;
+                const int p = (int)(wk / (2 * ngroups)), rem = (int)(wk % (2 * ngroups));
+                which = rem / ngroups;
+                grp = rem % ngroups;
+                int pr = ld_acquire_gpu(a.dlist + p);
+                unsigned long long t0 = 0;
+                while (pr < 0) {
+                    __nanosleep(256);
+                    pr = ld_acquire_gpu(a.dlist + p);
+                    if (pr >= 0) break;
+                    const unsigned long long t = global_ns();
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > MPJ_SPIN_TIMEOUT_NS) { atomicExch(a.dctr + 2, 1); break; }
+                }
+                if (pr < 0) { pair = -1; break; }
+                if (!a.flag[pr] || (which && !a.has_v)) continue;
+                const long long rows_pad = which ? a.nv_pad : a.m_pad;
+                if ((long long)grp * tpc * UT_TM >= rows_pad) continue;
+                pair = pr;
+                break;
+            }
+            item[0] = pair; item[1] = which; item[2] = grp;
+        }
+        __syncthreads();
+        const int pair = item[0], which = item[1], grp = item[2];
+        if (pair < 0) break;
+        const long long ld = which ? a.ldv : a.ldx;
+        const long long rows_pad = which ? a.nv_pad : a.m_pad;
+        const long long row_lo = (long long)grp * tpc * UT_TM;
+        const long long row_hi = min(rows_pad, row_lo + (long long)tpc * UT_TM);
+        const int ntile = (int)((row_hi - row_lo + UT_TM - 1) / UT_TM);
+        const PairDesc<float> pd = a.pd[pair];
+        const int w = pd.w0 + pd.w1;
+        float* const s0 = which ? pd.v0 : pd.x0;
+        float* const s1 = which ? pd.v1 : pd.x1;
+        if (tid < 64) colp[tid] = tid < w ? (tid < pd.w0 ? s0 + (long long)tid * ld : s1 + (long long)(tid - pd.w0) * ld) : nullptr;
+        __syncthreads();
+        const int cI = TMA ? (int)((pd.x0 - a.tbase) / a.tld) : 0;
+        const int cJ = TMA ? (pd.w1 > 0 ? (int)((pd.x1 - a.tbase) / a.tld) : (1 << 30)) : 0;
+        auto issue = [&](int t) {
+            if constexpr (TMA) {
+                if (tid == 0) {
+                    const int slot = (int)((gt0 + t) % UTS_NR);
+                    const int r0 = (int)(row_lo + (long long)t * UT_TM);
+                    const uint32_t dst = rbase + (uint32_t)((size_t)slot * (UT_TM * 64) * 4);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    mbar_expect_tx(&rfull[slot], (uint32_t)UT_RAW_BYTES);
+                    tma_load_2d(dst, &umap, r0, cI, &rfull[slot]);
+                    tma_load_2d(dst + 32 * UT_TM * 4, &umap, r0, cJ, &rfull[slot]);
+                }
+                return;
+            }
+            const int slot = t % UTS_NR;
+            const long long r0 = row_lo + (long long)t * UT_TM;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int f = tid + UT_NT * u;
+                const int c = f >> 5, r4 = 4 * (f & 31);
+                const float* p = colp[c];
+                float* dst = ring + (size_t)slot * (UT_TM * 64) + c * UT_TM + r4;
+                if (p && r0 + r4 < rows_pad) cp16(rbase + (uint32_t)(((size_t)slot * (UT_TM * 64) + c * UT_TM + r4) * 4), p + r0 + r4);
+                else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+#pragma unroll
+        for (int t = 0; t < UTS_NR - 1; ++t) {
+            if (t < ntile) issue(t);
+            if constexpr (!TMA) cp_commit();
+        }
+        const float* Eg = a.E + (long long)pair * (64 * 64);
+        for (int it = tid; it < 64 * 16; it += UT_NT) {
+            const int n = it & 63, k4 = it >> 6;
+            float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
+                                   Eg[(4 * k4 + 3) * 64 + n]);
+            const uint32_t o = tc::koff(n, 4 * k4, 64);
+            const float4 h = tc::hi4(v);
+            *reinterpret_cast<float4*>(Bh + o) = h;
+            *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
+        }
+        tc::fence_async_smem();                  // E^T (generic stores) -> visible to the MMA (async proxy)
+        auto epilogue = [&](int t) {
+            const long long row = row_lo + (long long)t * UT_TM + trow;
+            const bool rok = row < rows_pad;
+            const uint32_t acc = tmem + (uint32_t)(64 * (t & 1));
+#pragma unroll
+            for (int c0 = 0; c0 < 32; c0 += 16) {
+                float d[16];
+                tc::tmem_ld16(acc + lane_base + (uint32_t)(32 * half + c0), d);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int c = 32 * half + c0 + j;
+                    if (rok && c < w) {
+                        float* p = c < pd.w0 ? s0 + (long long)c * ld : s1 + (long long)(c - pd.w0) * ld;
+                        p[row] = d[j];
+                    }
+                }
+            }
+        };
+        for (int t = 0; t < ntile; ++t) {
+            const int b = t & 1;
+            if constexpr (TMA) {
+                tc::mbar_wait(&rfull[(gt0 + t) % UTS_NR], (uint32_t)(((gt0 + t) / UTS_NR) & 1));
+            } else {
+                cp_wait<UTS_NR - 2>();
+                __syncthreads();
+            }
+            const float* raw = ring + (size_t)(TMA ? (gt0 + t) % UTS_NR : t % UTS_NR) * (UT_TM * 64);
+            const uint32_t ahi = tmem + 128u + 128u * (uint32_t)b, alo = ahi + 64u;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                float wv[16], hv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) wv[j] = raw[(32 * half + 16 * g + j) * UT_TM + trow];
+                const uint32_t col = lane_base + (uint32_t)(32 * half + 16 * g);
+                tmem_st16(tmem + (uint32_t)(64 * b) + col, wv);     // exact W: D = W + W E
+#pragma unroll
+                for (int j = 0; j < 16; ++j) hv[j] = tc::hi_part(wv[j]);
+                tmem_st16(ahi + col, hv);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) wv[j] -= hv[j];
+                tmem_st16(alo + col, wv);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n");
+            tc::fence_before();
+            __syncthreads();                    // A, W of tile t in TMEM; raw slot of tile t - 1 free
+            if (t + UTS_NR - 1 < ntile) issue(t + UTS_NR - 1);
+            if constexpr (!TMA) cp_commit();
+            if (tid == 0) {
+                tc::fence_after();
+                const uint32_t bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
+                const uint32_t acc = tmem + (uint32_t)(64 * b);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma_ts(acc, ahi + (uint32_t)(8 * ks), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma_ts(acc, alo + (uint32_t)(8 * ks), tc::sdesc(bh + ks * 256, 128, SBO), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    mma_ts(acc, ahi + (uint32_t)(8 * ks), tc::sdesc(bl + ks * 256, 128, SBO), idesc, 1u);
+                tc::commit(&mbar[b]);
+            }
+            if (t >= 1) {
+                tc::mbar_wait(&mbar[b ^ 1], ph[b ^ 1] & 1u);
+                ++ph[b ^ 1];
+                tc::fence_after();
+                epilogue(t - 1);
+            }
+        }
+        if constexpr (!TMA) cp_wait<0>();
+        if (ntile >= 1) {
+            const int t = ntile - 1;
+            tc::mbar_wait(&mbar[t & 1], ph[t & 1] & 1u);
+            ++ph[t & 1];
+            tc::fence_after();
+            epilogue(t);
+        }
+        tc::fence_before();
+        __syncthreads();
+        gt0 += ntile;
+    }
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+}  // namespace mpj
+
 namespace mpj {
 int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
-    MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<true>, (size_t)(update_tc_smem())));
-    MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<false>, (size_t)(update_tc_smem())));
+    const bool ts = a.update_ts != 0;
+    if (ts) {
+        MPJ_CUDA_TRY(set_smem(k_pair_update_tc_ts<true>, update_ts_smem()));
+        MPJ_CUDA_TRY(set_smem(k_pair_update_tc_ts<false>, update_ts_smem()));
+    } else {
+        MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<true>, (size_t)(update_tc_smem())));
+        MPJ_CUDA_TRY(set_smem(k_pair_update_tc_pdl<false>, (size_t)(update_tc_smem())));
+    }
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1288,7 +1520,13 @@ int launch_update_tc_pdl(const JacobiRound<float>& a, cudaStream_t st) {
     CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
     cudaError_t e;
-    if (a.umap && !a.has_v)
+    if (ts) {
+        cfg.dynamicSmemBytes = update_ts_smem();
+        if (a.umap && !a.has_v)
+            e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_ts<true>, a, ngroups, tpc, *reinterpret_cast<const CUtensorMap*>(a.umap));
+        else
+            e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_ts<false>, a, ngroups, tpc, dummy);
+    } else if (a.umap && !a.has_v)
         e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl<true>, a, ngroups, tpc, *reinterpret_cast<const CUtensorMap*>(a.umap));
     else
         e = cudaLaunchKernelEx(&cfg, k_pair_update_tc_pdl<false>, a, ngroups, tpc, dummy);

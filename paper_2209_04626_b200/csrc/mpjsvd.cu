@@ -330,6 +330,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.gram_kt = gram_tma_kt(m_pad, h->opts.gram_kt);
     a.gram_variant = gram_v;
     a.update_tpc = h->opts.update_tpc;
+    a.update_ts = h->opts.update_variant == 1 ? 1 : 0;
     a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
@@ -1264,6 +1265,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->qr_panel_mode = 0;
     o->diag_timing = 0;
     o->refine_v = 0;
+    o->update_variant = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1278,7 +1280,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 13 ||
-        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1)
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

@@ -695,3 +695,16 @@ def test_gram_tma_warp_specialised_bitwise(mp, variant, kt):
     for x, y in zip(r0[:3], r1[:3]):
         assert torch.equal(x, y)
     assert r0[3]["sweeps32"] == r1[3]["sweeps32"] and r0[3]["sweeps64"] == r1[3]["sweeps64"]
+
+
+@pytest.mark.parametrize("extra", [{}, {"switch_u": 0}, {"virtual_shards": 2}])
+def test_update_a_in_tmem_bitwise(mp, extra):
+    """The fp32 update with its A operand (W hi / lo) in tensor memory (update_variant = 1, tcgen05.mma
+    A-from-TMEM, double buffered) computes the same products in the same order as the shared-memory-A update:
+    the whole SVD is bitwise equal (U-route TMA tiles, V-route cp.async tiles with V, sharded engine)."""
+    a = testmat.config_matrix("C3", 512)
+    r0 = mp.factor(dev(a), **extra)
+    r1 = mp.factor(dev(a), update_variant=1, **extra)
+    for x, y in zip(r0[:3], r1[:3]):
+        assert torch.equal(x, y)
+    assert r0[3]["sweeps32"] == r1[3]["sweeps32"] and r0[3]["sweeps64"] == r1[3]["sweeps64"]

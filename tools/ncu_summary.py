@@ -105,6 +105,7 @@ def report(path):
 
 # bench.py kernel keys <- ncu kernel-name prefixes
 TRAFFIC_KEYS = [("qrp_coop", "k_qrp_lazy"), ("pair_gram_f32", "k_pair_gram_tma"), ("pair_gram_f32", "k_pair_gram_tc"),
+                ("pair_gram_f32", "k_pair_gram_sw"),
                 ("pair_update_f32", "k_pair_update_tc"), ("pair_solve_f32", "k_pair_solve<float"),
                 ("pair_gram_f64", "k_pair_gram_dmma"), ("pair_update_f64", "k_pair_update_dmma"),
                 ("pair_solve_f64", "k_pair_solve<double")]
