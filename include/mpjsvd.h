@@ -149,8 +149,9 @@ typedef struct {
                                   1: PAPER.md:599-615 (sec. 3.4, reading c-23): refine Y without V, U_X = Y diag(1/||y_j||),
                                   V_X = qr(X^T U_X) by fp64 Householder QR, then one accumulating refinement from
                                   (X V_X, V := V_X) ("always converges in one sweep") */
-    int32_t update_variant;    /* fp32 tcgen05 update: 0 A operand (W hi/lo) in shared memory; 1 in tensor memory
-                                  (tcgen05.mma A-from-TMEM, double buffered); bitwise equal */
+    int32_t update_variant;    /* fp32 tcgen05 update: 1 (default) A operand (W hi/lo) in tensor memory (tcgen05.mma
+                                  A-from-TMEM, double buffered; C5 fp32 stage 569 -> 534 ms); 0 in shared memory
+                                  (round 1).  Bitwise equal */
 } mpjsvd_options;
 
 typedef struct {

@@ -1265,7 +1265,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->qr_panel_mode = 0;
     o->diag_timing = 0;
     o->refine_v = 0;
-    o->update_variant = 0;
+    o->update_variant = 1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
