@@ -187,12 +187,17 @@ struct BdqrState {
     long long it;      // total QR steps so far
 };
 
+// The rotation chain of the bidiagonal QR is one dependent sequence: r = sqrt(f^2 + g^2) and one reciprocal
+// instead of hypotf and two divisions (the scaled X keeps |f|, |g| <= ~1, so f^2 + g^2 cannot overflow; below
+// 2^-60 the scaled hypotf avoids underflow).  A few ulp from the oracle's hypotf / division (reading c-24).
 __device__ __forceinline__ void givens32(float f, float g, float& c, float& s, float& r) {
     if (g == 0.f) { c = 1.f; s = 0.f; r = f; return; }
     if (f == 0.f) { c = 0.f; s = 1.f; r = g; return; }
-    const float rr = hypotf(f, g);
-    c = f / rr;
-    s = g / rr;
+    float rr = __fsqrt_rn(__fmaf_rn(f, f, __fmul_rn(g, g)));
+    if (rr < 8.6736174e-19f) rr = hypotf(f, g);
+    const float ri = __frcp_rn(rr);
+    c = f * ri;
+    s = g * ri;
     r = rr;
 }
 

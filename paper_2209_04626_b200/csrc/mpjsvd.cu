@@ -60,7 +60,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC, S_QR_RDY,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_GATEC, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_GATEC, S_BIMG, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -335,6 +335,11 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
+    a.bimg = nullptr;
+    if (sizeof(T) == 4 && use_tc && a.update_ts && a.pdl) {
+        MPJ_TRY(ensure(h, S_BIMG, sizeof(float) * (size_t)npairs * 2 * 64 * 64));
+        a.bimg = P<float>(h, S_BIMG);
+    }
     // TMA-fed fp32 Gram: one tensor map over the matrix holding every local slab (the matrix itself on
     // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
     alignas(64) static thread_local unsigned char tmap_buf[128];
@@ -1094,6 +1099,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
         MPJ_TRY(apply_q_wy(dRt, n, (int)n, n_pad, P<double>(h, S_TAU_T), dVX, n_pad, n, P<double>(h, S_WY2), h->aux,
                            P<double>(h, S_TC_T), wy_cached_panels((int)n)));
         MPJ_TRY(scatter_rows_perm(dVX, n_pad, P<int>(h, S_PERM), dVout, n_pad, (int)n, h->aux));
+        // V's output copy (device, or host on the e2e path) on the auxiliary stream: it overlaps U's chain
+        MPJ_CUDA_TRY(cudaMemcpy2DAsync(V, sizeof(double) * ldv, dVout, sizeof(double) * n_pad, sizeof(double) * n, n,
+                                       v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->aux));
         MPJ_CUDA_TRY(cudaEventRecord(h->join, h->aux));
         gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
     }
@@ -1119,8 +1127,9 @@ int factor_impl(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t 
     // ---- outputs (device -> device, or device -> host on the e2e path)
     MPJ_CUDA_TRY(cudaMemcpy2DAsync(U, sizeof(double) * ldu, Ufin, sizeof(double) * ldUf, sizeof(double) * m, n,
                                    u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    MPJ_CUDA_TRY(cudaMemcpy2DAsync(V, sizeof(double) * ldv, dVout, sizeof(double) * n_pad, sizeof(double) * n, n,
-                                   v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (!v_chain)
+        MPJ_CUDA_TRY(cudaMemcpy2DAsync(V, sizeof(double) * ldv, dVout, sizeof(double) * n_pad, sizeof(double) * n, n,
+                                       v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaMemcpyAsync(S, P<double>(h, S_KEYS), sizeof(double) * n,
                                  s_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     MPJ_CUDA_TRY(cudaEventRecord(ev[9], st)); nvtx.close();
