@@ -545,8 +545,8 @@ __device__ __forceinline__ void tma_load_2d_g(uint32_t sdst, const CUtensorMap* 
         : "memory");
 }
 
-template <int GM_ST, int MINB>
-__global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_sw(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
+template <int GM_ST, int MINB, int NT = GT_NT>
+__global__ void __launch_bounds__(NT, MINB) k_pair_gram_sw(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
     constexpr int KT = 32;
     constexpr int STAGE = 128 * KT * 4;                 // 16 KB: raw I | raw J | lo I | lo J, 4 KB each
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_sw(JacobiRound<float>
     }
     if (!hasJ) {   // bye pair: M-rows 32..63 (raw J) stay zero in every stage
         for (int s = 0; s < GM_ST; ++s)
-            for (int i = tid; i < 4096 / 16; i += GT_NT)
+            for (int i = tid; i < 4096 / 16; i += NT)
                 reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4096)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         tc::fence_async_smem();
     }
@@ -596,8 +596,8 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_sw(JacobiRound<float>
         unsigned char* st = sm + (size_t)s * STAGE;
         tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {            // 512 raw float4 chunks, 4 per thread, linear
-            const int f = tid + GT_NT * u;
+        for (int u = 0; u < 512 / NT; ++u) {     // 512 raw float4 chunks, linear
+            const int f = tid + NT * u;
             const float4 x = reinterpret_cast<const float4*>(st)[f];
             reinterpret_cast<float4*>(st + 8192)[f] = tc::lo4(x, tc::hi4(x));
         }
@@ -625,20 +625,22 @@ __global__ void __launch_bounds__(GT_NT, MINB) k_pair_gram_sw(JacobiRound<float>
         if (tid == 0) tc::commit(&fin);
         tc::mbar_wait(&fin, 0);
         tc::fence_after();
+        if (tid < 128) {                         // TMEM lanes 0..127: warps 0..3
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+                for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+            }
         }
         __syncthreads();
-        for (int e = tid; e < 64 * 64; e += GT_NT) {
+        for (int e = tid; e < 64 * 64; e += NT) {
             const int p = e >> 6, q = e & 63;
             out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
         }
     } else {
-        for (int e = tid; e < 64 * 64; e += GT_NT) out[e] = 0.f;
+        for (int e = tid; e < 64 * 64; e += NT) out[e] = 0.f;
     }
     tc::fence_before();
     __syncthreads();
@@ -1157,7 +1159,7 @@ int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long r
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
-    if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 13) {
+    if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 15) {
         const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
         switch (a.gram_variant) {
             case 11:
@@ -1171,6 +1173,14 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
             case 13:
                 MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<8, 1>, gram_tma_smem<32, 8>()));
                 k_pair_gram_sw<8, 1><<<dim3(a.nsplit, a.npairs), GT_NT, gram_tma_smem<32, 8>(), st>>>(a, sm);
+                break;
+            case 14:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<4, 3, 256>, gram_tma_smem<32, 4>()));
+                k_pair_gram_sw<4, 3, 256><<<dim3(a.nsplit, a.npairs), 256, gram_tma_smem<32, 4>(), st>>>(a, sm);
+                break;
+            case 15:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<3, 4, 256>, gram_tma_smem<32, 3>()));
+                k_pair_gram_sw<3, 4, 256><<<dim3(a.nsplit, a.npairs), 256, gram_tma_smem<32, 3>(), st>>>(a, sm);
                 break;
             default:
                 MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<3, 4>, gram_tma_smem<32, 3>()));
@@ -1243,8 +1253,8 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
     if (tma) {
         const int k = gram_tma_kt(rows_pad, kt);
-        if ((variant == 9 && k == 32) || variant == 11) return 3;
-        if (variant == 10) return 4;
+        if ((variant == 9 && k == 32) || variant == 11 || variant == 14) return 3;
+        if (variant == 10 || variant == 15) return 4;
         if (variant == 12) return 2;
         if (variant == 13) return 1;
         return k == 32 ? 4 : 2;

@@ -284,7 +284,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     // Gram kernel variant: gram_tma = 2 (default) -> the 128-byte-swizzled TMA Gram, 4 stages at 3 CTAs/SM for
     // >= 6144 rows, 3 stages at 4 CTAs/SM below (measured); explicit variants 10..13 kept
     int gram_v = h->opts.gram_variant;
-    if (h->opts.gram_tma == 2 && (gram_v < 10 || gram_v > 13)) gram_v = m_pad >= 6144 ? 11 : 10;
+    if (h->opts.gram_tma == 2 && (gram_v < 10 || gram_v > 15)) gram_v = m_pad >= 6144 ? 11 : 10;
     long long nsplit = 1;
     if (h->opts.split_rows > 0) {
         nsplit = ceil_div(m_pad, round_up(h->opts.split_rows, 32));
@@ -330,13 +330,15 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.gram_kt = gram_tma_kt(m_pad, h->opts.gram_kt);
     a.gram_variant = gram_v;
     a.update_tpc = h->opts.update_tpc;
-    a.update_ts = h->opts.update_variant == 1 ? 1 : 0;
+    a.update_ts = h->opts.update_variant >= 1 ? 1 : 0;
     a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
     a.bimg = nullptr;
-    if (sizeof(T) == 4 && use_tc && a.update_ts && a.pdl) {
+    // update_variant 2: E^T hi/lo image written by the solve and bulk-copied by the update (measured slower: the
+    // image is written on the solve's critical path; C5 1.758 -> 1.772 s)
+    if (sizeof(T) == 4 && use_tc && h->opts.update_variant == 2 && a.pdl) {
         MPJ_TRY(ensure(h, S_BIMG, sizeof(float) * (size_t)npairs * 2 * 64 * 64));
         a.bimg = P<float>(h, S_BIMG);
     }
@@ -365,7 +367,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
                 a.tld = ldx;
             }
             if (base && !has_v && make_update_tmap(umap_buf, base, ldx, m_pad, cols) == 0) a.umap = umap_buf;
-            if (base && gram_v >= 10 && gram_v <= 13 &&
+            if (base && gram_v >= 10 && gram_v <= 15 &&
                 make_gram_tmap_sw128(smap_buf, base, ldx, m_pad, cols) == 0)
                 a.smap = smap_buf;
             if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols, a.gram_kt) == 0) {
@@ -1288,8 +1290,8 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
-    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 13 ||
-        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1)
+    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 15 ||
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 2)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;
