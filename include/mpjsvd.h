@@ -151,8 +151,7 @@ typedef struct {
                                   (X V_X, V := V_X) ("always converges in one sweep") */
     int32_t update_variant;    /* fp32 tcgen05 update: 1 (default) A operand (W hi/lo) in tensor memory (tcgen05.mma
                                   A-from-TMEM, double buffered; C5 fp32 stage 569 -> 534 ms); 0 in shared memory
-                                  (round 1); 2 as 1 with E^T hi/lo prepared by the solve (measured slower).
-                                  All bitwise equal */
+                                  (round 1).  Bitwise equal */
 } mpjsvd_options;
 
 typedef struct {

@@ -71,8 +71,6 @@ struct JacobiRound {
     int gram_variant;   // cp.async tcgen05 Gram variant
     int update_tpc;     // 0: auto
     int update_ts;      // 1: fp32 update with the A operand in tensor memory (k_pair_update_tc_ts)
-    float* bimg;        // fp32 tcgen05 update: per pair the 32 KB shared-memory image of E^T hi | lo (K-major,
-                        // written by k_pair_solve, bulk-copied by the update), or nullptr
     int diag;           // mpjsvd_options.diag_timing
 };
 

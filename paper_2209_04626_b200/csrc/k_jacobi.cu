@@ -650,29 +650,6 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
             const int k = e / W, j = e - (e / W) * W;
             E[e] = (k < w && j < w) ? sm.E[InnerSmem<T, W>::eidx(k, j)] : T(0);   // E[k][j] row-major
         }
-        if constexpr (sizeof(T) == 4 && W == 64) {
-            // the tcgen05 update's B operand, E^T split into hi | lo in the K-major SWIZZLE_NONE image of its
-            // shared memory (element (n, k) of E^T = E[k][n] at byte ((n/8)(64/4) + k/4) 128 + (n%8) 16 + (k%4) 4)
-            if (a.bimg) {
-                float* img = a.bimg + (long long)pair * (2 * 64 * 64);
-                for (int it = tid; it < 64 * 16; it += nt) {
-                    const int n = it & 63, k4 = it >> 6;
-                    float v[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int k = 4 * k4 + j;
-                        v[j] = (k < w && n < w) ? sm.E[InnerSmem<T, W>::eidx(k, n)] : T(0);
-                    }
-                    const int o = (((n >> 3) * 16 + k4) * 128 + (n & 7) * 16) / 4;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float hv = __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
-                        img[o + j] = hv;
-                        img[4096 + o + j] = v[j] - hv;
-                    }
-                }
-            }
-        }
     }
     if (sdbg) { sdbg[0] += c1 - c0; sdbg[2] += clock64() - c0; sdbg[4] += 1; }
     if (a.dlist) {                 // publish: E and flag of this pair are complete

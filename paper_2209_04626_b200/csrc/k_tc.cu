@@ -1299,18 +1299,15 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<floa
     float* ring = reinterpret_cast<float*>(sm + 32768);
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ __align__(8) uint64_t rfull[UTS_NR];
-    __shared__ __align__(8) uint64_t efull;
     __shared__ uint32_t tmem_base;
     __shared__ float* colp[64];
     __shared__ int item[3];
     const int tid = threadIdx.x, warp = tid >> 5;
     const int trow = tid & 127, half = tid >> 7;
-    uint32_t eph = 0;                                // completed E-image loads (parity of efull)
     if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         tc::mbar_init(&mbar[0]);
         tc::mbar_init(&mbar[1]);
-        tc::mbar_init(&efull);
         for (int q = 0; q < UTS_NR; ++q) tc::mbar_init(&rfull[q]);
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
@@ -1399,31 +1396,17 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<floa
             if (t < ntile) issue(t);
             if constexpr (!TMA) cp_commit();
         }
-        if (a.bimg) {
-            // E^T hi | lo image written by the pair's solve: one 32 KB bulk copy, waited for by the MMA thread
-            // only (the transposition of the first tile overlaps it)
-            if (tid == 0) {
-                asm volatile("fence.proxy.async;\n" ::: "memory");   // solve's generic stores -> async-proxy read
-                mbar_expect_tx(&efull, 32768u);
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];\n"
-                    ::"r"(tc::smem_u32(Bh)), "l"(a.bimg + (long long)pair * (2 * 64 * 64)), "r"(tc::smem_u32(&efull))
-                    : "memory");
-            }
-        } else {
-            const float* Eg = a.E + (long long)pair * (64 * 64);
-            for (int it = tid; it < 64 * 16; it += UT_NT) {
-                const int n = it & 63, k4 = it >> 6;
-                float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
-                                       Eg[(4 * k4 + 3) * 64 + n]);
-                const uint32_t o = tc::koff(n, 4 * k4, 64);
-                const float4 h = tc::hi4(v);
-                *reinterpret_cast<float4*>(Bh + o) = h;
-                *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
-            }
-            tc::fence_async_smem();              // E^T (generic stores) -> visible to the MMA (async proxy)
+        const float* Eg = a.E + (long long)pair * (64 * 64);
+        for (int it = tid; it < 64 * 16; it += UT_NT) {
+            const int n = it & 63, k4 = it >> 6;
+            float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
+                                   Eg[(4 * k4 + 3) * 64 + n]);
+            const uint32_t o = tc::koff(n, 4 * k4, 64);
+            const float4 h = tc::hi4(v);
+            *reinterpret_cast<float4*>(Bh + o) = h;
+            *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
         }
-        bool e_wait = a.bimg != nullptr;
+        tc::fence_async_smem();                  // E^T (generic stores) -> visible to the MMA (async proxy)
         auto epilogue = [&](int t) {
             const long long row = row_lo + (long long)t * UT_TM + trow;
             const bool rok = row < rows_pad;
@@ -1472,11 +1455,6 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<floa
             if (t + UTS_NR - 1 < ntile) issue(t + UTS_NR - 1);
             if constexpr (!TMA) cp_commit();
             if (tid == 0) {
-                if (e_wait) {                      // first tile of the item: the E^T image has landed
-                    tc::mbar_wait(&efull, eph & 1u);
-                    ++eph;
-                    e_wait = false;
-                }
                 tc::fence_after();
                 const uint32_t bh = tc::smem_u32(Bh), bl = tc::smem_u32(Bl);
                 const uint32_t acc = tmem + (uint32_t)(64 * b);

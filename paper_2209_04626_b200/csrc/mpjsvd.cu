@@ -60,7 +60,7 @@ enum Slot {
     S_A, S_A1, S_A1L, S_RT, S_X, S_Q, S_Y, S_G, S_WY, S_UX, S_VX, S_UBIG, S_VOUT,
     S_X32, S_V32, S_TAU_T0, S_TAU_P, S_TAU_T, S_PERM, S_RANK, S_KEYS, S_FLAGS, S_SCAL,
     S_PART, S_E, S_JFLAG, S_SWEEP, S_QR_PHYS, S_QR_POS, S_QR_VN1, S_QR_VN2, S_QR_CV, S_QR_CP, S_QR_CC, S_QR_RDY,
-    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_GATEC, S_BIMG, S_COUNT
+    S_IOTA, S_TMP1, S_TMP2, S_TAU_U, S_LMOD, S_POFF, S_WY2, S_GEMMWS2, S_TC_TALL, S_TC_P, S_TC_T, S_TC_Z, S_XNORM, S_A1N, S_U32, S_S32, S_SVDWS, S_SOUT, S_GEMMWS, S_QRPW, S_PTAB, S_SHX, S_SHV, S_HDR, S_STAGE, S_PUB, S_GATEC, S_COUNT
 };
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -330,18 +330,11 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.gram_kt = gram_tma_kt(m_pad, h->opts.gram_kt);
     a.gram_variant = gram_v;
     a.update_tpc = h->opts.update_tpc;
-    a.update_ts = h->opts.update_variant >= 1 ? 1 : 0;
+    a.update_ts = h->opts.update_variant == 1 ? 1 : 0;
     a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
-    a.bimg = nullptr;
-    // update_variant 2: E^T hi/lo image written by the solve and bulk-copied by the update (measured slower: the
-    // image is written on the solve's critical path; C5 1.758 -> 1.772 s)
-    if (sizeof(T) == 4 && use_tc && h->opts.update_variant == 2 && a.pdl) {
-        MPJ_TRY(ensure(h, S_BIMG, sizeof(float) * (size_t)npairs * 2 * 64 * 64));
-        a.bimg = P<float>(h, S_BIMG);
-    }
     // TMA-fed fp32 Gram: one tensor map over the matrix holding every local slab (the matrix itself on
     // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
     alignas(64) static thread_local unsigned char tmap_buf[128];
@@ -1291,7 +1284,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 15 ||
-        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 2)
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

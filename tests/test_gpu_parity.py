@@ -704,7 +704,7 @@ def test_update_a_in_tmem_bitwise(mp, extra):
     the whole SVD is bitwise equal (U-route TMA tiles, V-route cp.async tiles with V, sharded engine)."""
     a = testmat.config_matrix("C3", 512)
     r0 = mp.factor(dev(a), update_variant=0, **extra)
-    for v in (1, 2):
+    for v in (1,):
         r1 = mp.factor(dev(a), update_variant=v, **extra)
         for x, y in zip(r0[:3], r1[:3]):
             assert torch.equal(x, y)
