@@ -1,7 +1,8 @@
 """Small invocations of every kernel family for compute-sanitizer (one tool per run):
     compute-sanitizer --tool memcheck python tools/sanitize_run.py
-fp32 tcgen05 + PDL path (b = 32), FFMA fallback, b = 8/16 kernels, virtual shards, ragged and tall shapes,
-Alg. 4 RRQR, step-level entry points."""
+fp32 tcgen05 + PDL path (b = 32; swizzled TMA Gram, TMEM-A update, and the round-1 variants), FFMA fallback,
+b = 8/16 kernels, virtual shards, ragged and tall shapes, Alg. 4 RRQR, the sec. 3.4 V formation, the AUTO
+fp32 QR-SVD branch, step-level entry points."""
 import os
 import sys
 
@@ -22,7 +23,10 @@ def main():
     torch.cuda.set_device(0)
     cases = [("C1", 192, {}), ("C2", 130, {"block_cols": 16}), ("C5", 128, {"block_cols": 8}),
              ("C1", 128, {"fp32_tensor_cores": 0}), ("C3", 128, {"virtual_shards": 2}),
-             ("C1", 160, {"mp_rrqr": 1}), ("C1", 96, {"pdl_overlap": 0})]
+             ("C1", 160, {"mp_rrqr": 1}), ("C1", 96, {"pdl_overlap": 0}),
+             ("C3", 128, {"refine_v": 1}), ("C1", 128, {"path": 1, "tol_alg": 1e-3}),
+             ("C2", 160, {"gram_tma": 1}), ("C2", 160, {"gram_tma": 0}), ("C1", 192, {"update_variant": 0}),
+             ("C3", 128, {"switch_u": 0})]
     for name, n, opts in cases:
         a = testmat.config_matrix(name, n)
         U, S, V, st = mp.factor(dev(a), **opts)
