@@ -46,7 +46,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 SVD time at n=4096 and 8192 (1/2/4/8 B200); sweep HBM GB/s vs peak"
-SAMPLE_N = 1024          # oracle sample size for the CPU baseline
+SAMPLE_N = 2048          # largest oracle sample size for the CPU baseline
+SAMPLE_BUDGET_S = 150.0  # host seconds a whole --impl reference run may spend on its samples
+
+
+def sample_n_for(runs: int, cores: int) -> int:
+    """Largest sample size (<= SAMPLE_N) whose O-MIX run, repeated `runs` times, fits SAMPLE_BUDGET_S.
+    Cost model from the measured 1024^2 C5-recipe run (2.73 s on 16 cores of the GPU box host) scaled by n^3
+    and by the core count; the sample is what is measured, the model only picks its size."""
+    for n in (2048, 1792, 1536, 1280, 1024, 768, 512):
+        est = 2.73 * (n / 1024.0) ** 3 * 16.0 / max(1, cores)
+        if n <= SAMPLE_N and est * max(1, runs) <= SAMPLE_BUDGET_S:
+            return n
+    return 512
 
 
 def parse():
@@ -112,15 +124,16 @@ def dist_env():
 
 
 # ----------------------------------------------------------------- CPU oracle
-def oracle_sample(config: str, n_full: int, m_full: int):
+def oracle_sample(config: str, n_full: int, m_full: int, runs: int = 1):
     """Time O-MIX (oracle/, as it stands, all host threads) on the config's
-    recipe at n = SAMPLE_N and scale by the flop ratio to the full size."""
+    recipe at the largest sample size whose `runs` repetitions fit the host
+    budget (sample_n_for) and scale by the flop ratio to the full size."""
     import oracle
     import testmat
     import numpy as np
-    n_s = min(SAMPLE_N, n_full)
-    a = testmat.config_matrix(config, n_s)
     cores = len(os.sched_getaffinity(0))
+    n_s = min(sample_n_for(runs, cores), n_full)
+    a = testmat.config_matrix(config, n_s)
     t0 = time.perf_counter()
     _, s, _, st, rc = oracle.mixed_svd(a, nthreads=cores)
     dt = time.perf_counter() - t0
@@ -162,7 +175,7 @@ def run_reference(args):
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        cb = oracle_sample(args.config, n_full, m_full)
+        cb = oracle_sample(args.config, n_full, m_full, runs=args.warmup + args.steps)
         if i >= args.warmup:
             vals.append(cb["value"])
             last = cb

@@ -152,6 +152,9 @@ typedef struct {
     int32_t update_variant;    /* fp32 tcgen05 update: 1 (default) A operand (W hi/lo) in tensor memory (tcgen05.mma
                                   A-from-TMEM, double buffered; C5 fp32 stage 569 -> 534 ms); 0 in shared memory
                                   (round 1).  Bitwise equal */
+    int32_t qrp_panel_stages;  /* column-pivoted QR end-of-panel update: -1 (default) auto (a per-thread cp.async ring of
+                                  2 stages when it fits in shared memory), 0 register path (round 1), 2..4 forced.
+                                  Bitwise equal */
 } mpjsvd_options;
 
 typedef struct {

@@ -44,7 +44,8 @@ class Options(C.Structure):
                 ("cond_d_min", C.c_double), ("tail_frac", C.c_double), ("tail_cut_log2", C.c_int32),
                 ("gram_tma", C.c_int32), ("gram_kt", C.c_int32), ("gram_variant", C.c_int32),
                 ("update_tpc", C.c_int32), ("skip_unchanged", C.c_int32), ("qr_panel_mode", C.c_int32),
-                ("diag_timing", C.c_int32), ("refine_v", C.c_int32), ("update_variant", C.c_int32)]
+                ("diag_timing", C.c_int32), ("refine_v", C.c_int32), ("update_variant", C.c_int32),
+                ("qrp_panel_stages", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -16,6 +16,7 @@ void mpj_record_cuda_error(cudaError_t e, const char* what, const char* file, in
 
 // mpjsvd_options.diag_timing of the call in progress on this host thread (set at every entry point)
 extern thread_local int g_mpj_diag;
+extern thread_local int g_mpj_qrp_pe;   // options.qrp_panel_stages (-1 auto)
 
 // count of kernel launches issued by the engine (reported in stats)
 extern thread_local int64_t g_mpj_launches;

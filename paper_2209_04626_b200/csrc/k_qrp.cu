@@ -37,6 +37,7 @@ namespace mpj {
 
 constexpr int QP_NT = 512;
 constexpr int QP_NB = 32;
+constexpr int QP_PE_G = 4;      // columns per group of the end-of-panel ring
 constexpr int QP_PART_PT = 12;
 constexpr int QP_CAND_PL = 6;    // candidates per lane of the pivot warp: G <= 32 QP_CAND_PL   // partials per thread in the reflector reduction: G (QP_NB + 1) <= QP_NT QP_PART_PT
 
@@ -52,6 +53,7 @@ struct QrpArgs {
     T* v0g;     // n
     T* mug;     // n
     int nown;        // max owned columns per CTA
+    int pe_st;       // stages of the end-of-panel cp.async ring (0: register path)
     long long* dbg;  // optional phase timers (CTA 0), MPJSVD_QRP_TIMING=1
 };
 
@@ -143,9 +145,13 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     int* rflag = pcol + QP_NB;                      // nown: recompute flags
     int* own = rflag + nown;                        // nown: physical column of owned slot s (-1: none); the
                                                     // live columns are re-dealt round-robin at every panel end
-    int* phys = own + nown;                         // n: column at logical position (this CTA's copy)
-    int* pos = phys + n;                            // n: logical position of physical column
-    __shared__ int s_anyrec, s_piv;
+    // 16-bit (n <= 16384): the shared-memory footprint sets the L1 left for the GEMV's loads in flight
+    unsigned short* phys = reinterpret_cast<unsigned short*>(own + nown);   // n: column at logical position (this CTA's copy)
+    unsigned short* pos = phys + n;                 // n: logical position of physical column
+    int* lsl = reinterpret_cast<int*>(pos + n + (n & 1));   // nown: live owned slots at a panel end
+    // end-of-panel ring: stage s, column u of a group, thread t at ring[(s QP_PE_G + u) QP_NT + t]
+    T* ring = reinterpret_cast<T*>(qsm_raw + ((reinterpret_cast<size_t>(lsl + nown) - reinterpret_cast<size_t>(qsm_raw) + 15) & ~size_t(15)));
+    __shared__ int s_anyrec, s_piv, s_nl;
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const long long lda = a.lda;
     const T tol3z = sqrt(sizeof(T) == 8 ? T(1.1102230246251565e-16) : T(5.9604644775390625e-08));
@@ -458,6 +464,76 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         tmark(8);
         // ---------------- end of panel: apply the panel to the owned trailing columns
         if (panel_end) {
+          if (a.pe_st >= 2) {
+            // Every thread streams its own row of the live owned columns, QP_PE_G columns per group,
+            // through a private cp.async ring of pe_st stages (pe_st - 1 groups in flight while one is
+            // updated): the update is bound by the bytes in flight, which registers alone cap at one group.
+            if (tid == 0) {
+                int nl = 0;
+                for (int sl = 0; sl < nown; ++sl)
+                    if (lp(sl) > k) lsl[nl++] = sl;
+                s_nl = nl;
+            }
+            __syncthreads();
+            const int nl = s_nl, ngr = (nl + QP_PE_G - 1) / QP_PE_G, S = a.pe_st;
+            const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring + tid);
+            for (long long i0 = k + 1; i0 < m; i0 += QP_NT) {
+                const long long i = i0 + tid;
+                const bool rowok = i < m;
+                auto issue = [&](int g) {
+                    if (g < ngr && rowok) {
+                        const int st = g % S;
+#pragma unroll
+                        for (int u = 0; u < QP_PE_G; ++u) {
+                            const int q = g * QP_PE_G + u;
+                            if (q < nl) {
+                                const T* src = a.A + (long long)own[lsl[q]] * lda + i;
+                                const unsigned dst = rbase + (unsigned)(((st * QP_PE_G + u) * QP_NT) * sizeof(T));
+                                if constexpr (sizeof(T) == 8)
+                                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+                                else
+                                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+                            }
+                        }
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                };
+                for (int g = 0; g < S - 1; ++g) issue(g);
+                T vt[QP_NB];
+#pragma unroll
+                for (int t = 0; t < QP_NB; ++t) {
+                    vt[t] = 0.0;
+                    if (rowok && t <= jj) vt[t] = (t == jj) ? vs[i] : __ldcg(a.A + (long long)pcol[t] * lda + i) * v0p[t];
+                }
+                for (int g = 0; g < ngr; ++g) {
+                    issue(g + S - 1);
+                    // S - 1 newer groups may stay pending; group g has landed (each thread reads only its own copies)
+                    if (S == 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+                    else if (S == 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+                    else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                    if (!rowok) continue;
+                    const T* rs = ring + (g % S) * QP_PE_G * QP_NT + tid;
+                    T y[QP_PE_G];
+                    const T* Fs[QP_PE_G];
+#pragma unroll
+                    for (int u = 0; u < QP_PE_G; ++u) {
+                        const int q = g * QP_PE_G + u;
+                        Fs[u] = Fown + (size_t)lsl[q < nl ? q : 0] * QP_NB;
+                        y[u] = q < nl ? rs[u * QP_NT] : T(0);
+                    }
+#pragma unroll
+                    for (int t = 0; t < QP_NB; ++t)            // vt[t] = 0 for t > jj
+#pragma unroll
+                        for (int u = 0; u < QP_PE_G; ++u) y[u] -= vt[t] * Fs[u][t];
+#pragma unroll
+                    for (int u = 0; u < QP_PE_G; ++u) {
+                        const int q = g * QP_PE_G + u;
+                        if (q < nl) a.A[(long long)own[lsl[q]] * lda + i] = y[u];
+                    }
+                }
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            }
+          } else {
             for (long long i0 = k + 1; i0 < m; i0 += QP_NT) {
                 const long long i = i0 + tid;
                 if (i < m) {
@@ -487,6 +563,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
                     }
                 }
             }
+          }
             __syncthreads();
             for (int e = tid; e < nown * QP_NB; e += QP_NT) {
                 const int sl = e / QP_NB;
@@ -568,11 +645,17 @@ template <typename T>
 static size_t qrp_smem(int m, int n, int nown, int grid) {
     const size_t vsz = std::max((size_t)m, (size_t)grid * (QP_NB + 1));
     return sizeof(T) * (vsz + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
-           sizeof(int) * (QP_NB + 2 * (size_t)nown + 2 * (size_t)n) + 64;
+           sizeof(int) * (QP_NB + 3 * (size_t)nown + (size_t)n + 1) + 64;
+}
+
+// bytes of the end-of-panel ring with pe_st stages (after the 16-byte alignment of qrp_smem's layout)
+template <typename T>
+static size_t qrp_ring_bytes(int pe_st) {
+    return pe_st >= 2 ? 16 + sizeof(T) * (size_t)pe_st * QP_PE_G * QP_NT : 0;
 }
 
 template <typename T>
-static int qrp_lazy_grid_t(int m, int n, int* grid, int* nown) {
+static int qrp_lazy_grid_t(int m, int n, int* grid, int* nown, int* pe_st = nullptr) {
     void* fn = qrp_kernel_for<T>(m);
     if (!fn) return -7;
     int dev = 0, nsm = 0, per = 0;
@@ -580,10 +663,25 @@ static int qrp_lazy_grid_t(int m, int n, int* grid, int* nown) {
     MPJ_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int g = nsm;
     int no = (n + g - 1) / g;
+    if (n > 65535) return -7;   // 16-bit phys / pos
     if (g * (QP_NB + 1) > QP_NT * QP_PART_PT || g > 32 * QP_CAND_PL) return -7;
     size_t smem = qrp_smem<T>(m, n, no, g);
     if (smem > 227 * 1024) return -7;
+    // end-of-panel ring: 2 stages by default (measured, C5 panel phase 75 -> 67 ms; 3 or 4 stages take L1 from
+    // the GEMV pass: 226 -> 229 / 287 ms), or the forced count
+    int st = 0;
+    if (g_mpj_qrp_pe < 0) {
+        st = smem + qrp_ring_bytes<T>(2) <= 227 * 1024 ? 2 : 0;
+    } else if (g_mpj_qrp_pe >= 2 && smem + qrp_ring_bytes<T>(g_mpj_qrp_pe) <= 227 * 1024) {
+        st = g_mpj_qrp_pe;
+    }
+    smem += qrp_ring_bytes<T>(st);
+    if (pe_st) *pe_st = st;
     MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the smallest shared-memory carveout that holds the kernel: the rest of the 256 KB is L1, which stages the
+    // GEMV's loads in flight (measured: +48 KB of shared memory slowed the C5 GEMV pass 226 -> 287 ms)
+    const int pct = (int)std::min<size_t>(100, (smem + 1024 + 228 * 1024 / 100 - 1) * 100 / (228 * 1024));
+    MPJ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     MPJ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, QP_NT, smem));
     if (per < 1) return -7;
     *grid = g;
@@ -600,8 +698,8 @@ size_t qrp_lazy_work_doubles(int n, int grid) {
 template <typename T>
 static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* work, int* phys_out,
                       cudaStream_t st) {
-    int grid = 0, nown = 0;
-    int rc = qrp_lazy_grid_t<T>(m, n, &grid, &nown);
+    int grid = 0, nown = 0, pe_st = 0;
+    int rc = qrp_lazy_grid_t<T>(m, n, &grid, &nown, &pe_st);
     if (rc) return rc;
     void* fn = qrp_kernel_for<T>(m);
     QrpArgs<T> args;
@@ -617,6 +715,7 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
     args.v0g = args.part + (size_t)grid * (QP_NB + 1);
     args.mug = args.v0g + n;
     args.nown = nown;
+    args.pe_st = pe_st;
     args.dbg = nullptr;
     static long long* dbg = nullptr;
     if (g_mpj_diag & 1) {
@@ -624,7 +723,7 @@ static int qrp_lazy_t(T* A, long long lda, int m, int n, T* tau, QrWork& w, T* w
         args.dbg = dbg;
     }
     void* params[] = {&args};
-    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem<T>(m, n, nown, grid), st));
+    MPJ_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(QP_NT), params, qrp_smem<T>(m, n, nown, grid) + qrp_ring_bytes<T>(pe_st), st));
     MPJ_LAUNCHED();
     if (phys_out)
         MPJ_CUDA_TRY(cudaMemcpyAsync(phys_out, w.phys_all, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));

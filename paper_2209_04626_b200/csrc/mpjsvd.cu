@@ -25,6 +25,7 @@
 
 thread_local int64_t g_mpj_launches = 0;
 thread_local int g_mpj_diag = 0;
+thread_local int g_mpj_qrp_pe = -1;   // options.qrp_panel_stages of the calling handle
 static thread_local char g_last_cuda_err[512] = "no error";
 
 cudaError_t mpj_set_smem(const void* fn, size_t bytes) {
@@ -1189,6 +1190,7 @@ static int jacobi_entry(mpjsvd_handle h, T* X, int64_t m, int64_t n, int64_t ldx
                         bool is64) {
     if (!h || !X || m < 1 || n < 1 || ldx < m || (V && ldv < nv) || max_sweeps < 1) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32), nv_pad = round_up(nv > 0 ? nv : 1, 32);
     MPJ_TRY(ensure(h, S_TMP1, sizeof(T) * (size_t)m_pad * n));
@@ -1270,6 +1272,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->diag_timing = 0;
     o->refine_v = 0;
     o->update_variant = 1;
+    o->qrp_panel_stages = -1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1284,7 +1287,8 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 15 ||
-        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1)
+        o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1 ||
+        o.qrp_panel_stages < -1 || o.qrp_panel_stages == 1 || o.qrp_panel_stages > 4)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;
@@ -1488,6 +1492,7 @@ int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_
                   double* S, double* V, int64_t ldv, mpjsvd_stats* stats) {
     if (!h) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     const bool root = !h->comm.active() || h->comm.rank == 0;
     if (root && (!A || !U || !S || !V)) return MPJSVD_ERR_INVALID_ARG;
     if (n < 2 || m < n || (root && (lda < m || ldu < m || ldv < n))) return MPJSVD_ERR_INVALID_ARG;
@@ -1502,6 +1507,7 @@ int mpjsvd_gemm_f64(mpjsvd_handle h, int32_t transa, int32_t transb, int64_t M, 
                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (!h || !A || !B || !C) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     MPJ_TRY(ensure(h, S_GEMMWS, sizeof(double) * (size_t)(M > 0 ? M : 1) * (N > 0 ? N : 1) * 16));
     gemm_set_workspace(P<double>(h, S_GEMMWS), h->cap[S_GEMMWS] / sizeof(double));
     int rc = gemm_f64(transa, transb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h->stream);
@@ -1513,6 +1519,7 @@ int mpjsvd_inner_solve(mpjsvd_handle h, int32_t is_f64, void* G, void* E, int32_
                        int32_t max_inner, int32_t* rotations) {
     if (!h || !G || !E || w < 1 || w > 64 || count < 1) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     MPJ_TRY(ensure(h, S_TMP1, sizeof(int) * (size_t)count));
     int rc = is_f64 ? launch_inner_batch<double>((double*)G, (double*)E, w, tol_in, max_inner, count,
                                                   P<int>(h, S_TMP1), h->stream)
@@ -1543,6 +1550,7 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
               int32_t pivot) {
     if (!h || !A || !tau || m < n || n < 1 || lda < m) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long m_pad = round_up(m, 32);
@@ -1605,6 +1613,7 @@ int mpjsvd_qr(mpjsvd_handle h, double* A, int64_t m, int64_t n, int64_t lda, dou
 int mpjsvd_lift(mpjsvd_handle h, const float* V32, int64_t n, int64_t ldv32, double* Q, int64_t ldq) {
     if (!h || !V32 || !Q || n < 1 || ldv32 < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long n_pad = round_up(n, 32);
@@ -1635,6 +1644,7 @@ int mpjsvd_switch_u(mpjsvd_handle h, const double* X, int64_t n, int64_t ldx, co
                     double* Q, int64_t ldq, int32_t x_lower) {
     if (!h || !X || !Ulow || !Q || n < 1 || ldx < n || ldu < n || ldq < n) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
     const long long n_pad = round_up(n, 32);
@@ -1665,6 +1675,7 @@ int mpjsvd_qrsvd32(mpjsvd_handle h, const float* X32, int64_t n, int64_t ldx, do
     if (!h || !X32 || !U || n < 1 || ldx < n || ldu < n) return MPJSVD_ERR_INVALID_ARG;
     if (n > 16384) return MPJSVD_ERR_NOT_SUPPORTED;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); return MPJSVD_ERR_CUDA; }
     gemm_set_workspace(nullptr, 0);
     cudaStream_t st = h->stream;
@@ -1706,6 +1717,7 @@ int mpjsvd_apply_q(mpjsvd_handle h, const double* Vr, int64_t m, int64_t k, int6
                    int64_t ldc, int64_t ncols) {
     if (!h || !Vr || !tau || !C || k > m || ldv < m || ldc < m) return MPJSVD_ERR_INVALID_ARG;
     g_mpj_diag = h->opts.diag_timing;
+    g_mpj_qrp_pe = h->opts.qrp_panel_stages;
     gemm_set_workspace(nullptr, 0);
     MPJ_TRY(ensure(h, S_WY, sizeof(double) * apply_q_work_elems(m, ncols)));
     MPJ_TRY(apply_q_wy(Vr, m, (int)k, ldv, tau, C, ldc, ncols, P<double>(h, S_WY), h->stream));

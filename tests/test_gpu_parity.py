@@ -709,3 +709,18 @@ def test_update_a_in_tmem_bitwise(mp, extra):
         for x, y in zip(r0[:3], r1[:3]):
             assert torch.equal(x, y)
         assert r0[3]["sweeps32"] == r1[3]["sweeps32"] and r0[3]["sweeps64"] == r1[3]["sweeps64"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,pivot", [(8192, 600, 1), (2100, 700, 1), (700, 700, 1), (257, 100, 1), (4200, 900, 3)])
+def test_qrp_panel_ring_bitwise(mp, m, n, pivot):
+    """The lazy QRP's end-of-panel update through the per-thread cp.async ring (qrp_panel_stages = -1 auto,
+    2, 3) performs the same fused multiply-adds in the same order as the register path (0): packed factors,
+    tau and pivots are bitwise equal, including the fp32 QRP of Alg. 4 (pivot 3)."""
+    rng = np.random.default_rng(m * 7 + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-2, 2, n))
+    ref = mp.qr(dev(a), pivot=pivot, qrp_panel_stages=0)
+    for st in (-1, 2, 3):
+        out = mp.qr(dev(a), pivot=pivot, qrp_panel_stages=st)
+        for x, y in zip(ref, out):
+            assert torch.equal(x, y), st
