@@ -477,7 +477,11 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
             __syncthreads();
             const int nl = s_nl, ngr = (nl + QP_PE_G - 1) / QP_PE_G, S = a.pe_st;
             const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring + tid);
-            for (long long i0 = k + 1; i0 < m; i0 += QP_NT) {
+            // row chunks in a CTA-rotated order: every CTA reads the same panel columns (vt), and CTAs walking
+            // the rows in lockstep would all hit the same L2 lines at once
+            const long long nch = (m - k - 1 + QP_NT - 1) / QP_NT;
+            for (long long c = 0; c < nch; ++c) {
+                const long long i0 = k + 1 + ((c + cta) % nch) * QP_NT;
                 const long long i = i0 + tid;
                 const bool rowok = i < m;
                 auto issue = [&](int g) {
