@@ -155,6 +155,10 @@ typedef struct {
     int32_t qrp_panel_stages;  /* column-pivoted QR end-of-panel update: -1 (default) auto (a per-thread cp.async ring of
                                   2 stages when it fits in shared memory), 0 register path (round 1), 2..4 forced.
                                   Bitwise equal */
+    int32_t gram_pdl;          /* 1 (default): each Jacobi round's solve is a programmatic dependent of its Gram and
+                                  starts a pair as soon as that pair's row-slab partials are counted (per-pair counters),
+                                  overlapping the Gram's last wave; 0: the solve waits for the whole Gram.  Bitwise
+                                  equal */
 } mpjsvd_options;
 
 typedef struct {

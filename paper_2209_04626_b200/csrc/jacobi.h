@@ -51,6 +51,10 @@ struct JacobiRound {
     int* dlist;
     int* dctr;
     int pdl;            // 1: the update is launched as a programmatic dependent of the solve
+    // Gram -> solve overlap: the solve is a programmatic dependent of the Gram and waits per pair for
+    // gcnt[pair] == nsplit (each Gram CTA adds 1 after its partial is written; the solve zeroes it)
+    int* gcnt;
+    int gram_pdl;
     // fp32 tcgen05 Gram with TMA loads (k_tc.cu): host pointer to a CUtensorMap over the matrix that holds
     // every local slab (tbase, leading dimension tld), or nullptr (cp.async Gram)
     const void* tmap;
@@ -80,6 +84,25 @@ __device__ __forceinline__ bool pair_unchanged(const JacobiRound<T>& a, const Pa
     if (!a.skip) return false;
     const int since = a.gidx - a.R;
     return a.last_mod[pd.b0] < since && a.last_mod[pd.b1] < since;
+}
+
+// Gram CTA prologue under gram_pdl: the publication reset is visible, then the solve may launch
+template <typename T>
+__device__ __forceinline__ void gram_pdl_begin(const JacobiRound<T>& a) {
+    if (!a.gram_pdl) return;
+    __threadfence();
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+// Gram CTA epilogue under gram_pdl: this CTA's partial is written (every thread), count it for its pair
+template <typename T>
+__device__ __forceinline__ void gram_pdl_end(const JacobiRound<T>& a, int pair) {
+    if (!a.gram_pdl) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(a.gcnt + pair, 1);
+    }
 }
 
 // reset of the publication list by the first CTA of the round's Gram kernel

@@ -579,6 +579,20 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
         }
         return;
     }
+    if (a.gram_pdl) {
+        // launched beside the Gram: wait until every row slab of this pair has been counted
+        if (tid == 0) {
+            unsigned long long t0 = 0;
+            while (ld_acquire_gpu(a.gcnt + pair) < a.nsplit) {
+                __nanosleep(64);
+                const unsigned long long t = global_ns();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > MPJ_SPIN_TIMEOUT_NS) { atomicExch(a.dctr + 2, 1); break; }
+            }
+            a.gcnt[pair] = 0;      // next use: the next round's Gram, after this kernel
+        }
+        __syncthreads();
+    }
     // fixed-order reduction over row slabs (deterministic)
     const T* part = a.partial + (long long)pair * a.nsplit * (W * W);
     {
@@ -843,6 +857,7 @@ __device__ __forceinline__ void gram_warp(const double* const* colp, double* Wsm
 template <int W>
 __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
     reset_publication(a);
+    gram_pdl_begin(a);
     if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(16) unsigned char gram_smem[];
     double* Wsm = reinterpret_cast<double*>(gram_smem);
@@ -863,6 +878,7 @@ __global__ void __launch_bounds__(128) k_pair_gram_dmma(JacobiRound<double> a) {
         case 2: gram_warp<W, 2>(colp, Wsm, rbeg, ntile, out); break;
         default: gram_warp<W, 3>(colp, Wsm, rbeg, ntile, out); break;
     }
+    gram_pdl_end(a, pair);
 }
 static size_t gram_dmma_smem(int W) { return sizeof(double) * (size_t)GRAM_STAGES * W * GRAM_S + sizeof(long long) * W; }
 
@@ -1359,7 +1375,11 @@ template <> struct KName<double> {
 };
 
 template <typename T, int W>
-static int launch_round_w(const JacobiRound<T>& a, cudaStream_t st, const ProfHook* hook) {
+static int launch_round_w(const JacobiRound<T>& a0, cudaStream_t st, const ProfHook* hook) {
+    // Gram -> solve overlap only behind the Gram kernels that count their partials (gram_pdl_end)
+    JacobiRound<T> a = a0;
+    a.gram_pdl = a0.gram_pdl && (sizeof(T) == 8 || (W == 64 && a0.use_tc && a0.smap && a0.gram_variant >= 10 &&
+                                                     a0.gram_variant <= 15)) ? 1 : 0;
     if (hook) hook->begin(hook->ctx, KName<T>::gram);
     if constexpr (sizeof(T) == 8) {
         MPJ_CUDA_TRY(set_smem(k_pair_gram_dmma<W>, (size_t)(gram_dmma_smem(W))));
@@ -1386,7 +1406,26 @@ solve:
     const bool overlap = a.pdl && (sizeof(T) == 8 || (W == 64 && a.use_tc));
     const char* both = sizeof(T) == 4 ? "pair_solve_update_f32" : "pair_solve_update_f64";
     if (hook) hook->begin(hook->ctx, overlap ? both : KName<T>::solve);
-    k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
+    if (a.gram_pdl) {
+        // programmatic dependent of the Gram (per-pair counters, k_pair_solve)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)a.npairs);
+        cfg.blockDim = dim3(inner_nt<W>());
+        cfg.dynamicSmemBytes = sms;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_solve<T, W>, a);
+        if (e != cudaSuccess) {
+            mpj_record_cuda_error(e, "cudaLaunchKernelEx(solve)", __FILE__, __LINE__);
+            return -4;
+        }
+    } else {
+        k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
+    }
     MPJ_LAUNCHED();
     if (overlap) {
         int rc = 0;

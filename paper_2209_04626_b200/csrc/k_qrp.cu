@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
     // 16-bit (n <= 16384): the shared-memory footprint sets the L1 left for the GEMV's loads in flight
     unsigned short* phys = reinterpret_cast<unsigned short*>(own + nown);   // n: column at logical position (this CTA's copy)
     unsigned short* pos = phys + n;                 // n: logical position of physical column
-    int* lsl = reinterpret_cast<int*>(pos + n + (n & 1));   // nown: live owned slots at a panel end
+    int* lsl = reinterpret_cast<int*>(pos + n);     // nown: live owned slots at a panel end (2n shorts: 4-byte aligned)
     // end-of-panel ring: stage s, column u of a group, thread t at ring[(s QP_PE_G + u) QP_NT + t]
     T* ring = reinterpret_cast<T*>(qsm_raw + ((reinterpret_cast<size_t>(lsl + nown) - reinterpret_cast<size_t>(qsm_raw) + 15) & ~size_t(15)));
     __shared__ int s_anyrec, s_piv, s_nl;
@@ -649,7 +649,7 @@ template <typename T>
 static size_t qrp_smem(int m, int n, int nown, int grid) {
     const size_t vsz = std::max((size_t)m, (size_t)grid * (QP_NB + 1));
     return sizeof(T) * (vsz + (size_t)nown * QP_NB + 6 * (size_t)nown + 33 * 32 + 4 * QP_NB + 8) +
-           sizeof(int) * (QP_NB + 3 * (size_t)nown + (size_t)n + 1) + 64;
+           sizeof(int) * (QP_NB + 3 * (size_t)nown + (size_t)n) + 64;
 }
 
 // bytes of the end-of-panel ring with pe_st stages (after the 16-byte alignment of qrp_smem's layout)

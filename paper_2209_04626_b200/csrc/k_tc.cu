@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_gram_sw(JacobiRound<float> a,
     constexpr int STAGE = 128 * KT * 4;                 // 16 KB: raw I | raw J | lo I | lo J, 4 KB each
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
     reset_publication(a);
+    gram_pdl_begin(a);
     if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(1024) unsigned char gs_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gs_raw) + 1023) & ~(uintptr_t)1023);
@@ -642,6 +643,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_gram_sw(JacobiRound<float> a,
     } else {
         for (int e = tid; e < 64 * 64; e += NT) out[e] = 0.f;
     }
+    gram_pdl_end(a, pair);
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_free<64>(tmem);

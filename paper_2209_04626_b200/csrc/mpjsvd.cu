@@ -311,7 +311,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     MPJ_TRY(ensure(h, S_SWEEP, 64 * (sizeof(double) + 4 * sizeof(int))));
     MPJ_TRY(ensure(h, S_PTAB, sizeof(PairDesc<T>) * (size_t)R * npairs));
     MPJ_TRY(ensure_pinned(h, sizeof(PairDesc<T>) * (size_t)R * npairs));
-    MPJ_TRY(ensure(h, S_PUB, sizeof(int) * ((size_t)npairs + 4)));
+    MPJ_TRY(ensure(h, S_PUB, sizeof(int) * (2 * (size_t)npairs + 4)));
     double* d_off = P<double>(h, S_SWEEP);
     int* d_upd = reinterpret_cast<int*>(d_off + 64);
     int* d_inner = d_upd + 64;     // [64][2]
@@ -335,6 +335,9 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.diag = h->opts.diag_timing;
     a.dctr = P<int>(h, S_PUB);
     a.dlist = a.dctr + 4;
+    a.gcnt = a.dlist + npairs;
+    a.gram_pdl = h->opts.gram_pdl;
+    MPJ_CUDA_TRY(cudaMemsetAsync(a.gcnt, 0, sizeof(int) * (size_t)npairs, st));
     a.pdl = h->opts.pdl_overlap && (sizeof(T) == 8 || use_tc) ? 1 : 0;
     // TMA-fed fp32 Gram: one tensor map over the matrix holding every local slab (the matrix itself on
     // one GPU, the shard buffers otherwise); falls back to the cp.async Gram if the map cannot be made
@@ -1273,6 +1276,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->refine_v = 0;
     o->update_variant = 1;
     o->qrp_panel_stages = -1;
+    o->gram_pdl = 1;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1288,7 +1292,8 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
         return MPJSVD_ERR_INVALID_ARG;
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 15 ||
         o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1 ||
-        o.qrp_panel_stages < -1 || o.qrp_panel_stages == 1 || o.qrp_panel_stages > 4)
+        o.qrp_panel_stages < -1 || o.qrp_panel_stages == 1 || o.qrp_panel_stages > 4 ||
+        o.gram_pdl < 0 || o.gram_pdl > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

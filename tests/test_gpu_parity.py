@@ -724,3 +724,18 @@ def test_qrp_panel_ring_bitwise(mp, m, n, pivot):
         out = mp.qr(dev(a), pivot=pivot, qrp_panel_stages=st)
         for x, y in zip(ref, out):
             assert torch.equal(x, y), st
+
+
+@pytest.mark.parametrize("name,n,extra", [("C3", 512, {}), ("C5", 640, {"virtual_shards": 2}), ("C1", 300, {}),
+                                          ("C2", 256, {"refine_v": 1}), ("C3", 384, {"skip_unchanged": 0})])
+def test_gram_pdl_bitwise(mp, name, n, extra):
+    """The Jacobi rounds with the solve launched as a programmatic dependent of the Gram (gram_pdl = 1: per-pair
+    counters, a pair's solve starts when its row-slab partials are in) compute exactly what the serialised
+    rounds (0) compute: the whole SVD is bitwise equal (fp32 tcgen05 Gram, fp64 DMMA Gram, ragged widths,
+    exact skip on and off, the sharded engine)."""
+    a = testmat.config_matrix(name, n)
+    r0 = mp.factor(dev(a), gram_pdl=0, **extra)
+    r1 = mp.factor(dev(a), gram_pdl=1, **extra)
+    for x, y in zip(r0[:3], r1[:3]):
+        assert torch.equal(x, y)
+    assert r0[3]["sweeps32"] == r1[3]["sweeps32"] and r0[3]["sweeps64"] == r1[3]["sweeps64"]
