@@ -209,49 +209,54 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     return y * fma(-h * y, y, 1.5);
 }
 
+// rotation parameters from the pair's Gram entries (indices p < q): (c, s), t, c - 1; returns active
+template <typename T>
+__device__ __forceinline__ int rotation_from(bool valid, T gpp, T gqq, T gpq, T tol_in, T& c, T& sn, T& t, T& cm1) {
+    c = T(1); sn = T(0); t = T(0); cm1 = T(0);
+    // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||  (PAPER.md:293-294)
+    if (!(valid && gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq))) return 0;
+    // closest-to-identity rotation (reading c-3)
+    if constexpr (sizeof(T) == 4) {
+        // fp32 stage (an initial guess refined in fp64): MUFU rsqrt / fast
+        // division, a few ulp from the IEEE formulas (DESIGN.md c-14)
+        const float zeta = __fdividef(gqq - gpp, 2.0f * gpq);
+        if (fabsf(zeta) > RealTraits<float>::rsqrt_u) {
+            t = __fdividef(0.5f, zeta);
+        } else {
+            const float r1 = fmaf(zeta, zeta, 1.0f);
+            const float sq = r1 * rsqrtf(r1);
+            t = __fdividef(zeta >= 0.0f ? 1.0f : -1.0f, fabsf(zeta) + sq);
+        }
+        const float r2 = fmaf(t, t, 1.0f);
+        c = rsqrtf(r2);
+        sn = t * c;
+        cm1 = -__fdividef(t * t * c, 1.0f + r2 * c);
+    } else {
+        // fp64: the same formulas with MUFU reciprocal / rsqrt refined by two Newton steps (<= 2 ulp
+        // from the IEEE quotients and roots; the refinement's accuracy is set by the outer fp64
+        // Gram and update, the rotation only has to be orthogonal to u64: c^2 + s^2 = 1 + O(u64))
+        const double zeta = (gqq - gpp) * rcp_nr(2.0 * gpq);
+        if (fabs(zeta) > RealTraits<double>::rsqrt_u) {
+            t = 0.5 * rcp_nr(zeta);
+        } else {
+            const double r1 = fma(zeta, zeta, 1.0);
+            const double sq = r1 * rsqrt_nr(r1);
+            t = (zeta >= 0.0 ? 1.0 : -1.0) * rcp_nr(fabs(zeta) + sq);
+        }
+        const double r2 = fma(t, t, 1.0);
+        c = rsqrt_nr(r2);
+        sn = t * c;
+        cm1 = -(t * t * c) * rcp_nr(1.0 + r2 * c);
+    }
+    return 1;
+}
+
 // rotation parameters of pair k (indices p < q) into buffer `buf`; returns active
 template <typename T, int W>
 __device__ __forceinline__ int set_rotation(InnerSmem<T, W>& sm, int buf, int k, int q, int w, T gpp, T gqq, T gpq,
                                             T tol_in) {
-    int active = 0;
-    T c = T(1), sn = T(0), t = T(0), cm1 = T(0);
-    // Alg. 1 guard |x_q^T x_p| > eps ||x_p|| ||x_q||  (PAPER.md:293-294)
-    if (q < w && gpp > T(0) && gqq > T(0) && fabs(gpq) > tol_in * sqrt(gpp) * sqrt(gqq)) {
-        // closest-to-identity rotation (reading c-3)
-        if constexpr (sizeof(T) == 4) {
-            // fp32 stage (an initial guess refined in fp64): MUFU rsqrt / fast
-            // division, a few ulp from the IEEE formulas (DESIGN.md c-14)
-            const float zeta = __fdividef(gqq - gpp, 2.0f * gpq);
-            if (fabsf(zeta) > RealTraits<float>::rsqrt_u) {
-                t = __fdividef(0.5f, zeta);
-            } else {
-                const float r1 = fmaf(zeta, zeta, 1.0f);
-                const float sq = r1 * rsqrtf(r1);
-                t = __fdividef(zeta >= 0.0f ? 1.0f : -1.0f, fabsf(zeta) + sq);
-            }
-            const float r2 = fmaf(t, t, 1.0f);
-            c = rsqrtf(r2);
-            sn = t * c;
-            cm1 = -__fdividef(t * t * c, 1.0f + r2 * c);
-        } else {
-            // fp64: the same formulas with MUFU reciprocal / rsqrt refined by two Newton steps (<= 2 ulp
-            // from the IEEE quotients and roots; the refinement's accuracy is set by the outer fp64
-            // Gram and update, the rotation only has to be orthogonal to u64: c^2 + s^2 = 1 + O(u64))
-            const double zeta = (gqq - gpp) * rcp_nr(2.0 * gpq);
-            if (fabs(zeta) > RealTraits<double>::rsqrt_u) {
-                t = 0.5 * rcp_nr(zeta);
-            } else {
-                const double r1 = fma(zeta, zeta, 1.0);
-                const double sq = r1 * rsqrt_nr(r1);
-                t = (zeta >= 0.0 ? 1.0 : -1.0) * rcp_nr(fabs(zeta) + sq);
-            }
-            const double r2 = fma(t, t, 1.0);
-            c = rsqrt_nr(r2);
-            sn = t * c;
-            cm1 = -(t * t * c) * rcp_nr(1.0 + r2 * c);
-        }
-        active = 1;
-    }
+    T c, sn, t, cm1;
+    const int active = rotation_from<T>(q < w, gpp, gqq, gpq, tol_in, c, sn, t, cm1);
     Rot4<T> r4;
     r4.c = c;
     r4.s = sn;
@@ -555,30 +560,30 @@ __device__ int inner_solve_dev(InnerSmem<T, W>& sm, int w, T tol_in, int max_inn
 // ------------------------------------------------------------------------
 __device__ long long* g_solve_dbg = nullptr;   // phase clocks of k_pair_solve, CTA 0 (MPJSVD_SOLVE_TIMING=1)
 
-template <typename T, int W>
-__global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) {
-    long long* sdbg = (blockIdx.x == 0 && threadIdx.x == 0) ? g_solve_dbg : nullptr;
-    const long long c0 = sdbg ? clock64() : 0;
-    constexpr int GS = InnerSmem<T, W>::GS;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
-    const int pair = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    if (a.pdl) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // the update may start
-    const int w = a.pd[pair].w0 + a.pd[pair].w1;
-    if (pair_unchanged(a, a.pd[pair])) {
-        // same Gram as one sweep ago: same metric, no rotation (exact skip)
-        if (tid == 0) {
-            atomic_max_nonneg(a.sweep_off, a.pair_off[pair]);
-            atomicAdd(a.sweep_skip, 1);
-            a.flag[pair] = 0;
-            if (a.dlist) {
-                __threadfence();
-                const int pos = atomicAdd(a.dctr, 1);
-                st_release_gpu(a.dlist + pos, pair);
-            }
+// ---- pieces of a pair solve (k_pair_solve) ------------------------------------------------------------
+// exact skip: the pair's Gram equals the one of a sweep ago (same metric, no rotation); returns true if skipped
+template <typename T>
+__device__ __forceinline__ bool solve_skip_unchanged(const JacobiRound<T>& a, int pair) {
+    if (!pair_unchanged(a, a.pd[pair])) return false;
+    if (threadIdx.x == 0) {
+        atomic_max_nonneg(a.sweep_off, a.pair_off[pair]);
+        atomicAdd(a.sweep_skip, 1);
+        a.flag[pair] = 0;
+        if (a.dlist) {
+            __threadfence();
+            const int pos = atomicAdd(a.dctr, 1);
+            st_release_gpu(a.dlist + pos, pair);
         }
-        return;
     }
+    return true;
+}
+
+// the pair's Gram: wait for its row-slab partials (gram_pdl), fixed-order reduction into G (full symmetric,
+// row stride GS), pair metric max_{p<q} |g_pq| / (sqrt(g_pp) sqrt(g_qq)), flags / sweep statistics; returns
+// whether the pair rotates.  dsq: w scratch values, red: 32.
+template <typename T, int W, int NT>
+__device__ __forceinline__ bool solve_prologue(const JacobiRound<T>& a, int pair, int w, T* G, int GS, T* dsq, T* red) {
+    const int tid = threadIdx.x;
     if (a.gram_pdl) {
         // launched beside the Gram: wait until every row slab of this pair has been counted
         if (tid == 0) {
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
     {
         // each thread owns up to RE elements; the split loop is outermost so that the RE loads of one split
         // are in flight together (same summation order per element: split 0, 1, ...)
-        constexpr int RE = (W * W + inner_nt<W>() - 1) / inner_nt<W>();
+        constexpr int RE = (W * W + NT - 1) / NT;
         T acc[RE];
 #pragma unroll
         for (int u = 0; u < RE; ++u) acc[u] = T(0);
@@ -606,38 +611,35 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
             const T* ps = part + (long long)sp * (W * W);
 #pragma unroll
             for (int u = 0; u < RE; ++u) {
-                const int e = tid + u * nt;
+                const int e = tid + u * NT;
                 if (e < W * W) acc[u] += __ldcg(ps + e);
             }
         }
 #pragma unroll
         for (int u = 0; u < RE; ++u) {
-            const int e = tid + u * nt;
+            const int e = tid + u * NT;
             const int p = e / W, q = e - (e / W) * W;
             if (e < W * W && p < w && q < w && p >= q) {      // partials hold (at least) the lower triangle
-                sm.G[p * GS + q] = acc[u];
-                sm.G[q * GS + p] = acc[u];
+                G[p * GS + q] = acc[u];
+                G[q * GS + p] = acc[u];
             }
         }
     }
     __syncthreads();
-    // pair metric: max_{p<q} |g_pq| / (sqrt(g_pp) sqrt(g_qq))
-    T* dsq = sm.E;   // scratch (E is initialised inside the inner solve)
-    for (int p = tid; p < w; p += nt) dsq[p] = sqrt(sm.G[p * GS + p]);
+    for (int p = tid; p < w; p += NT) dsq[p] = sqrt(G[p * GS + p]);
     __syncthreads();
     T off = T(0);
-    for (int e = tid; e < w * w; e += nt) {
+    for (int e = tid; e < w * w; e += NT) {
         const int p = e / w, q = e - (e / w) * w;
         if (p < q) {
-            T gpp = sm.G[p * GS + p], gqq = sm.G[q * GS + q];
+            T gpp = G[p * GS + p], gqq = G[q * GS + q];
             if (gpp > T(0) && gqq > T(0)) {
-                T v = fabs(sm.G[p * GS + q]) / (dsq[p] * dsq[q]);
+                T v = fabs(G[p * GS + q]) / (dsq[p] * dsq[q]);
                 off = v > off ? v : off;
             }
         }
     }
-    off = block_max(off, sm.red);
-    const long long c1 = sdbg ? clock64() : 0;
+    off = block_max(off, red);
     const bool rotate = off > a.tol;
     if (tid == 0) {
         atomic_max_nonneg(a.sweep_off, (double)off);
@@ -651,29 +653,51 @@ __global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) 
             }
         }
     }
-    if (rotate) {
-        int used = 0;
-        inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
-        if (sdbg) { sdbg[1] += clock64() - c1; sdbg[3] += 1; }
-        if (tid == 0) {
-            atomicMax(a.sweep_inner, used);
-            atomicAdd(a.sweep_inner + 1, used);
-        }
-        T* E = a.E + (long long)pair * (W * W);
-        for (int e = tid; e < W * W; e += nt) {
-            const int k = e / W, j = e - (e / W) * W;
-            E[e] = (k < w && j < w) ? sm.E[InnerSmem<T, W>::eidx(k, j)] : T(0);   // E[k][j] row-major
-        }
+    return rotate;
+}
+
+// inner-solve statistics and publication of the solved pair (E and flag complete)
+template <typename T>
+__device__ __forceinline__ void solve_epilogue(const JacobiRound<T>& a, int pair, bool rotate, int used) {
+    if (rotate && threadIdx.x == 0) {
+        atomicMax(a.sweep_inner, used);
+        atomicAdd(a.sweep_inner + 1, used);
     }
-    if (sdbg) { sdbg[0] += c1 - c0; sdbg[2] += clock64() - c0; sdbg[4] += 1; }
-    if (a.dlist) {                 // publish: E and flag of this pair are complete
+    if (a.dlist) {
         __syncthreads();
-        if (tid == 0) {
+        if (threadIdx.x == 0) {
             __threadfence();
             const int pos = atomicAdd(a.dctr, 1);
             st_release_gpu(a.dlist + pos, pair);
         }
     }
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(inner_nt<W>()) k_pair_solve(JacobiRound<T> a) {
+    long long* sdbg = (blockIdx.x == 0 && threadIdx.x == 0) ? g_solve_dbg : nullptr;
+    const long long c0 = sdbg ? clock64() : 0;
+    constexpr int GS = InnerSmem<T, W>::GS;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    InnerSmem<T, W>& sm = *reinterpret_cast<InnerSmem<T, W>*>(smraw);
+    const int pair = blockIdx.x, tid = threadIdx.x;
+    if (a.pdl) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // the update may start
+    const int w = a.pd[pair].w0 + a.pd[pair].w1;
+    if (solve_skip_unchanged(a, pair)) return;
+    const bool rotate = solve_prologue<T, W, inner_nt<W>()>(a, pair, w, sm.G, GS, sm.E, sm.red);   // E: scratch
+    const long long c1 = sdbg ? clock64() : 0;
+    int used = 0;
+    if (rotate) {
+        inner_solve_dev<T, W>(sm, w, a.tol_in, a.max_inner, &used);
+        if (sdbg) { sdbg[1] += clock64() - c1; sdbg[3] += 1; }
+        T* E = a.E + (long long)pair * (W * W);
+        for (int e = tid; e < W * W; e += blockDim.x) {
+            const int k = e / W, j = e - (e / W) * W;
+            E[e] = (k < w && j < w) ? sm.E[InnerSmem<T, W>::eidx(k, j)] : T(0);   // E[k][j] row-major
+        }
+    }
+    if (sdbg) { sdbg[0] += c1 - c0; sdbg[2] += clock64() - c0; sdbg[4] += 1; }
+    solve_epilogue(a, pair, rotate, used);
 }
 
 // ------------------------------------------------------------------------
@@ -1406,8 +1430,8 @@ solve:
     const bool overlap = a.pdl && (sizeof(T) == 8 || (W == 64 && a.use_tc));
     const char* both = sizeof(T) == 4 ? "pair_solve_update_f32" : "pair_solve_update_f64";
     if (hook) hook->begin(hook->ctx, overlap ? both : KName<T>::solve);
-    if (a.gram_pdl) {
-        // programmatic dependent of the Gram (per-pair counters, k_pair_solve)
+    {
+        // a programmatic dependent of the Gram under gram_pdl (per-pair counters, solve_prologue)
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)a.npairs);
         cfg.blockDim = dim3(inner_nt<W>());
@@ -1417,14 +1441,12 @@ solve:
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = a.gram_pdl ? 1 : 0;
         cudaError_t e = cudaLaunchKernelEx(&cfg, k_pair_solve<T, W>, a);
         if (e != cudaSuccess) {
             mpj_record_cuda_error(e, "cudaLaunchKernelEx(solve)", __FILE__, __LINE__);
             return -4;
         }
-    } else {
-        k_pair_solve<T, W><<<a.npairs, inner_nt<W>(), sms, st>>>(a);
     }
     MPJ_LAUNCHED();
     if (overlap) {
