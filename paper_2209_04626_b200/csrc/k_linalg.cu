@@ -38,13 +38,16 @@ __device__ __forceinline__ void cpa16(double* dst, const double* src, int valid_
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src), "r"(sz));
 }
 
-// Stage a (rows x 16) k-slab of op(A) (rows = M direction) into S[k][r].
-// contiguous: op(A) element (r, k) at P[r + k*ld] (r fast); else at P[k + r*ld].
-template <int ROWS, int SROW>
-__device__ __forceinline__ void gm_stage(double* S, const double* __restrict__ P, long long ld, bool r_fast,
-                                         bool vec_ok, long long r0, long long k0, long long R, long long K) {
+// Stage a (rows x 16) k-slab of op(A) (rows = M direction).  KF = false: the operand is r-fast in memory
+// (element (r, k) at P[r + k*ld]) and lands k-major, S[k][r] (row stride SROW); KF = true: it is k-fast
+// (element (r, k) at P[k + r*ld]) and lands r-major, S[r][k] (row stride GM_SK), so that both layouts move
+// 16-byte runs (round 1 scattered k-fast operands into S[k][r] with one 8-byte cp.async per element).
+constexpr int GM_SK = GM_BK + 4;   // = 4 mod 16 doubles: conflict-free fragment loads along k
+template <int ROWS, int SROW, bool KF>
+__device__ __forceinline__ void gm_stage(double* S, const double* __restrict__ P, long long ld, bool vec_ok,
+                                         long long r0, long long k0, long long R, long long K) {
     const int tid = threadIdx.x;
-    if (r_fast && vec_ok) {
+    if (!KF && vec_ok) {
         // 16-byte chunks along r: ROWS/2 chunks per k
         for (int v = tid; v < GM_BK * (ROWS / 2); v += 256) {
             const int kk = v / (ROWS / 2), rr = (v % (ROWS / 2)) * 2;
@@ -53,32 +56,48 @@ __device__ __forceinline__ void gm_stage(double* S, const double* __restrict__ P
             const double* src = valid ? P + gr + gk * ld : P;
             cpa16(&S[kk * SROW + rr], src, valid);
         }
-    } else if (r_fast) {
+    } else if (!KF) {
         for (int v = tid; v < GM_BK * ROWS; v += 256) {
             const int kk = v / ROWS, rr = v % ROWS;
             const long long gr = r0 + rr, gk = k0 + kk;
             const bool valid = gr < R && gk < K;
             cpa8(&S[kk * SROW + rr], valid ? P + gr + gk * ld : P, valid);
         }
+    } else if (vec_ok) {
+        // 16-byte chunks along k: GM_BK/2 chunks per row
+        for (int v = tid; v < ROWS * (GM_BK / 2); v += 256) {
+            const int rr = v / (GM_BK / 2), kk = (v % (GM_BK / 2)) * 2;
+            const long long gr = r0 + rr, gk = k0 + kk;
+            int valid = (gr < R) ? (int)max(0LL, min(2LL, K - gk)) : 0;
+            const double* src = valid ? P + gk + gr * ld : P;
+            cpa16(&S[rr * GM_SK + kk], src, valid);
+        }
     } else {
-        // k fast in memory: consecutive threads walk k (coalesced), scatter into S[k][r]
         for (int v = tid; v < GM_BK * ROWS; v += 256) {
             const int kk = v % GM_BK, rr = v / GM_BK;
             const long long gr = r0 + rr, gk = k0 + kk;
             const bool valid = gr < R && gk < K;
-            cpa8(&S[kk * SROW + rr], valid ? P + gk + gr * ld : P, valid);
+            cpa8(&S[rr * GM_SK + kk], valid ? P + gk + gr * ld : P, valid);
         }
     }
 }
 
-__global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, long long N, long long K,
+template <bool AKF, bool BKF>
+constexpr size_t gemm_smem() {
+    return sizeof(double) * (size_t)GM_ST * ((AKF ? GM_BM * GM_SK : GM_BK * GM_SA) + (BKF ? GM_BN * GM_SK : GM_BK * GM_SB));
+}
+
+// AKF: op(A) is k-fast in memory (ta == 1); BKF: op(B) is k-fast (tb == 0)
+template <bool AKF, bool BKF>
+__global__ void __launch_bounds__(256) k_gemm_f64(long long M, long long N, long long K,
                                                   double alpha, const double* __restrict__ A, long long lda,
                                                   const double* __restrict__ B, long long ldb, double beta,
                                                   double* __restrict__ C, long long ldc, int vec_a, int vec_b,
                                                   long long kchunk, double* __restrict__ part, int shape) {
+    constexpr int ASZ = AKF ? GM_BM * GM_SK : GM_BK * GM_SA, BSZ = BKF ? GM_BN * GM_SK : GM_BK * GM_SB;
     extern __shared__ __align__(16) unsigned char gm_smem[];
-    double* As = reinterpret_cast<double*>(gm_smem);                  // [ST][BK][SA]
-    double* Bs = As + GM_ST * GM_BK * GM_SA;                          // [ST][BK][SB]
+    double* As = reinterpret_cast<double*>(gm_smem);                  // [ST][ASZ]
+    double* Bs = As + GM_ST * ASZ;                                    // [ST][BSZ]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;                          // 4 x 2 warps
     const long long i0 = (long long)blockIdx.x * GM_BM, j0 = (long long)blockIdx.y * GM_BN;
@@ -89,16 +108,16 @@ __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, l
     // shape bit 2: op(A) is upper triangular -> op(A)(i, k) = 0 for k < i: K range starts at the tile's first row
     if ((shape & 4) && kchunk == 0) {
         const long long k0 = min(K, (i0 / GM_BK) * GM_BK);
-        if (ta == 0) A += k0 * lda; else A += k0;
-        if (tb == 0) B += k0; else B += k0 * ldb;
+        if (!AKF) A += k0 * lda; else A += k0;
+        if (BKF) B += k0; else B += k0 * ldb;
         K -= k0;
     }
     // split-K: this CTA covers k in [kb, kb + kchunk) of op(A)/op(B); partial results go to part
     const long long kb = (long long)blockIdx.z * kchunk;
     if (kchunk > 0) {
         const long long ke = min(K, kb + kchunk);
-        if (ta == 0) A += kb * lda; else A += kb;
-        if (tb == 0) B += kb; else B += kb * ldb;
+        if (!AKF) A += kb * lda; else A += kb;
+        if (BKF) B += kb; else B += kb * ldb;
         K = ke - kb;
     }
     double acc[4][4][2];
@@ -110,8 +129,8 @@ __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, l
     // op(A) (i,k): ta == 0 -> A[i + k lda] (i fast); ta == 1 -> A[k + i lda]
     // op(B) (k,j): tb == 0 -> B[k + j ldb] (k fast); tb == 1 -> B[j + k ldb] (j fast)
     auto stage = [&](long long kt, int st) {
-        gm_stage<GM_BM, GM_SA>(As + st * GM_BK * GM_SA, A, lda, ta == 0, vec_a, i0, kt * GM_BK, M, K);
-        gm_stage<GM_BN, GM_SB>(Bs + st * GM_BK * GM_SB, B, ldb, tb == 1, vec_b, j0, kt * GM_BK, N, K);
+        gm_stage<GM_BM, GM_SA, AKF>(As + st * ASZ, A, lda, vec_a, i0, kt * GM_BK, M, K);
+        gm_stage<GM_BN, GM_SB, BKF>(Bs + st * BSZ, B, ldb, vec_b, j0, kt * GM_BK, N, K);
     };
 #pragma unroll
     for (int s0 = 0; s0 < GM_ST - 1; ++s0) {
@@ -123,15 +142,22 @@ __global__ void __launch_bounds__(256) k_gemm_f64(int ta, int tb, long long M, l
         __syncthreads();
         if (kt + GM_ST - 1 < nk) stage(kt + GM_ST - 1, (int)((kt + GM_ST - 1) % GM_ST));
         asm volatile("cp.async.commit_group;\n" ::);
-        const double* as = As + (kt % GM_ST) * GM_BK * GM_SA;
-        const double* bs = Bs + (kt % GM_ST) * GM_BK * GM_SB;
+        const double* as = As + (kt % GM_ST) * ASZ;
+        const double* bs = Bs + (kt % GM_ST) * BSZ;
 #pragma unroll
         for (int k0 = 0; k0 < GM_BK; k0 += 4) {
             double fa[4], fb[4];
+            const int kq = k0 + (lane & 3);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) fa[i] = as[(k0 + (lane & 3)) * GM_SA + wm * 32 + 8 * i + (lane >> 2)];
+            for (int i = 0; i < 4; ++i) {
+                const int m = wm * 32 + 8 * i + (lane >> 2);
+                fa[i] = AKF ? as[m * GM_SK + kq] : as[kq * GM_SA + m];
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) fb[j] = bs[(k0 + (lane & 3)) * GM_SB + wn * 32 + 8 * j + (lane >> 2)];
+            for (int j = 0; j < 4; ++j) {
+                const int nn = wn * 32 + 8 * j + (lane >> 2);
+                fb[j] = BKF ? bs[nn * GM_SK + kq] : bs[kq * GM_SB + nn];
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -180,11 +206,12 @@ void gemm_set_workspace(double* ws, size_t elems) {
     g_gemm_ws_elems = elems;
 }
 
-int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
-                const double* B, long long ldb, double beta, double* C, long long ldc, int shape, cudaStream_t st) {
-    if (M <= 0 || N <= 0) return 0;
-    const size_t smem = sizeof(double) * (size_t)GM_ST * GM_BK * (GM_SA + GM_SB);
-    MPJ_CUDA_TRY(set_smem(k_gemm_f64, smem));
+template <bool AKF, bool BKF>
+static int gemm_launch(long long M, long long N, long long K, double alpha, const double* A, long long lda,
+                       const double* B, long long ldb, double beta, double* C, long long ldc, int shape,
+                       cudaStream_t st) {
+    constexpr size_t smem = gemm_smem<AKF, BKF>();
+    MPJ_CUDA_TRY(set_smem(k_gemm_f64<AKF, BKF>, smem));
     const int vec_a = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
     const int vec_b = (ldb % 2 == 0) && (((uintptr_t)B & 15) == 0);
     dim3 grid((unsigned)ceil_div(M, GM_BM), (unsigned)ceil_div(N, GM_BN));
@@ -201,20 +228,29 @@ int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double al
         const long long kchunk = round_up(ceil_div(K, nsplit), GM_BK);
         nsplit = ceil_div(K, kchunk);
         grid.z = (unsigned)nsplit;
-        k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
-                                            kchunk, g_gemm_ws, 0);
+        k_gemm_f64<AKF, BKF><<<grid, 256, smem, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
+                                                      kchunk, g_gemm_ws, 0);
         MPJ_LAUNCHED();
         long long gr = ceil_div(M * N, 256);
         if (gr > 4096) gr = 4096;
         k_splitk_reduce<<<(unsigned)gr, 256, 0, st>>>(g_gemm_ws, (int)nsplit, M, N, alpha, beta, C, ldc);
         MPJ_LAUNCHED();
     } else {
-        k_gemm_f64<<<grid, 256, smem, st>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
-                                            0, nullptr, shape);
+        k_gemm_f64<AKF, BKF><<<grid, 256, smem, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, vec_a, vec_b,
+                                                      0, nullptr, shape);
         MPJ_LAUNCHED();
     }
     MPJ_CUDA_TRY(cudaGetLastError());
     return 0;
+}
+
+int gemm_f64_ex(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
+                const double* B, long long ldb, double beta, double* C, long long ldc, int shape, cudaStream_t st) {
+    if (M <= 0 || N <= 0) return 0;
+    if (ta == 0 && tb == 1) return gemm_launch<false, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, shape, st);
+    if (ta == 0 && tb == 0) return gemm_launch<false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, shape, st);
+    if (ta == 1 && tb == 1) return gemm_launch<true, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, shape, st);
+    return gemm_launch<true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, shape, st);
 }
 
 int gemm_f64(int ta, int tb, long long M, long long N, long long K, double alpha, const double* A, long long lda,
