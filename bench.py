@@ -286,8 +286,10 @@ def roofline_for(kernel: str, ms_total: float, launches: int, work: dict, peaks:
     elif bound == "alu64" and flops is not None:
         ach = flops / sec / 1e12
         peak = micro.get("dmma_tflops") or micro.get("dfma_tflops") or (148 * 64 * 2 * 1.965e9 / 1e12)
-        base.update({"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                     "peak_source": "measured DMMA (mma.sync f64) microbenchmark, profiles/peaks.json"})
+        # FP64 DMMA (mma.sync m8n8k4 f64) is the tensor pipe's fp64 path on sm_100a (no tcgen05 f64 kind)
+        base.update({"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "peak_source": "measured DMMA (mma.sync f64) microbenchmark, profiles/peaks.json "
+                                    "(MEASURED_PEAKS.json has no fp64 figure)"})
     elif bound == "alu32" and flops is not None:
         ach = flops / sec / 1e12
         peak = micro.get("ffma_tflops") or (148 * 128 * 2 * 1.965e9 / 1e12)

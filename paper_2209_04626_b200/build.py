@@ -41,6 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                     "-I", os.path.join(ROOT, "include"), "-I", CSRC]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    # experiment builds only (tools/): extra compile-time definitions, e.g. "-DMPJ_GM_BK=32"
+    flags += os.environ.get("MPJSVD_NVCC_FLAGS", "").split()
     objs = []
     procs = []
     for src in SOURCES:

@@ -19,7 +19,13 @@ namespace mpj {
 // copied with 16-byte cp.async, everything else (transposed operands,
 // ragged edges) with 8-byte cp.async; out-of-range elements are zero-filled.
 // ------------------------------------------------------------------------
-constexpr int GM_BM = 128, GM_BN = 64, GM_BK = 16, GM_ST = 3;
+#ifndef MPJ_GM_BK
+#define MPJ_GM_BK 16
+#endif
+#ifndef MPJ_GM_ST
+#define MPJ_GM_ST 3
+#endif
+constexpr int GM_BM = 128, GM_BN = 64, GM_BK = MPJ_GM_BK, GM_ST = MPJ_GM_ST;
 constexpr int GM_SA = GM_BM + 4, GM_SB = GM_BN + 4;
 
 __device__ __forceinline__ void dmma884_l(double& d0, double& d1, double a, double b) {
