@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MPJSVD_VERSION 130
+#define MPJSVD_VERSION 140   /* 1.4: options qrp_panel_stages, gram_pdl */
 #define MPJSVD_COMM_ID_BYTES 128
 
 /* return codes */
