@@ -1034,15 +1034,24 @@ __global__ void __launch_bounds__(G32_NT, 3) k_pair_gram_f32t(JacobiRound<float>
 // runs K = w/4 DMMA k-steps; the result is added in place into the staged
 // tile and stored back with coalesced 16-byte stores.
 // ------------------------------------------------------------------------
-constexpr int UD_NT = 256, UD_RC = 64, UD_TPC = 16;   // 2 CTAs per SM (smem ~104 KB each)
+#ifndef MPJ_UD_RC
+#define MPJ_UD_RC 64
+#endif
+#ifndef MPJ_UD_MINB
+#define MPJ_UD_MINB 2
+#endif
+constexpr int UD_NT = 256, UD_RC = MPJ_UD_RC, UD_TPC = 1024 / MPJ_UD_RC;   // 2 CTAs per SM (smem ~104 KB each)
+constexpr int UD_MINB = MPJ_UD_MINB;
+template <int W> constexpr int ud_rc() { return W >= 64 ? UD_RC : 64; }   // 8 rows per row-group warp at least
+template <int W> constexpr int ud_tpc() { return 1024 / ud_rc<W>(); }
 template <int W>
 constexpr size_t update_dmma_smem() {
-    return sizeof(double) * ((size_t)2 * W * (UD_RC + 4) + (size_t)W * (W + 4)) + sizeof(double*) * W;
+    return sizeof(double) * ((size_t)2 * W * (ud_rc<W>() + 4) + (size_t)W * (W + 4)) + sizeof(double*) * W;
 }
 
 template <int W>
-__global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma(JacobiRound<double> a) {
-    constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
+__global__ void __launch_bounds__(UD_NT, UD_MINB) k_pair_update_dmma(JacobiRound<double> a) {
+    constexpr int RC = ud_rc<W>(), SW = RC + 4, SE = W + 4, UD_TPC = ud_tpc<W>();
     constexpr int WC = W >= 64 ? 2 : 1, WR = (UD_NT / 32) / WC;
     constexpr int TM = RC / WR / 8, TN = W / WC / 8;
     extern __shared__ __align__(16) unsigned char upd_smem[];
@@ -1136,8 +1145,8 @@ __global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma(JacobiRound<doubl
 // published pair (k_pair_solve) and skips pairs that did not rotate.
 // ------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(UD_NT, 2) k_pair_update_dmma_pdl(JacobiRound<double> a, int ngroups) {
-    constexpr int RC = UD_RC, SW = RC + 4, SE = W + 4;
+__global__ void __launch_bounds__(UD_NT, UD_MINB) k_pair_update_dmma_pdl(JacobiRound<double> a, int ngroups) {
+    constexpr int RC = ud_rc<W>(), SW = RC + 4, SE = W + 4, UD_TPC = ud_tpc<W>();
     constexpr int WC = W >= 64 ? 2 : 1, WR = (UD_NT / 32) / WC;
     constexpr int TM = RC / WR / 8, TN = W / WC / 8;
     extern __shared__ __align__(16) unsigned char upd_smem[];
@@ -1261,10 +1270,10 @@ static int launch_update_dmma_pdl(const JacobiRound<double>& a, cudaStream_t st)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long rows_pad = a.m_pad > a.nv_pad ? a.m_pad : a.nv_pad;
-    const int ngroups = (int)((rows_pad + (long long)UD_TPC * UD_RC - 1) / ((long long)UD_TPC * UD_RC));
+    const int ngroups = (int)((rows_pad + 1023) / 1024);
     const long long items = (long long)a.npairs * 2 * ngroups;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(items < 2 * nsm ? items : 2 * nsm));   // 2 CTAs per SM
+    cfg.gridDim = dim3((unsigned)(items < UD_MINB * nsm ? items : UD_MINB * nsm));   // UD_MINB CTAs per SM
     cfg.blockDim = dim3(UD_NT);
     cfg.dynamicSmemBytes = dsm;
     cfg.stream = st;
@@ -1471,7 +1480,7 @@ solve:
     if constexpr (sizeof(T) == 8) {
         const size_t dsm = update_dmma_smem<W>();
         MPJ_CUDA_TRY(set_smem(k_pair_update_dmma<W>, (size_t)(dsm)));
-        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, (long long)UD_RC * UD_TPC), a.npairs, a.has_v ? 2 : 1),
+        k_pair_update_dmma<W><<<dim3((unsigned)ceil_div(rows_pad, 1024LL), a.npairs, a.has_v ? 2 : 1),
                                 UD_NT, dsm, st>>>(a);
     } else if (W == 64 && a.use_tc) {
         if constexpr (sizeof(T) == 4) launch_update_tc(a, st);
