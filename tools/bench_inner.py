@@ -36,5 +36,22 @@ def main():
               flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def phases():
+    """Per-warp-group end clocks of an inner round (diag_timing bit 8): critical warps, rotation warp, slowest
+    other G warp, slowest E warp, cycles from the round start (the round ends at the CTA barrier after all)."""
+    rng = np.random.default_rng(0)
+    count, w = 128, 64
+    for dtype in (torch.float32, torch.float64):
+        x = torch.from_numpy(rng.standard_normal((count, 512, w))).to(dtype).cuda()
+        g = (x.transpose(1, 2) @ x).contiguous()
+        h = mp.Handle(stream=torch.cuda.current_stream().cuda_stream, diag_timing=8)
+        mp.inner_solve(g, 1e-30, max_inner=2, handle=h)
+        torch.cuda.synchronize()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "phases":
+    phases()
