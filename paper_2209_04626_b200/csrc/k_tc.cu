@@ -649,6 +649,128 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_gram_sw(JacobiRound<float> a,
     if (warp == 0) tc::tmem_free<64>(tmem);
 }
 
+// k_pair_gram_sw_ws: k_pair_gram_sw with the work split by warps instead of a CTA barrier per tile.  Warp 0
+// (one lane) issues the TMA boxes and the MMAs; warps 1..4 (128 threads) write the lo parts of each stage as
+// soon as its boxes land and arrive on the stage's lo barrier (128 arrivals).  The lo warps run up to GM_ST
+// tiles ahead of the MMA lane, whose waits (lo parts, the previous tile's MMAs before a refill) no longer
+// hold them.  Same operand layout, MMA sequence and epilogue as k_pair_gram_sw: bitwise equal.
+template <int GM_ST, int MINB>
+__global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ws(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
+    constexpr int KT = 32, NT = 160;
+    constexpr int STAGE = 128 * KT * 4;                 // 16 KB: raw I | raw J | lo I | lo J, 4 KB each
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    reset_publication(a);
+    gram_pdl_begin(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
+    extern __shared__ __align__(1024) unsigned char gs_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gs_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], lo_ready[GM_ST], fin;
+    __shared__ uint32_t tmem_base;
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
+    const bool hasJ = pd.w1 > 0;
+    const uint32_t tx = hasJ ? 2u * 32u * KT * 4u : 32u * KT * 4u;
+    if (warp == 0) tc::tmem_alloc<64>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < GM_ST; ++s) {
+            tc::mbar_init(&full[s]);
+            tc::mbar_init(&done[s]);
+            mbar_init_n(&lo_ready[s], 128);
+        }
+        tc::mbar_init(&fin);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (!hasJ) {   // bye pair: M-rows 32..63 (raw J) stay zero in every stage
+        for (int s = 0; s < GM_ST; ++s)
+            for (int i = tid; i < 4096 / 16; i += NT)
+                reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4096)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tc::fence_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;
+    const long long rbeg = (long long)split * a.rows_per_split;
+    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const int ntile = (int)((rend - rbeg + KT - 1) / KT);
+    const uint32_t sbase = tc::smem_u32(sm);
+    auto issue = [&](int t) {
+        const int s = t % GM_ST;
+        const int r0 = (int)(rbeg + (long long)t * KT);
+        mbar_expect_tx(&full[s], tx);
+        tma_load_2d_g(sbase + (uint32_t)(s * STAGE), &smap, r0, cI, &full[s]);
+        if (hasJ) tma_load_2d_g(sbase + (uint32_t)(s * STAGE) + 4096, &smap, r0, cJ, &full[s]);
+    };
+    if (warp == 0) {
+        if (tid == 0) {
+            for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
+            for (int t = 0; t < ntile; ++t) {
+                const int s = t % GM_ST;
+                tc::mbar_wait(&lo_ready[s], (uint32_t)((t / GM_ST) & 1));
+                tc::fence_after();
+                const uint32_t base = sbase + (uint32_t)(s * STAGE);
+#pragma unroll
+                for (int ks = 0; ks < KT / 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(base + ks * 32);
+                    tc::mma(tmem, ad, ad, idesc, (t > 0 || ks > 0) ? 1u : 0u);
+                }
+                tc::commit(&done[s]);
+                if (t >= 1 && t - 1 + GM_ST < ntile) {
+                    const int sp = (t - 1) % GM_ST;
+                    tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
+                    issue(t - 1 + GM_ST);
+                }
+            }
+            if (ntile > 0) tc::commit(&fin);
+        }
+        __syncwarp();
+    } else {
+        const int lt = tid - 32;                  // 0..127
+        for (int t = 0; t < ntile; ++t) {
+            const int s = t % GM_ST;
+            unsigned char* st = sm + (size_t)s * STAGE;
+            tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
+#pragma unroll
+            for (int u = 0; u < 512 / 128; ++u) {     // 512 raw float4 chunks, linear
+                const int f = lt + 128 * u;
+                const float4 x = reinterpret_cast<const float4*>(st)[f];
+                reinterpret_cast<float4*>(st + 8192)[f] = tc::lo4(x, tc::hi4(x));
+            }
+            tc::fence_async_smem();
+            mbar_arrive(&lo_ready[s]);
+        }
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);
+    if (ntile > 0) {
+        tc::mbar_wait(&fin, 0);
+        tc::fence_after();
+        __syncthreads();                           // every stage consumed before red (stage 0) is overwritten
+        if (tid < 128) {                           // TMEM lanes 0..127: warps 0..3
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
+        }
+    } else {
+        for (int e = tid; e < 64 * 64; e += NT) out[e] = 0.f;
+    }
+    gram_pdl_end(a, pair);
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<64>(tmem);
+}
+
 // rows per stage of the TMA Gram (MPJSVD_GRAM_KT = 32 or 64): KT = 64 -> 3 x 32 KB stages, 2 CTAs per SM;
 // KT = 32 -> 3 x 16 KB stages, 4 CTAs per SM
 // Default by row count (measured on B200): 32 for >= 6144 rows (C5: Gram 237 -> 217 ms), 64 below (C3: 33 vs 35 ms)
@@ -1161,7 +1283,7 @@ int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long r
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
-    if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 15) {
+    if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 17) {
         const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
         switch (a.gram_variant) {
             case 11:
@@ -1183,6 +1305,14 @@ int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
             case 15:
                 MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<3, 4, 256>, gram_tma_smem<32, 3>()));
                 k_pair_gram_sw<3, 4, 256><<<dim3(a.nsplit, a.npairs), 256, gram_tma_smem<32, 3>(), st>>>(a, sm);
+                break;
+            case 16:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ws<4, 3>, gram_tma_smem<32, 4>()));
+                k_pair_gram_sw_ws<4, 3><<<dim3(a.nsplit, a.npairs), 160, gram_tma_smem<32, 4>(), st>>>(a, sm);
+                break;
+            case 17:
+                MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ws<6, 2>, gram_tma_smem<32, 6>()));
+                k_pair_gram_sw_ws<6, 2><<<dim3(a.nsplit, a.npairs), 160, gram_tma_smem<32, 6>(), st>>>(a, sm);
                 break;
             default:
                 MPJ_CUDA_TRY(set_smem(k_pair_gram_sw<3, 4>, gram_tma_smem<32, 3>()));
@@ -1255,9 +1385,9 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
     if (tma) {
         const int k = gram_tma_kt(rows_pad, kt);
-        if ((variant == 9 && k == 32) || variant == 11 || variant == 14) return 3;
+        if ((variant == 9 && k == 32) || variant == 11 || variant == 14 || variant == 16) return 3;
         if (variant == 10 || variant == 15) return 4;
-        if (variant == 12) return 2;
+        if (variant == 12 || variant == 17) return 2;
         if (variant == 13) return 1;
         return k == 32 ? 4 : 2;
     }
