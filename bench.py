@@ -329,8 +329,10 @@ def algorithmic_work(stats_list, n: int, b: int, world: int = 1, m: int | None =
             if tag == "f32":
                 upd_v = upd if v32 else 0
             else:
+                # the LAST v_sweeps64 sweeps accumulate V (sec. 3.4 V formation: the accumulating stage follows
+                # the refinement without V)
                 vsw = st.get("v_sweeps64", sweeps)
-                upd_v = sum(st["upd_trace64"][:vsw]) if vsw < sweeps else upd
+                upd_v = sum(st["upd_trace64"][sweeps - vsw:sweeps]) if vsw < sweeps else upd
             flops[u] = flops.get(u, 0.0) + (upd + upd_v) * 2.0 * n * w * w
             byts[u] = byts.get(u, 0.0) + (upd + upd_v) * 2 * float(n) * w * s
         flops["qrp_coop"] = flops.get("qrp_coop", 0.0) + 4.0 * n ** 3 / 3

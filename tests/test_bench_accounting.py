@@ -43,7 +43,7 @@ def test_accounting_v_route_and_refine_v():
     # sec. 3.4 V formation: only the last v_sweeps64 sweeps accumulate V
     st = dict(STATS, upd_trace64=[28, 4], v_sweeps64=1)
     work = bench.algorithmic_work([st], n, b)
-    assert work["bytes"]["pair_update_f64"] == ((28 + 4) + 28) * 2 * n * w * 8   # X: both sweeps, V: the first
+    assert work["bytes"]["pair_update_f64"] == ((28 + 4) + 4) * 2 * n * w * 8   # X: both sweeps, V: the last
 
 
 def test_roofline_entry_units():
