@@ -203,6 +203,20 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         const int buf = k & 1;
         const int jj = k % QP_NB;
         tmark(7);
+        // pass 1's row slice and its first rows of the panel's reflectors do not depend on the pivot: their loads
+        // are issued before the pivot is chosen (they overlap warp 0's candidate reduction)
+        constexpr int RS = QP_NT / 32;
+        const long long p1_S = (m - k + G - 1) / G;
+        const long long p1_r0 = k + (long long)cta * p1_S, p1_r1 = min((long long)m, p1_r0 + p1_S);
+        const int p1_lane = tid & 31, p1_wid = tid >> 5;
+        const T* pcl = p1_lane < jj ? a.A + (long long)pcol[p1_lane] * lda : nullptr;
+        const T rvl = p1_lane < jj ? v0p[p1_lane] : T(0);
+        T vpre[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = p1_r0 + p1_wid + u * RS;
+            vpre[u] = (p1_lane < jj && i < p1_r1) ? __ldcg(pcl + i) * rvl : T(0);
+        }
         // ---------------- pivot (largest partial norm, ties -> lowest logical index): warp 0
         if (tid < 32) {
             T bv = -1.0;
@@ -244,21 +258,18 @@ __global__ void __launch_bounds__(QP_NT, 1) k_qrp_lazy(QrpArgs<T> a) {
         // unnormalised x_t times 1/v0_t) so the pending update is a warp reduction and
         // lane t accumulates z_t = sum_i v_t(i) x_i directly.
         {
-            const long long rows = m - k;
-            const long long S = (rows + G - 1) / G;
-            const long long r0 = k + (long long)cta * S, r1 = min((long long)m, r0 + S);
-            const int lane = tid & 31, wid = tid >> 5;
+            const long long r0 = p1_r0, r1 = p1_r1;
+            const int lane = p1_lane, wid = p1_wid;
             T* pc = a.A + (long long)piv * lda;
-            const T* pcl = lane < jj ? a.A + (long long)pcol[lane] * lda : nullptr;
-            const T rvl = lane < jj ? v0p[lane] : 0.0, fl = lane < jj ? fpiv[lane] : 0.0;
+            const T fl = lane < jj ? fpiv[lane] : 0.0;
             T zl = 0.0, sx2 = 0.0;
-            constexpr int RS = QP_NT / 32;
             for (long long ib = r0 + wid; ib < r1; ib += 4 * RS) {
                 T vtv[4], xv[4];
+                const bool first = ib == r0 + wid;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const long long i = ib + u * RS;
-                    vtv[u] = (lane < jj && i < r1) ? __ldcg(pcl + i) * rvl : T(0);
+                    vtv[u] = first ? vpre[u] : ((lane < jj && i < r1) ? __ldcg(pcl + i) * rvl : T(0));
                     xv[u] = i < r1 ? __ldcg(pc + i) : T(0);
                 }
 #pragma unroll
