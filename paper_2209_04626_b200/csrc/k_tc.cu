@@ -1529,14 +1529,24 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<floa
             if constexpr (!TMA) cp_commit();
         }
         const float* Eg = a.E + (long long)pair * (64 * 64);
-        for (int it = tid; it < 64 * 16; it += UT_NT) {
-            const int n = it & 63, k4 = it >> 6;
-            float4 v = make_float4(Eg[(4 * k4 + 0) * 64 + n], Eg[(4 * k4 + 1) * 64 + n], Eg[(4 * k4 + 2) * 64 + n],
-                                   Eg[(4 * k4 + 3) * 64 + n]);
-            const uint32_t o = tc::koff(n, 4 * k4, 64);
-            const float4 h = tc::hi4(v);
-            *reinterpret_cast<float4*>(Bh + o) = h;
-            *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v, h);
+        {
+            // all 16 loads of a thread in flight before the first conversion (one L2 latency per item, not four)
+            constexpr int EQ = 64 * 16 / UT_NT;
+            float4 v[EQ];
+#pragma unroll
+            for (int q = 0; q < EQ; ++q) {
+                const int it = tid + UT_NT * q, n = it & 63, k4 = it >> 6;
+                v[q] = make_float4(__ldcg(Eg + (4 * k4 + 0) * 64 + n), __ldcg(Eg + (4 * k4 + 1) * 64 + n),
+                                   __ldcg(Eg + (4 * k4 + 2) * 64 + n), __ldcg(Eg + (4 * k4 + 3) * 64 + n));
+            }
+#pragma unroll
+            for (int q = 0; q < EQ; ++q) {
+                const int it = tid + UT_NT * q, n = it & 63, k4 = it >> 6;
+                const uint32_t o = tc::koff(n, 4 * k4, 64);
+                const float4 h = tc::hi4(v[q]);
+                *reinterpret_cast<float4*>(Bh + o) = h;
+                *reinterpret_cast<float4*>(Bl + o) = tc::lo4(v[q], h);
+            }
         }
         tc::fence_async_smem();                  // E^T (generic stores) -> visible to the MMA (async proxy)
         auto epilogue = [&](int t) {
