@@ -62,7 +62,7 @@ extern "C" {
 #define MPJSVD_ERR_CUDA (-4)          /* CUDA runtime error (see mpjsvd_last_cuda_error) */
 #define MPJSVD_ERR_NCCL (-5)          /* NCCL missing or failed (see mpjsvd_last_cuda_error) */
 #define MPJSVD_ERR_OUT_OF_MEMORY (-6)
-#define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1, block_cols unsupported, n > 16384 */
+#define MPJSVD_ERR_NOT_SUPPORTED (-7) /* e.g. num_gpus != 1, block_cols unsupported, n > 8192, m > 16384 */
 #define MPJSVD_ERR_BREAKDOWN (-8)     /* finite input, non-finite intermediate (fp32 stage overflow, switch) */
 
 /* path (Alg. 3 gates; reading c-15) */
@@ -194,7 +194,9 @@ void mpjsvd_default_options(mpjsvd_options* opts);
    Returns 0 or a negative error code; *h is NULL on error. */
 int mpjsvd_create(mpjsvd_handle* h, const mpjsvd_options* opts);
 
-/* The SVD.  See the conventions above.  stats may be NULL. */
+/* The SVD.  See the conventions above.  stats may be NULL.  Sizes: n <= 8192 (the column-pivoted QR keeps the
+   n-row pivot column in shared memory and 16 rows per thread in registers), m <= 16384 (m > n: a Householder QR
+   first); larger sizes return MPJSVD_ERR_NOT_SUPPORTED before any work. */
 int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_t lda,
                   double* U, int64_t ldu, double* S, double* V, int64_t ldv,
                   mpjsvd_stats* stats);

@@ -1502,7 +1502,7 @@ int mpjsvd_factor(mpjsvd_handle h, const double* A, int64_t m, int64_t n, int64_
     const bool root = !h->comm.active() || h->comm.rank == 0;
     if (root && (!A || !U || !S || !V)) return MPJSVD_ERR_INVALID_ARG;
     if (n < 2 || m < n || (root && (lda < m || ldu < m || ldv < n))) return MPJSVD_ERR_INVALID_ARG;
-    if (m > 16384 || n > 16384) return MPJSVD_ERR_NOT_SUPPORTED;
+    if (m > 16384 || n > 8192) return MPJSVD_ERR_NOT_SUPPORTED;   // QRP: n <= 16 rows x 512 threads
     if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); return MPJSVD_ERR_CUDA; }
     int rc = factor_impl(h, A, m, n, lda, U, ldu, S, V, ldv, stats);
     if (rc == MPJSVD_ERR_CUDA || rc == MPJSVD_ERR_OUT_OF_MEMORY) cudaGetLastError();

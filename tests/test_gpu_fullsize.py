@@ -130,3 +130,20 @@ def test_fullsize_exact_sigma(mp, handle):
     s = check_props(A, U, S, V)
     assert np.all(np.abs(s - sigma) / sigma <= kappa_bound(sigma, sigma[0] / sigma[-1]))
     assert np.max(np.abs(s - sigma) / sigma) <= 1e-11
+
+
+
+def test_size_limits(mp):
+    """The largest sizes the library accepts run in the full-size tests above (C5: n = 8192, the column-pivoted
+    QR's limit; C4: m = 16384 rows).  One more column, or one more row, is refused with MPJSVD_ERR_NOT_SUPPORTED
+    before any work (no partial run, no device fault), and the handle stays usable."""
+    h = mp.Handle(stream=torch.cuda.current_stream().cuda_stream)
+    for m, n in [(8193, 8193), (16385, 64)]:
+        A = torch.zeros((n, m), dtype=torch.float64, device="cuda").t()
+        with pytest.raises(mp.MpjsvdError) as e:
+            mp.factor(A, handle=h)
+        assert e.value.code == -7
+    a = testmat.config_matrix("C1", 64)
+    U, S, V, st = mp.factor(torch.from_numpy(np.ascontiguousarray(a.T)).t().cuda(), handle=h)
+    assert st["rc"] == 0
+    h.close()
