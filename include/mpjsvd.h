@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MPJSVD_VERSION 140   /* 1.4: options qrp_panel_stages, gram_pdl */
+#define MPJSVD_VERSION 150   /* 1.5: option l2_order */
 #define MPJSVD_COMM_ID_BYTES 128
 
 /* return codes */
@@ -160,6 +160,13 @@ typedef struct {
                                   starts a pair as soon as that pair's row-slab partials are counted (per-pair counters),
                                   overlapping the Gram's last wave; 0: the solve waits for the whole Gram.  Bitwise
                                   equal */
+    int32_t l2_order;          /* fp32 tcgen05 stage, L2-aware traversal (experiment switch): the Gram CTAs take
+                                  interleaved 32-row tiles (all pairs walk the rows top -> bottom in step) and the
+                                  update claims its tile groups bottom group first, so each kernel starts on the rows
+                                  the previous one touched last.  0 (default) off: contiguous row slabs, pair-major
+                                  update (measured on B200: no gain at C5); 1 on; -1 on when fp32 X
+                                  exceeds 96 MB and split_rows = 0.  The interleaved Gram sums its row-slab partials
+                                  over different row sets: results differ from 0 in rounding only (same parity bar) */
 } mpjsvd_options;
 
 typedef struct {

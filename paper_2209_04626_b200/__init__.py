@@ -45,7 +45,7 @@ class Options(C.Structure):
                 ("gram_tma", C.c_int32), ("gram_kt", C.c_int32), ("gram_variant", C.c_int32),
                 ("update_tpc", C.c_int32), ("skip_unchanged", C.c_int32), ("qr_panel_mode", C.c_int32),
                 ("diag_timing", C.c_int32), ("refine_v", C.c_int32), ("update_variant", C.c_int32),
-                ("qrp_panel_stages", C.c_int32), ("gram_pdl", C.c_int32)]
+                ("qrp_panel_stages", C.c_int32), ("gram_pdl", C.c_int32), ("l2_order", C.c_int32)]
 
 
 class Stats(C.Structure):

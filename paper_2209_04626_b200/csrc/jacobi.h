@@ -76,6 +76,11 @@ struct JacobiRound {
     int update_tpc;     // 0: auto
     int update_ts;      // 1: fp32 update with the A operand in tensor memory (k_pair_update_tc_ts)
     int diag;           // mpjsvd_options.diag_timing
+    // L2-aware traversal (mpjsvd_options.l2_order, resolved on the host; fp32 tcgen05 stage): consecutive kernels
+    // walk the rows of X in opposite directions, all pairs in step, so that the ~100 MB of X the previous kernel
+    // touched last are the first the next one reads (a 126 MB LRU-like L2 gives a cyclic 268 MB stream no hits).
+    int gram_il;        // 1: the Gram CTA (pair, split) takes the row tiles split, split + nsplit, ... (top -> bottom)
+    int upd_order;      // 1: the update's items are claimed tile group major, bottom group first
 };
 
 // the pair's blocks are unchanged since its previous evaluation (exactly one sweep ago)

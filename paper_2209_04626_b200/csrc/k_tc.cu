@@ -692,13 +692,17 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ws(JacobiRound<float
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tmem_base;
-    const long long rbeg = (long long)split * a.rows_per_split;
-    const long long rend = min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
-    const int ntile = (int)((rend - rbeg + KT - 1) / KT);
+    // row tiles of this CTA: its contiguous row slab, or (gram_il, DESIGN.md sec. 8 "L2-aware traversal") the
+    // tiles split, split + nsplit, ... of the whole row range, so that all CTAs walk the rows top -> bottom in step
+    const bool il = a.gram_il != 0;
+    const long long rbeg = il ? (long long)split * KT : (long long)split * a.rows_per_split;
+    const long long rend = il ? (long long)a.m_pad : min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const long long rstep = il ? (long long)a.nsplit * KT : (long long)KT;
+    const int ntile = rend > rbeg ? (int)((rend - rbeg + rstep - 1) / rstep) : 0;
     const uint32_t sbase = tc::smem_u32(sm);
     auto issue = [&](int t) {
         const int s = t % GM_ST;
-        const int r0 = (int)(rbeg + (long long)t * KT);
+        const int r0 = (int)(rbeg + (long long)t * rstep);
         mbar_expect_tx(&full[s], tx);
         tma_load_2d_g(sbase + (uint32_t)(s * STAGE), &smap, r0, cI, &full[s]);
         if (hasJ) tma_load_2d_g(sbase + (uint32_t)(s * STAGE) + 4096, &smap, r0, cJ, &full[s]);
@@ -1460,9 +1464,18 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<floa
             while (true) {
                 const long long wk = atomicAdd(a.dctr + 1, 1);
                 if (wk >= total) break;
-                const int p = (int)(wk / (2 * ngroups)), rem = (int)(wk % (2 * ngroups));
-                which = rem / ngroups;
-                grp = rem % ngroups;
+                int p, rem;
+                if (a.upd_order) {   // tile group major, bottom group first (the rows the Gram read last)
+                    p = (int)(wk % a.npairs);
+                    rem = (int)(wk / a.npairs);
+                    which = rem / ngroups;
+                    grp = ngroups - 1 - rem % ngroups;
+                } else {
+                    p = (int)(wk / (2 * ngroups));
+                    rem = (int)(wk % (2 * ngroups));
+                    which = rem / ngroups;
+                    grp = rem % ngroups;
+                }
                 int pr = ld_acquire_gpu(a.dlist + p);
                 unsigned long long t0 = 0;
                 while (pr < 0) {

@@ -376,6 +376,21 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
             }
         }
     }
+    // L2-aware traversal (options.l2_order): the warp-specialised swizzled Gram takes interleaved
+    // row tiles top -> bottom and the TMEM-A update claims its tile groups bottom group first.  Off by default
+    // (measured on B200: no change at C5, the round kernels are not DRAM-bandwidth bound).
+    // -1: on when the fp32 X does not fit in L2 (> 96 MB) and the row slabs are the automatic ones
+    a.gram_il = 0;
+    a.upd_order = 0;
+    if constexpr (sizeof(T) == 4) {
+        const bool capable = use_tc && a.smap && gram_v >= 16 && gram_v <= 17;
+        const bool big = (double)m_pad * (double)n * sizeof(T) > 96.0 * 1024 * 1024;
+        const int lo = h->opts.l2_order;
+        if (capable && (lo == 1 || (lo < 0 && big && h->opts.split_rows == 0))) {
+            a.gram_il = 1;
+            a.upd_order = a.update_ts ? 1 : 0;
+        }
+    }
     MPJ_CUDA_TRY(cudaMemsetAsync(a.dctr, 0, sizeof(int) * 4, st));
     // exact skip of unchanged pairs (every block's last-rotation round: one array per process; across NCCL
     // ranks the entry travels with the block in the per-round exchange)
@@ -1278,6 +1293,7 @@ void mpjsvd_default_options(mpjsvd_options* o) {
     o->update_variant = 1;
     o->qrp_panel_stages = -1;
     o->gram_pdl = 1;
+    o->l2_order = 0;
 }
 
 int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
@@ -1294,7 +1310,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 17 ||
         o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1 ||
         o.qrp_panel_stages < -1 || o.qrp_panel_stages == 1 || o.qrp_panel_stages > 4 ||
-        o.gram_pdl < 0 || o.gram_pdl > 1)
+        o.gram_pdl < 0 || o.gram_pdl > 1 || o.l2_order < -1 || o.l2_order > 1)
         return MPJSVD_ERR_INVALID_ARG;
     mpjsvd_handle h = new (std::nothrow) mpjsvd_handle_s();
     if (!h) return MPJSVD_ERR_OUT_OF_MEMORY;

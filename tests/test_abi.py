@@ -40,7 +40,7 @@ def test_strerror_and_defaults():
     o = mp.default_options()
     assert o.block_cols == 32 and o.tol_mult64 == 4.0 and o.inner_tol_div == 8
     assert o.max_sweeps32 == 20 and o.max_sweeps64 == 30 and o.x_from_lq == 1
-    assert mp.lib().mpjsvd_version() == 140
+    assert mp.lib().mpjsvd_version() == 150
     assert o.virtual_shards == 1 and o.split_rows == 0
 
 

@@ -619,10 +619,13 @@ def test_refine_v_vs_oracle(mp, name, n, extra):
     ({"block_cols": 16}, {"b": 16}),
     ({"x_from_lq": 0}, {"x_from_lq": 0}),
     ({"max_inner32": 2}, {"max_inner32": 2}),
+    ({"l2_order": 1}, {}),
+    ({"l2_order": 1, "switch_u": 0}, {"switch_u": 0}),
 ])
 def test_option_paths_vs_oracle(mp, opts, oopts):
     """Non-default implementation paths (FFMA fp32 stage, serial solve/update, V-route without overlap,
-    b = 16 (SIMT kernels), X = R, two fp32 inner sweeps) against the oracle run with the same
+    b = 16 (SIMT kernels), X = R, two fp32 inner sweeps, the L2-aware traversal: interleaved Gram row
+    tiles and the bottom-up tile-group-major update) against the oracle run with the same
     algorithmic options: valid SVD, tiered sigma bound, sweeps +-1."""
     a = testmat.config_matrix("C3", 384)
     U, S, V, st = mp.factor(dev(a), **opts)
@@ -635,6 +638,24 @@ def test_option_paths_vs_oracle(mp, opts, oopts):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
     if not opts.get("x_from_lq", 1) == 0:
         assert abs(st["sweeps32"] - sto["sweeps32"]) <= 1
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(200, 200), (352, 352), (1000, 77), (6144, 256)])
+def test_l2_order_ragged_vs_oracle(mp, m, n):
+    """l2_order = 1 (interleaved Gram row tiles, bottom-up group-major update) on ragged block widths, odd block
+    counts (bye pairs), a tall input and the 32-row-stage Gram's row count: sigma against the oracle within the
+    parity bar, valid SVD, and the same sweep counts as the default traversal (the two differ in rounding only)."""
+    a = testmat.config_matrix("C1", n) if m == n else testmat.config_matrix("C4", n, m=m)
+    r0 = mp.factor(dev(a))
+    r1 = mp.factor(dev(a), l2_order=1)
+    U, S, V = host(r1[0]), host(r1[1]), host(r1[2])
+    check_svd(a, U, S, V)
+    so = oracle.mixed_svd(a)[1]
+    if m == n:
+        assert np.max(np.abs(S - so) / so) <= 1e-12
+    else:
+        assert np.all(np.abs(S - so) / so <= tiered(so, kappa_s(a)))
+    assert abs(r1[3]["sweeps32"] - r0[3]["sweeps32"]) <= 1 and abs(r1[3]["sweeps64"] - r0[3]["sweeps64"]) <= 1
 
 
 @pytest.mark.parametrize("name,n", [("exact", 64), ("C1", 256), ("C3", 500), ("C2", 384), ("C5", 1000)])
