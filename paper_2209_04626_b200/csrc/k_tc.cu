@@ -1217,6 +1217,7 @@ __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_pdl(JacobiRound<flo
 // ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
+int launch_gram_sw_ta(const JacobiRound<float>& a, cudaStream_t st);   // TMEM-A Gram, defined with its kernel below
 // Gram variants (KT rows per stage, ST stages, CTAs per SM); MPJSVD_GRAM_VARIANT selects one (experiments)
 struct GramVariant {
     void (*fn)(JacobiRound<float>);
@@ -1287,6 +1288,7 @@ int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long r
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
+    if (a.smap && a.gram_variant >= 18 && a.gram_variant <= 19) return launch_gram_sw_ta(a, st);
     if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 17) {
         const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
         switch (a.gram_variant) {
@@ -1389,8 +1391,8 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
     if (tma) {
         const int k = gram_tma_kt(rows_pad, kt);
-        if ((variant == 9 && k == 32) || variant == 11 || variant == 14 || variant == 16) return 3;
-        if (variant == 10 || variant == 15) return 4;
+        if ((variant == 9 && k == 32) || variant == 11 || variant == 14 || variant == 16 || variant == 18) return 3;
+        if (variant == 10 || variant == 15 || variant == 19) return 4;
         if (variant == 12 || variant == 17) return 2;
         if (variant == 13) return 1;
         return k == 32 ? 4 : 2;
@@ -1405,6 +1407,182 @@ int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
 
 
 namespace mpj {
+
+// tcgen05.mma with the A operand in tensor memory (the "TS" form: A K-major, lane = M-row, one column per K element)
+__device__ __forceinline__ void mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "r"(atmem), "l"(bd), "r"(idesc), "r"(acc));
+}
+
+// ------------------------------------------------------------------------
+// k_pair_gram_sw_ta: the warp-specialised swizzled Gram (k_pair_gram_sw_ws) with the A operand [H ; L] in TENSOR
+// MEMORY.  k_pair_gram_sw_ws is bound by shared-memory traffic (per 32-row tile: 8 KB landed by TMA, 8 KB read and
+// 8 KB of lo parts written by the lo warps, 24 KB read by the MMAs: A = [H ; L] 16 KB + B = H 8 KB).  Here a stage is
+// only the 8 KB of raw columns (B = H, read by the MMA through the same SWIZZLE_128B descriptor): thread m of the
+// four conversion warps owns TMEM lane m = M-row m of A, reads its column's 32 rows (one swizzled 128-byte row,
+// conflict-free 16-byte chunks), and writes hi (m < 64) or lo = x - hi (m >= 64) into the tile's A buffer with
+// tcgen05.st (column = K element); the MMAs are the A-from-TMEM form (mma_ts).  No lo parts in shared memory, no
+// async-proxy fence: 32 KB of shared-memory traffic per tile instead of 48, and GM_ST stages of 8 KB instead of
+// 16 KB (twice the tiles in flight in the same footprint).  A is double buffered (TMEM columns 64..95 / 96..127
+// next to the 64 accumulator columns; 128 allocated): the conversion of tile t waits for the MMAs of tile t - 2.
+// Same products in the same order as k_pair_gram_sw_ws: bitwise equal on equal row sets.
+// ------------------------------------------------------------------------
+template <int GM_ST, int MINB>
+__global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
+    constexpr int KT = 32, NT = 160;
+    constexpr int STAGE = 64 * KT * 4;                  // 8 KB: raw I | raw J, 4 KB each
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    reset_publication(a);
+    gram_pdl_begin(a);
+    if (pair_unchanged(a, a.pd[blockIdx.y])) return;
+    extern __shared__ __align__(1024) unsigned char gta_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gta_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], a_ready[2], fin;
+    __shared__ uint32_t tmem_base;
+    const int pair = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const PairDesc<float> pd = a.pd[pair];
+    const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
+    const bool hasJ = pd.w1 > 0;
+    const uint32_t tx = hasJ ? 2u * 32u * KT * 4u : 32u * KT * 4u;
+    if (warp == 0) tc::tmem_alloc<128>(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < GM_ST; ++s) {
+            tc::mbar_init(&full[s]);
+            tc::mbar_init(&done[s]);
+        }
+        mbar_init_n(&a_ready[0], 128);
+        mbar_init_n(&a_ready[1], 128);
+        tc::mbar_init(&fin);
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (!hasJ) {   // bye pair: N-rows 32..63 (raw J) stay zero in every stage
+        for (int s = 0; s < GM_ST; ++s)
+            for (int i = tid; i < 4096 / 16; i += NT)
+                reinterpret_cast<float4*>(sm + (size_t)s * STAGE + 4096)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tc::fence_async_smem();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base;                    // columns [0, 64): accumulator; [64, 128): two A buffers
+    const bool il = a.gram_il != 0;
+    const long long rbeg = il ? (long long)split * KT : (long long)split * a.rows_per_split;
+    const long long rend = il ? (long long)a.m_pad : min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
+    const long long rstep = il ? (long long)a.nsplit * KT : (long long)KT;
+    const int ntile = rend > rbeg ? (int)((rend - rbeg + rstep - 1) / rstep) : 0;
+    const uint32_t sbase = tc::smem_u32(sm);
+    auto issue = [&](int t) {
+        const int s = t % GM_ST;
+        const int r0 = (int)(rbeg + (long long)t * rstep);
+        mbar_expect_tx(&full[s], tx);
+        tma_load_2d_g(sbase + (uint32_t)(s * STAGE), &smap, r0, cI, &full[s]);
+        if (hasJ) tma_load_2d_g(sbase + (uint32_t)(s * STAGE) + 4096, &smap, r0, cJ, &full[s]);
+    };
+    if (warp == 0) {
+        if (tid == 0) {
+            for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
+            for (int t = 0; t < ntile; ++t) {
+                const int s = t % GM_ST, ab = t & 1;
+                tc::mbar_wait(&a_ready[ab], (uint32_t)((t >> 1) & 1));
+                tc::fence_after();
+                const uint32_t base = sbase + (uint32_t)(s * STAGE);
+                const uint32_t abuf = tmem + 64u + 32u * (uint32_t)ab;
+#pragma unroll
+                for (int ks = 0; ks < KT / 8; ++ks)
+                    mma_ts(tmem, abuf + (uint32_t)(8 * ks), sdesc_sw128(base + ks * 32), idesc, (t > 0 || ks > 0) ? 1u : 0u);
+                tc::commit(&done[s]);
+                if (t >= 1 && t - 1 + GM_ST < ntile) {
+                    const int sp = (t - 1) % GM_ST;
+                    tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
+                    issue(t - 1 + GM_ST);
+                }
+            }
+            if (ntile > 0) tc::commit(&fin);
+        }
+        __syncwarp();
+    } else {
+        // conversion warps 1..4: warp w may touch TMEM lanes 32 (w % 4) .. + 31
+        const int m = 32 * (warp & 3) + (tid & 31);       // M-row of A = TMEM lane
+        const int c = m & 63;                             // column of W = [X_I X_J]
+        const bool lo = m >= 64;
+        const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+        for (int t = 0; t < ntile; ++t) {
+            const int s = t % GM_ST, ab = t & 1;
+            const unsigned char* row = sm + (size_t)s * STAGE + c * 128;
+            if (t >= 2) {                                 // the MMAs of tile t - 2 have read this A buffer
+                tc::mbar_wait(&done[(t - 2) % GM_ST], (uint32_t)(((t - 2) / GM_ST) & 1));
+                tc::fence_after();
+            }
+            tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
+            float4 x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = *reinterpret_cast<const float4*>(row + ((j ^ (c & 7)) << 4));
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 xv = x[4 * g + j];
+                    const float4 h = tc::hi4(xv);
+                    const float4 o = lo ? tc::lo4(xv, h) : h;
+                    v[4 * j + 0] = o.x; v[4 * j + 1] = o.y; v[4 * j + 2] = o.z; v[4 * j + 3] = o.w;
+                }
+                tmem_st16(tmem + lane_base + 64u + 32u * (uint32_t)ab + 16u * (uint32_t)g, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n");
+            tc::fence_before();
+            mbar_arrive(&a_ready[ab]);
+        }
+    }
+    float* out = a.partial + ((long long)pair * a.nsplit + split) * (64 * 64);
+    float* red = reinterpret_cast<float*>(sm);
+    if (ntile > 0) {
+        tc::mbar_wait(&fin, 0);
+        tc::fence_after();
+        __syncthreads();                           // every stage consumed before red (stage 0..) is overwritten
+        if (tid < 128) {                           // TMEM lanes 0..127: warps 0..3
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[tid * 65 + c0 + j] = v[j];
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * 64; e += NT) {
+            const int p = e >> 6, q = e & 63;
+            out[e] = red[p * 65 + q] + red[(64 + p) * 65 + q] + red[(64 + q) * 65 + p];
+        }
+    } else {
+        for (int e = tid; e < 64 * 64; e += NT) out[e] = 0.f;
+    }
+    gram_pdl_end(a, pair);
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<128>(tmem);
+}
+
+template <int ST>
+constexpr size_t gram_ta_smem() { return (size_t)ST * 8192 + 1024; }
+
+// launcher of the TMEM-A Gram (gram_variant 18: 8 stages at 3 CTAs/SM; 19: 6 stages at 4 CTAs/SM)
+int launch_gram_sw_ta(const JacobiRound<float>& a, cudaStream_t st) {
+    const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
+    if (a.gram_variant == 19) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<6, 4>, gram_ta_smem<6>()));
+        k_pair_gram_sw_ta<6, 4><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<6>(), st>>>(a, sm);
+    } else {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 3><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
+    }
+    MPJ_LAUNCHED();
+    return 0;
+}
+
 // ------------------------------------------------------------------------
 // k_pair_update_tc_ts: k_pair_update_tc_pdl with the A operand (W_hi, W_lo) in TENSOR MEMORY instead of shared
 // memory (tcgen05.mma ... [d], [a_tmem], b_desc: the "TS" form, A K-major, lane = row, one column per
@@ -1418,12 +1596,6 @@ namespace mpj {
 constexpr int UTS_NR = 6;
 constexpr size_t update_ts_smem() { return 32768 + (size_t)UTS_NR * UT_RAW_BYTES + 1024; }
 
-__device__ __forceinline__ void mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dtmem),
-        "r"(atmem), "l"(bd), "r"(idesc), "r"(acc));
-}
 
 template <bool TMA>
 __global__ void __launch_bounds__(UT_NT, 1) k_pair_update_tc_ts(JacobiRound<float> a, int ngroups, int tpc,

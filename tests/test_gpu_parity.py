@@ -704,12 +704,14 @@ def test_auto_qrsvd_branch_larger_vs_oracle(mp):
     assert abs(st["sweeps64"] - sto["sweeps64"]) <= 1
 
 
-@pytest.mark.parametrize("variant,kt", [(8, 0), (9, 0), (8, 32), (9, 32), (10, 0), (11, 0), (10, 32), (16, 0), (17, 0)])
+@pytest.mark.parametrize("variant,kt", [(8, 0), (9, 0), (8, 32), (9, 32), (10, 0), (11, 0), (10, 32), (16, 0), (17, 0),
+                                        (18, 0), (19, 0)])
 def test_gram_tma_warp_specialised_bitwise(mp, variant, kt):
     """Gram kernel variants with the same MMA sequence as k_pair_gram_tma: 8 / 9 warp-specialised (producer +
     MMA lane, lo-part warps, per-stage mbarriers instead of a CTA barrier per tile), 10 / 11 the 128-byte-
-    swizzled operand layout fed by 2-D TMA boxes (3 / 4 stages): the whole SVD is bitwise equal when the row
-    slabs are the same (split_rows fixed)."""
+    swizzled operand layout fed by 2-D TMA boxes (3 / 4 stages), 16 / 17 its warp-specialised form, 18 / 19 the
+    same with the A operand [H ; L] in tensor memory (8 / 6 stages of raw columns only): the whole SVD is bitwise
+    equal when the row slabs are the same (split_rows fixed)."""
     a = testmat.config_matrix("C3", 512)
     r0 = mp.factor(dev(a), split_rows=128, gram_kt=kt)
     r1 = mp.factor(dev(a), split_rows=128, gram_kt=kt, gram_variant=variant)
