@@ -1412,7 +1412,7 @@ static int launch_round_w(const JacobiRound<T>& a0, cudaStream_t st, const ProfH
     // Gram -> solve overlap only behind the Gram kernels that count their partials (gram_pdl_end)
     JacobiRound<T> a = a0;
     a.gram_pdl = a0.gram_pdl && (sizeof(T) == 8 || (W == 64 && a0.use_tc && a0.smap && a0.gram_variant >= 10 &&
-                                                     a0.gram_variant <= 19)) ? 1 : 0;
+                                                     a0.gram_variant <= 26)) ? 1 : 0;
     if (hook) hook->begin(hook->ctx, KName<T>::gram);
     if constexpr (sizeof(T) == 8) {
         MPJ_CUDA_TRY(set_smem(k_pair_gram_dmma<W>, (size_t)(gram_dmma_smem(W))));

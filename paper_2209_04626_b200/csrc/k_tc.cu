@@ -1288,7 +1288,7 @@ int make_gram_tmap_sw128(void* out, const float* base, long long ld, long long r
 }
 
 int launch_gram_tc(const JacobiRound<float>& a, cudaStream_t st) {
-    if (a.smap && a.gram_variant >= 18 && a.gram_variant <= 19) return launch_gram_sw_ta(a, st);
+    if (a.smap && a.gram_variant >= 18 && a.gram_variant <= 26) return launch_gram_sw_ta(a, st);
     if (a.smap && a.gram_variant >= 10 && a.gram_variant <= 17) {
         const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
         switch (a.gram_variant) {
@@ -1391,9 +1391,9 @@ int launch_update_tc(const JacobiRound<float>& a, cudaStream_t st) {
 int gram_tc_ctas_per_sm(long long rows_pad, int tma, int kt, int variant) {
     if (tma) {
         const int k = gram_tma_kt(rows_pad, kt);
-        if ((variant == 9 && k == 32) || variant == 11 || variant == 14 || variant == 16 || variant == 18) return 3;
+        if ((variant == 9 && k == 32) || variant == 11 || variant == 14 || variant == 16 || variant == 18 || variant == 22 || variant == 23 || variant == 25) return 3;
         if (variant == 10 || variant == 15 || variant == 19) return 4;
-        if (variant == 12 || variant == 17) return 2;
+        if (variant == 12 || variant == 17 || variant == 20 || variant == 21 || variant == 24 || variant == 26) return 2;
         if (variant == 13) return 1;
         return k == 32 ? 4 : 2;
     }
@@ -1429,9 +1429,9 @@ __device__ __forceinline__ void mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t 
 // next to the 64 accumulator columns; 128 allocated): the conversion of tile t waits for the MMAs of tile t - 2.
 // Same products in the same order as k_pair_gram_sw_ws: bitwise equal on equal row sets.
 // ------------------------------------------------------------------------
-template <int GM_ST, int MINB>
-__global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
-    constexpr int KT = 32, NT = 160;
+template <int GM_ST, int MINB, int NA, int LAG = 1, int CG = 1>
+__global__ void __launch_bounds__(32 + 128 * CG, MINB) k_pair_gram_sw_ta(JacobiRound<float> a, const __grid_constant__ CUtensorMap smap) {
+    constexpr int KT = 32, NT = 32 + 128 * CG;          // warp 0: TMA + MMA lane; CG groups of 4 conversion warps
     constexpr int STAGE = 64 * KT * 4;                  // 8 KB: raw I | raw J, 4 KB each
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
     reset_publication(a);
@@ -1439,7 +1439,7 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
     if (pair_unchanged(a, a.pd[blockIdx.y])) return;
     extern __shared__ __align__(1024) unsigned char gta_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gta_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], a_ready[2], fin;
+    __shared__ __align__(8) uint64_t full[GM_ST], done[GM_ST], a_ready[NA], fin;
     __shared__ uint32_t tmem_base;
     const int pair = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -1447,14 +1447,15 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
     const int cI = (int)((pd.x0 - a.tbase) / a.tld), cJ = (int)((pd.x1 - a.tbase) / a.tld);
     const bool hasJ = pd.w1 > 0;
     const uint32_t tx = hasJ ? 2u * 32u * KT * 4u : 32u * KT * 4u;
-    if (warp == 0) tc::tmem_alloc<128>(&tmem_base);
+    constexpr int TCOLS = 64 + 32 * NA <= 128 ? 128 : 256;   // accumulator + NA A buffers of 32 columns
+    static_assert(64 + 32 * NA <= 256, "TMEM columns");
+    if (warp == 0) tc::tmem_alloc<TCOLS>(&tmem_base);
     if (tid == 0) {
         for (int s = 0; s < GM_ST; ++s) {
             tc::mbar_init(&full[s]);
             tc::mbar_init(&done[s]);
         }
-        mbar_init_n(&a_ready[0], 128);
-        mbar_init_n(&a_ready[1], 128);
+        for (int q = 0; q < NA; ++q) mbar_init_n(&a_ready[q], 128);
         tc::mbar_init(&fin);
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
@@ -1467,7 +1468,7 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t tmem = tmem_base;                    // columns [0, 64): accumulator; [64, 128): two A buffers
+    const uint32_t tmem = tmem_base;                    // columns [0, 64): accumulator; then NA A buffers of 32
     const bool il = a.gram_il != 0;
     const long long rbeg = il ? (long long)split * KT : (long long)split * a.rows_per_split;
     const long long rend = il ? (long long)a.m_pad : min(rbeg + (long long)a.rows_per_split, (long long)a.m_pad);
@@ -1485,8 +1486,8 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
         if (tid == 0) {
             for (int t = 0; t < GM_ST && t < ntile; ++t) issue(t);
             for (int t = 0; t < ntile; ++t) {
-                const int s = t % GM_ST, ab = t & 1;
-                tc::mbar_wait(&a_ready[ab], (uint32_t)((t >> 1) & 1));
+                const int s = t % GM_ST, ab = t % NA;
+                tc::mbar_wait(&a_ready[ab], (uint32_t)((t / NA) & 1));
                 tc::fence_after();
                 const uint32_t base = sbase + (uint32_t)(s * STAGE);
                 const uint32_t abuf = tmem + 64u + 32u * (uint32_t)ab;
@@ -1494,26 +1495,31 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
                 for (int ks = 0; ks < KT / 8; ++ks)
                     mma_ts(tmem, abuf + (uint32_t)(8 * ks), sdesc_sw128(base + ks * 32), idesc, (t > 0 || ks > 0) ? 1u : 0u);
                 tc::commit(&done[s]);
-                if (t >= 1 && t - 1 + GM_ST < ntile) {
-                    const int sp = (t - 1) % GM_ST;
-                    tc::mbar_wait(&done[sp], (uint32_t)(((t - 1) / GM_ST) & 1));
-                    issue(t - 1 + GM_ST);
+                // refill the stage of tile t - LAG: with LAG = 1 this lane waits for the completion of the MMAs it
+                // issued one iteration ago (issue -> mbarrier latency on the critical path of every tile); LAG >= 2
+                // finds them complete, at the price of LAG - 1 tiles of prefetch distance
+                if (t >= LAG && t - LAG + GM_ST < ntile) {
+                    const int sp = (t - LAG) % GM_ST;
+                    tc::mbar_wait(&done[sp], (uint32_t)(((t - LAG) / GM_ST) & 1));
+                    issue(t - LAG + GM_ST);
                 }
             }
             if (ntile > 0) tc::commit(&fin);
         }
         __syncwarp();
     } else {
-        // conversion warps 1..4: warp w may touch TMEM lanes 32 (w % 4) .. + 31
+        // conversion warps (CG groups of four; group g takes the tiles t = g, g + CG, ...): warp w may touch TMEM
+        // lanes 32 (w % 4) .. + 31
+        const int grp = (warp - 1) >> 2;
         const int m = 32 * (warp & 3) + (tid & 31);       // M-row of A = TMEM lane
         const int c = m & 63;                             // column of W = [X_I X_J]
         const bool lo = m >= 64;
         const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-        for (int t = 0; t < ntile; ++t) {
-            const int s = t % GM_ST, ab = t & 1;
+        for (int t = grp; t < ntile; t += CG) {
+            const int s = t % GM_ST, ab = t % NA;
             const unsigned char* row = sm + (size_t)s * STAGE + c * 128;
-            if (t >= 2) {                                 // the MMAs of tile t - 2 have read this A buffer
-                tc::mbar_wait(&done[(t - 2) % GM_ST], (uint32_t)(((t - 2) / GM_ST) & 1));
+            if (t >= NA) {                                // the MMAs of tile t - NA have read this A buffer
+                tc::mbar_wait(&done[(t - NA) % GM_ST], (uint32_t)(((t - NA) / GM_ST) & 1));
                 tc::fence_after();
             }
             tc::mbar_wait(&full[s], (uint32_t)((t / GM_ST) & 1));
@@ -1563,21 +1569,43 @@ __global__ void __launch_bounds__(160, MINB) k_pair_gram_sw_ta(JacobiRound<float
     gram_pdl_end(a, pair);
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_free<128>(tmem);
+    if (warp == 0) tc::tmem_free<TCOLS>(tmem);
 }
 
 template <int ST>
 constexpr size_t gram_ta_smem() { return (size_t)ST * 8192 + 1024; }
 
-// launcher of the TMEM-A Gram (gram_variant 18: 8 stages at 3 CTAs/SM; 19: 6 stages at 4 CTAs/SM)
+// launcher of the TMEM-A Gram (gram_variant 18: 8 stages at 3 CTAs/SM, 2 A buffers; 19: 6 stages at 4 CTAs/SM;
+// 20 / 21: 12 / 8 stages at 2 CTAs/SM with 6 A buffers (256 TMEM columns))
 int launch_gram_sw_ta(const JacobiRound<float>& a, cudaStream_t st) {
     const CUtensorMap& sm = *reinterpret_cast<const CUtensorMap*>(a.smap);
     if (a.gram_variant == 19) {
-        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<6, 4>, gram_ta_smem<6>()));
-        k_pair_gram_sw_ta<6, 4><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<6>(), st>>>(a, sm);
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<6, 4, 2>, gram_ta_smem<6>()));
+        k_pair_gram_sw_ta<6, 4, 2><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<6>(), st>>>(a, sm);
+    } else if (a.gram_variant == 20) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<12, 2, 6>, gram_ta_smem<12>()));
+        k_pair_gram_sw_ta<12, 2, 6><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<12>(), st>>>(a, sm);
+    } else if (a.gram_variant == 21) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 2, 6>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 2, 6><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
+    } else if (a.gram_variant == 22) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3, 2, 2>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 3, 2, 2><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
+    } else if (a.gram_variant == 23) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3, 2, 3>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 3, 2, 3><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
+    } else if (a.gram_variant == 25) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3, 2, 1, 2>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 3, 2, 1, 2><<<dim3(a.nsplit, a.npairs), 288, gram_ta_smem<8>(), st>>>(a, sm);
+    } else if (a.gram_variant == 26) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<12, 2, 6, 1, 2>, gram_ta_smem<12>()));
+        k_pair_gram_sw_ta<12, 2, 6, 1, 2><<<dim3(a.nsplit, a.npairs), 288, gram_ta_smem<12>(), st>>>(a, sm);
+    } else if (a.gram_variant == 24) {
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<12, 2, 6, 3>, gram_ta_smem<12>()));
+        k_pair_gram_sw_ta<12, 2, 6, 3><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<12>(), st>>>(a, sm);
     } else {
-        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3>, gram_ta_smem<8>()));
-        k_pair_gram_sw_ta<8, 3><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
+        MPJ_CUDA_TRY(set_smem(k_pair_gram_sw_ta<8, 3, 2>, gram_ta_smem<8>()));
+        k_pair_gram_sw_ta<8, 3, 2><<<dim3(a.nsplit, a.npairs), 160, gram_ta_smem<8>(), st>>>(a, sm);
     }
     MPJ_LAUNCHED();
     return 0;

@@ -287,7 +287,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     // Measured: C5 Gram 179.8 -> 172.8 ms per step against the shared-memory-A kernel
     // (k_pair_gram_sw_ws, variant 16; bitwise equal), which had replaced the CTA-barrier kernel (variants 11 / 10)
     int gram_v = h->opts.gram_variant;
-    if (h->opts.gram_tma == 2 && (gram_v < 10 || gram_v > 19)) gram_v = 18;
+    if (h->opts.gram_tma == 2 && (gram_v < 10 || gram_v > 26)) gram_v = 18;
     long long nsplit = 1;
     if (h->opts.split_rows > 0) {
         nsplit = ceil_div(m_pad, round_up(h->opts.split_rows, 32));
@@ -366,7 +366,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
                 a.tld = ldx;
             }
             if (base && !has_v && make_update_tmap(umap_buf, base, ldx, m_pad, cols) == 0) a.umap = umap_buf;
-            if (base && gram_v >= 10 && gram_v <= 19 &&
+            if (base && gram_v >= 10 && gram_v <= 26 &&
                 make_gram_tmap_sw128(smap_buf, base, ldx, m_pad, cols) == 0)
                 a.smap = smap_buf;
             if (base && make_gram_tmap(tmap_buf, base, ldx, m_pad, cols, a.gram_kt) == 0) {
@@ -384,7 +384,7 @@ int run_block_jacobi(mpjsvd_handle h, JStore<T>& S, long long ldx, long long m_p
     a.gram_il = 0;
     a.upd_order = 0;
     if constexpr (sizeof(T) == 4) {
-        const bool capable = use_tc && a.smap && gram_v >= 16 && gram_v <= 19;
+        const bool capable = use_tc && a.smap && gram_v >= 16 && gram_v <= 26;
         const bool big = (double)m_pad * (double)n * sizeof(T) > 96.0 * 1024 * 1024;
         const int lo = h->opts.l2_order;
         if (capable && (lo == 1 || (lo < 0 && big && h->opts.split_rows == 0))) {
@@ -1308,7 +1308,7 @@ int mpjsvd_create(mpjsvd_handle* out, const mpjsvd_options* opts) {
     if (!(o.tol_mult32 > 0) || !(o.tol_mult64 > 0) || o.inner_tol_div < 1 || o.max_sweeps32 < 1 ||
         o.max_sweeps64 < 1 || o.max_inner < 1 || o.max_inner32 < 1 || (o.path != 0 && o.path != 1 && o.path != 2))
         return MPJSVD_ERR_INVALID_ARG;
-    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 19 ||
+    if ((o.gram_kt != 0 && o.gram_kt != 32 && o.gram_kt != 64) || o.gram_tma < 0 || o.gram_tma > 2 || o.gram_variant < 0 || o.gram_variant > 26 ||
         o.update_tpc < 0 || o.qr_panel_mode < 0 || o.qr_panel_mode > 2 || o.refine_v < 0 || o.refine_v > 1 || o.update_variant < 0 || o.update_variant > 1 ||
         o.qrp_panel_stages < -1 || o.qrp_panel_stages == 1 || o.qrp_panel_stages > 4 ||
         o.gram_pdl < 0 || o.gram_pdl > 1 || o.l2_order < -1 || o.l2_order > 1)

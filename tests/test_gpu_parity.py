@@ -705,7 +705,7 @@ def test_auto_qrsvd_branch_larger_vs_oracle(mp):
 
 
 @pytest.mark.parametrize("variant,kt", [(8, 0), (9, 0), (8, 32), (9, 32), (10, 0), (11, 0), (10, 32), (16, 0), (17, 0),
-                                        (18, 0), (19, 0)])
+                                        (18, 0), (19, 0), (20, 0), (21, 0), (22, 0), (23, 0), (24, 0), (25, 0), (26, 0)])
 def test_gram_tma_warp_specialised_bitwise(mp, variant, kt):
     """Gram kernel variants with the same MMA sequence as k_pair_gram_tma: 8 / 9 warp-specialised (producer +
     MMA lane, lo-part warps, per-stage mbarriers instead of a CTA barrier per tile), 10 / 11 the 128-byte-
