@@ -139,7 +139,9 @@ typedef struct {
                                   8 / 9 warp-specialised; 10..13 the swizzled kernel with 3 / 4 / 6 / 8 stages, 14 / 15
                                   with 256 threads, 16 / 17 warp-specialised swizzled kernel with 4 / 6 stages, 18 / 19
                                   the same with the A operand [H ; L] in tensor memory (8 / 6 stages of raw columns
-                                  only); 0 (default): 18.  10..19 are bitwise equal on equal row slabs */
+                                  only), 20..26 measured shapes of 18 (2 CTAs/SM with 6 A buffers, refill lag, two
+                                  conversion warp groups); 0 (default): 18.  10..26 are bitwise
+                                  equal on equal row slabs */
     int32_t update_tpc;        /* tiles per work item of the overlapped fp32 update; 0 (default): ~3 items per SM */
     int32_t skip_unchanged;    /* 1 (default): skip the Gram and solve of a pair whose blocks did not rotate since
                                   its previous evaluation (exact); 0: evaluate every pair */
